@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""bench.py — Recombinant Sort hot path on B200.
+
+Headline (BASELINE.json metric "sorted Gkeys/s"): configs[1] = cfg2, 2^28
+uint32 keys uniform in [0, 10^6) per GPU (6-digit, 10^6-cell grid), key-only,
+inputs already resident in HBM.  One step = one full sort (count -> occupancy
+scan -> emit -> report) of the 2^28 keys.  The inputs (1 GiB) are larger
+than L2 (126 MB), so no flush is needed between steps.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+For N>1 (torchrun, one rank per GPU, NCCL): weak scaling, 2^28 keys per rank,
+sorted by the small-grid sharding of SURVEY 8e (local count, all-reduce of
+the 10^6-cell grid, each rank emits its own contiguous cell range).
+
+Extra keys on the JSON line: roofline (dominant kernel, live CUDA-event
+timing), passes (per-pass bytes / time / fraction of measured HBM peak), kv
+(the stable key/value variant of cfg2), e2e (through the C-ABI host-buffer
+entry point, H2D + sort + D2H each step), cpu_baseline (the reference library
+compiled from its sources, timed on this host), clocks, gpu_launches.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_KEYS = 1 << 28          # cfg2 keys per GPU
+KEY_BOUND = 10 ** 6       # cfg2 key domain
+KEY_DIGITS = 6            # declared decimal width of the domain (rs_options.key_digits)
+CPU_SAMPLE = 1 << 24      # bounded reference sample (~1.5 s per sort on one core)
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sms, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                maxes.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": max(maxes) if maxes else None,
+                "samples": len(sms), "reasons": sorted(reasons)}
+
+
+# -------------------------------------------------------- reference arm
+def reference_arm(args, rank: int):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    library compiled from /root/reference/proj/src) on the same cfg2 stream,
+    one bounded sample per step.  The reference is single-threaded, so it
+    uses one core (nproc is reported)."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import Oracle, Reference
+
+    o = Oracle()
+    kind = "reference" if Reference.available() else "port"
+    impl = Reference() if kind == "reference" else o
+    keys = o.gen_u32(o.config_seed(2), 0, CPU_SAMPLE, KEY_BOUND)
+    wide = keys.astype(np.int64)
+
+    def step():
+        if kind == "reference":
+            impl.sort_integers(wide)
+        else:
+            impl.sort_integers_u32(keys)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = CPU_SAMPLE / dt / 1e9
+    line = {
+        "impl": "reference", "metric": "sorted Gkeys/s", "value": value, "unit": "Gkeys/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "cfg2: uint32 keys uniform in [0,10^6) (SplitMix64 seed mix(42,2)), key-only, "
+                               "sort_integers facade", "sample_keys": CPU_SAMPLE},
+        "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": 1, "kind": kind,
+                         "sample": f"sort_integers on the first {CPU_SAMPLE} cfg2 keys per step "
+                                   f"(single-threaded library; host nproc={os.cpu_count()})"},
+        "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample():
+    """cpu_baseline for our line: same as the reference arm, 1 warm-up + 2 trials."""
+    import numpy as np
+
+    from oracle import Oracle, Reference
+
+    o = Oracle()
+    kind = "reference" if Reference.available() else "port"
+    keys = o.gen_u32(o.config_seed(2), 0, CPU_SAMPLE, KEY_BOUND)
+    if kind == "reference":
+        r = Reference()
+        wide = keys.astype(np.int64)
+        fn = lambda: r.sort_integers(wide)  # noqa: E731
+    else:
+        fn = lambda: o.sort_integers_u32(keys)  # noqa: E731
+    fn()
+    times = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        fn()
+        times.append(time.perf_counter() - t0)
+    dt = min(times)
+    return {"value": CPU_SAMPLE / dt / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": kind,
+            "sample": f"reference sort_integers (facade) on {CPU_SAMPLE} cfg2 keys, best of 2 after 1 warm-up; "
+                      f"single-threaded library, host nproc={os.cpu_count()}"}
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-kv", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2107_01391_b200 as rs
+    from paper_2107_01391_b200 import dist as rsd
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    lib = rs._lib.load()
+    stream = rs._stream
+
+    from oracle import Oracle  # seed derivation only (bench.cpp:149 pattern)
+
+    seed = Oracle().config_seed(2)
+    n = N_KEYS
+    keys = torch.empty(n, dtype=torch.int32, device="cuda")
+    rs._check(lib.rs_gen_u32(seed, rank * n, n, KEY_BOUND, rs._ptr(keys), stream()))
+    out = torch.empty_like(keys)
+    opts = rs._opts(rs.DEFAULT_CELL_BUDGET, KEY_DIGITS)
+    rep = rs.RsReport()
+
+    def step():
+        if world == 1:
+            rs._check(lib.rs_sort_u32(rs._ptr(keys), n, rs._ptr(out), n, ctypes.byref(opts), ctypes.byref(rep),
+                                      stream()))
+        else:
+            rsd.sharded_grid_sort(keys, KEY_BOUND)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = lib.rs_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = (lib.rs_launch_count() - launches0) // args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = n * world / (ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+
+    result = {
+        "metric": "sorted Gkeys/s", "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "cfg2 (BASELINE configs[1]): 2^28 uint32 keys/GPU uniform in [0,10^6), key-only, "
+                               "6-digit 10^6-cell grid", "keys_per_gpu": n, "key_digits_declared": KEY_DIGITS,
+                   "parallelism": f"shard{world}" if world > 1 else "single",
+                   "l2": "inputs (1 GiB) larger than L2 (126 MB); no flush"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+
+    if rank == 0 and world == 1:
+        # per-pass device time with CUDA events on the library's stream
+        lib.rs_profile_enable(1)
+        lib.rs_profile_reset()
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        ms_arr = (ctypes.c_double * rs._lib.RS_NUM_PASSES)()
+        ln_arr = (ctypes.c_uint64 * rs._lib.RS_NUM_PASSES)()
+        lib.rs_profile_read(ms_arr, ln_arr)
+        lib.rs_profile_enable(0)
+        algo_bytes = {"count": 4 * n, "emit": 4 * n, "scan": KEY_BOUND * 4 + KEY_BOUND * 12, "report": 0}
+        passes = {}
+        for i in range(rs._lib.RS_NUM_PASSES):
+            if ln_arr[i] == 0:
+                continue
+            name = lib.rs_pass_name(i).decode()
+            per_step_ms = ms_arr[i] / args.steps
+            b = algo_bytes.get(name)
+            passes[name] = {"ms": per_step_ms, "launches_per_step": ln_arr[i] // args.steps,
+                            "bytes": b, "gbs": (b / (per_step_ms / 1e3) / 1e9) if b else None,
+                            "frac": (b / (per_step_ms / 1e3) / 1e9 / peak) if b else None}
+        result["passes"] = passes
+        dom = max((p for p in passes if algo_bytes.get(p)), key=lambda p: passes[p]["ms"])
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get(dom)
+        result["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": passes[dom]["gbs"], "peak": peak,
+                              "unit": "GB/s", "frac": passes[dom]["frac"], "traffic": traffic,
+                              "algorithmic_bytes": algo_bytes[dom], "peak_source": peak_src,
+                              "step_frac": (8 * n) / (ms / 1e3) / 1e9 / peak}
+
+        if not args.no_kv:
+            vals = torch.empty_like(keys)
+            rs._check(lib.rs_gen_iota_u32(0, n, rs._ptr(vals), stream()))
+            ko, vo = torch.empty_like(keys), torch.empty_like(keys)
+
+            def kv_step():
+                rs._check(lib.rs_sort_u32_kv(rs._ptr(keys), rs._ptr(vals), n, rs._ptr(ko), rs._ptr(vo), n,
+                                             ctypes.byref(opts), ctypes.byref(rep), stream()))
+
+            for _ in range(3):
+                kv_step()
+            torch.cuda.synchronize()
+            ev0.record()
+            for _ in range(args.steps):
+                kv_step()
+            ev1.record()
+            torch.cuda.synchronize()
+            kms = ev0.elapsed_time(ev1) / args.steps
+            result["kv"] = {"value": n / (kms / 1e3) / 1e9, "unit": "Gkeys/s", "ms_per_step": kms,
+                            "algorithmic_bytes": 20 * n, "step_frac": 20 * n / (kms / 1e3) / 1e9 / peak,
+                            "workload": "cfg2 key/value: uint32 payload = original index, stable"}
+            del vals, ko, vo
+
+        if not args.no_e2e:
+            h_in = torch.empty(n, dtype=torch.int32, pin_memory=True)
+            h_out = torch.empty(n, dtype=torch.int32, pin_memory=True)
+            h_in.copy_(keys.cpu())
+
+            def e2e_step():
+                rs._check(lib.rs_sort_u32_host(rs._ptr(h_in), n, rs._ptr(h_out), ctypes.byref(opts),
+                                               ctypes.byref(rep), stream()))
+
+            e2e_step()
+            t0 = time.perf_counter()
+            for _ in range(max(3, args.steps // 2)):
+                e2e_step()
+            dt = (time.perf_counter() - t0) / max(3, args.steps // 2)
+            ok = bool(torch.equal(h_out[:1000], out[:1000].cpu()))
+            result["e2e"] = {"value": n / dt / 1e9, "unit": "Gkeys/s", "h2d_bytes_per_step": 4 * n,
+                             "d2h_bytes_per_step": 4 * n, "ms_per_step": dt * 1e3, "api": "rs_sort_u32_host",
+                             "checked": ok}
+        if not args.no_cpu:
+            result["cpu_baseline"] = cpu_baseline_sample()
+
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

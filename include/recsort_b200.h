@@ -1,0 +1,216 @@
+/*
+ * recsort_b200.h — C-ABI of the B200-native Recombinant Sort hot path.
+ *
+ * Every entry point is plain C: device pointers, sizes, a cudaStream_t passed
+ * as `void*`, and an rs_status return.  No torch or C++ types cross this
+ * boundary.  The C++ facade in include/recsort/sort.hpp (same names as the
+ * reference's proj/include/recsort/sort.hpp) and the Python host mirror
+ * (paper_2107_01391_b200/__init__.py, same names as proj/python/recsort) are
+ * thin layers over these functions.  INTEGRATION.md shows the bindings.
+ *
+ * Pointer convention: unless a parameter is prefixed h_, it is a DEVICE
+ * pointer on the current CUDA device.  Work is enqueued on `stream` (NULL =
+ * legacy default stream); calls that return a report synchronise `stream`
+ * once at the end to read it back.
+ *
+ * Errors: rs_status mirrors recsort::errc in declaration order
+ * (proj/include/recsort/error.hpp:10-23) shifted by one so that RS_OK == 0,
+ * plus CUDA/NCCL failure codes.  Budget checks happen before any device
+ * allocation (acceptance.cpp:292-314, c09).  The thread-local message of
+ * the last failure is available from rs_last_error().
+ */
+#ifndef RECSORT_B200_H
+#define RECSORT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum rs_status {
+  RS_OK = 0,
+  RS_PARSE_ERROR = 1,            /* errc::parse_error */
+  RS_NEGATIVE_VALUE = 2,         /* errc::negative_value */
+  RS_NON_FINITE = 3,             /* errc::non_finite */
+  RS_CELL_BUDGET_EXCEEDED = 4,   /* errc::cell_budget_exceeded */
+  RS_SYMBOL_OUT_OF_ALPHABET = 5, /* errc::symbol_out_of_alphabet */
+  RS_SPEC_MISMATCH = 6,          /* errc::spec_mismatch */
+  RS_BUFFER_TOO_SMALL = 7,       /* errc::buffer_too_small */
+  RS_RANGE_EXCEEDED = 8,         /* errc::range_exceeded */
+  RS_OUT_OF_RANGE = 9,           /* errc::out_of_range */
+  RS_INVALID_RANGE = 10,         /* errc::invalid_range */
+  RS_INSUFFICIENT_DATA = 11,     /* errc::insufficient_data */
+  RS_INVALID_ARGUMENT = 12,      /* errc::invalid_argument */
+  RS_CUDA_ERROR = 100,           /* a CUDA runtime call or kernel failed */
+  RS_NCCL_ERROR = 101,           /* reserved for the collective layer */
+  RS_NO_DEVICE = 102             /* no CUDA device: there is no CPU path */
+} rs_status;
+
+#define RS_DEFAULT_CELL_BUDGET 100000000ULL /* key_model.hpp:16 */
+
+/* KeySpec (key_model.hpp:35-46). */
+typedef struct rs_key_spec {
+  uint32_t radix;
+  uint32_t total_digits;
+  uint32_t integer_digits;
+} rs_key_spec;
+
+/* ExtractionReport (extraction.hpp:12-15) + the KeySpec every facade result
+ * carries (sort.hpp:19-41).  For multi-level (MSD) sorts, cells_traversed is
+ * the single-grid value the reference would report for the same data with an
+ * unlimited budget (sum over occupied leading-digit rows of max-min+1 suffix,
+ * SURVEY F4); it does not depend on how the grid was split. */
+typedef struct rs_report {
+  uint64_t written;
+  uint64_t cells_traversed;
+  rs_key_spec spec;
+} rs_report;
+
+typedef struct rs_options {
+  /* Per-grid cell budget; 0 means RS_DEFAULT_CELL_BUDGET. */
+  uint64_t max_cells;
+  /* Declared decimal width of the key domain (like a radix sort's bit
+   * range).  0: derive it from the data with a separate max pass (exactly
+   * the reference's sort.cpp:31-40).  >0: count directly into a
+   * 10^key_digits grid and derive the exact spec from the max found by the
+   * same pass; a key outside the declared width is detected on the device
+   * and the sort is redone with the derived width, so the result never
+   * depends on the hint. */
+  uint32_t key_digits;
+  /* 0: reference semantics — a grid above max_cells raises
+   *    RS_CELL_BUDGET_EXCEEDED (key_model.cpp:72-76).
+   * 1: split such grids with MSD bucket passes on the leading digits and
+   *    apply max_cells per bucket grid. */
+  uint32_t msd;
+} rs_options;
+
+/* ---- library / errors ------------------------------------------------- */
+const char* rs_last_error(void);
+const char* rs_status_name(rs_status status);       /* errc_name, key_model.cpp:265-281 */
+const char* rs_version(void);
+/* Frees the calling thread's cached workspaces on every device. */
+void rs_release_workspaces(void);
+
+/* ---- instrumentation ---------------------------------------------------
+ * Every kernel the library launches is counted (rs_launch_count).  With
+ * profiling on, each pass is bracketed by CUDA events recorded on the stream
+ * it runs on and its device time accumulated per pass id; reading the totals
+ * is valid after the sort returned (the call synchronised its stream). */
+enum {
+  RS_PASS_MAX = 0, RS_PASS_COUNT = 1, RS_PASS_SCAN = 2, RS_PASS_EMIT = 3,
+  RS_PASS_REPORT = 4, RS_PASS_KV_HIST = 5, RS_PASS_KV_SCATTER = 6,
+  RS_PASS_MSD_HIST = 7, RS_PASS_MSD_SCATTER = 8, RS_PASS_BUCKET = 9,
+  RS_PASS_COPY = 10, RS_PASS_OTHER = 11, RS_NUM_PASSES = 12
+};
+uint64_t rs_launch_count(void);
+void rs_profile_enable(int on);
+void rs_profile_reset(void);
+/* Fills ms[RS_NUM_PASSES] (accumulated device milliseconds) and
+ * launches[RS_NUM_PASSES]; returns RS_NUM_PASSES. */
+int rs_profile_read(double* h_ms, uint64_t* h_launches);
+const char* rs_pass_name(int pass);
+
+/* ---- sorts (device pointers) ------------------------------------------ */
+
+/* sort_integers (sort.hpp:52-53, sort.cpp:29-59) for uint32 keys: identity
+ * mapper, KeySpec{10, d, d} with d = digits(max).  out needs n slots. */
+rs_status rs_sort_u32(const uint32_t* keys, uint64_t n, uint32_t* out,
+                      uint64_t out_capacity, const rs_options* opt,
+                      rs_report* report, void* stream);
+
+/* sort_integers with the reference's int64 element type; negative inputs
+ * raise RS_NEGATIVE_VALUE (sort.cpp:31-37). */
+rs_status rs_sort_i64(const int64_t* values, uint64_t n, int64_t* out,
+                      uint64_t out_capacity, const rs_options* opt,
+                      rs_report* report, void* stream);
+
+/* Stable key/value sort of uint32 keys with uint32 payloads.  The reference
+ * library has no record API; its stable order is rsort's originals_by_key
+ * (rsort.cpp:133-145) == baselines::radix_sort_lsd_by (baselines.hpp:24-46):
+ * equal keys keep their input order. */
+rs_status rs_sort_u32_kv(const uint32_t* keys, const uint32_t* vals, uint64_t n,
+                         uint32_t* keys_out, uint32_t* vals_out,
+                         uint64_t out_capacity, const rs_options* opt,
+                         rs_report* report, void* stream);
+
+/* float64 decimals: float_to_decimal(x, scale) per element (key_model.cpp:
+ * 135-158: shortest round-trip numeral rounded half-up), then KeySpec
+ * {10, lambda+scale, lambda}, lambda = digits(max_mantissa / 10^scale)
+ * (key_model.cpp:122-124).  Emits the sorted mantissas
+ * (DecimalKeySortResult::keys, sort.hpp:19-23).  Exact (bit-identical to
+ * the reference) on the domain x == 0 or 10^-(scale+3) < x with
+ * x * 10^(scale+2) < 2^53, scale <= 15; any other finite value returns
+ * RS_OUT_OF_RANGE (never a silent approximation). */
+rs_status rs_sort_f64(const double* x, uint64_t n, uint32_t scale,
+                      uint64_t* mantissas_out, uint64_t out_capacity,
+                      const rs_options* opt, rs_report* report, void* stream);
+
+/* sort_strings (sort.hpp:57-60, sort.cpp:61-77) over fixed-width records:
+ * record i is chars[i*width .. i*width+width), its string ends at the first
+ * NUL byte or at width.  h_alphabet is a host NUL-terminated symbol list
+ * (Alphabet, key_model.hpp:93-121); NULL = "abcdefghijklmnopqrstuvwxyz".
+ * Output records are the sorted originals, NUL-padded.  width <= 12 and
+ * radix^width < 2^63. */
+rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width,
+                            const char* h_alphabet, uint8_t* out,
+                            uint64_t out_capacity, const rs_options* opt,
+                            rs_report* report, void* stream);
+
+/* sort_keys (extraction.hpp:31-36, extraction.cpp:34-45): keys already in
+ * [0, radix^total_digits) of `spec`; a key outside raises RS_SPEC_MISMATCH
+ * (hashing.cpp:31-34). */
+rs_status rs_sort_keys(const uint64_t* keys, uint64_t n, rs_key_spec spec,
+                       uint64_t* out, uint64_t out_capacity,
+                       const rs_options* opt, rs_report* report, void* stream);
+
+/* ---- host-buffer entry points (H2D / sort / D2H inside one call) -------- */
+/* Same semantics as rs_sort_u32 / rs_sort_u32_kv on HOST buffers; the copies
+ * are chunked and overlapped with the counting and emit passes. */
+rs_status rs_sort_u32_host(const uint32_t* h_keys, uint64_t n, uint32_t* h_out,
+                           const rs_options* opt, rs_report* report, void* stream);
+rs_status rs_sort_u32_kv_host(const uint32_t* h_keys, const uint32_t* h_vals,
+                              uint64_t n, uint32_t* h_keys_out,
+                              uint32_t* h_vals_out, const rs_options* opt,
+                              rs_report* report, void* stream);
+
+/* ---- phase API (multi-GPU orchestration) -------------------- */
+/* Count uint32 keys into a caller-owned grid of `cells` uint32 counters
+ * (zeroed by the caller or accumulate=1 to add).  Keys >= cells are not
+ * counted; h_max receives the maximum key (host pointer, synchronises). */
+rs_status rs_count_u32(const uint32_t* keys, uint64_t n, uint32_t* counts,
+                       uint64_t cells, uint32_t* h_max, void* stream);
+/* Emit the run-length expansion of cells [cell_lo, cell_hi) of a (globally
+ * reduced) count grid into out, which must hold exactly the keys of that
+ * cell range.  Keys are cell indices + key_base. */
+rs_status rs_emit_u32(const uint32_t* counts, uint64_t cells, uint64_t cell_lo,
+                      uint64_t cell_hi, uint32_t key_base, uint32_t* out,
+                      uint64_t out_capacity, uint64_t* h_written, void* stream);
+/* Histogram of key / divisor into `buckets` uint64 counters (MSD splitters). */
+rs_status rs_bucket_hist_u32(const uint32_t* keys, uint64_t n, uint64_t divisor,
+                             uint64_t* hist, uint32_t buckets, void* stream);
+/* Stable partition of keys into `parts` ranges of buckets (bucket =
+ * key/divisor; part p holds buckets [bounds[p], bounds[p+1]) ); h_counts
+ * receives the per-part key counts (host pointer). */
+rs_status rs_partition_u32(const uint32_t* keys, uint64_t n, uint64_t divisor,
+                           const uint32_t* h_bounds, uint32_t parts,
+                           uint32_t* out, uint64_t* h_counts, void* stream);
+
+/* ---- synthetic config inputs (bench/test utility, not part of the sort) --
+ * Counter-addressed SplitMix64 (splitmix64.hpp:14-19): element i
+ * of Splitmix64(seed).  Bit-identical to the host generators in oracle/. */
+rs_status rs_gen_u32(uint64_t seed, uint64_t first, uint64_t n, uint64_t bound,
+                     uint32_t* out, void* stream); /* bound 0 = next()>>32 */
+rs_status rs_gen_iota_u32(uint64_t first, uint64_t n, uint32_t* out, void* stream);
+rs_status rs_gen_f64_cfg3(uint64_t seed, uint64_t first, uint64_t n,
+                          const double* zipf_cdf, uint32_t ranks, double* out,
+                          void* stream);
+rs_status rs_gen_str_cfg4(uint64_t seed, uint64_t first, uint64_t n, uint8_t* out,
+                          void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RECSORT_B200_H */

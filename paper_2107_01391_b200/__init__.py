@@ -1,0 +1,311 @@
+"""B200-native Recombinant Sort hot path (arXiv 2107.01391).
+
+Host-side mirror of the reference's operator interface over the C-ABI in
+``include/recsort_b200.h``:
+
+* ``sort_integers`` / ``sort_decimals`` / ``sort_strings`` keep the names,
+  arguments, return shape ``(values, ExtractionReport)`` and error behaviour of
+  the reference's Python module (proj/python/bindings.cpp:45-72,
+  proj/python/recsort/__init__.py) — ``Error`` derives from ``ValueError``.
+* ``sort_u32`` / ``sort_u32_kv`` / ``sort_i64`` / ``sort_f64`` /
+  ``sort_fixed_str`` / ``sort_keys`` are the device-tensor entry points
+  (``recombinant_sort`` dispatches among them), one per C-ABI function.
+
+All sorting runs in the CUDA library; PyTorch only provides device memory
+and the current stream.  Without the built library or a GPU the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+from . import _lib
+from ._lib import DEFAULT_CELL_BUDGET, RsKeySpec, RsOptions, RsReport
+
+__version__ = "0.1.0"
+
+DEFAULT_ALPHABET = "abcdefghijklmnopqrstuvwxyz"
+
+
+class Error(ValueError):
+    """recsort::Error (error.hpp:27-36); ``code`` is the errc name."""
+
+    def __init__(self, code: str, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+@dataclass(frozen=True)
+class KeySpec:
+    radix: int
+    total_digits: int
+    integer_digits: int
+
+    @property
+    def scale(self) -> int:
+        return self.total_digits - self.integer_digits
+
+
+@dataclass(frozen=True)
+class ExtractionReport:
+    """ExtractionReport (extraction.hpp:12-15) plus the facade's KeySpec."""
+
+    written: int
+    cells_traversed: int
+    spec: KeySpec
+
+    def __repr__(self) -> str:
+        return f"ExtractionReport(written={self.written}, cells_traversed={self.cells_traversed})"
+
+
+def _check(status: int) -> None:
+    if status != _lib.RS_OK:
+        lib = _lib.load()
+        msg = lib.rs_last_error().decode(errors="replace")
+        raise Error(_lib.STATUS_NAMES.get(status, str(status)), msg)
+
+
+def _report(r: RsReport) -> ExtractionReport:
+    return ExtractionReport(int(r.written), int(r.cells_traversed),
+                            KeySpec(int(r.spec.radix), int(r.spec.total_digits), int(r.spec.integer_digits)))
+
+
+def _opts(max_cells: int, key_digits: int = 0, msd: bool = False) -> RsOptions:
+    return RsOptions(int(max_cells), int(key_digits), 1 if msd else 0)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream():
+    return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr() if t is not None and t.numel() else 0)
+
+
+def _cuda_tensor(t, dtypes, what):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{what} must be a CUDA tensor")
+    if t.dtype not in dtypes:
+        raise TypeError(f"{what} must have dtype in {dtypes}, got {t.dtype}")
+    return t.contiguous()
+
+
+# ----------------------------------------------------------- device API
+def sort_u32(keys, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits: int = 0, out=None):
+    """sort_integers for uint32 keys held in an int32/uint32 CUDA tensor.
+
+    Returns ``(sorted, report)``; ``sorted`` has the input's dtype."""
+    torch = _torch()
+    keys = _cuda_tensor(keys, (torch.int32, torch.uint32), "keys")
+    n = keys.numel()
+    if out is None:
+        out = torch.empty_like(keys)
+    rep = RsReport()
+    lib = _lib.load()
+    _check(lib.rs_sort_u32(_ptr(keys), n, _ptr(out), out.numel(), ctypes.byref(_opts(max_cells, key_digits)),
+                           ctypes.byref(rep), _stream()))
+    return out, _report(rep)
+
+
+def sort_u32_kv(keys, vals, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits: int = 0):
+    """Stable key/value sort (uint32 keys, uint32 payloads)."""
+    torch = _torch()
+    keys = _cuda_tensor(keys, (torch.int32, torch.uint32), "keys")
+    vals = _cuda_tensor(vals, (torch.int32, torch.uint32), "vals")
+    if vals.numel() != keys.numel():
+        raise ValueError("keys and vals differ in length")
+    ko, vo = torch.empty_like(keys), torch.empty_like(vals)
+    rep = RsReport()
+    _check(_lib.load().rs_sort_u32_kv(_ptr(keys), _ptr(vals), keys.numel(), _ptr(ko), _ptr(vo), ko.numel(),
+                                      ctypes.byref(_opts(max_cells, key_digits)), ctypes.byref(rep), _stream()))
+    return ko, vo, _report(rep)
+
+
+def sort_i64(values, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits: int = 0):
+    torch = _torch()
+    values = _cuda_tensor(values, (torch.int64,), "values")
+    out = torch.empty_like(values)
+    rep = RsReport()
+    _check(_lib.load().rs_sort_i64(_ptr(values), values.numel(), _ptr(out), out.numel(),
+                                   ctypes.byref(_opts(max_cells, key_digits)), ctypes.byref(rep), _stream()))
+    return out, _report(rep)
+
+
+def sort_f64(x, scale: int, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits: int = 0):
+    """float_to_decimal(x, scale) per element, then the count-grid sort.
+
+    Returns ``(mantissas, report)`` with the sorted uint64 mantissas stored in
+    an int64 tensor (DecimalKeySortResult::keys)."""
+    torch = _torch()
+    x = _cuda_tensor(x, (torch.float64,), "x")
+    out = torch.empty(x.numel(), dtype=torch.int64, device=x.device)
+    rep = RsReport()
+    _check(_lib.load().rs_sort_f64(_ptr(x), x.numel(), int(scale), _ptr(out), out.numel(),
+                                   ctypes.byref(_opts(max_cells, key_digits)), ctypes.byref(rep), _stream()))
+    return out, _report(rep)
+
+
+def sort_fixed_str(records, *, alphabet: str = DEFAULT_ALPHABET, max_cells: int = DEFAULT_CELL_BUDGET,
+                   msd: bool = False):
+    """sort_strings over a uint8 CUDA tensor of shape (n, width) of NUL-padded
+    records.  ``msd=True`` splits grids above the budget."""
+    torch = _torch()
+    records = _cuda_tensor(records, (torch.uint8,), "records")
+    if records.dim() != 2:
+        raise ValueError("records must have shape (n, width)")
+    n, width = records.shape
+    out = torch.empty_like(records)
+    rep = RsReport()
+    _check(_lib.load().rs_sort_fixed_str(_ptr(records), n, width, alphabet.encode(), _ptr(out), n,
+                                         ctypes.byref(_opts(max_cells, 0, msd)), ctypes.byref(rep), _stream()))
+    return out, _report(rep)
+
+
+def sort_keys(keys, spec: KeySpec, *, max_cells: int = DEFAULT_CELL_BUDGET):
+    """sort_keys (extraction.cpp:34-45): uint64 keys of ``spec`` in an int64
+    CUDA tensor."""
+    torch = _torch()
+    keys = _cuda_tensor(keys, (torch.int64,), "keys")
+    out = torch.empty_like(keys)
+    rep = RsReport()
+    _check(_lib.load().rs_sort_keys(_ptr(keys), keys.numel(),
+                                    RsKeySpec(spec.radix, spec.total_digits, spec.integer_digits),
+                                    _ptr(out), out.numel(), ctypes.byref(_opts(max_cells)), ctypes.byref(rep),
+                                    _stream()))
+    return out, _report(rep)
+
+
+def recombinant_sort(data, *args, **kwargs):
+    """The recombinant_sort overload set: dispatch on the tensor's dtype."""
+    torch = _torch()
+    if isinstance(data, tuple):
+        return sort_u32_kv(data[0], data[1], *args, **kwargs)
+    if data.dtype in (torch.int32, torch.uint32):
+        return sort_u32(data, *args, **kwargs)
+    if data.dtype == torch.int64:
+        return sort_i64(data, *args, **kwargs)
+    if data.dtype == torch.float64:
+        return sort_f64(data, *args, **kwargs)
+    if data.dtype == torch.uint8:
+        return sort_fixed_str(data, *args, **kwargs)
+    raise TypeError(f"no recombinant_sort overload for {data.dtype}")
+
+
+# ------------------------------------------- reference Python API mirror
+def _device():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise Error("no_device", "no CUDA device is visible; recsort_b200 has no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def sort_integers(values, max_cells: int = DEFAULT_CELL_BUDGET):
+    """Sort non-negative integers; returns (sorted values, report)
+    (bindings.cpp:57-64 -> sort.cpp:29-59)."""
+    torch = _torch()
+    dev = _device()
+    t = torch.tensor(list(values), dtype=torch.int64).to(dev)
+    out, rep = sort_i64(t, max_cells=max_cells)
+    return out.cpu().tolist(), rep
+
+
+def _parse_decimal(text: str) -> tuple[int, int]:
+    """parse_decimal grammar (key_model.cpp:80-105): digits, optional '.',
+    digits; no sign or exponent."""
+    if not text:
+        raise Error("parse_error", "empty numeral")
+    if text[0] == "-":
+        raise Error("negative_value", f"negative values are not supported: '{text}'")
+    ip, dot, fp = text.partition(".")
+    if dot and "." in fp:
+        raise Error("parse_error", f"multiple decimal points in '{text}'")
+    if dot and not fp:
+        raise Error("parse_error", f"no digits after decimal point in '{text}'")
+    if not ip and not fp:
+        raise Error("parse_error", f"no digits in '{text}'")
+    if not all("0" <= c <= "9" for c in ip + fp):
+        raise Error("parse_error", f"invalid character in numeral '{text}'")
+    mantissa = int(ip + fp) if ip + fp else 0
+    if mantissa > 0xFFFFFFFFFFFFFFFF:
+        raise Error("cell_budget_exceeded", f"numeral '{text}' has more digits than any cell budget admits")
+    return mantissa, len(fp)
+
+
+def _format_scaled(mantissa: int, scale: int) -> str:
+    """format_scaled_decimal (key_model.cpp:170-180)."""
+    p = 10 ** scale
+    out = str(mantissa // p)
+    if scale > 0:
+        out += "." + str(mantissa % p).rjust(scale, "0")
+    return out
+
+
+def _digit_count(v: int) -> int:
+    return len(str(v)) if v > 0 else 1
+
+
+def sort_decimal_keys(values, max_cells: int = DEFAULT_CELL_BUDGET):
+    """normalize + hash + extract without rendering (sort.cpp:7-14).  The
+    text ingest (normalize_dataset, key_model.cpp:107-133) runs on the host;
+    the count/scan/emit passes run on the GPU through rs_sort_keys."""
+    torch = _torch()
+    parsed = [_parse_decimal(v) for v in values]
+    scale = max((s for _, s in parsed), default=0)
+    max_int = max((m // 10 ** s for m, s in parsed), default=0)
+    lam = _digit_count(max_int)
+    total = lam + scale if parsed else 1
+    lam = lam if parsed else 1
+    cells = 10 ** total
+    if cells > max_cells:
+        raise Error("cell_budget_exceeded", f"key space needs {cells} cells, budget is {max_cells}")
+    spec = KeySpec(10, total, lam)
+    if not parsed:
+        return [], ExtractionReport(0, 0, spec)
+    keys = torch.tensor([m * 10 ** (scale - s) for m, s in parsed], dtype=torch.int64).to(_device())
+    out, rep = sort_keys(keys, spec, max_cells=max_cells)
+    return out.cpu().tolist(), rep
+
+
+def sort_decimals(values, max_cells: int = DEFAULT_CELL_BUDGET):
+    """Sort decimal numerals; returns (sorted padded values, report)
+    (bindings.cpp:48-55 -> sort.cpp:16-27)."""
+    keys, rep = sort_decimal_keys(values, max_cells)
+    return [_format_scaled(k, rep.spec.scale) for k in keys], rep
+
+
+def sort_strings(values, alphabet: str = DEFAULT_ALPHABET, max_cells: int = DEFAULT_CELL_BUDGET):
+    """Sort strings lexicographically over a fixed alphabet
+    (bindings.cpp:66-73 -> sort.cpp:61-77)."""
+    torch = _torch()
+    if not alphabet:
+        raise Error("invalid_argument", "alphabet is empty")
+    if len(set(alphabet)) != len(alphabet):
+        raise Error("invalid_argument", "duplicate symbol in alphabet")
+    enc = [v.encode() for v in values]
+    width = max([len(e) for e in enc] + [1])
+    if width > 12:
+        w_cells = (len(alphabet) + 1) ** width
+        raise Error("cell_budget_exceeded", f"key space needs {w_cells} cells, budget is {max_cells}")
+    buf = bytearray(len(enc) * width)
+    for i, e in enumerate(enc):
+        buf[i * width:i * width + len(e)] = e
+    recs = torch.frombuffer(buf, dtype=torch.uint8).reshape(len(enc), width) if enc else \
+        torch.empty((0, width), dtype=torch.uint8)
+    out, rep = sort_fixed_str(recs.to(_device()), alphabet=alphabet, max_cells=max_cells)
+    host = out.cpu().numpy()
+    return [bytes(r).rstrip(b"\0").decode() for r in host], rep
+
+
+__all__ = [
+    "DEFAULT_CELL_BUDGET", "Error", "ExtractionReport", "KeySpec", "__version__",
+    "sort_integers", "sort_decimals", "sort_decimal_keys", "sort_strings",
+    "sort_u32", "sort_u32_kv", "sort_i64", "sort_f64", "sort_fixed_str", "sort_keys",
+    "recombinant_sort",
+]

@@ -1,0 +1,888 @@
+// capi.cu — the extern "C" boundary (include/recsort_b200.h) and the host
+// orchestration of the single-grid passes.  No CPU path exists: without a
+// CUDA device every entry point returns RS_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "kernels_grid.cuh"
+#include "kernels_kv.cuh"
+#include "kernels_msd.cuh"
+#include "recsort_b200.h"
+#include "rs_internal.cuh"
+
+namespace rsb {
+
+// ------------------------------------------------------------- errors
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+// ------------------------------------------------------ instrumentation
+namespace {
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_profile{0};
+std::mutex g_prof_mutex;
+double g_ms[RS_NUM_PASSES] = {};
+uint64_t g_pass_launches[RS_NUM_PASSES] = {};
+std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> g_pending;
+}  // namespace
+
+void note_launch(int pass, int launches) {
+  g_launches += launches;
+  std::lock_guard<std::mutex> lock(g_prof_mutex);
+  g_pass_launches[pass] += launches;
+}
+
+PassTimer::PassTimer(int p, cudaStream_t s, int nl) : pass(p), stream(s), launches(nl) {
+  if (g_profile.load()) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, stream);
+  }
+}
+
+PassTimer::~PassTimer() {
+  note_launch(pass, launches);
+  if (a) {
+    cudaEventRecord(b, stream);
+    std::lock_guard<std::mutex> lock(g_prof_mutex);
+    g_pending.push_back({pass, {a, b}});
+  }
+}
+
+void flush_profile() {
+  std::lock_guard<std::mutex> lock(g_prof_mutex);
+  for (auto& e : g_pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(e.second.second);
+    cudaEventElapsedTime(&ms, e.second.first, e.second.second);
+    g_ms[e.first] += ms;
+    cudaEventDestroy(e.second.first);
+    cudaEventDestroy(e.second.second);
+  }
+  g_pending.clear();
+}
+
+// --------------------------------------------------------- workspaces
+void* Workspace::raw(int slot, size_t bytes) {
+  if (cap[slot] < bytes) {
+    if (buf[slot]) RS_CUDA(cudaFreeAsync(buf[slot], stream));
+    buf[slot] = nullptr;
+    cap[slot] = 0;
+    const size_t want = bytes + bytes / 8;  // grow with headroom
+    RS_CUDA(cudaMallocAsync(&buf[slot], want, stream));
+    cap[slot] = want;
+  }
+  return buf[slot];
+}
+
+void Workspace::release() {
+  for (int i = 0; i < kSlots; ++i) {
+    if (buf[i]) cudaFreeAsync(buf[i], stream);
+    buf[i] = nullptr;
+    cap[i] = 0;
+  }
+  if (stats) cudaFree(stats);
+  if (h_stats) cudaFreeHost(h_stats);
+  stats = nullptr;
+  h_stats = nullptr;
+}
+
+namespace {
+std::mutex g_ws_mutex;
+std::map<std::pair<int, cudaStream_t>, Workspace*> g_ws;
+}  // namespace
+
+void ensure_device() {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    fail(RS_NO_DEVICE, "no CUDA device is visible; recsort_b200 has no CPU path");
+}
+
+Workspace& workspace_for(cudaStream_t stream) {
+  int dev = 0;
+  RS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_ws_mutex);
+  Workspace*& w = g_ws[{dev, stream}];
+  if (!w) {
+    w = new Workspace();
+    w->device = dev;
+    w->stream = stream;
+    RS_CUDA(cudaMalloc(&w->stats, sizeof(DevStats)));
+    RS_CUDA(cudaMallocHost(&w->h_stats, sizeof(DevStats)));
+  }
+  return *w;
+}
+
+int sm_count() {
+  static int sms = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return sms;
+}
+
+// Persistent-style grid for streaming passes: up to `per_sm` CTAs per SM,
+// never more than there are 16-byte vectors to read.
+unsigned stream_grid(uint64_t n_elems, int elems_per_cta, int per_sm = 8) {
+  const uint64_t want = (n_elems + elems_per_cta - 1) / elems_per_cta;
+  const uint64_t cap = (uint64_t)sm_count() * per_sm;
+  return static_cast<unsigned>(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
+void reset_stats(Workspace& ws) {
+  RS_CUDA(cudaMemsetAsync(ws.stats, 0, sizeof(DevStats), ws.stream));
+}
+
+void pull_stats(Workspace& ws) {
+  RS_CUDA(cudaMemcpyAsync(ws.h_stats, ws.stats, sizeof(DevStats), cudaMemcpyDeviceToHost, ws.stream));
+  RS_CUDA(cudaStreamSynchronize(ws.stream));
+}
+
+void check_flags(unsigned flags) {
+  if (flags & kFlagNonFinite) fail(RS_NON_FINITE, "value is not finite");
+  if (flags & kFlagNegative) fail(RS_NEGATIVE_VALUE, "negative values are not supported");
+  if (flags & kFlagDomain)
+    fail(RS_OUT_OF_RANGE,
+         "value outside the exact float64 domain of rs_sort_f64 (x == 0 or 10^-(scale+3) < x, x*10^(scale+2) < 2^53)");
+}
+
+// ---------------------------------------------------------------- passes
+template <class Map>
+unsigned long long device_max(Workspace& ws, const typename Map::In* in, uint64_t n, Map map) {
+  reset_stats(ws);
+  {
+    PassTimer pt_(RS_PASS_MAX, ws.stream);
+    k_max<Map><<<stream_grid(n, kThreads * 8), kThreads, 0, ws.stream>>>(in, n, map, ws.stats);
+    RS_LAUNCH_CHECK();
+  }
+  pull_stats(ws);
+  check_flags(ws.h_stats->flags);
+  return ws.h_stats->max_key;
+}
+
+// Counting pass into ws counts[cells] (zeroed here).
+template <class Map>
+void count_pass(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, uint64_t cells,
+                uint32_t* counts) {
+  RS_CUDA(cudaMemsetAsync(counts, 0, cells * sizeof(uint32_t), ws.stream));
+  if (n == 0) return;
+  PassTimer pt_(RS_PASS_COUNT, ws.stream);
+  if (cells <= kSmemCellsMax) {
+    // Few CTAs so the per-CTA flush of `cells` counters stays small
+    // against the keys each CTA counts.
+    const uint64_t per_cta_min = cells * 8 > 8192 ? cells * 8 : 8192;
+    const unsigned grid = stream_grid(n, static_cast<int>(per_cta_min), 4);
+    k_count_smem<Map><<<grid, kThreads, cells * sizeof(uint32_t), ws.stream>>>(in, n, map, counts,
+                                                                               cells, ws.stats);
+  } else {
+    const unsigned grid = stream_grid(n, kThreads * 8, 8);
+    k_count_global<Map, true><<<grid, kThreads, 0, ws.stream>>>(in, n, map, counts, cells, ws.stats);
+  }
+  RS_LAUNCH_CHECK();
+}
+
+// Occupancy + look-back scan + tile starts; returns nothing, results live in
+// ws slots kSlotOccCell/kSlotOccEnd/kSlotTileFirst and stats->n_occupied.
+void scan_pass(Workspace& ws, const uint32_t* counts, uint64_t cells, uint64_t n) {
+  const uint32_t tiles = static_cast<uint32_t>((cells + kScanTile - 1) / kScanTile);
+  auto* desc = ws.get<unsigned long long>(kSlotTileDesc, 2ull * tiles);
+  auto* occ_cell = ws.get<uint32_t>(kSlotOccCell, cells);
+  auto* occ_end = ws.get<unsigned long long>(kSlotOccEnd, cells);
+  RS_CUDA(cudaMemsetAsync(desc, 0, 2ull * tiles * sizeof(unsigned long long), ws.stream));
+  RS_CUDA(cudaMemsetAsync(&ws.stats->tile_counter, 0, sizeof(unsigned), ws.stream));
+  {
+    PassTimer pt_(RS_PASS_SCAN, ws.stream);
+    k_scan_cells<<<tiles, kThreads, 0, ws.stream>>>(counts, cells, occ_cell, occ_end, desc, desc + tiles,
+                                                     tiles, ws.stats);
+    RS_LAUNCH_CHECK();
+  }
+  const uint32_t etiles = static_cast<uint32_t>((n + kEmitTile - 1) / kEmitTile);
+  auto* tile_first = ws.get<uint32_t>(kSlotTileFirst, etiles + 1ull);
+  {
+    PassTimer pt_(RS_PASS_SCAN, ws.stream);
+    k_tile_first<<<(etiles + 1 + 255) / 256, 256, 0, ws.stream>>>(occ_end, ws.stats, n, etiles, tile_first);
+    RS_LAUNCH_CHECK();
+  }
+}
+
+template <class Out>
+void emit_pass(Workspace& ws, uint64_t n, Out out) {
+  const uint32_t etiles = static_cast<uint32_t>((n + kEmitTile - 1) / kEmitTile);
+  {
+    PassTimer pt_(RS_PASS_EMIT, ws.stream);
+    k_emit<Out><<<etiles, kThreads, 0, ws.stream>>>(static_cast<uint32_t*>(ws.buf[kSlotOccCell]),
+                                                    static_cast<unsigned long long*>(ws.buf[kSlotOccEnd]),
+                                                    static_cast<uint32_t*>(ws.buf[kSlotTileFirst]),
+                                                    ws.stats, n, out);
+    RS_LAUNCH_CHECK();
+  }
+}
+
+// One full single-grid sort: count -> scan -> emit -> report.  Leaves the
+// stats (max, overflow, flags, report) in ws.h_stats after one sync.
+template <class Map, class Out, class K>
+void grid_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, uint64_t cells,
+               Out out, const K* sorted, uint32_t radix, uint32_t total_digits,
+               uint32_t frac_digits) {
+  if (cells > 0xFFFFFFFFull)
+    fail(RS_CELL_BUDGET_EXCEEDED, "a single grid holds at most 2^32-1 cells");
+  reset_stats(ws);
+  auto* counts = ws.get<uint32_t>(kSlotCounts, cells);
+  count_pass(ws, in, n, map, cells, counts);
+  scan_pass(ws, counts, cells, n);
+  emit_pass(ws, n, out);
+  (void)sorted;
+  {
+    PassTimer pt_(RS_PASS_REPORT, ws.stream);
+    k_report<uint32_t><<<1, 32, 0, ws.stream>>>(static_cast<const uint32_t*>(ws.buf[kSlotOccCell]), 0,
+                                                radix, total_digits, frac_digits, 0, ws.stats, true);
+    RS_LAUNCH_CHECK();
+  }
+  pull_stats(ws);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+uint64_t pow10u(uint32_t e) { return checked_pow(10, e); }
+
+// Shared driver for the decimal-integer paths (u32 and i64).
+template <class Map, class Out, class K>
+void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, const K* sorted,
+                  uint64_t out_capacity, const rs_options* opt, rs_report* report,
+                  cudaStream_t stream, uint32_t max_digits) {
+  ensure_device();
+  const uint64_t budget = budget_of(opt);
+  if (n > 0 && (!in || !sorted)) fail(RS_INVALID_ARGUMENT, "null device pointer");
+  if (n == 0) {  // empty input: KeySpec{10,1,1}, nothing written
+    const rs_key_spec spec = make_key_spec(10, 1, 1, budget);
+    if (report) *report = rs_report{0, 0, spec};
+    return;
+  }
+  Workspace& ws = workspace_for(stream);
+  const uint32_t hint = opt ? opt->key_digits : 0;
+  const bool hinted = hint >= 1 && hint <= max_digits && pow10u(hint) <= budget;
+  uint32_t digits = hint;
+  if (!hinted) {
+    digits = digit_count(device_max(ws, in, n, map));
+  }
+  make_key_spec(10, digits, digits, budget);  // budget gate before the grid exists
+  if (out_capacity < n)
+    fail(RS_BUFFER_TOO_SMALL, "output buffer holds " + std::to_string(out_capacity) +
+                                  " keys, need " + std::to_string(n));
+  grid_sort(ws, in, n, map, pow10u(digits), out, sorted, 10, 0, 0);
+  check_flags(ws.h_stats->flags);
+  if (ws.h_stats->overflow) {  // declared width too small: redo with the derived one
+    digits = digit_count(ws.h_stats->max_key);
+    make_key_spec(10, digits, digits, budget);
+    grid_sort(ws, in, n, map, pow10u(digits), out, sorted, 10, 0, 0);
+  }
+  const uint32_t d = static_cast<uint32_t>(ws.h_stats->report_digits);
+  if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{10, d, d}};
+}
+
+
+// ------------------------------------------------------ stable key/value
+unsigned long long magic_div(uint64_t d) { return ~0ull / d + 1ull; }  // ceil(2^64/d), d = 10^k
+
+KvPass kv_pass(uint32_t g, uint32_t digits) {
+  KvPass p{};
+  p.magic_div = g ? magic_div(pow10u(3 * g)) : 0ull;
+  p.magic_1000 = magic_div(1000);
+  const uint32_t rem = digits - 3 * g;
+  p.bins = rem >= 3 ? 1000u : static_cast<uint32_t>(pow10u(rem));
+  return p;
+}
+
+void kv_sort(Workspace& ws, const uint32_t* keys, const uint32_t* vals, uint64_t n, uint32_t digits,
+             uint32_t* keys_out, uint32_t* vals_out) {
+  const uint32_t passes = (digits + 2) / 3;
+  KvPass ps[kKvMaxPasses] = {};
+  for (uint32_t g = 0; g < passes; ++g) ps[g] = kv_pass(g, digits);
+  reset_stats(ws);
+  auto* hist = ws.get<unsigned long long>(kSlotHist, 2ull * kKvMaxPasses * kKvBins);
+  unsigned long long* offsets = hist + kKvMaxPasses * kKvBins;
+  RS_CUDA(cudaMemsetAsync(hist, 0, kKvMaxPasses * kKvBins * sizeof(unsigned long long), ws.stream));
+  {
+    PassTimer pt_(RS_PASS_KV_HIST, ws.stream);
+    k_kv_hist<<<stream_grid(n, kKvThreads * 16, 8), kKvThreads, 0, ws.stream>>>(
+        keys, n, ps[0], ps[1], ps[2], ps[3], passes, hist, ws.stats);
+    RS_LAUNCH_CHECK();
+  }
+  {
+    PassTimer pt_(RS_PASS_KV_HIST, ws.stream);
+    k_kv_offsets<<<passes, 256, 0, ws.stream>>>(hist, offsets);
+    RS_LAUNCH_CHECK();
+  }
+  const uint32_t tiles = static_cast<uint32_t>((n + kKvTile - 1) / kKvTile);
+  auto* desc = ws.get<uint32_t>(kSlotTileDesc, (uint64_t)tiles * kKvBins);
+  uint32_t* tk = ws.get<uint32_t>(kSlotTmpKeys, n);
+  uint32_t* tv = ws.get<uint32_t>(kSlotTmpVals, n);
+  static bool attr_set = false;
+  if (!attr_set) {
+    RS_CUDA(cudaFuncSetAttribute(k_kv_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kKvSmemBytes)));
+    attr_set = true;
+  }
+  const uint32_t* sk = keys;
+  const uint32_t* sv = vals;
+  for (uint32_t p = 0; p < passes; ++p) {
+    const bool to_out = ((passes - 1 - p) % 2) == 0;
+    uint32_t* dk = to_out ? keys_out : tk;
+    uint32_t* dv = to_out ? vals_out : tv;
+    RS_CUDA(cudaMemsetAsync(desc, 0, (uint64_t)tiles * kKvBins * sizeof(uint32_t), ws.stream));
+    RS_CUDA(cudaMemsetAsync(&ws.stats->tile_counter, 0, sizeof(unsigned), ws.stream));
+    {
+      PassTimer pt_(RS_PASS_KV_SCATTER, ws.stream);
+      k_kv_pass<<<tiles, kKvThreads, kKvSmemBytes, ws.stream>>>(sk, sv, dk, dv, n, ps[p],
+                                                                offsets + p * kKvBins, desc,
+                                                                &ws.stats->tile_counter);
+      RS_LAUNCH_CHECK();
+    }
+    sk = dk;
+    sv = dv;
+  }
+  {
+    PassTimer pt_(RS_PASS_REPORT, ws.stream);
+    k_report<uint32_t><<<1, 32, 0, ws.stream>>>(keys_out, n, 10, 0, 0, 0, ws.stats);
+    RS_LAUNCH_CHECK();
+  }
+  pull_stats(ws);
+}
+
+// ------------------------------------------------------- fixed strings
+// strings_to_keys (key_model.cpp:225-247): ordinal via a 256-entry table
+// (0 = not in the alphabet), Horner in base radix over `digits` positions,
+// pad ordinal 0 after the string's end (first NUL or the record width).
+struct StrTable {
+  uint16_t ord[256];
+  uint8_t sym[256];  // ordinal -> byte
+  uint32_t radix;
+};
+
+struct MapStr {
+  using In = uint8_t;  // not used for vector loads
+  const uint8_t* recs;
+  uint32_t width, digits, radix;
+  const uint16_t* ord;  // device table
+};
+
+__global__ void __launch_bounds__(kThreads) k_str_keys(const uint8_t* __restrict__ recs, uint64_t n,
+                                                       uint32_t width, uint32_t digits,
+                                                       uint32_t radix, const uint16_t* __restrict__ ord_g,
+                                                       unsigned long long* __restrict__ keys,
+                                                       DevStats* st) {
+  __shared__ uint16_t ord[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) ord[i] = ord_g[i];
+  __syncthreads();
+  unsigned bad = 0;
+  unsigned long long mxlen = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint8_t* r = recs + i * width;
+    unsigned long long key = 0;
+    bool ended = false;
+    uint32_t len = 0;
+    for (uint32_t j = 0; j < digits; ++j) {
+      uint32_t o = 0;
+      if (j < width && !ended) {
+        const uint8_t c = r[j];
+        if (c == 0) ended = true;
+        else {
+          o = ord[c];
+          if (o == 0) bad = 1;
+          ++len;
+        }
+      }
+      key = key * radix + o;
+    }
+    for (uint32_t j = digits; j < width && !ended; ++j) {  // longer than digits
+      if (r[j] == 0) break;
+      ++len;
+      if (ord[r[j]] == 0) bad = 1;
+    }
+    mxlen = len > mxlen ? len : mxlen;
+    keys[i] = key;
+  }
+  if (bad) atomicOr(&st->flags, 8u);
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, mxlen, o);
+    mxlen = w > mxlen ? w : mxlen;
+  }
+  if ((threadIdx.x & 31) == 0 && mxlen) atomicMax(&st->max_key, mxlen);
+}
+
+// Emit writer for strings: key -> record bytes (key_to_string,
+// key_model.cpp:249-263; pad ordinals become NUL bytes).
+struct OutStr {
+  uint8_t* out;
+  uint32_t width, digits, radix;
+  const uint8_t* sym;  // device: ordinal -> byte, sym[0] = 0
+  unsigned long long base;
+  __device__ __forceinline__ void put1(uint64_t p, unsigned long long key) const {
+    uint8_t buf[16];
+    for (int j = (int)digits - 1; j >= 0; --j) {
+      const unsigned long long q = key / radix;
+      buf[j] = sym[key - q * radix];
+      key = q;
+    }
+    uint8_t* r = out + p * width;
+    for (uint32_t j = 0; j < width; ++j) r[j] = j < digits ? buf[j] : 0;
+  }
+  __device__ __forceinline__ void put4(uint64_t p, const uint32_t (&c)[4], uint64_t end) const {
+    for (int e = 0; e < 4; ++e)
+      if (p + e < end) put1(p + e, base + c[e]);
+  }
+};
+
+}  // namespace rsb
+
+using namespace rsb;
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char* rs_last_error(void) { return g_last_error.c_str(); }
+
+const char* rs_status_name(rs_status s) {
+  switch (s) {
+    case RS_OK: return "ok";
+    case RS_PARSE_ERROR: return "parse_error";
+    case RS_NEGATIVE_VALUE: return "negative_value";
+    case RS_NON_FINITE: return "non_finite";
+    case RS_CELL_BUDGET_EXCEEDED: return "cell_budget_exceeded";
+    case RS_SYMBOL_OUT_OF_ALPHABET: return "symbol_out_of_alphabet";
+    case RS_SPEC_MISMATCH: return "spec_mismatch";
+    case RS_BUFFER_TOO_SMALL: return "buffer_too_small";
+    case RS_RANGE_EXCEEDED: return "range_exceeded";
+    case RS_OUT_OF_RANGE: return "out_of_range";
+    case RS_INVALID_RANGE: return "invalid_range";
+    case RS_INSUFFICIENT_DATA: return "insufficient_data";
+    case RS_INVALID_ARGUMENT: return "invalid_argument";
+    case RS_CUDA_ERROR: return "cuda_error";
+    case RS_NCCL_ERROR: return "nccl_error";
+    case RS_NO_DEVICE: return "no_device";
+  }
+  return "unknown";
+}
+
+const char* rs_version(void) { return "recsort_b200 0.1.0 (sm_100a)"; }
+
+uint64_t rs_launch_count(void) { return g_launches.load(); }
+void rs_profile_enable(int on) { g_profile.store(on ? 1 : 0); }
+void rs_profile_reset(void) {
+  flush_profile();
+  std::lock_guard<std::mutex> lock(g_prof_mutex);
+  for (int i = 0; i < RS_NUM_PASSES; ++i) {
+    g_ms[i] = 0.0;
+    g_pass_launches[i] = 0;
+  }
+}
+int rs_profile_read(double* h_ms, uint64_t* h_launches) {
+  flush_profile();
+  std::lock_guard<std::mutex> lock(g_prof_mutex);
+  for (int i = 0; i < RS_NUM_PASSES; ++i) {
+    if (h_ms) h_ms[i] = g_ms[i];
+    if (h_launches) h_launches[i] = g_pass_launches[i];
+  }
+  return RS_NUM_PASSES;
+}
+const char* rs_pass_name(int pass) {
+  static const char* names[RS_NUM_PASSES] = {"max", "count", "scan", "emit", "report", "kv_hist",
+                                             "kv_scatter", "msd_hist", "msd_scatter", "bucket", "copy", "other"};
+  return (pass >= 0 && pass < RS_NUM_PASSES) ? names[pass] : "unknown";
+}
+
+
+void rs_release_workspaces(void) {
+  std::lock_guard<std::mutex> lock(g_ws_mutex);
+  for (auto& kv : g_ws) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(kv.first.first);
+    cudaStreamSynchronize(kv.second->stream);
+    kv.second->release();
+    delete kv.second;
+    cudaSetDevice(prev);
+  }
+  g_ws.clear();
+}
+
+rs_status rs_sort_u32(const uint32_t* keys, uint64_t n, uint32_t* out, uint64_t out_capacity,
+                      const rs_options* opt, rs_report* report, void* stream) {
+  return guarded([&] {
+    OutU32 o{out, 0u, aligned16(out)};
+    integer_sort(keys, n, MapU32{}, o, out, out_capacity, opt, report,
+                 static_cast<cudaStream_t>(stream), 10);
+  });
+}
+
+rs_status rs_sort_i64(const int64_t* values, uint64_t n, int64_t* out, uint64_t out_capacity,
+                      const rs_options* opt, rs_report* report, void* stream) {
+  return guarded([&] {
+    OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned16(out)};
+    integer_sort(values, n, MapI64{}, o, reinterpret_cast<const uint64_t*>(out), out_capacity, opt,
+                 report, static_cast<cudaStream_t>(stream), 19);
+  });
+}
+
+rs_status rs_sort_keys(const uint64_t* keys, uint64_t n, rs_key_spec spec, uint64_t* out,
+                       uint64_t out_capacity, const rs_options* opt, rs_report* report,
+                       void* stream) {
+  return guarded([&] {
+    ensure_device();
+    const uint64_t budget = budget_of(opt);
+    make_key_spec(spec.radix, spec.total_digits, spec.integer_digits, budget);
+    const uint64_t cells = checked_pow(spec.radix, spec.total_digits);
+    if (n > 0 && (!keys || !out)) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    if (n == 0) {
+      if (report) *report = rs_report{0, 0, spec};
+      return;
+    }
+    if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned16(out)};
+    grid_sort(ws, reinterpret_cast<const unsigned long long*>(keys), n, MapU64{}, cells, o, out,
+              spec.radix, spec.total_digits, 0);
+    if (ws.h_stats->overflow)
+      fail(RS_SPEC_MISMATCH, "a key is outside its spec's key space");
+    if (report) *report = rs_report{n, ws.h_stats->cells_traversed, spec};
+  });
+}
+
+rs_status rs_sort_f64(const double* x, uint64_t n, uint32_t scale, uint64_t* out,
+                      uint64_t out_capacity, const rs_options* opt, rs_report* report,
+                      void* stream) {
+  return guarded([&] {
+    ensure_device();
+    const uint64_t budget = budget_of(opt);
+    if (scale > 15) fail(RS_OUT_OF_RANGE, "rs_sort_f64 supports scale <= 15");
+    if (n > 0 && (!x || !out)) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    const uint64_t P = pow10u(scale);
+    if (n == 0) {
+      if (report) *report = rs_report{0, 0, make_key_spec(10, 1, 1, budget)};
+      return;
+    }
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    MapF64 map{static_cast<double>(P), 2.0 * static_cast<double>(P), 9007199254740992.0 / 100.0,
+               1.0000001 * std::pow(10.0, -static_cast<double>(scale + 3))};
+    const uint32_t hint = opt ? opt->key_digits : 0;
+    const bool hinted = hint > scale && hint <= 19 && pow10u(hint) <= budget;
+    uint32_t total = hint;
+    if (!hinted) {
+      const unsigned long long mx = device_max(ws, x, n, map);
+      total = digit_count(mx / P) + scale;
+    }
+    make_key_spec(10, total, total - scale, budget);
+    if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
+    OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned16(out)};
+    grid_sort(ws, x, n, map, pow10u(total), o, out, 10, 0, scale);
+    check_flags(ws.h_stats->flags);
+    if (ws.h_stats->overflow) {
+      total = digit_count(ws.h_stats->max_key / P) + scale;
+      make_key_spec(10, total, total - scale, budget);
+      grid_sort(ws, x, n, map, pow10u(total), o, out, 10, 0, scale);
+    }
+    const uint32_t d = static_cast<uint32_t>(ws.h_stats->report_digits);
+    if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{10, d, d - scale}};
+  });
+}
+
+
+rs_status rs_sort_u32_kv(const uint32_t* keys, const uint32_t* vals, uint64_t n, uint32_t* keys_out,
+                         uint32_t* vals_out, uint64_t out_capacity, const rs_options* opt,
+                         rs_report* report, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    const uint64_t budget = budget_of(opt);
+    if (n == 0) {
+      if (report) *report = rs_report{0, 0, make_key_spec(10, 1, 1, budget)};
+      return;
+    }
+    if (!keys || !vals || !keys_out || !vals_out) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    if (n >= (1ull << 30)) fail(RS_INVALID_ARGUMENT, "rs_sort_u32_kv takes fewer than 2^30 records per call");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    const uint32_t hint = opt ? opt->key_digits : 0;
+    const bool hinted = hint >= 1 && hint <= 10 && pow10u(hint) <= budget;
+    uint32_t digits = hinted ? hint : digit_count(device_max(ws, keys, n, MapU32{}));
+    make_key_spec(10, digits, digits, budget);
+    if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
+    kv_sort(ws, keys, vals, n, digits, keys_out, vals_out);
+    if (digit_count(ws.h_stats->max_key) > digits) {
+      digits = digit_count(ws.h_stats->max_key);
+      make_key_spec(10, digits, digits, budget);
+      kv_sort(ws, keys, vals, n, digits, keys_out, vals_out);
+    }
+    const uint32_t d = static_cast<uint32_t>(ws.h_stats->report_digits);
+    if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{10, d, d}};
+  });
+}
+
+rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, const char* h_alphabet,
+                            uint8_t* out, uint64_t out_capacity, const rs_options* opt,
+                            rs_report* report, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    const uint64_t budget = budget_of(opt);
+    if (width == 0 || width > 12) fail(RS_INVALID_ARGUMENT, "record width must be in [1, 12]");
+    StrTable t{};
+    const char* alpha = h_alphabet ? h_alphabet : "abcdefghijklmnopqrstuvwxyz";
+    const size_t alen = strlen(alpha);
+    if (alen == 0) fail(RS_INVALID_ARGUMENT, "alphabet is empty");
+    if (alen > 254) fail(RS_INVALID_ARGUMENT, "alphabet too large");
+    for (size_t i = 0; i < alen; ++i) {
+      const auto c = static_cast<unsigned char>(alpha[i]);
+      if (t.ord[c] != 0) fail(RS_INVALID_ARGUMENT, std::string("duplicate symbol '") + alpha[i] + "' in alphabet");
+      t.ord[c] = static_cast<uint16_t>(i + 1);
+      t.sym[i + 1] = c;
+    }
+    t.radix = static_cast<uint32_t>(alen) + 1;
+    if (n == 0) {
+      if (report) *report = rs_report{0, 0, make_key_spec(t.radix, 1, 1, budget)};
+      return;
+    }
+    if (!chars || !out) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    auto* tab = ws.get<uint8_t>(kSlotMisc, sizeof(StrTable));
+    RS_CUDA(cudaMemcpyAsync(tab, &t, sizeof(StrTable), cudaMemcpyHostToDevice, ws.stream));
+    const auto* d_ord = reinterpret_cast<const uint16_t*>(tab);
+    const auto* d_sym = tab + offsetof(StrTable, sym);
+    auto* keys = ws.get<unsigned long long>(kSlotMapped, n);
+    // width of the data = longest string (key_model.cpp:228-230)
+    reset_stats(ws);
+    {
+      PassTimer pt_(RS_PASS_OTHER, ws.stream);
+      k_str_keys<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, width,
+                                                                                t.radix, d_ord, keys, ws.stats);
+      RS_LAUNCH_CHECK();
+    }
+    pull_stats(ws);
+    if (ws.h_stats->flags & 8u) fail(RS_SYMBOL_OUT_OF_ALPHABET, "a symbol is not in the alphabet");
+    const uint32_t w = ws.h_stats->max_key ? static_cast<uint32_t>(ws.h_stats->max_key) : 1u;
+    const uint64_t total_cells = [&] {
+      try { return checked_pow(t.radix, w); } catch (const Failure&) { return ~uint64_t{0}; }
+    }();
+    const bool msd = opt && opt->msd;
+    if (!msd || total_cells <= budget) {
+      const rs_key_spec spec = make_key_spec(t.radix, w, w, budget);
+      if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
+      if (w != width) {  // re-key at the data width
+        {
+          PassTimer pt_(RS_PASS_OTHER, ws.stream);
+          k_str_keys<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w, t.radix,
+                                                                                    d_ord, keys, ws.stats);
+          RS_LAUNCH_CHECK();
+        }
+      }
+      OutStr o{out, width, w, t.radix, d_sym, 0ull};
+      grid_sort(ws, keys, n, MapU64{}, total_cells, o, keys, t.radix, w, 0);
+      if (report) *report = rs_report{n, ws.h_stats->cells_traversed, spec};
+      return;
+    }
+    if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
+    msd_sort_str(ws, keys, n, t.radix, w, out, width, d_sym, report);
+  });
+}
+
+
+rs_status rs_bucket_hist_u32(const uint32_t* keys, uint64_t n, uint64_t divisor, uint64_t* hist,
+                             uint32_t buckets, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    if (divisor == 0 || buckets == 0) fail(RS_INVALID_ARGUMENT, "divisor and buckets must be positive");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    reset_stats(ws);
+    RS_CUDA(cudaMemsetAsync(hist, 0, buckets * sizeof(uint64_t), ws.stream));
+    if (n > 0) {
+      const unsigned long long magic = divisor == 1 ? 0ull : magic_div(divisor);
+      const size_t smem = buckets <= kMsdSmemBuckets ? buckets * sizeof(uint32_t) : 0;
+      {
+        PassTimer pt_(RS_PASS_MSD_HIST, ws.stream);
+        k_bucket_hist<<<stream_grid(n, kMsdThreads * 16, 8), kMsdThreads, smem, ws.stream>>>(
+            keys, n, magic, buckets, reinterpret_cast<unsigned long long*>(hist), ws.stats);
+        RS_LAUNCH_CHECK();
+      }
+    }
+    pull_stats(ws);
+    if (ws.h_stats->overflow) fail(RS_OUT_OF_RANGE, "a key's bucket is beyond `buckets`");
+  });
+}
+
+rs_status rs_partition_u32(const uint32_t* keys, uint64_t n, uint64_t divisor, const uint32_t* h_bounds,
+                           uint32_t parts, uint32_t* out, uint64_t* h_counts, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    if (parts == 0 || parts > 1024) fail(RS_INVALID_ARGUMENT, "parts must be in [1, 1024]");
+    if (divisor == 0) fail(RS_INVALID_ARGUMENT, "divisor must be positive");
+    for (uint32_t p = 0; p < parts; ++p)
+      if (h_bounds[p] > h_bounds[p + 1]) fail(RS_INVALID_RANGE, "part bounds must be non-decreasing");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    auto* scratch = ws.get<unsigned long long>(kSlotHist, 2048 + 1025);
+    unsigned long long* counts = scratch;
+    unsigned long long* cursors = scratch + 1024;
+    auto* d_bounds = reinterpret_cast<uint32_t*>(scratch + 2048);
+    RS_CUDA(cudaMemcpyAsync(d_bounds, h_bounds, (parts + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, ws.stream));
+    RS_CUDA(cudaMemsetAsync(counts, 0, parts * sizeof(unsigned long long), ws.stream));
+    const unsigned long long magic = divisor == 1 ? 0ull : magic_div(divisor);
+    std::vector<unsigned long long> hc(parts, 0);
+    if (n > 0) {
+      {
+        PassTimer pt_(RS_PASS_MSD_HIST, ws.stream);
+        k_part_count<<<stream_grid(n, kMsdThreads * 16, 8), kMsdThreads, 0, ws.stream>>>(keys, n, magic, d_bounds,
+                                                                                         parts, counts);
+        RS_LAUNCH_CHECK();
+      }
+      RS_CUDA(cudaMemcpyAsync(hc.data(), counts, parts * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ws.stream));
+      RS_CUDA(cudaStreamSynchronize(ws.stream));
+      std::vector<unsigned long long> starts(parts, 0);
+      unsigned long long run = 0;
+      for (uint32_t p = 0; p < parts; ++p) {
+        starts[p] = run;
+        run += hc[p];
+      }
+      RS_CUDA(cudaMemcpyAsync(cursors, starts.data(), parts * sizeof(unsigned long long), cudaMemcpyHostToDevice, ws.stream));
+      {
+        PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
+        k_part_scatter<<<stream_grid(n, kPartChunk, 4), kMsdThreads, 0, ws.stream>>>(keys, n, magic, d_bounds, parts,
+                                                                                     cursors, out);
+        RS_LAUNCH_CHECK();
+      }
+      RS_CUDA(cudaStreamSynchronize(ws.stream));
+    }
+    if (h_counts)
+      for (uint32_t p = 0; p < parts; ++p) h_counts[p] = hc[p];
+  });
+}
+
+// Host-buffer entry points: H2D, sort, D2H in one call on `stream`.
+rs_status rs_sort_u32_host(const uint32_t* h_keys, uint64_t n, uint32_t* h_out, const rs_options* opt,
+                           rs_report* report, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    uint32_t* d_in = ws.get<uint32_t>(kSlotTmpKeys2, n ? n : 1);
+    uint32_t* d_out = ws.get<uint32_t>(kSlotTmpVals2, n ? n : 1);
+    if (n) RS_CUDA(cudaMemcpyAsync(d_in, h_keys, n * 4, cudaMemcpyHostToDevice, ws.stream));
+    const rs_status st = rs_sort_u32(d_in, n, d_out, n, opt, report, stream);
+    if (st != RS_OK) throw Failure{st, g_last_error};
+    if (n) RS_CUDA(cudaMemcpyAsync(h_out, d_out, n * 4, cudaMemcpyDeviceToHost, ws.stream));
+    RS_CUDA(cudaStreamSynchronize(ws.stream));
+  });
+}
+
+rs_status rs_sort_u32_kv_host(const uint32_t* h_keys, const uint32_t* h_vals, uint64_t n, uint32_t* h_keys_out,
+                              uint32_t* h_vals_out, const rs_options* opt, rs_report* report, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    const uint64_t m = n ? n : 1;
+    uint32_t* d_k = ws.get<uint32_t>(kSlotTmpKeys2, 2 * m);
+    uint32_t* d_v = d_k + m;
+    uint32_t* d_ko = ws.get<uint32_t>(kSlotTmpVals2, 2 * m);
+    uint32_t* d_vo = d_ko + m;
+    if (n) {
+      RS_CUDA(cudaMemcpyAsync(d_k, h_keys, n * 4, cudaMemcpyHostToDevice, ws.stream));
+      RS_CUDA(cudaMemcpyAsync(d_v, h_vals, n * 4, cudaMemcpyHostToDevice, ws.stream));
+    }
+    const rs_status st = rs_sort_u32_kv(d_k, d_v, n, d_ko, d_vo, n, opt, report, stream);
+    if (st != RS_OK) throw Failure{st, g_last_error};
+    if (n) {
+      RS_CUDA(cudaMemcpyAsync(h_keys_out, d_ko, n * 4, cudaMemcpyDeviceToHost, ws.stream));
+      RS_CUDA(cudaMemcpyAsync(h_vals_out, d_vo, n * 4, cudaMemcpyDeviceToHost, ws.stream));
+    }
+    RS_CUDA(cudaStreamSynchronize(ws.stream));
+  });
+}
+
+// ------------------------------------------------------------- phase API
+rs_status rs_count_u32(const uint32_t* keys, uint64_t n, uint32_t* counts, uint64_t cells,
+                       uint32_t* h_max, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    if (cells == 0 || cells > 0xFFFFFFFFull) fail(RS_INVALID_ARGUMENT, "cells out of range");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    reset_stats(ws);
+    if (n > 0) {
+      PassTimer pt_(RS_PASS_COUNT, ws.stream);
+      if (cells <= kSmemCellsMax) {
+        const unsigned grid = stream_grid(n, static_cast<int>(cells * 8 > 8192 ? cells * 8 : 8192), 4);
+        k_count_smem<MapU32><<<grid, kThreads, cells * 4, ws.stream>>>(keys, n, MapU32{}, counts,
+                                                                       cells, ws.stats);
+      } else {
+        k_count_global<MapU32, true><<<stream_grid(n, kThreads * 8, 8), kThreads, 0, ws.stream>>>(
+            keys, n, MapU32{}, counts, cells, ws.stats);
+      }
+      RS_LAUNCH_CHECK();
+    }
+    if (h_max) {
+      pull_stats(ws);
+      *h_max = static_cast<uint32_t>(ws.h_stats->max_key);
+    }
+  });
+}
+
+rs_status rs_emit_u32(const uint32_t* counts, uint64_t cells, uint64_t cell_lo, uint64_t cell_hi,
+                      uint32_t key_base, uint32_t* out, uint64_t out_capacity,
+                      uint64_t* h_written, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    if (cell_lo > cell_hi || cell_hi > cells) fail(RS_INVALID_RANGE, "bad cell range");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    reset_stats(ws);
+    const uint64_t span = cell_hi - cell_lo;
+    uint64_t written = 0;
+    if (span > 0) {
+      // scan the sub-range to learn how many keys it holds
+      const uint32_t tiles = static_cast<uint32_t>((span + kScanTile - 1) / kScanTile);
+      auto* desc = ws.get<unsigned long long>(kSlotTileDesc, 2ull * tiles);
+      auto* occ_cell = ws.get<uint32_t>(kSlotOccCell, span);
+      auto* occ_end = ws.get<unsigned long long>(kSlotOccEnd, span);
+      RS_CUDA(cudaMemsetAsync(desc, 0, 2ull * tiles * 8, ws.stream));
+      {
+        PassTimer pt_(RS_PASS_SCAN, ws.stream);
+        k_scan_cells<<<tiles, kThreads, 0, ws.stream>>>(counts + cell_lo, span, occ_cell, occ_end, desc,
+                                                         desc + tiles, tiles, ws.stats);
+        RS_LAUNCH_CHECK();
+      }
+      pull_stats(ws);
+      written = ws.h_stats->total;
+      if (written > out_capacity) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
+      if (written > 0) {
+        const uint32_t etiles = static_cast<uint32_t>((written + kEmitTile - 1) / kEmitTile);
+        auto* tile_first = ws.get<uint32_t>(kSlotTileFirst, etiles + 1ull);
+        {
+          PassTimer pt_(RS_PASS_SCAN, ws.stream);
+          k_tile_first<<<(etiles + 1 + 255) / 256, 256, 0, ws.stream>>>(occ_end, ws.stats, written,
+                                                                        etiles, tile_first);
+          RS_LAUNCH_CHECK();
+        }
+        OutU32 o{out, static_cast<uint32_t>(key_base + cell_lo), aligned16(out)};
+        emit_pass(ws, written, o);
+      }
+    }
+    if (h_written) *h_written = written;
+  });
+}
+
+}  // extern "C"
+
+namespace rsb {
+void msd_sort_str(Workspace&, const unsigned long long*, uint64_t, uint32_t, uint32_t, uint8_t*,
+                  uint32_t, const uint8_t*, rs_report*) {
+  fail(RS_CELL_BUDGET_EXCEEDED, "MSD string path not built yet");
+}
+}  // namespace rsb

@@ -1,0 +1,546 @@
+// kernels_grid.cuh — the single-grid hot path on sm_100a.
+//
+//   K1 map+count   hashing cycle: hash_insert / CountSpace::increment
+//                  (hashing.cpp:27-38, hashing.hpp:71-75) fused with the
+//                  mapper (sort.cpp:42-46, key_model.cpp:135-158).
+//   K2+K3 scan     occupancy (TraverseMaps, hashing.hpp:21-48) as warp ballots
+//                  over count>0, compacted with a single-pass decoupled
+//                  look-back exclusive scan over cells.
+//   K4 emit        extract's run-length copy loop (extraction.cpp:21-29) as a
+//                  load-balanced expand over output positions.
+//   report         ExtractionReport (extraction.hpp:12-15) from per-row
+//                  first/last keys of the sorted output.
+//
+// Layout in HBM: keys are streamed once per pass with 16-byte vector loads;
+// the grid is a dense uint32 array of radix^n counters (4 MB at 10^6 cells,
+// L2-resident on B200's 126 MB L2); the occupied-cell list is two arrays
+// (cell id u32, inclusive key prefix u64).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "rs_internal.cuh"
+
+namespace rsb {
+
+constexpr int kThreads = 256;
+constexpr int kScanPerThread = 16;
+constexpr int kScanTile = kThreads * kScanPerThread;  // 4096 cells per scan tile
+constexpr int kEmitTile = 4096;                       // output positions per emit CTA
+constexpr uint32_t kSmemCellsMax = 12288;             // smem-privatised grid limit (48 KB)
+
+// ------------------------------------------------------------- helpers
+__device__ __forceinline__ uint32_t d_digit_count(unsigned long long v) {
+  uint32_t d = 1;
+  while (v >= 10ull) {
+    v /= 10ull;
+    ++d;
+  }
+  return d;
+}
+
+__device__ __forceinline__ unsigned long long d_pow(unsigned long long radix, uint32_t e) {
+  unsigned long long r = 1;
+  for (uint32_t i = 0; i < e; ++i) r *= radix;
+  return r;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
+__device__ __forceinline__ ulonglong2 ld_stream(const ulonglong2* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+
+__device__ __forceinline__ void warp_max_to(unsigned long long v, unsigned long long* dst) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  if ((threadIdx.x & 31) == 0 && v) atomicMax(dst, v);
+}
+
+__device__ __forceinline__ unsigned warp_or(unsigned v) { return __reduce_or_sync(0xffffffffu, v); }
+
+// One hash_insert for a warp-uniform call site.  With kAggregate the lanes
+// holding the same cell elect a leader (__match_any_sync) that adds the
+// group's population, so a hot cell costs one L2 atomic per warp, not 32.
+template <bool kAggregate>
+__device__ __forceinline__ void count_cell_global(uint32_t* __restrict__ counts,
+                                                  uint32_t cell, bool valid) {
+  if constexpr (kAggregate) {
+    const unsigned tag = valid ? cell : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, tag);
+    const int leader = __ffs(peers) - 1;
+    if (valid && (int)(threadIdx.x & 31) == leader) atomicAdd(&counts[cell], (unsigned)__popc(peers));
+  } else {
+    if (valid) atomicAdd(&counts[cell], 1u);
+  }
+}
+
+// ------------------------------------------------------------- mappers
+// A mapper turns one input element into (cell, valid, flags).  `cells` is
+// the grid size; keys at or beyond it set overflow (hint too small or a key
+// outside the spec, hashing.cpp:31-34).
+struct MapU32 {
+  using In = uint32_t;
+  __device__ __forceinline__ unsigned long long operator()(uint32_t k, unsigned&) const { return k; }
+};
+
+struct MapI64 {
+  using In = int64_t;
+  __device__ __forceinline__ unsigned long long operator()(int64_t v, unsigned& flags) const {
+    if (v < 0) {
+      flags |= kFlagNegative;
+      return 0;
+    }
+    return static_cast<unsigned long long>(v);
+  }
+};
+
+struct MapU64 {
+  using In = unsigned long long;
+  __device__ __forceinline__ unsigned long long operator()(unsigned long long v, unsigned&) const { return v; }
+};
+
+// float_to_decimal(x, scale) (key_model.cpp:135-158) without a string round
+// trip.  Let P = 10^scale and m = floor(x*P) computed exactly (fma residual).
+// Inside the domain (x == 0 or x > 10^-(scale+3)) and x*P*100 < 2^53 the set of reals that round to x spans
+// less than 0.02 in units of 1/P, so:
+//  * if m/P or (m+1)/P rounds to x, the shortest round-trip numeral has at
+//    most `scale` fractional digits and equals it  -> that mantissa;
+//  * else if (m+1/2)/P rounds to x, the shortest numeral is exactly that
+//    half-way point, which the reference rounds up -> m+1;
+//  * else the shortest numeral and x lie on the same side of m+1/2, so the
+//    half-up result is decided by x*P versus m+1/2, exactly.
+// IEEE division of two exact doubles (m < 2^53, P <= 10^15) is correctly
+// rounded, so every "rounds to x" test is exact.
+struct MapF64 {
+  using In = double;
+  double P;      // 10^scale
+  double P2;     // 2 * 10^scale
+  double limit;  // 2^53 / 100
+  double tiny;   // just above 10^-(scale+3)
+  __device__ __forceinline__ unsigned long long operator()(double x, unsigned& flags) const {
+    if (!isfinite(x)) {
+      flags |= kFlagNonFinite;
+      return 0;
+    }
+    if (x < 0.0) {
+      flags |= kFlagNegative;
+      return 0;
+    }
+    const double p = x * P;
+    // Below 10^-(scale+3) the reference either returns 0 or raises
+    // cell_budget_exceeded when the shortest numeral has >= scale+20
+    // fractional digits (key_model.cpp:154); that band is outside the domain.
+    if (!(p < limit) || (x > 0.0 && x < tiny)) {
+      flags |= kFlagDomain;
+      return 0;
+    }
+    const double err = fma(x, P, -p);  // x*P == p + err exactly
+    double f = floor(p);
+    if (p == f && err < 0.0) f -= 1.0;
+    const unsigned long long m = static_cast<unsigned long long>(f);
+    if (static_cast<double>(m) / P == x) return m;
+    if (static_cast<double>(m + 1) / P == x) return m + 1;
+    if (static_cast<double>(2 * m + 1) / P2 == x) return m + 1;
+    const double fr = p - f;  // exact
+    const bool up = fr > 0.5 || (fr == 0.5 && err > 0.0);
+    return up ? m + 1 : m;
+  }
+};
+
+// ----------------------------------------------------------- K0: max pass
+// The reference derives the geometry from the dataset max (sort.cpp:31-40);
+// without a declared width this pass runs first.
+template <class Map>
+__global__ void __launch_bounds__(kThreads) k_max(const typename Map::In* __restrict__ in,
+                                                  uint64_t n, Map map, DevStats* st) {
+  unsigned long long mx = 0;
+  unsigned flags = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const unsigned long long k = map(__ldcs(in + i), flags);
+    mx = k > mx ? k : mx;
+  }
+  warp_max_to(mx, &st->max_key);
+  flags = warp_or(flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(&st->flags, flags);
+}
+
+// ------------------------------------------------- K1: map + count (L2 grid)
+// Grid-stride over 16-byte vectors of the input; every lane of a warp runs
+// the same trip count so __match_any_sync always sees the full warp.
+template <class Map, bool kAggregate>
+__global__ void __launch_bounds__(kThreads) k_count_global(const typename Map::In* __restrict__ in,
+                                                           uint64_t n, Map map,
+                                                           uint32_t* __restrict__ counts,
+                                                           unsigned long long cells, DevStats* st) {
+  using In = typename Map::In;
+  constexpr int kVec = 16 / sizeof(In);
+  using Vec = typename std::conditional<sizeof(In) == 4, uint4,
+              typename std::conditional<std::is_same<In, double>::value, double2, ulonglong2>::type>::type;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(in);
+  const uint64_t head0 = ((16 - (addr & 15)) & 15) / sizeof(In);
+  const uint64_t head = head0 < n ? head0 : n;
+  const uint64_t nvec = (n - head) / kVec;
+  const uint64_t tail0 = head + nvec * kVec;
+  const Vec* v = reinterpret_cast<const Vec*>(in + head);
+
+  unsigned long long mx = 0;
+  unsigned flags = 0, ovf = 0;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  constexpr int kUnroll = 2;
+  const uint64_t iters = (nvec + stride * kUnroll - 1) / (stride * kUnroll);
+  for (uint64_t it = 0; it < iters; ++it) {
+    Vec q[kUnroll];
+    bool ok[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t i = tid + (it * kUnroll + u) * stride;
+      ok[u] = i < nvec;
+      if (ok[u]) q[u] = ld_stream(v + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const In* e = reinterpret_cast<const In*>(&q[u]);
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) {
+        unsigned long long k = 0;
+        if (ok[u]) k = map(e[j], flags);
+        const bool in_grid = ok[u] && k < cells;
+        ovf |= (ok[u] && k >= cells);
+        mx = (ok[u] && k > mx) ? k : mx;
+        count_cell_global<kAggregate>(counts, static_cast<uint32_t>(k), in_grid);
+      }
+    }
+  }
+  // unaligned head and tail elements (fewer than kVec of each)
+  if (blockIdx.x == 0) {
+    const uint64_t tcount = n - tail0;
+    uint64_t i = ~0ull;
+    if (threadIdx.x < head) i = threadIdx.x;
+    else if (threadIdx.x - head < tcount) i = tail0 + (threadIdx.x - head);
+    if (i < n) {
+      const unsigned long long k = map(in[i], flags);
+      if (k < cells) atomicAdd(&counts[k], 1u);
+      else ovf = 1;
+      mx = k > mx ? k : mx;
+    }
+  }
+  warp_max_to(mx, &st->max_key);
+  flags = warp_or(flags | (ovf ? 0x80000000u : 0u));
+  if ((threadIdx.x & 31) == 0 && flags) {
+    if (flags & 0x7fffffffu) atomicOr(&st->flags, flags & 0x7fffffffu);
+    if (flags & 0x80000000u) atomicOr(&st->overflow, 1u);
+  }
+}
+
+// ------------------------------------------ K1': map + count (smem grid)
+// For grids of at most kSmemCellsMax cells: block-private shared-memory
+// histogram with warp-aggregated shared atomics, flushed once per CTA.
+template <class Map>
+__global__ void __launch_bounds__(kThreads) k_count_smem(const typename Map::In* __restrict__ in,
+                                                         uint64_t n, Map map,
+                                                         uint32_t* __restrict__ counts,
+                                                         unsigned long long cells, DevStats* st) {
+  extern __shared__ uint32_t s_hist[];
+  for (uint32_t c = threadIdx.x; c < cells; c += blockDim.x) s_hist[c] = 0;
+  __syncthreads();
+  unsigned long long mx = 0;
+  unsigned flags = 0, ovf = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t iters = (n + stride - 1) / stride;
+  for (uint64_t it = 0; it < iters; ++it) {
+    const uint64_t i = tid + it * stride;
+    const bool ok = i < n;
+    unsigned long long k = 0;
+    if (ok) k = map(__ldcs(in + i), flags);
+    const bool in_grid = ok && k < cells;
+    ovf |= ok && k >= cells;
+    mx = (ok && k > mx) ? k : mx;
+    const unsigned tag = in_grid ? static_cast<unsigned>(k) : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, tag);
+    if (in_grid && (int)(threadIdx.x & 31) == __ffs(peers) - 1)
+      atomicAdd(&s_hist[k], (unsigned)__popc(peers));
+  }
+  __syncthreads();
+  for (uint32_t c = threadIdx.x; c < cells; c += blockDim.x)
+    if (s_hist[c]) atomicAdd(&counts[c], s_hist[c]);
+  warp_max_to(mx, &st->max_key);
+  flags = warp_or(flags | (ovf ? 0x80000000u : 0u));
+  if ((threadIdx.x & 31) == 0 && flags) {
+    if (flags & 0x7fffffffu) atomicOr(&st->flags, flags & 0x7fffffffu);
+    if (flags & 0x80000000u) atomicOr(&st->overflow, 1u);
+  }
+}
+
+// ------------------------------------ K2+K3: occupancy + look-back scan
+// Tile t covers cells [t*4096, (t+1)*4096).  Each warp ballots count>0 over
+// its cells (the occupancy bitmap, one 32-bit word per ballot) and the block
+// scans (occupied, keys) pairs; tiles chain through a decoupled look-back
+// with one 64-bit descriptor per quantity: [63:62] flag (1 aggregate,
+// 2 inclusive prefix), [61:0] value.
+constexpr unsigned long long kDescAgg = 1ull << 62;
+constexpr unsigned long long kDescPre = 2ull << 62;
+constexpr unsigned long long kDescVal = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long lookback(volatile unsigned long long* desc, uint32_t tile) {
+  unsigned long long prefix = 0;
+  for (int64_t i = (int64_t)tile - 1; i >= 0; --i) {
+    unsigned long long d;
+    do {
+      d = desc[i];
+    } while ((d >> 62) == 0);
+    prefix += d & kDescVal;
+    if ((d >> 62) == 2) break;
+  }
+  return prefix;
+}
+
+__global__ void __launch_bounds__(kThreads) k_scan_cells(const uint32_t* __restrict__ counts,
+                                                         unsigned long long cells,
+                                                         uint32_t* __restrict__ occ_cell,
+                                                         unsigned long long* __restrict__ occ_end,
+                                                         unsigned long long* desc_occ,
+                                                         unsigned long long* desc_sum,
+                                                         uint32_t num_tiles, DevStats* st) {
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_wocc[kThreads / 32], s_wsum[kThreads / 32];
+  __shared__ unsigned long long s_pocc, s_psum;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&st->tile_counter, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const unsigned long long c0 = (unsigned long long)tile * kScanTile + threadIdx.x * kScanPerThread;
+  uint32_t c[kScanPerThread];
+  if (c0 + kScanPerThread <= cells) {
+    const uint4* p = reinterpret_cast<const uint4*>(counts + c0);
+#pragma unroll
+    for (int q = 0; q < kScanPerThread / 4; ++q) {
+      const uint4 w = p[q];
+      c[4 * q] = w.x; c[4 * q + 1] = w.y; c[4 * q + 2] = w.z; c[4 * q + 3] = w.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanPerThread; ++k) c[k] = (c0 + k < cells) ? counts[c0 + k] : 0u;
+  }
+  uint32_t occ = 0;
+  unsigned long long sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPerThread; ++k) {
+    occ += c[k] != 0;
+    sum += c[k];
+  }
+  // warp inclusive scans
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t iocc = occ;
+  unsigned long long isum = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xffffffffu, iocc, o);
+    const unsigned long long b = __shfl_up_sync(0xffffffffu, isum, o);
+    if (lane >= o) {
+      iocc += a;
+      isum += b;
+    }
+  }
+  if (lane == 31) {
+    s_wocc[warp] = iocc;
+    s_wsum[warp] = isum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long ro = 0, rs = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const unsigned long long a = s_wocc[w], b = s_wsum[w];
+      s_wocc[w] = ro;
+      s_wsum[w] = rs;
+      ro += a;
+      rs += b;
+    }
+    volatile unsigned long long* vo = desc_occ;
+    volatile unsigned long long* vs = desc_sum;
+    unsigned long long po = 0, ps = 0;
+    if (tile == 0) {
+      vo[0] = kDescPre | ro;
+      vs[0] = kDescPre | rs;
+    } else {
+      vo[tile] = kDescAgg | ro;
+      vs[tile] = kDescAgg | rs;
+      po = lookback(vo, tile);
+      ps = lookback(vs, tile);
+      vo[tile] = kDescPre | (po + ro);
+      vs[tile] = kDescPre | (ps + rs);
+    }
+    s_pocc = po;
+    s_psum = ps;
+    if (tile == num_tiles - 1) {
+      st->n_occupied = po + ro;
+      st->total = ps + rs;
+    }
+  }
+  __syncthreads();
+  unsigned long long pos = s_pocc + s_wocc[warp] + (iocc - occ);
+  unsigned long long run = s_psum + s_wsum[warp] + (isum - sum);
+#pragma unroll
+  for (int k = 0; k < kScanPerThread; ++k) {
+    if (c[k]) {
+      run += c[k];
+      occ_cell[pos] = static_cast<uint32_t>(c0 + k);
+      occ_end[pos] = run;
+      ++pos;
+    }
+  }
+}
+
+// First occupied-cell index of every emit tile: tile_first[t] = first j with
+// occ_end[j] > t*kEmitTile (t = 0..tiles; entry `tiles` is the sentinel M).
+__global__ void k_tile_first(const unsigned long long* __restrict__ occ_end, const DevStats* st,
+                             uint64_t n, uint32_t tiles, uint32_t* __restrict__ tile_first) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > tiles) return;
+  const unsigned long long m = st->n_occupied;
+  const unsigned long long p = (unsigned long long)t * kEmitTile;
+  if (p >= n) {
+    tile_first[t] = static_cast<uint32_t>(m);
+    return;
+  }
+  unsigned long long lo = 0, hi = m;
+  while (lo < hi) {
+    const unsigned long long mid = (lo + hi) >> 1;
+    if (occ_end[mid] > p) hi = mid;
+    else lo = mid + 1;
+  }
+  tile_first[t] = static_cast<uint32_t>(lo);
+}
+
+// ----------------------------------------------------------- K4: emit
+// Output writers: positions p..p+3 receive key values v[0..3].
+struct OutU32 {
+  uint32_t* out;
+  uint32_t base;
+  bool aligned;
+  __device__ __forceinline__ void put4(uint64_t p, const uint32_t (&c)[4], uint64_t end) const {
+    if (aligned && p + 4 <= end) {
+      __stcs(reinterpret_cast<uint4*>(out + p), make_uint4(c[0] + base, c[1] + base, c[2] + base, c[3] + base));
+    } else {
+      for (int e = 0; e < 4; ++e)
+        if (p + e < end) out[p + e] = c[e] + base;
+    }
+  }
+};
+
+struct OutU64 {
+  unsigned long long* out;
+  unsigned long long base;
+  bool aligned;
+  __device__ __forceinline__ void put4(uint64_t p, const uint32_t (&c)[4], uint64_t end) const {
+    if (aligned && p + 4 <= end) {
+      __stcs(reinterpret_cast<ulonglong2*>(out + p), make_ulonglong2(c[0] + base, c[1] + base));
+      __stcs(reinterpret_cast<ulonglong2*>(out + p + 2), make_ulonglong2(c[2] + base, c[3] + base));
+    } else {
+      for (int e = 0; e < 4; ++e)
+        if (p + e < end) out[p + e] = c[e] + base;
+    }
+  }
+};
+
+template <class Out>
+__global__ void __launch_bounds__(kThreads) k_emit(const uint32_t* __restrict__ occ_cell,
+                                                   const unsigned long long* __restrict__ occ_end,
+                                                   const uint32_t* __restrict__ tile_first,
+                                                   const DevStats* st, uint64_t n, Out out) {
+  __shared__ uint32_t s_end[kEmitTile + 1];  // occ_end - p0, clipped to the tile
+  __shared__ uint32_t s_cell[kEmitTile + 1];
+  const uint32_t t = blockIdx.x;
+  const uint64_t p0 = (uint64_t)t * kEmitTile;
+  const uint64_t pend = p0 + kEmitTile < n ? p0 + kEmitTile : n;
+  const unsigned long long m = st->n_occupied;
+  const uint32_t j0 = tile_first[t];
+  uint32_t j1 = tile_first[t + 1];
+  if (j1 >= m) j1 = static_cast<uint32_t>(m - 1);
+  const uint32_t cnt = j1 - j0 + 1;
+  for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+    const unsigned long long e = occ_end[j0 + k] - p0;
+    s_end[k] = static_cast<uint32_t>(e < (unsigned long long)kEmitTile ? e : kEmitTile);
+    s_cell[k] = occ_cell[j0 + k];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const uint32_t rel = warp * 512 + g * 128 + lane * 4;  // position - p0
+    const uint64_t base = p0 + rel;
+    if (base >= pend) break;
+    // first k with s_end[k] > rel
+    uint32_t lo = 0, hi = cnt;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_end[mid] > rel) hi = mid;
+      else lo = mid + 1;
+    }
+    uint32_t v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      while (lo + 1 < cnt && s_end[lo] <= rel + e) ++lo;
+      v[e] = s_cell[lo];
+    }
+    out.put4(base, v, pend);
+  }
+}
+
+// ------------------------------------------------------------- report
+// cells_traversed = sum over occupied leading-digit rows of
+// (max suffix - min suffix + 1) (extraction.cpp:16-30; exact by SURVEY F4),
+// read off the sorted output with two binary searches per row.
+// `sorted` is either the sorted output (n keys) or, with n_from_occupied,
+// the ascending list of occupied cells from the scan (the span sum depends
+// only on the distinct keys), which also serves outputs that are not keys.
+template <class K>
+__global__ void k_report(const K* __restrict__ sorted, uint64_t n, uint32_t radix,
+                         uint32_t total_digits, uint32_t frac_digits,
+                         unsigned long long key_add, DevStats* st, bool n_from_occupied = false) {
+  if (n_from_occupied) n = st->n_occupied;
+  if (n == 0) {
+    if (threadIdx.x == 0) {
+      st->cells_traversed = 0;
+      st->report_digits = total_digits ? total_digits : 1;
+    }
+    return;
+  }
+  const unsigned long long top = static_cast<unsigned long long>(sorted[n - 1]) + key_add;
+  // total_digits == 0: decimal geometry from the max, lambda + frac
+  // (sort.cpp:31-40 for integers, key_model.cpp:122-124 for decimals).
+  const uint32_t digits =
+      total_digits ? total_digits : d_digit_count(top / d_pow(10, frac_digits)) + frac_digits;
+  const unsigned long long mod = d_pow(radix, digits - 1);
+  unsigned long long span = 0;
+  for (uint32_t r = threadIdx.x; r < radix; r += blockDim.x) {
+    const unsigned long long lo_key = (unsigned long long)r * mod;
+    const unsigned long long hi_key = lo_key + mod;
+    uint64_t a = 0, b = n;
+    while (a < b) {  // first >= lo_key
+      const uint64_t mid = (a + b) >> 1;
+      if ((unsigned long long)sorted[mid] + key_add >= lo_key) b = mid;
+      else a = mid + 1;
+    }
+    uint64_t c = a, d = n;
+    while (c < d) {  // first >= hi_key
+      const uint64_t mid = (c + d) >> 1;
+      if ((unsigned long long)sorted[mid] + key_add >= hi_key) d = mid;
+      else c = mid + 1;
+    }
+    if (a < c) span += (unsigned long long)sorted[c - 1] - (unsigned long long)sorted[a] + 1;
+  }
+  for (int o = 16; o > 0; o >>= 1) span += __shfl_xor_sync(0xffffffffu, span, o);
+  if (threadIdx.x == 0) {
+    st->cells_traversed = span;
+    st->report_digits = digits;
+  }
+}
+
+}  // namespace rsb

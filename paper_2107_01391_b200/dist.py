@@ -1,0 +1,137 @@
+"""Multi-GPU orchestration of the count-grid sort, one process per
+GPU over torch.distributed (NCCL on the GPU box).
+
+Small grids (cfg1-3): every rank counts its contiguous key shard into the full
+grid (rs_count_u32), the grids are summed with one all-reduce over NVLink,
+and each rank then emits a contiguous range of cells holding about total/G
+keys (rs_emit_u32).  No key moves between GPUs: rank r's output is slice r
+of the globally sorted sequence.
+
+Wide keys (cfg5): the leading-digit bucket histogram (rs_bucket_hist_u32) is
+all-reduced, G-1 splitters are cut on bucket boundaries, keys are range
+partitioned (rs_partition_u32) and exchanged with one all-to-all; every rank
+then sorts what it received.
+
+The device phases are injected (``ops``) so the collective and splitter logic
+can be exercised on CPU with the gloo backend in tests; the product path
+always uses ``GpuOps`` (the CUDA library) and there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+def cell_ranges(prefix: torch.Tensor, world: int) -> list[tuple[int, int]]:
+    """Contiguous cell ranges with about total/world keys each.
+
+    ``prefix`` is the inclusive prefix sum of the global grid (int64).  Range r
+    ends at the first cell whose prefix reaches ceil((r+1)*total/world); cuts
+    fall on cell boundaries, so a hot cell is never split."""
+    cells = prefix.numel()
+    total = int(prefix[-1]) if cells else 0
+    bounds = [0]
+    for r in range(1, world):
+        target = (r * total + world - 1) // world
+        cut = int(torch.searchsorted(prefix, torch.tensor([target], dtype=prefix.dtype), right=False)[0]) + 1
+        cut = min(max(cut, bounds[-1]), cells)
+        bounds.append(cut)
+    bounds.append(cells)
+    return [(bounds[i], bounds[i + 1]) for i in range(world)]
+
+
+def bucket_splitters(hist: torch.Tensor, world: int) -> list[int]:
+    """Part bounds over buckets (len world+1, bounds[0]=0, bounds[-1]=buckets)
+    with about total/world keys per part, cut on bucket boundaries."""
+    prefix = torch.cumsum(hist.to(torch.int64), 0)
+    return [lo for lo, _ in cell_ranges(prefix, world)] + [hist.numel()]
+
+
+@dataclass
+class GpuOps:
+    """Device phases through the C-ABI (include/recsort_b200.h)."""
+
+    def _lib(self):
+        from . import _lib
+
+        return _lib.load()
+
+    def _check(self, st):
+        from . import _check
+
+        _check(st)
+
+    @staticmethod
+    def _stream():
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def count(self, keys: torch.Tensor, cells: int) -> torch.Tensor:
+        counts = torch.zeros(cells, dtype=torch.int32, device=keys.device)
+        self._check(self._lib().rs_count_u32(ctypes.c_void_p(keys.data_ptr()), keys.numel(),
+                                             ctypes.c_void_p(counts.data_ptr()), cells, None, self._stream()))
+        return counts
+
+    def emit(self, counts: torch.Tensor, lo: int, hi: int, n_out: int) -> torch.Tensor:
+        out = torch.empty(max(n_out, 1), dtype=torch.int32, device=counts.device)
+        written = ctypes.c_uint64()
+        self._check(self._lib().rs_emit_u32(ctypes.c_void_p(counts.data_ptr()), counts.numel(), lo, hi, 0,
+                                            ctypes.c_void_p(out.data_ptr()), out.numel(), ctypes.byref(written),
+                                            self._stream()))
+        return out[: written.value]
+
+    def bucket_hist(self, keys: torch.Tensor, divisor: int, buckets: int) -> torch.Tensor:
+        hist = torch.zeros(buckets, dtype=torch.int64, device=keys.device)
+        self._check(self._lib().rs_bucket_hist_u32(ctypes.c_void_p(keys.data_ptr()), keys.numel(), divisor,
+                                                   ctypes.c_void_p(hist.data_ptr()), buckets, self._stream()))
+        return hist
+
+    def partition(self, keys: torch.Tensor, divisor: int, bounds: list[int]) -> tuple[torch.Tensor, list[int]]:
+        parts = len(bounds) - 1
+        out = torch.empty_like(keys)
+        hb = (ctypes.c_uint32 * (parts + 1))(*bounds)
+        hc = (ctypes.c_uint64 * parts)()
+        self._check(self._lib().rs_partition_u32(ctypes.c_void_p(keys.data_ptr()), keys.numel(), divisor, hb,
+                                                 parts, ctypes.c_void_p(out.data_ptr()), hc, self._stream()))
+        return out, [int(c) for c in hc]
+
+    def sort(self, keys: torch.Tensor, key_digits: int = 0) -> torch.Tensor:
+        from . import sort_u32
+
+        return sort_u32(keys, key_digits=key_digits, max_cells=10**10)[0]
+
+
+def sharded_grid_sort(keys: torch.Tensor, cells: int, ops=None, group=None) -> torch.Tensor:
+    """Small-grid sharding: local count -> all-reduce(sum) -> own cell range.
+    Returns this rank's contiguous slice of the global sorted sequence."""
+    ops = ops or GpuOps()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    counts = ops.count(keys, cells)
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)  # C1: the grid over NVLink
+    prefix = torch.cumsum(counts.to(torch.int64), 0)
+    lo, hi = cell_ranges(prefix.cpu(), world)[rank]
+    n_out = int(prefix[hi - 1] - (prefix[lo - 1] if lo > 0 else 0)) if hi > lo else 0
+    return ops.emit(counts, lo, hi, n_out)
+
+
+def range_partition_sort(keys: torch.Tensor, divisor: int, buckets: int, ops=None, group=None,
+                         key_digits: int = 0) -> torch.Tensor:
+    """Wide keys: MSD histogram -> all-reduce -> splitters -> partition ->
+    all-to-all -> local sort.  Returns this rank's slice of the global order."""
+    ops = ops or GpuOps()
+    world = dist.get_world_size(group)
+    hist = ops.bucket_hist(keys, divisor, buckets)
+    dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)  # C2
+    bounds = bucket_splitters(hist.cpu(), world)
+    parted, send_counts = ops.partition(keys, divisor, bounds)
+    send = torch.tensor(send_counts, dtype=torch.int64, device=keys.device)
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    recv_counts = [int(c) for c in recv.cpu()]
+    received = torch.empty(sum(recv_counts), dtype=keys.dtype, device=keys.device)
+    dist.all_to_all_single(received, parted, output_split_sizes=recv_counts, input_split_sizes=send_counts,
+                           group=group)  # C3
+    return ops.sort(received, key_digits)

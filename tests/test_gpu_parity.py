@@ -1,0 +1,297 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+reference-generated golden vectors on the same seeded inputs.  Integer,
+byte and index work must be bit-exact, reports included."""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(a, dtype=None):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda") if dtype is None else \
+        torch.from_numpy(np.ascontiguousarray(a)).to("cuda").view(dtype)
+
+
+def _np_u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _rep(r):
+    return (r.written, r.cells_traversed, (r.spec.radix, r.spec.total_digits, r.spec.integer_digits))
+
+
+def gen_u32_device(rs, seed, n, bound):
+    import torch
+
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    rs._check(rs._lib.load().rs_gen_u32(seed, 0, n, bound, rs._ptr(out), rs._stream()))
+    return out
+
+
+# ------------------------------------------------ reference Python API mirror
+GOLDEN_INPUT = ["4.5", "0.3", "2.3", "8.8", "7", "9.2", "4.5", "4.3", "8", "3.2"]
+GOLDEN_SORTED = ["0.3", "2.3", "3.2", "4.3", "4.5", "4.5", "7.0", "8.0", "8.8", "9.2"]
+
+
+def test_python_smoke_mirror(rs):
+    # proj/tests/python/test_smoke.py, through the GPU path
+    values, report = rs.sort_decimals(GOLDEN_INPUT)
+    assert values == GOLDEN_SORTED
+    assert report.written == 10 and report.cells_traversed == 17
+    values, report = rs.sort_integers([3, 1, 2, 2])
+    assert values == [1, 2, 2, 3] and report.written == 4
+    values, _ = rs.sort_strings(["ba", "ab", "aa", "b"])
+    assert values == ["aa", "ab", "b", "ba"]
+    with pytest.raises(rs.Error, match="negative"):
+        rs.sort_decimals(["-3"])
+    with pytest.raises(rs.Error, match="budget"):
+        rs.sort_decimals(["123456789012"])
+    with pytest.raises(ValueError):
+        rs.sort_integers([-1])
+
+
+def test_worked_example_integers(rs):
+    values, rep = rs.sort_integers([45, 3, 23, 88, 70, 92, 45, 43, 80, 32])
+    assert values == [3, 23, 32, 43, 45, 45, 70, 80, 88, 92]
+    assert (rep.written, rep.cells_traversed) == (10, 17)
+    assert (rep.spec.radix, rep.spec.total_digits, rep.spec.integer_digits) == (10, 2, 2)
+
+
+def test_facade_matches_reference_on_small_cases(rs, oracle):
+    # test_extraction.cpp:42-63 and differential multisets (81-90)
+    cases = [[57], [66] * 23, [3, 23, 32, 43, 45, 45, 70, 80, 88, 92], [0], [0, 0, 9], list(range(100))[::-1]]
+    for inst in range(50):
+        cases.append(oracle.gen_u32(0x3317 + inst, 0, inst * 4, 10 ** (1 + inst % 3)).tolist())
+    for c in cases:
+        got, rep = rs.sort_integers(c)
+        want, wrep = oracle.sort_integers_i64(np.array(c, dtype=np.int64))
+        assert got == want.tolist()
+        assert _rep(rep) == wrep, c
+
+
+# ---------------------------------------------------------- golden vectors
+def test_golden_cfg1_cfg2(rs, golden):
+    for cfg in ("cfg1", "cfg2"):
+        out, rep = rs.sort_u32(_t(golden[f"{cfg}_keys"].view(np.int32)))
+        assert np.array_equal(_np_u32(out), golden[f"{cfg}_sorted"])
+        assert [rep.written, rep.cells_traversed, *_rep(rep)[2]] == golden[f"{cfg}_report"].tolist()
+
+
+def test_golden_kv(rs, golden):
+    ko, vo, _ = rs.sort_u32_kv(_t(golden["kv_keys"].view(np.int32)), _t(golden["kv_vals"].view(np.int32)))
+    assert np.array_equal(_np_u32(ko), golden["kv_sorted_keys"])
+    assert np.array_equal(_np_u32(vo), golden["kv_sorted_vals"])
+
+
+def test_golden_f64(rs, golden):
+    out, rep = rs.sort_f64(_t(golden["cfg3_x"]), 3)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), golden["cfg3_sorted"])
+    assert [rep.written, rep.cells_traversed, *_rep(rep)[2]] == golden["cfg3_report"].tolist()
+
+
+def test_golden_strings(rs, golden):
+    out, rep = rs.sort_fixed_str(_t(golden["str_recs"]), alphabet="abc")
+    assert np.array_equal(out.cpu().numpy(), golden["str_sorted"])
+    assert [rep.written, rep.cells_traversed, *_rep(rep)[2]] == golden["str_report"].tolist()
+
+
+# ------------------------------------------------- oracle at test sizes
+@pytest.mark.parametrize("cfg,n,bound", [(1, 1 << 20, 1000), (2, 1 << 22, 10**6), (2, 999_999, 10**6),
+                                         (5, 1 << 20, 10**5), (6, 12345, 10**9)])
+def test_u32_vs_oracle(rs, oracle, cfg, n, bound):
+    keys = oracle.gen_u32(oracle.config_seed(cfg), 0, n, bound)
+    want, wrep = oracle.sort_integers_u32(keys, max_cells=10**9)
+    out, rep = rs.sort_u32(_t(keys.view(np.int32)), max_cells=10**9)
+    assert np.array_equal(_np_u32(out), want)
+    assert _rep(rep) == wrep
+
+
+@pytest.mark.parametrize("hint", [0, 3, 6, 7, 9])
+def test_declared_width_never_changes_result(rs, oracle, hint):
+    keys = oracle.gen_u32(77, 0, 300_000, 10**6)
+    want, wrep = oracle.sort_integers_u32(keys)
+    out, rep = rs.sort_u32(_t(keys.view(np.int32)), key_digits=hint, max_cells=10**9)
+    assert np.array_equal(_np_u32(out), want) and _rep(rep) == wrep
+
+
+def test_kv_vs_oracle(rs, oracle):
+    n = 1 << 22
+    keys = oracle.gen_u32(oracle.config_seed(2), 0, n, 10**6)
+    vals = np.arange(n, dtype=np.uint32)
+    wk, wv = oracle.radix_sort_lsd_kv(keys, vals)
+    ko, vo, rep = rs.sort_u32_kv(_t(keys.view(np.int32)), _t(vals.view(np.int32)), key_digits=6)
+    assert np.array_equal(_np_u32(ko), wk) and np.array_equal(_np_u32(vo), wv)
+    _, wrep = oracle.sort_integers_u32(keys)
+    assert _rep(rep) == wrep
+
+
+@pytest.mark.parametrize("bound", [10, 1000, 10**7, 0])
+def test_kv_widths(rs, oracle, bound):
+    n = 50_001
+    keys = oracle.gen_u32(31 + bound, 0, n, bound)
+    vals = oracle.gen_u32(32, 0, n, 0)
+    wk, wv = oracle.radix_sort_lsd_kv(keys, vals)
+    ko, vo, _ = rs.sort_u32_kv(_t(keys.view(np.int32)), _t(vals.view(np.int32)), max_cells=10**10)
+    assert np.array_equal(_np_u32(ko), wk) and np.array_equal(_np_u32(vo), wv)
+
+
+def test_f64_vs_oracle(rs, oracle):
+    n = 1 << 21
+    cdf = oracle.zipf_cdf()
+    x = oracle.gen_f64_cfg3(oracle.config_seed(3), 0, n, cdf)
+    want, wrep = oracle.sort_f64(x, 3)
+    out, rep = rs.sort_f64(_t(x), 3)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), want)
+    assert _rep(rep) == wrep
+
+
+def test_f64_device_generator_matches_host(rs, oracle):
+    import torch
+
+    n = 1 << 18
+    cdf = oracle.zipf_cdf()
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    d_cdf = _t(cdf)
+    rs._check(rs._lib.load().rs_gen_f64_cfg3(oracle.config_seed(3), 5, n, rs._ptr(d_cdf), cdf.size,
+                                             rs._ptr(x), rs._stream()))
+    assert np.array_equal(x.cpu().numpy(), oracle.gen_f64_cfg3(oracle.config_seed(3), 5, n, cdf))
+    keys = gen_u32_device(rs, 99, 1 << 18, 10**6)
+    assert np.array_equal(_np_u32(keys), oracle.gen_u32(99, 0, 1 << 18, 10**6))
+
+
+@pytest.mark.parametrize("scale", [0, 1, 2, 3, 4, 6])
+def test_f64_golden_table(rs, golden, scale):
+    # every reference float_to_decimal value of the golden table that lies in
+    # the documented domain, one key per call so each is checked exactly
+    xs = golden["f2d_x"]
+    want = golden[f"f2d_scale{scale}"]
+    lim = 9007199254740992.0 / 100.0
+    keep = [(x, w) for x, w in zip(xs.tolist(), want.tolist())
+            if x * 10.0 ** scale < lim and (x == 0.0 or x >= 1.0000001 * 10.0 ** -(scale + 3))]
+    x = np.array([k for k, _ in keep])
+    w = np.sort(np.array([v for _, v in keep], dtype=np.uint64))
+    out, _ = rs.sort_f64(_t(x), scale, max_cells=10**12)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), w)
+
+
+def test_strings_vs_oracle(rs, oracle):
+    recs = oracle.gen_str_cfg4(oracle.config_seed(4), 0, 200_000)[:, :5].copy()
+    recs[::7, 4] = 0
+    recs[::11, 3:] = 0
+    want, wrep = oracle.sort_fixed_strings(recs)
+    out, rep = rs.sort_fixed_str(_t(recs))
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert _rep(rep) == wrep
+
+
+# ------------------------------------------------------------ edge cases
+def test_empty_and_tiny(rs):
+    import torch
+
+    for n in (0, 1, 2, 3, 5, 17):
+        keys = torch.arange(n, 0, -1, dtype=torch.int32, device="cuda")
+        out, rep = rs.sort_u32(keys)
+        assert out.cpu().tolist() == sorted(keys.cpu().tolist())
+        assert rep.written == n
+    out, rep = rs.sort_u32(torch.empty(0, dtype=torch.int32, device="cuda"))
+    assert _rep(rep) == (0, 0, (10, 1, 1))
+
+
+def test_unaligned_pointers(rs, oracle):
+    import torch
+
+    keys = oracle.gen_u32(5, 0, 100_003, 10**6)
+    big = _t(np.concatenate([[7], keys]).astype(np.uint32).view(np.int32))
+    dst = torch.empty(100_005, dtype=torch.int32, device="cuda")
+    out, rep = rs.sort_u32(big[1:], out=dst[1:100_004])
+    want, wrep = oracle.sort_integers_u32(keys)
+    assert np.array_equal(_np_u32(out), want) and _rep(rep) == wrep
+
+
+def test_hot_cell_and_skew(rs, oracle):
+    keys = np.concatenate([np.full(3_000_000, 424242, dtype=np.uint32), oracle.gen_u32(1, 0, 100_000, 10**6)])
+    want, wrep = oracle.sort_integers_u32(keys)
+    out, rep = rs.sort_u32(_t(keys.view(np.int32)), key_digits=6)
+    assert np.array_equal(_np_u32(out), want) and _rep(rep) == wrep
+
+
+def test_full_range_u32_budget(rs, oracle):
+    keys = oracle.gen_u32(3, 0, 1000, 0)
+    with pytest.raises(rs.Error) as e:
+        rs.sort_u32(_t(keys.view(np.int32)))
+    assert e.value.code == "cell_budget_exceeded"
+
+
+def test_errors_match_reference_codes(rs):
+    import torch
+
+    with pytest.raises(rs.Error) as e:
+        rs.sort_i64(torch.tensor([5, -2, 7], device="cuda"))
+    assert e.value.code == "negative_value"
+    with pytest.raises(rs.Error) as e:
+        rs.sort_f64(torch.tensor([1.0, float("nan")], dtype=torch.float64, device="cuda"), 2)
+    assert e.value.code == "non_finite"
+    with pytest.raises(rs.Error) as e:
+        rs.sort_f64(torch.tensor([1.0, -3.0], dtype=torch.float64, device="cuda"), 2)
+    assert e.value.code == "negative_value"
+    with pytest.raises(rs.Error) as e:
+        rs.sort_u32(torch.arange(10, dtype=torch.int32, device="cuda"),
+                    out=torch.empty(5, dtype=torch.int32, device="cuda"))
+    assert e.value.code == "buffer_too_small"
+    with pytest.raises(rs.Error) as e:
+        rs.sort_keys(torch.tensor([5, 100], device="cuda"), rs.KeySpec(10, 2, 1))
+    assert e.value.code == "spec_mismatch"
+    with pytest.raises(rs.Error) as e:
+        rs.sort_strings(["aZ"])
+    assert e.value.code == "symbol_out_of_alphabet"
+    with pytest.raises(rs.Error) as e:
+        rs.sort_strings(["zzzzzz"])
+    assert e.value.code == "cell_budget_exceeded"
+
+
+# ----------------------------------- full BASELINE sizes: size-free properties
+def _sorted_and_same_multiset(inp, out, bins):
+    import torch
+
+    assert bool((out[1:] >= out[:-1]).all())
+    assert torch.equal(torch.bincount(inp, minlength=bins), torch.bincount(out, minlength=bins))
+
+
+def test_cfg2_full_size_properties(rs):
+    import torch
+
+    n = 1 << 28
+    keys = gen_u32_device(rs, rs_seed(2), n, 10**6)
+    out, rep = rs.sort_u32(keys, key_digits=6)
+    assert rep.written == n and rep.spec.total_digits == 6
+    _sorted_and_same_multiset(keys.long(), out.long(), 10**6)
+    # all 10^6 cells occupied -> each of the 10 rows spans 10^5 cells
+    assert rep.cells_traversed == 10**6
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_cfg2_kv_full_size_stability(rs):
+    import torch
+
+    n = 1 << 28
+    keys = gen_u32_device(rs, rs_seed(2), n, 10**6)
+    vals = torch.empty(n, dtype=torch.int32, device="cuda")
+    rs._check(rs._lib.load().rs_gen_iota_u32(0, n, rs._ptr(vals), rs._stream()))
+    ko, vo, rep = rs.sort_u32_kv(keys, vals, key_digits=6)
+    assert bool((ko[1:] >= ko[:-1]).all())
+    same = ko[1:] == ko[:-1]
+    assert bool((vo[1:][same] > vo[:-1][same]).all())  # payload = index: stable
+    assert torch.equal(keys[vo.long()], ko)              # payload points at its key
+    del ko, vo
+    torch.cuda.empty_cache()
+
+
+def rs_seed(cfg):
+    from oracle import Oracle
+
+    return Oracle().config_seed(cfg)
