@@ -57,8 +57,8 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
-        self.gpu = gpu
+    def __init__(self, gpu: str):
+        self.gpu = gpu  # nvidia-smi -i accepts the GPU UUID
         self.proc = None
         self.path = None
 
@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kv", action="store_true")
+    ap.add_argument("--no-clock-window", action="store_true",
+                    help="skip the untimed steps around the timed region (for ncu launch lists)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -224,24 +226,38 @@ def main():
         else:
             rsd.sharded_grid_sort(keys, KEY_BOUND)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches0 = lib.rs_launch_count()
+    try:
+        gpu_id = "GPU-" + str(torch.cuda.get_device_properties(local_rank).uuid)
+    except Exception:
+        gpu_id = str(local_rank)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    # The sampler (100 ms period) runs across an extended warm-up (>= 0.5 s
+    # of untimed steps), the timed region and 0.3 s of trailing untimed
+    # steps, so its samples bracket the timed region under the same load.
+    with ClockSampler(gpu_id) as clk:
+        for _ in range(args.warmup):
+            step()
         torch.cuda.synchronize()
+        t_end = time.perf_counter() + (0.0 if args.no_clock_window else 0.5)
+        while time.perf_counter() < t_end:
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches0 = lib.rs_launch_count()
         ev0.record()
         for _ in range(args.steps):
             step()
         ev1.record()
         torch.cuda.synchronize()
+        launches = (lib.rs_launch_count() - launches0) // args.steps
+        t_end = time.perf_counter() + (0.0 if args.no_clock_window else 0.3)
+        while time.perf_counter() < t_end:
+            step()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
-    launches = (lib.rs_launch_count() - launches0) // args.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

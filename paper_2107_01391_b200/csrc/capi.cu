@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <atomic>
 #include <map>
@@ -15,6 +16,7 @@
 
 #include "kernels_grid.cuh"
 #include "kernels_kv.cuh"
+#include "kernels_two_level.cuh"
 #include "kernels_msd.cuh"
 #include "recsort_b200.h"
 #include "rs_internal.cuh"
@@ -175,23 +177,114 @@ unsigned long long device_max(Workspace& ws, const typename Map::In* in, uint64_
   return ws.h_stats->max_key;
 }
 
-// Counting pass into ws counts[cells] (zeroed here).
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Exclusive scan of `count` uint32 values (decoupled look-back); the grand
+// total lands in *total (device).
+void exscan_u32(Workspace& ws, const uint32_t* in, uint64_t count, uint32_t* out,
+                unsigned long long* total) {
+  const uint32_t tiles = static_cast<uint32_t>((count + kScanTile - 1) / kScanTile);
+  auto* desc = ws.get<unsigned long long>(kSlotDesc2, tiles + 1ull);
+  RS_CUDA(cudaMemsetAsync(desc, 0, (tiles + 1ull) * sizeof(unsigned long long), ws.stream));
+  auto* ticket = reinterpret_cast<unsigned*>(desc + tiles);
+  PassTimer pt_(RS_PASS_SCAN, ws.stream);
+  k_exscan_u32<<<tiles, kThreads, 0, ws.stream>>>(in, count, out, desc, ticket, total, tiles);
+  RS_LAUNCH_CHECK();
+}
+
+// Geometry of the two-level split: ~1000 inner cells per outer bucket
+// (10^6 = 1000 x 1000), at most kTlMaxBuckets buckets.
+bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
+  if (cells <= kSmemCellsMax || cells > 0xFFFFFFFFull) return false;
+  uint64_t B = (cells + 999) / 1000;
+  if (B > kTlMaxBuckets) B = kTlMaxBuckets;
+  const uint64_t S = (cells + B - 1) / B;
+  if (S > kTlMaxInner) return false;
+  t.cells = cells;
+  t.S = static_cast<uint32_t>(S);
+  t.B = static_cast<uint32_t>((cells + S - 1) / S);
+  t.magic = ~0ull / S + 1ull;  // ceil(2^64 / S) for S not a power of two
+  if ((S & (S - 1)) == 0) t.magic = 1ull << (64 - __builtin_ctzll(S));
+  const uint64_t tiles = (n + kTlTile - 1) / kTlTile;
+  uint64_t G = (uint64_t)sm_count() * 8;
+  if (G > tiles) G = tiles ? tiles : 1;
+  const uint64_t tiles_per = (tiles + G - 1) / G;
+  t.chunk = tiles_per * kTlTile;
+  t.G = static_cast<uint32_t>((n + t.chunk - 1) / t.chunk);
+  if (t.G == 0) t.G = 1;
+  return true;
+}
+
+template <class Map>
+void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, const TwoLevel& t,
+                     uint32_t* counts) {
+  const bool al = aligned16(in);
+  const uint64_t bg = (uint64_t)t.B * t.G;
+  auto* cta_hist = ws.get<uint32_t>(kSlotCtaHist, bg);
+  auto* cta_off = ws.get<uint32_t>(kSlotCtaOff, bg);
+  auto* bstart = ws.get<uint32_t>(kSlotBucketStart, t.B + 1ull);
+  auto* lows = ws.get<uint16_t>(kSlotLows, n + 8);
+  auto* total = ws.get<unsigned long long>(kSlotScratch, 4);
+  {
+    PassTimer pt_(RS_PASS_MSD_HIST, ws.stream);
+    k_outer_hist<Map><<<t.G, kTlThreads, 0, ws.stream>>>(in, n, map, t, al, cta_hist, ws.stats);
+    RS_LAUNCH_CHECK();
+  }
+  exscan_u32(ws, cta_hist, bg, cta_off, total);
+  {
+    PassTimer pt_(RS_PASS_SCAN, ws.stream);
+    k_bucket_starts<<<(t.B + 1 + 255) / 256, 256, 0, ws.stream>>>(cta_off, t, total, bstart);
+    RS_LAUNCH_CHECK();
+  }
+  static bool attr = false;
+  if (!attr) {
+    RS_CUDA(cudaFuncSetAttribute(k_outer_scatter<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kOuterScatterSmem)));
+    attr = true;
+  }
+  {
+    PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
+    k_outer_scatter<Map><<<t.G, kTlThreads, kOuterScatterSmem, ws.stream>>>(in, n, map, t, al, cta_off, lows);
+    RS_LAUNCH_CHECK();
+  }
+  RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
+  const uint64_t slice = std::max<uint64_t>(16384, 16ull * t.S);
+  const uint64_t nslices = (n + slice - 1) / slice;
+  {
+    PassTimer pt_(RS_PASS_COUNT, ws.stream);
+    k_inner_count<<<static_cast<unsigned>(nslices), kTlThreads, t.S * sizeof(uint32_t), ws.stream>>>(
+        lows, n, bstart, t, slice, counts);
+    RS_LAUNCH_CHECK();
+  }
+}
+
+// Counting pass into ws counts[cells] (zeroed here): a shared-memory grid
+// when it fits, the two-level split up to 4096 x 16384 cells, L2 atomics
+// beyond that.
 template <class Map>
 void count_pass(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, uint64_t cells,
                 uint32_t* counts) {
+  if (n == 0) {
+    RS_CUDA(cudaMemsetAsync(counts, 0, cells * sizeof(uint32_t), ws.stream));
+    return;
+  }
+  TwoLevel t{};
+  if (plan_two_level(cells, n, t)) {
+    two_level_count(ws, in, n, map, t, counts);
+    return;
+  }
   RS_CUDA(cudaMemsetAsync(counts, 0, cells * sizeof(uint32_t), ws.stream));
-  if (n == 0) return;
   PassTimer pt_(RS_PASS_COUNT, ws.stream);
   if (cells <= kSmemCellsMax) {
     // Few CTAs so the per-CTA flush of `cells` counters stays small
     // against the keys each CTA counts.
     const uint64_t per_cta_min = cells * 8 > 8192 ? cells * 8 : 8192;
-    const unsigned grid = stream_grid(n, static_cast<int>(per_cta_min), 4);
+    const unsigned grid = stream_grid(n, static_cast<int>(per_cta_min), 8);
     k_count_smem<Map><<<grid, kThreads, cells * sizeof(uint32_t), ws.stream>>>(in, n, map, counts,
                                                                                cells, ws.stats);
   } else {
     const unsigned grid = stream_grid(n, kThreads * 8, 8);
-    k_count_global<Map, true><<<grid, kThreads, 0, ws.stream>>>(in, n, map, counts, cells, ws.stats);
+    k_count_global<Map, false><<<grid, kThreads, 0, ws.stream>>>(in, n, map, counts, cells, ws.stats);
   }
   RS_LAUNCH_CHECK();
 }
@@ -256,8 +349,6 @@ void grid_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, u
   pull_stats(ws);
 }
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
 uint64_t pow10u(uint32_t e) { return checked_pow(10, e); }
 
 // Shared driver for the decimal-integer paths (u32 and i64).
@@ -299,58 +390,52 @@ void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, cons
 // ------------------------------------------------------ stable key/value
 unsigned long long magic_div(uint64_t d) { return ~0ull / d + 1ull; }  // ceil(2^64/d), d = 10^k
 
-KvPass kv_pass(uint32_t g, uint32_t digits) {
+KvPass kv_pass(uint32_t g, uint32_t digits, uint64_t n) {
   KvPass p{};
   p.magic_div = g ? magic_div(pow10u(3 * g)) : 0ull;
   p.magic_1000 = magic_div(1000);
   const uint32_t rem = digits - 3 * g;
   p.bins = rem >= 3 ? 1000u : static_cast<uint32_t>(pow10u(rem));
+  const uint64_t tiles = (n + kKvTile - 1) / kKvTile;
+  uint64_t G = (uint64_t)sm_count() * 3;
+  if (G > tiles) G = tiles ? tiles : 1;
+  p.chunk = ((tiles + G - 1) / G) * kKvTile;
+  p.G = static_cast<uint32_t>((n + p.chunk - 1) / p.chunk);
   return p;
 }
 
 void kv_sort(Workspace& ws, const uint32_t* keys, const uint32_t* vals, uint64_t n, uint32_t digits,
              uint32_t* keys_out, uint32_t* vals_out) {
   const uint32_t passes = (digits + 2) / 3;
-  KvPass ps[kKvMaxPasses] = {};
-  for (uint32_t g = 0; g < passes; ++g) ps[g] = kv_pass(g, digits);
   reset_stats(ws);
-  auto* hist = ws.get<unsigned long long>(kSlotHist, 2ull * kKvMaxPasses * kKvBins);
-  unsigned long long* offsets = hist + kKvMaxPasses * kKvBins;
-  RS_CUDA(cudaMemsetAsync(hist, 0, kKvMaxPasses * kKvBins * sizeof(unsigned long long), ws.stream));
-  {
-    PassTimer pt_(RS_PASS_KV_HIST, ws.stream);
-    k_kv_hist<<<stream_grid(n, kKvThreads * 16, 8), kKvThreads, 0, ws.stream>>>(
-        keys, n, ps[0], ps[1], ps[2], ps[3], passes, hist, ws.stats);
-    RS_LAUNCH_CHECK();
-  }
-  {
-    PassTimer pt_(RS_PASS_KV_HIST, ws.stream);
-    k_kv_offsets<<<passes, 256, 0, ws.stream>>>(hist, offsets);
-    RS_LAUNCH_CHECK();
-  }
-  const uint32_t tiles = static_cast<uint32_t>((n + kKvTile - 1) / kKvTile);
-  auto* desc = ws.get<uint32_t>(kSlotTileDesc, (uint64_t)tiles * kKvBins);
   uint32_t* tk = ws.get<uint32_t>(kSlotTmpKeys, n);
   uint32_t* tv = ws.get<uint32_t>(kSlotTmpVals, n);
   static bool attr_set = false;
   if (!attr_set) {
-    RS_CUDA(cudaFuncSetAttribute(k_kv_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RS_CUDA(cudaFuncSetAttribute(k_kv_chunk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kKvSmemBytes)));
     attr_set = true;
   }
+  auto* total = ws.get<unsigned long long>(kSlotScratch, 4);
   const uint32_t* sk = keys;
   const uint32_t* sv = vals;
-  for (uint32_t p = 0; p < passes; ++p) {
-    const bool to_out = ((passes - 1 - p) % 2) == 0;
+  for (uint32_t g = 0; g < passes; ++g) {
+    const KvPass p = kv_pass(g, digits, n);
+    const uint64_t bg = (uint64_t)p.bins * p.G;
+    auto* hist = ws.get<uint32_t>(kSlotCtaHist, bg);
+    auto* off = ws.get<uint32_t>(kSlotCtaOff, bg);
+    const bool to_out = ((passes - 1 - g) % 2) == 0;
     uint32_t* dk = to_out ? keys_out : tk;
     uint32_t* dv = to_out ? vals_out : tv;
-    RS_CUDA(cudaMemsetAsync(desc, 0, (uint64_t)tiles * kKvBins * sizeof(uint32_t), ws.stream));
-    RS_CUDA(cudaMemsetAsync(&ws.stats->tile_counter, 0, sizeof(unsigned), ws.stream));
+    {
+      PassTimer pt_(RS_PASS_KV_HIST, ws.stream);
+      k_kv_chunk_hist<<<p.G, kKvThreads, 0, ws.stream>>>(sk, n, p, aligned16(sk), hist, ws.stats);
+      RS_LAUNCH_CHECK();
+    }
+    exscan_u32(ws, hist, bg, off, total);
     {
       PassTimer pt_(RS_PASS_KV_SCATTER, ws.stream);
-      k_kv_pass<<<tiles, kKvThreads, kKvSmemBytes, ws.stream>>>(sk, sv, dk, dv, n, ps[p],
-                                                                offsets + p * kKvBins, desc,
-                                                                &ws.stats->tile_counter);
+      k_kv_chunk_scatter<<<p.G, kKvThreads, kKvSmemBytes, ws.stream>>>(sk, sv, dk, dv, n, p, off);
       RS_LAUNCH_CHECK();
     }
     sk = dk;

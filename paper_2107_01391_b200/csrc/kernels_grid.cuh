@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) k_count_global(const typename Map::I
 
 // ------------------------------------------ K1': map + count (smem grid)
 // For grids of at most kSmemCellsMax cells: block-private shared-memory
-// histogram with warp-aggregated shared atomics, flushed once per CTA.
+// histogram, flushed once per CTA.
 template <class Map>
 __global__ void __launch_bounds__(kThreads) k_count_smem(const typename Map::In* __restrict__ in,
                                                          uint64_t n, Map map,
@@ -263,10 +263,9 @@ __global__ void __launch_bounds__(kThreads) k_count_smem(const typename Map::In*
     const bool in_grid = ok && k < cells;
     ovf |= ok && k >= cells;
     mx = (ok && k > mx) ? k : mx;
-    const unsigned tag = in_grid ? static_cast<unsigned>(k) : 0xffffffffu;
-    const unsigned peers = __match_any_sync(0xffffffffu, tag);
-    if (in_grid && (int)(threadIdx.x & 31) == __ffs(peers) - 1)
-      atomicAdd(&s_hist[k], (unsigned)__popc(peers));
+    // plain shared atomics: __match_any_sync aggregation measured ~10x
+    // slower on B200 for uniform keys (profiles/r1_microbench.txt)
+    if (in_grid) atomicAdd(&s_hist[k], 1u);
   }
   __syncthreads();
   for (uint32_t c = threadIdx.x; c < cells; c += blockDim.x)

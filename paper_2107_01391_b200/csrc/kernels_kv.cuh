@@ -2,22 +2,21 @@
 //
 // The reference has no record API; its stable order is rsort's
 // originals_by_key (rsort.cpp:133-145) == baselines::radix_sort_lsd_by
-// (baselines.hpp:24-46), which makes base-10 LSD passes.  Here a pass takes
-// a group of three decimal digits (radix 1000 = a 10x10x10 sub-grid of the
-// Cartesian count space), so a 6-digit key needs two stable passes instead
-// of six.  Because stable order is unique, the output is bit-identical to
-// the reference's for any stable schedule.
+// (baselines.hpp:24-46), which makes base-10 LSD passes.  Here a pass takes a
+// group of three decimal digits (radix 1000: a 10x10x10 sub-grid of the
+// Cartesian count space), so a 6-digit key needs two stable passes instead of
+// six.  Stable order is unique, so the output is bit-identical to the
+// reference's for any stable schedule.
 //
-// Per pass (one kernel, single-pass "onesweep" structure):
-//   * tiles of 4096 records get ordered ids from an atomic ticket;
-//   * each warp ranks its records stably with __match_any_sync over the
-//     group digit and a warp-private shared histogram;
-//   * the tile's per-digit counts are published and each digit's prefix over
-//     earlier tiles is found by decoupled look-back (32-bit descriptors:
-//     [31:30] flag, [29:0] count; n < 2^30 per call);
-//   * records are staged in shared memory in digit order and written out so
-//     consecutive threads store consecutive addresses of a digit run.
-// Digit offsets of every pass come from one histogram pre-pass over the keys.
+// Per pass (reduce-then-scan, deterministic):
+//   k_kv_chunk_hist     per-CTA digit counts over a contiguous chunk      R4
+//   exscan              [bins][G] -> each CTA's start in every digit run
+//   k_kv_chunk_scatter  the CTA walks its chunk tile by tile in order; each
+//                       warp ranks its records stably with 10 ballots over
+//                       the digit bits (no __match_any_sync, which measured
+//                       ~10x slower on B200), the tile is staged in shared
+//                       memory in digit order and written so consecutive
+//                       threads store consecutive addresses of a run  R8 + W8
 #pragma once
 
 #include <cuda_runtime.h>
@@ -29,24 +28,29 @@
 namespace rsb {
 
 constexpr int kKvThreads = 256;
-constexpr int kKvItems = 16;                        // records per thread
-constexpr int kKvTile = kKvThreads * kKvItems;      // 4096 records per tile
-constexpr int kKvBins = 1000;                       // three decimal digits
-constexpr int kKvMaxPasses = 4;                     // 10-digit uint32 keys
-constexpr size_t kKvSmemBytes = kKvBins * 8 + 2 * kKvTile * 4 + kKvBins * 4 +
-                                (kKvThreads / 32) * kKvBins * 2 + kKvTile * 2;
-constexpr uint32_t kKvAgg = 1u << 30, kKvPre = 2u << 30, kKvVal = (1u << 30) - 1;
+constexpr int kKvItems = 16;                    // records per thread per tile
+constexpr int kKvTile = kKvThreads * kKvItems;  // 4096 records
+constexpr int kKvBins = 1000;                   // three decimal digits
+constexpr int kKvBits = 10;                     // 1000 < 2^10
+constexpr int kKvMaxPasses = 4;                 // 10-digit uint32 keys
+constexpr int kKvWarps = kKvThreads / 32;
+constexpr size_t kKvSmemBytes = kKvWarps * kKvBins * 2  // s_wh
+                                + kKvBins * 4 * 3        // s_cnt, s_start, s_cur
+                                + kKvTile * 4 * 2        // s_keys, s_vals
+                                + kKvTile * 2            // s_dig
+                                + 64 * 4;
 
-// Exact floor(n / D) for 32-bit n with M = ceil(2^64 / D) (error n*e/2^64 <
-// 1/D because n, e < 2^32).
+// Exact floor(n / D) for 32-bit n with M = ceil(2^64 / D).
 __device__ __forceinline__ uint32_t div_magic(uint32_t n, unsigned long long m) {
   return static_cast<uint32_t>(__umul64hi(static_cast<unsigned long long>(n), m));
 }
 
 struct KvPass {
-  unsigned long long magic_div;  // divides by 10^(3*pass)
-  unsigned long long magic_1000; // divides by 1000
-  uint32_t bins;                 // 1000, or 10^(remaining digits) on the top pass
+  unsigned long long magic_div;   // divides by 10^(3*pass) (0: identity)
+  unsigned long long magic_1000;  // divides by 1000
+  uint32_t bins;                  // 1000, or 10^(remaining digits) on the top pass
+  uint64_t chunk;                 // records per CTA (multiple of kKvTile)
+  uint32_t G;                     // CTAs
 };
 
 __device__ __forceinline__ uint32_t kv_digit(uint32_t key, const KvPass& p) {
@@ -54,26 +58,38 @@ __device__ __forceinline__ uint32_t kv_digit(uint32_t key, const KvPass& p) {
   return q - 1000u * div_magic(q, p.magic_1000);
 }
 
-// Pre-pass: all group-digit histograms at once (+ max for the geometry).
-__global__ void __launch_bounds__(kKvThreads) k_kv_hist(const uint32_t* __restrict__ keys, uint64_t n,
-                                                        KvPass p0, KvPass p1, KvPass p2, KvPass p3,
-                                                        uint32_t passes,
-                                                        unsigned long long* __restrict__ hist,
-                                                        DevStats* st) {
-  __shared__ uint32_t s_hist[kKvMaxPasses * kKvBins];
-  for (int i = threadIdx.x; i < kKvMaxPasses * kKvBins; i += blockDim.x) s_hist[i] = 0;
+__global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __restrict__ keys, uint64_t n,
+                                                              KvPass p, bool aligned,
+                                                              uint32_t* __restrict__ hist,  // [bins][G]
+                                                              DevStats* st) {
+  __shared__ uint32_t s_h[kKvBins];
+  for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) s_h[b] = 0;
   __syncthreads();
-  const KvPass ps[kKvMaxPasses] = {p0, p1, p2, p3};
+  const uint64_t c0 = (uint64_t)blockIdx.x * p.chunk;
+  const uint64_t c1 = c0 + p.chunk < n ? c0 + p.chunk : n;
   unsigned long long mx = 0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t k = __ldcs(keys + i);
-    mx = k > mx ? k : mx;
-    for (uint32_t p = 0; p < passes; ++p) atomicAdd(&s_hist[p * kKvBins + kv_digit(k, ps[p])], 1u);
+  for (uint64_t base = c0; base < c1; base += kKvTile) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i0 = base + q * 1024 + threadIdx.x * 4;
+      uint32_t v[4];
+      if (aligned && i0 + 4 <= c1) {
+        const uint4 w = __ldcs(reinterpret_cast<const uint4*>(keys + i0));
+        v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+      } else {
+        for (int e = 0; e < 4; ++e) v[e] = i0 + e < c1 ? keys[i0 + e] : 0u;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (i0 + e < c1) {
+          mx = v[e] > mx ? v[e] : mx;
+          atomicAdd(&s_h[kv_digit(v[e], p)], 1u);
+        }
+      }
+    }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < (int)passes * kKvBins; i += blockDim.x)
-    if (s_hist[i]) atomicAdd(&hist[i], (unsigned long long)s_hist[i]);
+  for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) hist[(uint64_t)b * p.G + blockIdx.x] = s_h[b];
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long w = __shfl_xor_sync(0xffffffffu, mx, o);
     mx = w > mx ? w : mx;
@@ -81,162 +97,132 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_hist(const uint32_t* __restri
   if ((threadIdx.x & 31) == 0 && mx) atomicMax(&st->max_key, mx);
 }
 
-// Exclusive scan of each pass's histogram into digit offsets (1 block/pass).
-__global__ void k_kv_offsets(const unsigned long long* __restrict__ hist,
-                             unsigned long long* __restrict__ offsets) {
-  const int p = blockIdx.x;
-  __shared__ unsigned long long s[kKvBins];
-  for (int i = threadIdx.x; i < kKvBins; i += blockDim.x) s[i] = hist[p * kKvBins + i];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long run = 0;
-    for (int i = 0; i < kKvBins; ++i) {
-      const unsigned long long c = s[i];
-      s[i] = run;
-      run += c;
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kKvBins; i += blockDim.x) offsets[p * kKvBins + i] = s[i];
-}
-
-// One stable LSD pass.
-__global__ void __launch_bounds__(kKvThreads) k_kv_pass(const uint32_t* __restrict__ keys_in,
-                                                        const uint32_t* __restrict__ vals_in,
-                                                        uint32_t* __restrict__ keys_out,
-                                                        uint32_t* __restrict__ vals_out, uint64_t n,
-                                                        KvPass pass,
-                                                        const unsigned long long* __restrict__ offsets,
-                                                        uint32_t* desc, unsigned* tile_counter) {
-  // dynamic shared memory (kKvSmemBytes), carved:
+__global__ void __launch_bounds__(kKvThreads) k_kv_chunk_scatter(const uint32_t* __restrict__ keys_in,
+                                                                 const uint32_t* __restrict__ vals_in,
+                                                                 uint32_t* __restrict__ keys_out,
+                                                                 uint32_t* __restrict__ vals_out, uint64_t n,
+                                                                 KvPass p, const uint32_t* __restrict__ off) {
   extern __shared__ __align__(16) unsigned char kv_smem[];
-  unsigned long long* s_base = reinterpret_cast<unsigned long long*>(kv_smem);   // [kKvBins]
-  uint32_t* s_keys = reinterpret_cast<uint32_t*>(s_base + kKvBins);             // [kKvTile]
-  uint32_t* s_vals = s_keys + kKvTile;                                          // [kKvTile]
-  uint32_t* s_cnt = s_vals + kKvTile;                                           // [kKvBins]
-  uint16_t (*s_wh)[kKvBins] = reinterpret_cast<uint16_t (*)[kKvBins]>(s_cnt + kKvBins);  // [8][kKvBins]
-  uint16_t* s_dig = &s_wh[kKvThreads / 32][0];                                  // [kKvTile]
-  __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_scan[kKvThreads];
+  uint32_t* s_keys = reinterpret_cast<uint32_t*>(kv_smem);  // [kKvTile]
+  uint32_t* s_vals = s_keys + kKvTile;                      // [kKvTile]
+  uint32_t* s_cnt = s_vals + kKvTile;                       // [kKvBins]
+  uint32_t* s_start = s_cnt + kKvBins;                      // [kKvBins]
+  uint32_t* s_cur = s_start + kKvBins;                      // [kKvBins]
+  uint16_t* s_wh = reinterpret_cast<uint16_t*>(s_cur + kKvBins);  // [kKvWarps][kKvBins]
+  uint16_t* s_dig = s_wh + kKvWarps * kKvBins;                    // [kKvTile]
+  __shared__ uint32_t s_scan[kKvWarps];
+  __shared__ uint32_t s_total;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-  for (int i = threadIdx.x; i < (kKvThreads / 32) * kKvBins; i += blockDim.x)
-    (&s_wh[0][0])[i] = 0;
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t t0 = (uint64_t)tile * kKvTile;
-
-  // striped load: record t0 + warp*512 + j*32 + lane
-  uint32_t k[kKvItems], v[kKvItems], rank[kKvItems];
-  uint16_t d[kKvItems];
-#pragma unroll
-  for (int j = 0; j < kKvItems; ++j) {
-    const uint64_t i = t0 + warp * (kKvItems * 32) + j * 32 + lane;
-    const bool ok = i < n;
-    k[j] = ok ? __ldcs(keys_in + i) : 0u;
-    v[j] = ok ? __ldcs(vals_in + i) : 0u;
-    d[j] = ok ? static_cast<uint16_t>(kv_digit(k[j], pass)) : static_cast<uint16_t>(0xffff);
-  }
-  // warp-level stable ranks
   const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-  for (int j = 0; j < kKvItems; ++j) {
-    const unsigned peers = __match_any_sync(0xffffffffu, d[j]);
-    const bool ok = d[j] != 0xffff;
-    uint32_t base = 0;
-    if (ok) base = s_wh[warp][d[j]];
-    __syncwarp();
-    if (ok && (peers & lt) == 0) s_wh[warp][d[j]] = static_cast<uint16_t>(base + __popc(peers));
-    __syncwarp();
-    rank[j] = base + __popc(peers & lt);
-  }
+  for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) s_cur[b] = off[(uint64_t)b * p.G + blockIdx.x];
+  for (int i = threadIdx.x; i < kKvWarps * kKvBins; i += blockDim.x) s_wh[i] = 0;
+  const uint64_t c0 = (uint64_t)blockIdx.x * p.chunk;
+  const uint64_t c1 = c0 + p.chunk < n ? c0 + p.chunk : n;
+  uint16_t* wh = s_wh + warp * kKvBins;
   __syncthreads();
-  // per digit: exclusive prefix across warps, tile count
-  for (int b = threadIdx.x; b < kKvBins; b += blockDim.x) {
-    uint32_t run = 0;
+
+  for (uint64_t t0 = c0; t0 < c1; t0 += kKvTile) {
+    // striped load: record t0 + warp*512 + j*32 + lane (input order =
+    // warp-major, then j, then lane)
+    uint32_t k[kKvItems], v[kKvItems], rank[kKvItems];
+    uint32_t d[kKvItems];
 #pragma unroll
-    for (int w = 0; w < kKvThreads / 32; ++w) {
-      const uint32_t c = s_wh[w][b];
-      s_wh[w][b] = static_cast<uint16_t>(run);
-      run += c;
+    for (int j = 0; j < kKvItems; ++j) {
+      const uint64_t i = t0 + warp * (kKvItems * 32) + j * 32 + lane;
+      const bool ok = i < c1;
+      k[j] = ok ? __ldcs(keys_in + i) : 0u;
+      v[j] = ok ? __ldcs(vals_in + i) : 0u;
+      d[j] = ok ? kv_digit(k[j], p) : 0xffffu;
     }
-    s_cnt[b] = run;
-  }
-  __syncthreads();
-  // publish aggregates, look back, publish inclusive prefixes
-  volatile uint32_t* vdesc = desc;
-  for (int b = threadIdx.x; b < (int)pass.bins; b += blockDim.x) {
-    const uint32_t c = s_cnt[b];
-    unsigned long long prefix = 0;
-    if (tile == 0) {
-      vdesc[b] = kKvPre | c;
-    } else {
-      vdesc[(uint64_t)tile * kKvBins + b] = kKvAgg | c;
-      for (int64_t t = (int64_t)tile - 1; t >= 0; --t) {
-        uint32_t x;
-        do {
-          x = vdesc[(uint64_t)t * kKvBins + b];
-        } while ((x >> 30) == 0);
-        prefix += x & kKvVal;
-        if ((x >> 30) == 2) break;
+    // stable warp ranks: peers = lanes with the same digit, from 10 ballots
+#pragma unroll
+    for (int j = 0; j < kKvItems; ++j) {
+      const bool ok = d[j] != 0xffffu;
+      unsigned peers = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+      for (int b = 0; b < kKvBits; ++b) {
+        const bool bit = (d[j] >> b) & 1u;
+        const unsigned bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
       }
-      vdesc[(uint64_t)tile * kKvBins + b] = kKvPre | static_cast<uint32_t>(prefix + c);
-    }
-    s_base[b] = offsets[b] + prefix;
-  }
-  // tile-local exclusive scan of s_cnt over digits (4 digits per thread)
-  {
-    uint32_t loc[4], sum = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int b = threadIdx.x * 4 + q;
-      loc[q] = b < kKvBins ? s_cnt[b] : 0u;
-      sum += loc[q];
-    }
-    uint32_t inc = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    if (lane == 31) s_scan[warp] = inc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t r = 0;
-      for (int w = 0; w < kKvThreads / 32; ++w) {
-        const uint32_t c = s_scan[w];
-        s_scan[w] = r;
-        r += c;
-      }
+      uint32_t base = 0;
+      if (ok) base = wh[d[j]];
+      __syncwarp();
+      if (ok && (peers & lt) == 0) wh[d[j]] = static_cast<uint16_t>(base + __popc(peers));
+      __syncwarp();
+      rank[j] = base + __popc(peers & lt);
     }
     __syncthreads();
-    uint32_t run = s_scan[warp] + inc - sum;
+    // per digit: exclusive prefix across warps (in s_wh) and tile count
+    for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) {
+      uint32_t run = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int b = threadIdx.x * 4 + q;
-      if (b < kKvBins) s_cnt[b] = run;
-      run += loc[q];
+      for (int w = 0; w < kKvWarps; ++w) {
+        const uint32_t c = s_wh[w * kKvBins + b];
+        s_wh[w * kKvBins + b] = static_cast<uint16_t>(run);
+        run += c;
+      }
+      s_cnt[b] = run;
     }
-  }
-  __syncthreads();
-  // stage in digit order
+    __syncthreads();
+    // tile-local exclusive scan over digits (4 per thread)
+    {
+      uint32_t loc[4], sum = 0;
 #pragma unroll
-  for (int j = 0; j < kKvItems; ++j) {
-    if (d[j] != 0xffff) {
-      const uint32_t pos = s_cnt[d[j]] + s_wh[warp][d[j]] + rank[j];
-      s_keys[pos] = k[j];
-      s_vals[pos] = v[j];
-      s_dig[pos] = d[j];
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t b = threadIdx.x * 4 + q;
+        loc[q] = b < p.bins ? s_cnt[b] : 0u;
+        sum += loc[q];
+      }
+      uint32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) s_scan[warp] = inc;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t r = 0;
+        for (int w = 0; w < kKvWarps; ++w) {
+          const uint32_t c = s_scan[w];
+          s_scan[w] = r;
+          r += c;
+        }
+        s_total = r;
+      }
+      __syncthreads();
+      uint32_t run = s_scan[warp] + inc - sum;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t b = threadIdx.x * 4 + q;
+        if (b < p.bins) s_start[b] = run;
+        run += loc[q];
+      }
     }
-  }
-  __syncthreads();
-  const uint64_t valid = n - t0 < (uint64_t)kKvTile ? n - t0 : (uint64_t)kKvTile;
-  for (uint32_t i = threadIdx.x; i < valid; i += blockDim.x) {
-    const uint32_t b = s_dig[i];
-    const unsigned long long g = s_base[b] + (i - s_cnt[b]);
-    keys_out[g] = s_keys[i];
-    vals_out[g] = s_vals[i];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kKvItems; ++j) {
+      if (d[j] != 0xffffu) {
+        const uint32_t pos = s_start[d[j]] + wh[d[j]] + rank[j];
+        s_keys[pos] = k[j];
+        s_vals[pos] = v[j];
+        s_dig[pos] = static_cast<uint16_t>(d[j]);
+      }
+    }
+    __syncthreads();
+    const uint32_t total = s_total;
+    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
+      const uint32_t b = s_dig[i];
+      const uint32_t g = s_cur[b] + (i - s_start[b]);
+      keys_out[g] = s_keys[i];
+      vals_out[g] = s_vals[i];
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) s_cur[b] += s_cnt[b];
+    for (int i = threadIdx.x; i < kKvWarps * kKvBins; i += blockDim.x) s_wh[i] = 0;
+    __syncthreads();
   }
 }
 

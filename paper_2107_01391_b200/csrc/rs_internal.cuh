@@ -110,7 +110,7 @@ enum : unsigned { kFlagNegative = 1u, kFlagNonFinite = 2u, kFlagDomain = 4u };
 struct Workspace {
   int device = -1;
   cudaStream_t stream = nullptr;
-  static constexpr int kSlots = 12;
+  static constexpr int kSlots = 20;
   void* buf[kSlots] = {};
   size_t cap[kSlots] = {};
   DevStats* stats = nullptr;   // device
@@ -156,6 +156,12 @@ enum Slot : int {
   kSlotMisc = 9,
   kSlotTmpKeys2 = 10,
   kSlotTmpVals2 = 11,
+  kSlotCtaHist = 12,    // per-CTA outer histograms [B][G]
+  kSlotCtaOff = 13,     // their exclusive scan
+  kSlotBucketStart = 14,
+  kSlotLows = 15,       // partitioned inner digits (uint16)
+  kSlotDesc2 = 16,      // look-back descriptors of the second scan
+  kSlotScratch = 17,
 };
 
 }  // namespace rsb
