@@ -192,11 +192,13 @@ void exscan_u32(Workspace& ws, const uint32_t* in, uint64_t count, uint32_t* out
   RS_LAUNCH_CHECK();
 }
 
-// Geometry of the two-level split: ~1000 inner cells per outer bucket
-// (10^6 = 1000 x 1000), at most kTlMaxBuckets buckets.
+// Geometry of the two-level split: ~10^4 inner cells per outer bucket
+// (10^6 = 100 x 10^4).  Few outer buckets keep the partition's write runs
+// long (~40 keys per 4096-key tile); 10^4 inner counters (40 KB) still fit a
+// shared histogram.  At most kTlMaxBuckets buckets.
 bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
   if (cells <= kSmemCellsMax || cells > 0xFFFFFFFFull) return false;
-  uint64_t B = (cells + 999) / 1000;
+  uint64_t B = (cells + 9999) / 10000;
   if (B > kTlMaxBuckets) B = kTlMaxBuckets;
   const uint64_t S = (cells + B - 1) / B;
   if (S > kTlMaxInner) return false;
@@ -248,7 +250,7 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
     RS_LAUNCH_CHECK();
   }
   RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
-  const uint64_t slice = std::max<uint64_t>(16384, 16ull * t.S);
+  const uint64_t slice = std::max<uint64_t>(65536, 16ull * t.S);
   const uint64_t nslices = (n + slice - 1) / slice;
   {
     PassTimer pt_(RS_PASS_COUNT, ws.stream);
@@ -518,7 +520,7 @@ struct OutStr {
   uint32_t width, digits, radix;
   const uint8_t* sym;  // device: ordinal -> byte, sym[0] = 0
   unsigned long long base;
-  __device__ __forceinline__ void put1(uint64_t p, unsigned long long key) const {
+  __device__ __forceinline__ void put_key(uint64_t p, unsigned long long key) const {
     uint8_t buf[16];
     for (int j = (int)digits - 1; j >= 0; --j) {
       const unsigned long long q = key / radix;
@@ -528,9 +530,10 @@ struct OutStr {
     uint8_t* r = out + p * width;
     for (uint32_t j = 0; j < width; ++j) r[j] = j < digits ? buf[j] : 0;
   }
+  __device__ __forceinline__ void put1(uint64_t p, uint32_t c) const { put_key(p, base + c); }
   __device__ __forceinline__ void put4(uint64_t p, const uint32_t (&c)[4], uint64_t end) const {
     for (int e = 0; e < 4; ++e)
-      if (p + e < end) put1(p + e, base + c[e]);
+      if (p + e < end) put_key(p + e, base + c[e]);
   }
 };
 

@@ -29,7 +29,8 @@ namespace rsb {
 constexpr int kThreads = 256;
 constexpr int kScanPerThread = 16;
 constexpr int kScanTile = kThreads * kScanPerThread;  // 4096 cells per scan tile
-constexpr int kEmitTile = 4096;                       // output positions per emit CTA
+constexpr int kEmitTile = 8192;                       // output positions per emit CTA
+constexpr int kEmitCap = 2048;                        // occupied cells staged per emit tile
 constexpr uint32_t kSmemCellsMax = 12288;             // smem-privatised grid limit (48 KB)
 
 // ------------------------------------------------------------- helpers
@@ -423,6 +424,7 @@ struct OutU32 {
   uint32_t* out;
   uint32_t base;
   bool aligned;
+  __device__ __forceinline__ void put1(uint64_t p, uint32_t c) const { out[p] = c + base; }
   __device__ __forceinline__ void put4(uint64_t p, const uint32_t (&c)[4], uint64_t end) const {
     if (aligned && p + 4 <= end) {
       __stcs(reinterpret_cast<uint4*>(out + p), make_uint4(c[0] + base, c[1] + base, c[2] + base, c[3] + base));
@@ -437,6 +439,7 @@ struct OutU64 {
   unsigned long long* out;
   unsigned long long base;
   bool aligned;
+  __device__ __forceinline__ void put1(uint64_t p, uint32_t c) const { out[p] = c + base; }
   __device__ __forceinline__ void put4(uint64_t p, const uint32_t (&c)[4], uint64_t end) const {
     if (aligned && p + 4 <= end) {
       __stcs(reinterpret_cast<ulonglong2*>(out + p), make_ulonglong2(c[0] + base, c[1] + base));
@@ -448,13 +451,20 @@ struct OutU64 {
   }
 };
 
+// Each CTA writes output positions [t*8192, (t+1)*8192).  Dense tile (at
+// most kEmitCap occupied cells reach it): the cells' run ends are staged in
+// shared memory (relative to the tile) and every warp writes 1024
+// consecutive positions as 16-byte stores, lane-contiguous; a lane finds the
+// cell of its first position by binary search and then walks forward (the
+// positions only grow).  Sparse tile (more cells than kEmitCap, i.e. runs of
+// ~4 keys or fewer): cell-driven, each thread writes whole runs.
 template <class Out>
 __global__ void __launch_bounds__(kThreads) k_emit(const uint32_t* __restrict__ occ_cell,
                                                    const unsigned long long* __restrict__ occ_end,
                                                    const uint32_t* __restrict__ tile_first,
                                                    const DevStats* st, uint64_t n, Out out) {
-  __shared__ uint32_t s_end[kEmitTile + 1];  // occ_end - p0, clipped to the tile
-  __shared__ uint32_t s_cell[kEmitTile + 1];
+  __shared__ uint32_t s_end[kEmitCap + 1];  // occ_end - p0, clipped to the tile
+  __shared__ uint32_t s_cell[kEmitCap + 1];
   const uint32_t t = blockIdx.x;
   const uint64_t p0 = (uint64_t)t * kEmitTile;
   const uint64_t pend = p0 + kEmitTile < n ? p0 + kEmitTile : n;
@@ -463,6 +473,17 @@ __global__ void __launch_bounds__(kThreads) k_emit(const uint32_t* __restrict__ 
   uint32_t j1 = tile_first[t + 1];
   if (j1 >= m) j1 = static_cast<uint32_t>(m - 1);
   const uint32_t cnt = j1 - j0 + 1;
+  if (cnt > kEmitCap) {
+    for (uint32_t j = j0 + threadIdx.x; j <= j1; j += blockDim.x) {
+      const unsigned long long a0 = j ? occ_end[j - 1] : 0ull;
+      const unsigned long long a = a0 > p0 ? a0 : p0;
+      const unsigned long long b0 = occ_end[j];
+      const unsigned long long b = b0 < pend ? b0 : pend;
+      const uint32_t cell = occ_cell[j];
+      for (unsigned long long q = a; q < b; ++q) out.put1(q, cell);
+    }
+    return;
+  }
   for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) {
     const unsigned long long e = occ_end[j0 + k] - p0;
     s_end[k] = static_cast<uint32_t>(e < (unsigned long long)kEmitTile ? e : kEmitTile);
@@ -470,23 +491,28 @@ __global__ void __launch_bounds__(kThreads) k_emit(const uint32_t* __restrict__ 
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    const uint32_t rel = warp * 512 + g * 128 + lane * 4;  // position - p0
-    const uint64_t base = p0 + rel;
-    if (base >= pend) break;
-    // first k with s_end[k] > rel
+  constexpr int kPerWarp = kEmitTile / (kThreads / 32);  // 1024
+  uint32_t k = 0;
+  {
+    const uint32_t rel = warp * kPerWarp + lane * 4;
     uint32_t lo = 0, hi = cnt;
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
       if (s_end[mid] > rel) hi = mid;
       else lo = mid + 1;
     }
+    k = lo < cnt ? lo : cnt - 1;
+  }
+#pragma unroll
+  for (int g = 0; g < kPerWarp / 128; ++g) {
+    const uint32_t rel = warp * kPerWarp + g * 128 + lane * 4;  // position - p0
+    const uint64_t base = p0 + rel;
+    if (base >= pend) break;
     uint32_t v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      while (lo + 1 < cnt && s_end[lo] <= rel + e) ++lo;
-      v[e] = s_cell[lo];
+      while (k + 1 < cnt && s_end[k] <= rel + e) ++k;
+      v[e] = s_cell[k];
     }
     out.put4(base, v, pend);
   }

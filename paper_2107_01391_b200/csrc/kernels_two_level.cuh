@@ -91,22 +91,34 @@ __global__ void __launch_bounds__(kTlThreads) k_outer_hist(const typename Map::I
   const uint64_t c1 = c0 + t.chunk < n ? c0 + t.chunk : n;
   unsigned long long mx = 0;
   unsigned flags = 0, ovf = 0;
+  // software pipeline: the next tile's four vectors are in flight while
+  // the current tile is counted
+  In cur[4][4], nxt[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Load4<In>::run(in, c0 + q * 1024 + threadIdx.x * 4, c1, aligned, cur[q]);
   for (uint64_t base = c0; base < c1; base += kTlTile) {
+    const uint64_t nb = base + kTlTile;
+    if (nb < c1) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Load4<In>::run(in, nb + q * 1024 + threadIdx.x * 4, c1, aligned, nxt[q]);
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint64_t i0 = base + q * 1024 + threadIdx.x * 4;
-      In v[4];
-      Load4<In>::run(in, i0, c1, aligned, v);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         if (i0 + e < c1) {
-          const unsigned long long k = map(v[e], flags);
+          const unsigned long long k = map(cur[q][e], flags);
           mx = k > mx ? k : mx;
           if (k < t.cells) atomicAdd(&s_h[tl_bucket(static_cast<uint32_t>(k), t)], 1u);
           else ovf = 1;
         }
       }
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cur[q][e] = nxt[q][e];
   }
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) cta_hist[(uint64_t)b * t.G + blockIdx.x] = s_h[b];
@@ -200,15 +212,22 @@ __global__ void __launch_bounds__(kTlThreads) k_outer_scatter(const typename Map
   const uint64_t c0 = (uint64_t)blockIdx.x * t.chunk;
   const uint64_t c1 = c0 + t.chunk < n ? c0 + t.chunk : n;
   const uint32_t per_thread_b = (t.B + kTlThreads - 1) / kTlThreads;
+  In cur[4][4], nxt[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Load4<In>::run(in, c0 + q * 1024 + threadIdx.x * 4, c1, aligned, cur[q]);
   for (uint64_t base = c0; base < c1; base += kTlTile) {
     for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) s_cnt[b] = 0;
     __syncthreads();
+    const uint64_t nb = base + kTlTile;
+    if (nb < c1) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Load4<In>::run(in, nb + q * 1024 + threadIdx.x * 4, c1, aligned, nxt[q]);
+    }
     uint32_t bk[16], lo[16], rk[16];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint64_t i0 = base + q * 1024 + threadIdx.x * 4;
-      In v[4];
-      Load4<In>::run(in, i0, c1, aligned, v);
+      In (&v)[4] = cur[q];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         bk[q * 4 + e] = 0xffffffffu;
@@ -282,6 +301,10 @@ __global__ void __launch_bounds__(kTlThreads) k_outer_scatter(const typename Map
       const uint32_t end = (b + 1 < t.B) ? s_cnt[b + 1] : staged;
       s_cur[b] += end - start;
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cur[q][e] = nxt[q][e];
     __syncthreads();
   }
 }
