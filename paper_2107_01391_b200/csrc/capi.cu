@@ -192,6 +192,28 @@ void exscan_u32(Workspace& ws, const uint32_t* in, uint64_t count, uint32_t* out
   RS_LAUNCH_CHECK();
 }
 
+// floor(x / d) == (x * magic) >> shift for every 32-bit x, with magic < 2^32
+// so the product is one 32x32->64 multiply (exact when the rounding excess
+// magic*d - 2^shift stays below 2^(shift-32)).
+bool div_magic32(uint64_t d, unsigned long long& magic, uint32_t& shift) {
+  if (d == 1) {
+    magic = 1;
+    shift = 0;
+    return true;
+  }
+  for (uint32_t L = 32; L < 64; ++L) {
+    const unsigned __int128 p = (unsigned __int128)1 << L;
+    const unsigned __int128 m = (p + d - 1) / d;
+    if (m >= ((unsigned __int128)1 << 32)) break;
+    if (m * d - p < ((unsigned __int128)1 << (L - 32))) {
+      magic = static_cast<unsigned long long>(m);
+      shift = L;
+      return true;
+    }
+  }
+  return false;
+}
+
 // Geometry of the two-level split: ~10^4 inner cells per outer bucket
 // (10^6 = 100 x 10^4).  Few outer buckets keep the partition's write runs
 // long (~40 keys per 4096-key tile); 10^4 inner counters (40 KB) still fit a
@@ -205,10 +227,9 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
   t.cells = cells;
   t.S = static_cast<uint32_t>(S);
   t.B = static_cast<uint32_t>((cells + S - 1) / S);
-  t.magic = ~0ull / S + 1ull;  // ceil(2^64 / S) for S not a power of two
-  if ((S & (S - 1)) == 0) t.magic = 1ull << (64 - __builtin_ctzll(S));
+  if (!div_magic32(S, t.magic, t.shift)) return false;
   const uint64_t tiles = (n + kTlTile - 1) / kTlTile;
-  uint64_t G = (uint64_t)sm_count() * 8;
+  uint64_t G = (uint64_t)sm_count() * 8;  // one wave: 8 CTAs of 256 threads per SM
   if (G > tiles) G = tiles ? tiles : 1;
   const uint64_t tiles_per = (tiles + G - 1) / G;
   t.chunk = tiles_per * kTlTile;
@@ -229,7 +250,8 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
   auto* total = ws.get<unsigned long long>(kSlotScratch, 4);
   {
     PassTimer pt_(RS_PASS_MSD_HIST, ws.stream);
-    k_outer_hist<Map><<<t.G, kTlThreads, 0, ws.stream>>>(in, n, map, t, al, cta_hist, ws.stats);
+    k_outer_hist<Map><<<t.G, kTlThreads, t.B * sizeof(uint32_t), ws.stream>>>(in, n, map, t, al, cta_hist,
+                                                                           ws.stats);
     RS_LAUNCH_CHECK();
   }
   exscan_u32(ws, cta_hist, bg, cta_off, total);
@@ -238,15 +260,13 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
     k_bucket_starts<<<(t.B + 1 + 255) / 256, 256, 0, ws.stream>>>(cta_off, t, total, bstart);
     RS_LAUNCH_CHECK();
   }
-  static bool attr = false;
-  if (!attr) {
+  const size_t smem = kOuterScatterSmem(t.B);
+  if (smem > 48 * 1024)
     RS_CUDA(cudaFuncSetAttribute(k_outer_scatter<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kOuterScatterSmem)));
-    attr = true;
-  }
+                                 static_cast<int>(smem)));
   {
     PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
-    k_outer_scatter<Map><<<t.G, kTlThreads, kOuterScatterSmem, ws.stream>>>(in, n, map, t, al, cta_off, lows);
+    k_outer_scatter<Map><<<t.G, kTlThreads, smem, ws.stream>>>(in, n, map, t, al, cta_off, lows);
     RS_LAUNCH_CHECK();
   }
   RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
@@ -394,8 +414,8 @@ unsigned long long magic_div(uint64_t d) { return ~0ull / d + 1ull; }  // ceil(2
 
 KvPass kv_pass(uint32_t g, uint32_t digits, uint64_t n) {
   KvPass p{};
-  p.magic_div = g ? magic_div(pow10u(3 * g)) : 0ull;
-  p.magic_1000 = magic_div(1000);
+  div_magic32(pow10u(3 * g), p.magic_div, p.shift_div);
+  div_magic32(1000, p.magic_1000, p.shift_1000);
   const uint32_t rem = digits - 3 * g;
   p.bins = rem >= 3 ? 1000u : static_cast<uint32_t>(pow10u(rem));
   const uint64_t tiles = (n + kKvTile - 1) / kKvTile;

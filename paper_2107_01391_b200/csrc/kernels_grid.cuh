@@ -508,11 +508,18 @@ __global__ void __launch_bounds__(kThreads) k_emit(const uint32_t* __restrict__ 
     const uint32_t rel = warp * kPerWarp + g * 128 + lane * 4;  // position - p0
     const uint64_t base = p0 + rel;
     if (base >= pend) break;
+    while (k + 1 < cnt && s_end[k] <= rel) ++k;
     uint32_t v[4];
+    const uint32_t c = s_cell[k];
+    if (s_end[k] >= rel + 4 || k + 1 == cnt) {  // the four positions share a cell
+      v[0] = v[1] = v[2] = v[3] = c;
+    } else {
+      uint32_t kk = k;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      while (k + 1 < cnt && s_end[k] <= rel + e) ++k;
-      v[e] = s_cell[k];
+      for (int e = 0; e < 4; ++e) {
+        while (kk + 1 < cnt && s_end[kk] <= rel + e) ++kk;
+        v[e] = s_cell[kk];
+      }
     }
     out.put4(base, v, pend);
   }

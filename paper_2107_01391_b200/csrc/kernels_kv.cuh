@@ -40,22 +40,18 @@ constexpr size_t kKvSmemBytes = kKvWarps * kKvBins * 2  // s_wh
                                 + kKvTile * 2            // s_dig
                                 + 64 * 4;
 
-// Exact floor(n / D) for 32-bit n with M = ceil(2^64 / D).
-__device__ __forceinline__ uint32_t div_magic(uint32_t n, unsigned long long m) {
-  return static_cast<uint32_t>(__umul64hi(static_cast<unsigned long long>(n), m));
-}
-
 struct KvPass {
-  unsigned long long magic_div;   // divides by 10^(3*pass) (0: identity)
-  unsigned long long magic_1000;  // divides by 1000
+  unsigned long long magic_div;   // floor(k / 10^(3*pass)) = (k * magic_div) >> shift_div
+  unsigned long long magic_1000;  // floor(q / 1000) = (q * magic_1000) >> shift_1000
+  uint32_t shift_div, shift_1000;
   uint32_t bins;                  // 1000, or 10^(remaining digits) on the top pass
   uint64_t chunk;                 // records per CTA (multiple of kKvTile)
   uint32_t G;                     // CTAs
 };
 
 __device__ __forceinline__ uint32_t kv_digit(uint32_t key, const KvPass& p) {
-  const uint32_t q = p.magic_div ? div_magic(key, p.magic_div) : key;
-  return q - 1000u * div_magic(q, p.magic_1000);
+  const uint32_t q = static_cast<uint32_t>((static_cast<unsigned long long>(key) * p.magic_div) >> p.shift_div);
+  return q - 1000u * static_cast<uint32_t>((static_cast<unsigned long long>(q) * p.magic_1000) >> p.shift_1000);
 }
 
 __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __restrict__ keys, uint64_t n,

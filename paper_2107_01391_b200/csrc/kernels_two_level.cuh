@@ -39,13 +39,14 @@ struct TwoLevel {
   unsigned long long cells;  // grid size C
   uint32_t S;                // inner cells per bucket
   uint32_t B;                // outer buckets = ceil(C / S)
-  unsigned long long magic;  // ceil(2^64 / S): bucket = umulhi(cell, magic) (cell < 2^32)
+  unsigned long long magic;  // bucket = (cell * magic) >> shift, exact for cell < 2^32
+  uint32_t shift;
   uint64_t chunk;            // keys per CTA (multiple of kTlTile)
   uint32_t G;                // CTAs in K1a / K1b
 };
 
 __device__ __forceinline__ uint32_t tl_bucket(uint32_t cell, const TwoLevel& t) {
-  return static_cast<uint32_t>(__umul64hi(static_cast<unsigned long long>(cell), t.magic));
+  return static_cast<uint32_t>((static_cast<unsigned long long>(cell) * t.magic) >> t.shift);
 }
 
 // Loads element i of a tile: thread t owns elements 4t..4t+3 of each
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(kTlThreads) k_outer_hist(const typename Map::I
                                                            uint32_t* __restrict__ cta_hist,  // [B][G]
                                                            DevStats* st) {
   using In = typename Map::In;
-  __shared__ uint32_t s_h[kTlMaxBuckets];
+  extern __shared__ uint32_t s_h[];  // [B]
   for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) s_h[b] = 0;
   __syncthreads();
   const uint64_t c0 = (uint64_t)blockIdx.x * t.chunk;
@@ -189,10 +190,13 @@ __global__ void __launch_bounds__(kThreads) k_exscan_u32(const uint32_t* __restr
 }
 
 // ------------------------------------------------------------ K1b
-// Shared layout: s_cur[B] running global cursor of this CTA per bucket,
-// s_cnt[B] tile counts -> tile-local starts, staging of inner digits and
-// bucket ids in bucket order.
-constexpr size_t kOuterScatterSmem = kTlMaxBuckets * 4 * 2 + kTlTile * 2 * 2 + 64 * 4;
+// Dynamic shared layout (kOuterScatterSmem(B)): s_cur[B] running global
+// cursor of this CTA per bucket, s_cnt[B+1] tile counts -> tile-local starts,
+// s_low[kTlTile] inner digits staged in bucket order.  After staging, each
+// warp copies whole bucket runs, lanes on consecutive elements.
+__host__ __device__ constexpr size_t kOuterScatterSmem(uint32_t B) {
+  return ((size_t)B * 4 * 2 + 16 + kTlTile * 2 + 15) & ~size_t(15);
+}
 
 template <class Map>
 __global__ void __launch_bounds__(kTlThreads) k_outer_scatter(const typename Map::In* __restrict__ in, uint64_t n,
@@ -202,11 +206,9 @@ __global__ void __launch_bounds__(kTlThreads) k_outer_scatter(const typename Map
   using In = typename Map::In;
   extern __shared__ __align__(16) unsigned char tl_smem[];
   uint32_t* s_cur = reinterpret_cast<uint32_t*>(tl_smem);
-  uint32_t* s_cnt = s_cur + kTlMaxBuckets;
-  uint16_t* s_low = reinterpret_cast<uint16_t*>(s_cnt + kTlMaxBuckets);
-  uint16_t* s_bkt = s_low + kTlTile;
-  uint32_t* s_scan = reinterpret_cast<uint32_t*>(s_bkt + kTlTile);
-  __shared__ uint32_t s_staged;
+  uint32_t* s_cnt = s_cur + t.B;  // [B+1]
+  uint16_t* s_low = reinterpret_cast<uint16_t*>(tl_smem + (((size_t)t.B * 8 + 16 + 15) & ~size_t(15)));
+  __shared__ uint32_t s_scan[kTlThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) s_cur[b] = cta_off[(uint64_t)b * t.G + blockIdx.x];
   const uint64_t c0 = (uint64_t)blockIdx.x * t.chunk;
@@ -216,7 +218,7 @@ __global__ void __launch_bounds__(kTlThreads) k_outer_scatter(const typename Map
 #pragma unroll
   for (int q = 0; q < 4; ++q) Load4<In>::run(in, c0 + q * 1024 + threadIdx.x * 4, c1, aligned, cur[q]);
   for (uint64_t base = c0; base < c1; base += kTlTile) {
-    for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) s_cnt[b] = 0;
+    for (uint32_t b = threadIdx.x; b <= t.B; b += blockDim.x) s_cnt[b] = 0;
     __syncthreads();
     const uint64_t nb = base + kTlTile;
     if (nb < c1) {
@@ -227,13 +229,12 @@ __global__ void __launch_bounds__(kTlThreads) k_outer_scatter(const typename Map
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint64_t i0 = base + q * 1024 + threadIdx.x * 4;
-      In (&v)[4] = cur[q];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         bk[q * 4 + e] = 0xffffffffu;
         if (i0 + e < c1) {
           unsigned flags = 0;
-          const unsigned long long k = map(v[e], flags);
+          const unsigned long long k = map(cur[q][e], flags);
           if (k < t.cells) {
             const uint32_t b = tl_bucket(static_cast<uint32_t>(k), t);
             bk[q * 4 + e] = b;
@@ -244,7 +245,8 @@ __global__ void __launch_bounds__(kTlThreads) k_outer_scatter(const typename Map
       }
     }
     __syncthreads();
-    // exclusive scan of s_cnt over buckets (per_thread_b consecutive per thread)
+    // exclusive scan of s_cnt over buckets (per_thread_b consecutive per
+    // thread); s_cnt[B] becomes the number of staged keys
     {
       uint32_t sum = 0;
       const uint32_t b0 = threadIdx.x * per_thread_b;
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(kTlThreads) k_outer_scatter(const typename Map
           s_scan[w] = r;
           r += c;
         }
-        s_staged = r;
+        s_cnt[t.B] = r;
       }
       __syncthreads();
       uint32_t run = s_scan[warp] + inc - sum;
@@ -279,28 +281,18 @@ __global__ void __launch_bounds__(kTlThreads) k_outer_scatter(const typename Map
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (bk[j] != 0xffffffffu) {
-        const uint32_t pos = s_cnt[bk[j]] + rk[j];
-        s_low[pos] = static_cast<uint16_t>(lo[j]);
-        s_bkt[pos] = static_cast<uint16_t>(bk[j]);
-      }
-    }
+    for (int j = 0; j < 16; ++j)
+      if (bk[j] != 0xffffffffu) s_low[s_cnt[bk[j]] + rk[j]] = static_cast<uint16_t>(lo[j]);
     __syncthreads();
     // keys outside the grid were never staged (K1a flagged the overflow and
-    // the sort is redone with the derived width)
-    const uint32_t staged = s_staged;
-    for (uint32_t i = threadIdx.x; i < staged; i += blockDim.x) {
-      const uint32_t b = s_bkt[i];
-      lows[s_cur[b] + (i - s_cnt[b])] = s_low[i];
+    // the sort is redone with the derived width).  One warp per bucket run.
+    for (uint32_t b = warp; b < t.B; b += kTlThreads / 32) {
+      const uint32_t s = s_cnt[b], e = s_cnt[b + 1];
+      uint16_t* dst = lows + s_cur[b] - s;
+      for (uint32_t i = s + lane; i < e; i += 32) dst[i] = s_low[i];
     }
     __syncthreads();
-    // advance the per-bucket cursors by this tile's counts
-    for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) {
-      const uint32_t start = s_cnt[b];
-      const uint32_t end = (b + 1 < t.B) ? s_cnt[b + 1] : staged;
-      s_cur[b] += end - start;
-    }
+    for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) s_cur[b] += s_cnt[b + 1] - s_cnt[b];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
