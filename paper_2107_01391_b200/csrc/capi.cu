@@ -215,11 +215,11 @@ bool div_magic32(uint64_t d, unsigned long long& magic, uint32_t& shift) {
 }
 
 // Geometry of the two-level split: ~10^4 inner cells per outer bucket
-// (10^6 = 100 x 10^4).  Few outer buckets keep the partition's write runs
-// long (~40 keys per 4096-key tile); 10^4 inner counters (40 KB) still fit a
+// (10^6 = 100 x 10^4).  Few outer buckets keep each tile's bucket runs long
+// (~80 keys per 8192-key tile); 10^4 inner counters (40 KB) still fit a
 // shared histogram.  At most kTlMaxBuckets buckets.
 bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
-  if (cells <= kSmemCellsMax || cells > 0xFFFFFFFFull) return false;
+  if (cells <= kSmemCellsMax || cells > 0xFFFFFFFFull || n >= 0xFFFFFFFFull) return false;
   uint64_t B = (cells + 9999) / 10000;
   if (B > kTlMaxBuckets) B = kTlMaxBuckets;
   const uint64_t S = (cells + B - 1) / B;
@@ -228,13 +228,9 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
   t.S = static_cast<uint32_t>(S);
   t.B = static_cast<uint32_t>((cells + S - 1) / S);
   if (!div_magic32(S, t.magic, t.shift)) return false;
-  const uint64_t tiles = (n + kTlTile - 1) / kTlTile;
-  uint64_t G = (uint64_t)sm_count() * 8;  // one wave: 8 CTAs of 256 threads per SM
-  if (G > tiles) G = tiles ? tiles : 1;
-  const uint64_t tiles_per = (tiles + G - 1) / G;
-  t.chunk = tiles_per * kTlTile;
-  t.G = static_cast<uint32_t>((n + t.chunk - 1) / t.chunk);
-  if (t.G == 0) t.G = 1;
+  t.T = static_cast<uint32_t>((n + kTlTile - 1) / kTlTile);
+  // groups of >= 16*S keys keep the per-group flush of S counters small
+  t.target = std::max<uint64_t>(16ull * S, 131072);
   return true;
 }
 
@@ -242,40 +238,35 @@ template <class Map>
 void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, const TwoLevel& t,
                      uint32_t* counts) {
   const bool al = aligned16(in);
-  const uint64_t bg = (uint64_t)t.B * t.G;
-  auto* cta_hist = ws.get<uint32_t>(kSlotCtaHist, bg);
-  auto* cta_off = ws.get<uint32_t>(kSlotCtaOff, bg);
-  auto* bstart = ws.get<uint32_t>(kSlotBucketStart, t.B + 1ull);
-  auto* lows = ws.get<uint16_t>(kSlotLows, n + 8);
+  const uint64_t bt = (uint64_t)t.B * t.T;
+  auto* cnt_bm = ws.get<uint32_t>(kSlotCtaHist, bt);
+  auto* off_bm = ws.get<uint32_t>(kSlotCtaOff, bt);
+  auto* start_tm = ws.get<uint16_t>(kSlotBucketStart, bt);
+  auto* lows = ws.get<uint16_t>(kSlotLows, (uint64_t)t.T * kTlTile);
   auto* total = ws.get<unsigned long long>(kSlotScratch, 4);
-  {
-    PassTimer pt_(RS_PASS_MSD_HIST, ws.stream);
-    k_outer_hist<Map><<<t.G, kTlThreads, t.B * sizeof(uint32_t), ws.stream>>>(in, n, map, t, al, cta_hist,
-                                                                           ws.stats);
-    RS_LAUNCH_CHECK();
-  }
-  exscan_u32(ws, cta_hist, bg, cta_off, total);
-  {
-    PassTimer pt_(RS_PASS_SCAN, ws.stream);
-    k_bucket_starts<<<(t.B + 1 + 255) / 256, 256, 0, ws.stream>>>(cta_off, t, total, bstart);
-    RS_LAUNCH_CHECK();
-  }
-  const size_t smem = kOuterScatterSmem(t.B);
+  auto* work = ws.get<uint32_t>(kSlotMisc, t.B + 1ull);
+  const size_t smem = kTilePartitionSmem(t.B);
   if (smem > 48 * 1024)
-    RS_CUDA(cudaFuncSetAttribute(k_outer_scatter<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RS_CUDA(cudaFuncSetAttribute(k_tile_partition<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   {
     PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
-    k_outer_scatter<Map><<<t.G, kTlThreads, smem, ws.stream>>>(in, n, map, t, al, cta_off, lows);
+    k_tile_partition<Map><<<t.T, kTlThreads, smem, ws.stream>>>(in, n, map, t, al, lows, cnt_bm, start_tm,
+                                                                ws.stats);
+    RS_LAUNCH_CHECK();
+  }
+  exscan_u32(ws, cnt_bm, bt, off_bm, total);
+  {
+    PassTimer pt_(RS_PASS_SCAN, ws.stream);
+    k_work_list<<<1, 1024, 0, ws.stream>>>(off_bm, total, t, work);
     RS_LAUNCH_CHECK();
   }
   RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
-  const uint64_t slice = std::max<uint64_t>(65536, 16ull * t.S);
-  const uint64_t nslices = (n + slice - 1) / slice;
+  const uint64_t max_groups = n / t.target + t.B + 1;
   {
     PassTimer pt_(RS_PASS_COUNT, ws.stream);
-    k_inner_count<<<static_cast<unsigned>(nslices), kTlThreads, t.S * sizeof(uint32_t), ws.stream>>>(
-        lows, n, bstart, t, slice, counts);
+    k_inner_gather<<<static_cast<unsigned>(max_groups), kGatherThreads, t.S * sizeof(uint32_t), ws.stream>>>(
+        lows, off_bm, cnt_bm, start_tm, work, total, t, counts);
     RS_LAUNCH_CHECK();
   }
 }
@@ -414,7 +405,10 @@ unsigned long long magic_div(uint64_t d) { return ~0ull / d + 1ull; }  // ceil(2
 
 KvPass kv_pass(uint32_t g, uint32_t digits, uint64_t n) {
   KvPass p{};
-  div_magic32(pow10u(3 * g), p.magic_div, p.shift_div);
+  if (!div_magic32(pow10u(3 * g), p.magic_div, p.shift_div)) {  // 10^9: 64-bit high product
+    p.magic_div = magic_div(pow10u(3 * g));
+    p.shift_div = 64;
+  }
   div_magic32(1000, p.magic_1000, p.shift_1000);
   const uint32_t rem = digits - 3 * g;
   p.bins = rem >= 3 ? 1000u : static_cast<uint32_t>(pow10u(rem));

@@ -50,7 +50,9 @@ struct KvPass {
 };
 
 __device__ __forceinline__ uint32_t kv_digit(uint32_t key, const KvPass& p) {
-  const uint32_t q = static_cast<uint32_t>((static_cast<unsigned long long>(key) * p.magic_div) >> p.shift_div);
+  const uint32_t q = p.shift_div == 64
+                         ? static_cast<uint32_t>(__umul64hi(static_cast<unsigned long long>(key), p.magic_div))
+                         : static_cast<uint32_t>((static_cast<unsigned long long>(key) * p.magic_div) >> p.shift_div);
   return q - 1000u * static_cast<uint32_t>((static_cast<unsigned long long>(q) * p.magic_1000) >> p.shift_1000);
 }
 

@@ -8,17 +8,20 @@
 // digits pick one of B outer buckets and the trailing digits one of S inner
 // cells (10^6 = 1000 x 1000):
 //
-//   K1a outer_hist     per-CTA shared histogram of the outer digit over a
-//                      contiguous chunk of keys (+ max / flags)        R4
-//   scan               exclusive scan of the [B][G] per-CTA counts (look-back)
-//   K1b outer_scatter  re-read the chunk, stage each tile in shared memory in
-//                      bucket order, write the inner digit as uint16
-//                      into bucket-contiguous order                     R4 + W2
-//   K2  inner_count    slices of the partitioned inner digits, shared
-//                      histogram over S cells, one flush per slice into
-//                      the dense count grid                             R2
+//   K1 tile_partition  one CTA per 8192-key tile: map each key to its cell,
+//                      counting-sort the tile by outer bucket in shared
+//                      memory and write the inner digits (uint16) back to
+//                      the tile's own slot, fully coalesced; per-(bucket,
+//                      tile) counts and in-tile starts go to two small
+//                      tables; max / flags / overflow fused               R4 + W2
+//   scan               exclusive scan of the bucket-major [B][T] counts
+//   work list          each bucket cut into groups of ~target keys
+//   K2 inner_gather    one CTA per group: gathers the bucket's runs (~80
+//                      keys each) from consecutive tiles, shared histogram
+//                      over the S inner cells, one flush into the dense
+//                      count grid                                        R2
 // after which the occupancy scan and the load-balanced emit run unchanged.
-// The outer partition is unordered within a bucket: only counts matter.
+// No histogram pre-pass is needed: each tile sorts only itself.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -30,10 +33,12 @@
 
 namespace rsb {
 
-constexpr int kTlThreads = 256;
-constexpr int kTlTile = 4096;               // keys per tile (16 per thread)
-constexpr uint32_t kTlMaxBuckets = 4096;    // outer buckets (smem hist <= 16 KB)
-constexpr uint32_t kTlMaxInner = 16384;     // inner cells (smem hist <= 64 KB)
+constexpr int kTlThreads = 512;
+constexpr int kTlPerThread = 16;
+constexpr int kTlTile = kTlThreads * kTlPerThread;  // 8192 keys per tile
+constexpr uint32_t kTlMaxBuckets = 4096;            // outer buckets
+constexpr uint32_t kTlMaxInner = 16384;             // inner cells (smem hist <= 64 KB)
+constexpr int kGatherThreads = 256;
 
 struct TwoLevel {
   unsigned long long cells;  // grid size C
@@ -41,22 +46,21 @@ struct TwoLevel {
   uint32_t B;                // outer buckets = ceil(C / S)
   unsigned long long magic;  // bucket = (cell * magic) >> shift, exact for cell < 2^32
   uint32_t shift;
-  uint64_t chunk;            // keys per CTA (multiple of kTlTile)
-  uint32_t G;                // CTAs in K1a / K1b
+  uint32_t T;                // tiles = ceil(n / kTlTile)
+  uint64_t target;           // keys per K2 group
 };
 
 __device__ __forceinline__ uint32_t tl_bucket(uint32_t cell, const TwoLevel& t) {
   return static_cast<uint32_t>((static_cast<unsigned long long>(cell) * t.magic) >> t.shift);
 }
 
-// Loads element i of a tile: thread t owns elements 4t..4t+3 of each
-// 1024-element quarter (16-byte vectors when the input is aligned).
 __device__ __forceinline__ uint32_t from_bits32(uint32_t w, uint32_t*) { return w; }
 __device__ __forceinline__ int32_t from_bits32(uint32_t w, int32_t*) { return static_cast<int32_t>(w); }
 __device__ __forceinline__ double from_bits64(unsigned long long w, double*) { return __longlong_as_double(static_cast<long long>(w)); }
 __device__ __forceinline__ unsigned long long from_bits64(unsigned long long w, unsigned long long*) { return w; }
 __device__ __forceinline__ int64_t from_bits64(unsigned long long w, int64_t*) { return static_cast<int64_t>(w); }
 
+// Elements i0..i0+3 (16-byte vector loads when the input is aligned).
 template <class In>
 struct Load4 {
   __device__ __forceinline__ static void run(const In* p, uint64_t i0, uint64_t n, bool aligned, In (&v)[4]) {
@@ -77,59 +81,6 @@ struct Load4 {
     }
   }
 };
-
-// ------------------------------------------------------------ K1a
-template <class Map>
-__global__ void __launch_bounds__(kTlThreads) k_outer_hist(const typename Map::In* __restrict__ in, uint64_t n,
-                                                           Map map, TwoLevel t, bool aligned,
-                                                           uint32_t* __restrict__ cta_hist,  // [B][G]
-                                                           DevStats* st) {
-  using In = typename Map::In;
-  extern __shared__ uint32_t s_h[];  // [B]
-  for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) s_h[b] = 0;
-  __syncthreads();
-  const uint64_t c0 = (uint64_t)blockIdx.x * t.chunk;
-  const uint64_t c1 = c0 + t.chunk < n ? c0 + t.chunk : n;
-  unsigned long long mx = 0;
-  unsigned flags = 0, ovf = 0;
-  // software pipeline: the next tile's four vectors are in flight while
-  // the current tile is counted
-  In cur[4][4], nxt[4][4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) Load4<In>::run(in, c0 + q * 1024 + threadIdx.x * 4, c1, aligned, cur[q]);
-  for (uint64_t base = c0; base < c1; base += kTlTile) {
-    const uint64_t nb = base + kTlTile;
-    if (nb < c1) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) Load4<In>::run(in, nb + q * 1024 + threadIdx.x * 4, c1, aligned, nxt[q]);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint64_t i0 = base + q * 1024 + threadIdx.x * 4;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (i0 + e < c1) {
-          const unsigned long long k = map(cur[q][e], flags);
-          mx = k > mx ? k : mx;
-          if (k < t.cells) atomicAdd(&s_h[tl_bucket(static_cast<uint32_t>(k), t)], 1u);
-          else ovf = 1;
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) cur[q][e] = nxt[q][e];
-  }
-  __syncthreads();
-  for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) cta_hist[(uint64_t)b * t.G + blockIdx.x] = s_h[b];
-  warp_max_to(mx, &st->max_key);
-  flags = warp_or(flags | (ovf ? 0x80000000u : 0u));
-  if ((threadIdx.x & 31) == 0 && flags) {
-    if (flags & 0x7fffffffu) atomicOr(&st->flags, flags & 0x7fffffffu);
-    if (flags & 0x80000000u) atomicOr(&st->overflow, 1u);
-  }
-}
 
 // ---------------------------------------- exclusive scan (look-back), u32
 // out[i] = sum(in[0..i)); also writes the grand total to *total.  Tiles of
@@ -189,179 +140,226 @@ __global__ void __launch_bounds__(kThreads) k_exscan_u32(const uint32_t* __restr
   }
 }
 
-// ------------------------------------------------------------ K1b
-// Dynamic shared layout (kOuterScatterSmem(B)): s_cur[B] running global
-// cursor of this CTA per bucket, s_cnt[B+1] tile counts -> tile-local starts,
-// s_low[kTlTile] inner digits staged in bucket order.  After staging, each
-// warp copies whole bucket runs, lanes on consecutive elements.
-__host__ __device__ constexpr size_t kOuterScatterSmem(uint32_t B) {
-  return ((size_t)B * 4 * 2 + 16 + kTlTile * 2 + 15) & ~size_t(15);
+// ------------------------------------------------------------- K1
+// Shared layout (kTilePartitionSmem(B)): s_cnt[B+1] counts -> starts,
+// s_low[kTlTile] inner digits in bucket order.
+__host__ __device__ constexpr size_t kTilePartitionSmem(uint32_t B) {
+  return (((size_t)B + 1) * 4 + 15) / 16 * 16 + (size_t)kTlTile * 2;
 }
 
 template <class Map>
-__global__ void __launch_bounds__(kTlThreads) k_outer_scatter(const typename Map::In* __restrict__ in, uint64_t n,
-                                                              Map map, TwoLevel t, bool aligned,
-                                                              const uint32_t* __restrict__ cta_off,  // [B][G]
-                                                              uint16_t* __restrict__ lows) {
+__global__ void __launch_bounds__(kTlThreads) k_tile_partition(const typename Map::In* __restrict__ in, uint64_t n,
+                                                               Map map, TwoLevel t, bool aligned,
+                                                               uint16_t* __restrict__ lows,       // [T][kTlTile]
+                                                               uint32_t* __restrict__ cnt_bm,     // [B][T]
+                                                               uint16_t* __restrict__ start_tm,   // [T][B]
+                                                               DevStats* st) {
   using In = typename Map::In;
   extern __shared__ __align__(16) unsigned char tl_smem[];
-  uint32_t* s_cur = reinterpret_cast<uint32_t*>(tl_smem);
-  uint32_t* s_cnt = s_cur + t.B;  // [B+1]
-  uint16_t* s_low = reinterpret_cast<uint16_t*>(tl_smem + (((size_t)t.B * 8 + 16 + 15) & ~size_t(15)));
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(tl_smem);
+  uint16_t* s_low = reinterpret_cast<uint16_t*>(tl_smem + (((size_t)t.B + 1) * 4 + 15) / 16 * 16);
   __shared__ uint32_t s_scan[kTlThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) s_cur[b] = cta_off[(uint64_t)b * t.G + blockIdx.x];
-  const uint64_t c0 = (uint64_t)blockIdx.x * t.chunk;
-  const uint64_t c1 = c0 + t.chunk < n ? c0 + t.chunk : n;
-  const uint32_t per_thread_b = (t.B + kTlThreads - 1) / kTlThreads;
-  In cur[4][4], nxt[4][4];
+  const uint32_t tile = blockIdx.x;
+  const uint64_t base = (uint64_t)tile * kTlTile;
+  const uint64_t end = base + kTlTile < n ? base + kTlTile : n;
+  for (uint32_t b = threadIdx.x; b <= t.B; b += blockDim.x) s_cnt[b] = 0;
+  __syncthreads();
+  unsigned long long mx = 0;
+  unsigned flags = 0, ovf = 0;
+  uint32_t pk[kTlPerThread];  // bucket << 16 | rank   (0xffffffff = not counted)
+  uint16_t lo[kTlPerThread];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) Load4<In>::run(in, c0 + q * 1024 + threadIdx.x * 4, c1, aligned, cur[q]);
-  for (uint64_t base = c0; base < c1; base += kTlTile) {
-    for (uint32_t b = threadIdx.x; b <= t.B; b += blockDim.x) s_cnt[b] = 0;
-    __syncthreads();
-    const uint64_t nb = base + kTlTile;
-    if (nb < c1) {
+  for (int q = 0; q < kTlPerThread / 4; ++q) {
+    const uint64_t i0 = base + q * (kTlThreads * 4) + threadIdx.x * 4;
+    In v[4];
+    Load4<In>::run(in, i0, end, aligned, v);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) Load4<In>::run(in, nb + q * 1024 + threadIdx.x * 4, c1, aligned, nxt[q]);
-    }
-    uint32_t bk[16], lo[16], rk[16];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint64_t i0 = base + q * 1024 + threadIdx.x * 4;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        bk[q * 4 + e] = 0xffffffffu;
-        if (i0 + e < c1) {
-          unsigned flags = 0;
-          const unsigned long long k = map(cur[q][e], flags);
-          if (k < t.cells) {
-            const uint32_t b = tl_bucket(static_cast<uint32_t>(k), t);
-            bk[q * 4 + e] = b;
-            lo[q * 4 + e] = static_cast<uint32_t>(k) - b * t.S;
-            rk[q * 4 + e] = atomicAdd(&s_cnt[b], 1u);
-          }
+    for (int e = 0; e < 4; ++e) {
+      pk[q * 4 + e] = 0xffffffffu;
+      lo[q * 4 + e] = 0;
+      if (i0 + e < end) {
+        const unsigned long long k = map(v[e], flags);
+        mx = k > mx ? k : mx;
+        if (k < t.cells) {
+          const uint32_t b = tl_bucket(static_cast<uint32_t>(k), t);
+          lo[q * 4 + e] = static_cast<uint16_t>(static_cast<uint32_t>(k) - b * t.S);
+          pk[q * 4 + e] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
+        } else {
+          ovf = 1;
         }
       }
     }
-    __syncthreads();
-    // exclusive scan of s_cnt over buckets (per_thread_b consecutive per
-    // thread); s_cnt[B] becomes the number of staged keys
-    {
-      uint32_t sum = 0;
-      const uint32_t b0 = threadIdx.x * per_thread_b;
-      for (uint32_t j = 0; j < per_thread_b; ++j)
-        if (b0 + j < t.B) sum += s_cnt[b0 + j];
-      uint32_t inc = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      if (lane == 31) s_scan[warp] = inc;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t r = 0;
-        for (int w = 0; w < kTlThreads / 32; ++w) {
-          const uint32_t c = s_scan[w];
-          s_scan[w] = r;
-          r += c;
-        }
-        s_cnt[t.B] = r;
-      }
-      __syncthreads();
-      uint32_t run = s_scan[warp] + inc - sum;
-      for (uint32_t j = 0; j < per_thread_b; ++j) {
-        if (b0 + j < t.B) {
-          const uint32_t c = s_cnt[b0 + j];
-          s_cnt[b0 + j] = run;  // tile-local start of bucket
-          run += c;
-        }
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (bk[j] != 0xffffffffu) s_low[s_cnt[bk[j]] + rk[j]] = static_cast<uint16_t>(lo[j]);
-    __syncthreads();
-    // keys outside the grid were never staged (K1a flagged the overflow and
-    // the sort is redone with the derived width).  One warp per bucket run.
-    for (uint32_t b = warp; b < t.B; b += kTlThreads / 32) {
-      const uint32_t s = s_cnt[b], e = s_cnt[b + 1];
-      uint16_t* dst = lows + s_cur[b] - s;
-      for (uint32_t i = s + lane; i < e; i += 32) dst[i] = s_low[i];
-    }
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) s_cur[b] += s_cnt[b + 1] - s_cnt[b];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) cur[q][e] = nxt[q][e];
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------- K2
-// Slice j of the partitioned inner digits covers [j*L, (j+1)*L).  Buckets
-// overlapping it are walked in order; each gets a shared histogram over its
-// S cells, flushed once into counts[b*S + c].
-__global__ void __launch_bounds__(kTlThreads) k_inner_count(const uint16_t* __restrict__ lows, uint64_t n,
-                                                            const uint32_t* __restrict__ bucket_start,  // [B+1]
-                                                            TwoLevel t, uint64_t slice,
-                                                            uint32_t* __restrict__ counts) {
-  extern __shared__ uint32_t s_c[];  // [S]
-  __shared__ uint32_t s_b0;
-  const uint64_t p0 = (uint64_t)blockIdx.x * slice;
-  const uint64_t p1 = p0 + slice < n ? p0 + slice : n;
-  if (threadIdx.x == 0) {  // last bucket whose start <= p0
-    uint32_t lo = 0, hi = t.B;
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (bucket_start[mid] <= p0) lo = mid;
-      else hi = mid;
-    }
-    s_b0 = lo;
   }
   __syncthreads();
-  for (uint32_t b = s_b0; b < t.B && bucket_start[b] < p1; ++b) {
-    const uint64_t a = bucket_start[b] > p0 ? bucket_start[b] : p0;
-    const uint64_t e = bucket_start[b + 1] < p1 ? bucket_start[b + 1] : p1;
-    if (a >= e) continue;
-    for (uint32_t c = threadIdx.x; c < t.S; c += blockDim.x) s_c[c] = 0;
-    __syncthreads();
-    // 8 inner digits (16 bytes) per thread per step where aligned
-    uint64_t i = a + threadIdx.x;
-    const uint64_t a8 = (a + 7) & ~7ull;
-    if (a8 < e) {
-      for (uint64_t h = a + threadIdx.x; h < a8; h += blockDim.x) atomicAdd(&s_c[lows[h]], 1u);
-      const uint64_t nv = (e - a8) / 8;
-      const uint4* v = reinterpret_cast<const uint4*>(lows + a8);
-      for (uint64_t q = threadIdx.x; q < nv; q += blockDim.x) {
-        const uint4 w = __ldcs(v + q);
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          atomicAdd(&s_c[ws[k] & 0xffffu], 1u);
-          atomicAdd(&s_c[ws[k] >> 16], 1u);
-        }
-      }
-      i = a8 + nv * 8 + threadIdx.x;
+  // counts out (bucket-major for the scan), then exclusive scan in place
+  const uint32_t per = (t.B + kTlThreads - 1) / kTlThreads;
+  const uint32_t b0 = threadIdx.x * per;
+  uint32_t sum = 0;
+  for (uint32_t j = 0; j < per; ++j) {
+    const uint32_t b = b0 + j;
+    if (b < t.B) {
+      const uint32_t c = s_cnt[b];
+      cnt_bm[(uint64_t)b * t.T + tile] = c;
+      sum += c;
     }
-    for (; i < e; i += blockDim.x) atomicAdd(&s_c[lows[i]], 1u);
-    __syncthreads();
-    const unsigned long long cb = (unsigned long long)b * t.S;
-    for (uint32_t c = threadIdx.x; c < t.S; c += blockDim.x)
-      if (s_c[c] && cb + c < t.cells) atomicAdd(&counts[cb + c], s_c[c]);
-    __syncthreads();
+  }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_scan[warp] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t r = 0;
+    for (int w = 0; w < kTlThreads / 32; ++w) {
+      const uint32_t c = s_scan[w];
+      s_scan[w] = r;
+      r += c;
+    }
+  }
+  __syncthreads();
+  uint32_t run = s_scan[warp] + inc - sum;
+  for (uint32_t j = 0; j < per; ++j) {
+    const uint32_t b = b0 + j;
+    if (b < t.B) {
+      const uint32_t c = s_cnt[b];
+      s_cnt[b] = run;
+      start_tm[(uint64_t)tile * t.B + b] = static_cast<uint16_t>(run);
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kTlPerThread; ++j)
+    if (pk[j] != 0xffffffffu) s_low[s_cnt[pk[j] >> 16] + (pk[j] & 0xffffu)] = lo[j];
+  __syncthreads();
+  // the whole tile slot, 16-byte stores (entries past the counted keys are
+  // never read: K2 reads exactly each bucket's run)
+  uint4* dst = reinterpret_cast<uint4*>(lows + base);
+  const uint4* src = reinterpret_cast<const uint4*>(s_low);
+  for (uint32_t i = threadIdx.x; i < kTlTile / 8; i += blockDim.x) __stcs(dst + i, src[i]);
+  warp_max_to(mx, &st->max_key);
+  flags = warp_or(flags | (ovf ? 0x80000000u : 0u));
+  if ((threadIdx.x & 31) == 0 && flags) {
+    if (flags & 0x7fffffffu) atomicOr(&st->flags, flags & 0x7fffffffu);
+    if (flags & 0x80000000u) atomicOr(&st->overflow, 1u);
   }
 }
 
-// bucket_start[b] = cta_off[b*G] (first CTA's offset), bucket_start[B] = total.
-__global__ void k_bucket_starts(const uint32_t* __restrict__ cta_off, TwoLevel t,
-                                const unsigned long long* total, uint32_t* __restrict__ bucket_start) {
-  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b < t.B) bucket_start[b] = cta_off[(uint64_t)b * t.G];
-  if (b == t.B) bucket_start[b] = static_cast<uint32_t>(*total);
+// ------------------------------------------------------ K2 work list
+// groups[b] = ceil(total_b / target); work_start = exclusive scan (one CTA,
+// B <= 4096).  off_bm is the exclusive scan of cnt_bm, so bucket b's keys
+// are [off_bm[b*T], off_bm[(b+1)*T]) in bucket-major order.
+__global__ void k_work_list(const uint32_t* __restrict__ off_bm, const unsigned long long* total, TwoLevel t,
+                            uint32_t* __restrict__ work_start) {
+  __shared__ uint32_t s_w[1024];
+  const uint32_t per = (t.B + blockDim.x - 1) / blockDim.x;
+  uint32_t g[8];
+  uint32_t sum = 0;
+  for (uint32_t j = 0; j < per && j < 8; ++j) {
+    const uint32_t b = threadIdx.x * per + j;
+    g[j] = 0;
+    if (b < t.B) {
+      const unsigned long long lo = off_bm[(uint64_t)b * t.T];
+      const unsigned long long hi = (b + 1 < t.B) ? off_bm[(uint64_t)(b + 1) * t.T] : *total;
+      g[j] = static_cast<uint32_t>((hi - lo + t.target - 1) / t.target);
+    }
+    sum += g[j];
+  }
+  s_w[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t r = 0;
+    for (uint32_t i = 0; i < blockDim.x; ++i) {
+      const uint32_t c = s_w[i];
+      s_w[i] = r;
+      r += c;
+    }
+    work_start[t.B] = r;
+  }
+  __syncthreads();
+  uint32_t run = s_w[threadIdx.x];
+  for (uint32_t j = 0; j < per && j < 8; ++j) {
+    const uint32_t b = threadIdx.x * per + j;
+    if (b < t.B) work_start[b] = run;
+    run += g[j];
+  }
+}
+
+// --------------------------------------------------------------- K2
+// CTA w -> bucket b (work_start[b] <= w < work_start[b+1]), group g = w -
+// work_start[b], bucket-local key range [g*target, (g+1)*target).  Tiles are
+// found by binary search over off_bm[b][*]; each warp walks tiles and its
+// lanes count the run's inner digits into the shared histogram.
+__global__ void __launch_bounds__(kGatherThreads) k_inner_gather(const uint16_t* __restrict__ lows,
+                                                                 const uint32_t* __restrict__ off_bm,
+                                                                 const uint32_t* __restrict__ cnt_bm,
+                                                                 const uint16_t* __restrict__ start_tm,
+                                                                 const uint32_t* __restrict__ work_start,
+                                                                 const unsigned long long* total, TwoLevel t,
+                                                                 uint32_t* __restrict__ counts) {
+  extern __shared__ uint32_t s_c[];  // [S]
+  __shared__ uint32_t s_b, s_t0, s_t1;
+  __shared__ unsigned long long s_k0, s_k1;
+  const uint32_t w = blockIdx.x;
+  if (w >= work_start[t.B]) return;
+  if (threadIdx.x == 0) {
+    uint32_t lo = 0, hi = t.B;  // last b with work_start[b] <= w
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (work_start[mid] <= w) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t b = lo;
+    const uint32_t g = w - work_start[b];
+    const uint32_t* row = off_bm + (uint64_t)b * t.T;
+    const unsigned long long bstart = row[0];
+    const unsigned long long bend = (b + 1 < t.B) ? off_bm[(uint64_t)(b + 1) * t.T] : *total;
+    unsigned long long k0 = bstart + (unsigned long long)g * t.target;
+    unsigned long long k1 = k0 + t.target < bend ? k0 + t.target : bend;
+    // first tile whose run ends after k0: last t with row[t] <= k0
+    uint32_t a = 0, z = t.T;
+    while (z - a > 1) {
+      const uint32_t mid = (a + z) >> 1;
+      if (row[mid] <= k0) a = mid;
+      else z = mid;
+    }
+    uint32_t c = a, e = t.T;  // first t with row[t] >= k1
+    while (c < e) {
+      const uint32_t mid = (c + e) >> 1;
+      if (row[mid] >= k1) e = mid;
+      else c = mid + 1;
+    }
+    s_b = b;
+    s_t0 = a;
+    s_t1 = c;
+    s_k0 = k0;
+    s_k1 = k1;
+  }
+  for (uint32_t i = threadIdx.x; i < t.S; i += blockDim.x) s_c[i] = 0;
+  __syncthreads();
+  const uint32_t b = s_b;
+  const unsigned long long k0 = s_k0, k1 = s_k1;
+  const uint32_t* row = off_bm + (uint64_t)b * t.T;
+  const uint32_t* crow = cnt_bm + (uint64_t)b * t.T;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t tt = s_t0 + warp; tt < s_t1; tt += kGatherThreads / 32) {
+    const unsigned long long r0 = row[tt];
+    const unsigned long long r1 = r0 + crow[tt];
+    const unsigned long long a = r0 > k0 ? r0 : k0;
+    const unsigned long long z = r1 < k1 ? r1 : k1;
+    if (a >= z) continue;
+    const uint16_t* src = lows + (uint64_t)tt * kTlTile + start_tm[(uint64_t)tt * t.B + b] + (a - r0);
+    const uint32_t len = static_cast<uint32_t>(z - a);
+    for (uint32_t i = lane; i < len; i += 32) atomicAdd(&s_c[src[i]], 1u);
+  }
+  __syncthreads();
+  const unsigned long long cb = (unsigned long long)b * t.S;
+  for (uint32_t c = threadIdx.x; c < t.S; c += blockDim.x)
+    if (s_c[c] && cb + c < t.cells) atomicAdd(&counts[cb + c], s_c[c]);
 }
 
 }  // namespace rsb
