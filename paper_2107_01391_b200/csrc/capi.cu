@@ -216,10 +216,10 @@ bool div_magic32(uint64_t d, unsigned long long& magic, uint32_t& shift) {
 
 // Geometry of the two-level split: ~10^4 inner cells per outer bucket
 // (10^6 = 100 x 10^4).  Few outer buckets keep each tile's bucket runs long
-// (~80 keys per 8192-key tile); 10^4 inner counters (40 KB) still fit a
-// shared histogram.  At most kTlMaxBuckets buckets.
+// (~40 keys per 4096-key tile); 10^4 inner counters (40 KB) still fit a
+// shared histogram.
 bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
-  if (cells <= kSmemCellsMax || cells > 0xFFFFFFFFull || n >= 0xFFFFFFFFull) return false;
+  if (cells <= kSmemCellsMax || cells > 0xFFFFFFFFull || n >= 0x7FFFFFFFull * 16) return false;
   uint64_t B = (cells + 9999) / 10000;
   if (B > kTlMaxBuckets) B = kTlMaxBuckets;
   const uint64_t S = (cells + B - 1) / B;
@@ -229,8 +229,17 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
   t.B = static_cast<uint32_t>((cells + S - 1) / S);
   if (!div_magic32(S, t.magic, t.shift)) return false;
   t.T = static_cast<uint32_t>((n + kTlTile - 1) / kTlTile);
-  // groups of >= 16*S keys keep the per-group flush of S counters small
-  t.target = std::max<uint64_t>(16ull * S, 131072);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_page_partition<MapU32>, kTlThreads,
+                                                kPagePartitionSmem(t.B));
+  if (per_sm < 1) per_sm = 1;
+  uint64_t G = (uint64_t)sm_count() * per_sm;  // one persistent wave
+  if (G > t.T) G = t.T;
+  t.G = static_cast<uint32_t>(G);
+  const uint64_t tiles_per = (t.T + G - 1) / G;
+  t.pages_per_cta = static_cast<uint32_t>(tiles_per * (kTlTile / kPage) + t.B);
+  // groups of ~16*S keys keep the per-group flush of S counters small
+  t.group_pages = static_cast<uint32_t>(std::max<uint64_t>(128, 16ull * S / kPage));
   return true;
 }
 
@@ -238,35 +247,40 @@ template <class Map>
 void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, const TwoLevel& t,
                      uint32_t* counts) {
   const bool al = aligned16(in);
-  const uint64_t bt = (uint64_t)t.B * t.T;
-  auto* cnt_bm = ws.get<uint32_t>(kSlotCtaHist, bt);
-  auto* off_bm = ws.get<uint32_t>(kSlotCtaOff, bt);
-  auto* start_tm = ws.get<uint16_t>(kSlotBucketStart, bt);
-  auto* lows = ws.get<uint16_t>(kSlotLows, (uint64_t)t.T * kTlTile);
+  const uint64_t P = (uint64_t)t.G * t.pages_per_cta;
+  const uint64_t bg = (uint64_t)t.B * t.G;
+  auto* pages = ws.get<uint16_t>(kSlotLows, P * kPage);
+  auto* page_bucket = ws.get<uint16_t>(kSlotBucketStart, P);
+  auto* page_fill = ws.get<uint16_t>(kSlotTmpVals2, P);
+  auto* pc_bm = ws.get<uint32_t>(kSlotCtaHist, bg);
+  auto* po_bm = ws.get<uint32_t>(kSlotCtaOff, bg);
+  auto* list = ws.get<uint32_t>(kSlotTmpKeys2, P);
   auto* total = ws.get<unsigned long long>(kSlotScratch, 4);
   auto* work = ws.get<uint32_t>(kSlotMisc, t.B + 1ull);
-  const size_t smem = kTilePartitionSmem(t.B);
+  const size_t smem = kPagePartitionSmem(t.B);
   if (smem > 48 * 1024)
-    RS_CUDA(cudaFuncSetAttribute(k_tile_partition<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RS_CUDA(cudaFuncSetAttribute(k_page_partition<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   {
     PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
-    k_tile_partition<Map><<<t.T, kTlThreads, smem, ws.stream>>>(in, n, map, t, al, lows, cnt_bm, start_tm,
-                                                                ws.stats);
+    k_page_partition<Map><<<t.G, kTlThreads, smem, ws.stream>>>(in, n, map, t, al, pages, page_bucket,
+                                                                page_fill, pc_bm, ws.stats);
     RS_LAUNCH_CHECK();
   }
-  exscan_u32(ws, cnt_bm, bt, off_bm, total);
+  exscan_u32(ws, pc_bm, bg, po_bm, total);
   {
-    PassTimer pt_(RS_PASS_SCAN, ws.stream);
-    k_work_list<<<1, 1024, 0, ws.stream>>>(off_bm, total, t, work);
+    PassTimer pt_(RS_PASS_SCAN, ws.stream, 2);
+    k_page_list<<<t.G, 256, t.B * sizeof(uint32_t), ws.stream>>>(page_bucket, po_bm, pc_bm, t, list);
+    RS_LAUNCH_CHECK();
+    k_page_work<<<1, kTlMaxBuckets, 0, ws.stream>>>(po_bm, total, t, work);
     RS_LAUNCH_CHECK();
   }
   RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
-  const uint64_t max_groups = n / t.target + t.B + 1;
+  const uint64_t max_groups = P / t.group_pages + t.B + 1;
   {
     PassTimer pt_(RS_PASS_COUNT, ws.stream);
-    k_inner_gather<<<static_cast<unsigned>(max_groups), kGatherThreads, t.S * sizeof(uint32_t), ws.stream>>>(
-        lows, off_bm, cnt_bm, start_tm, work, total, t, counts);
+    k_page_count<<<static_cast<unsigned>(max_groups), kGatherThreads, t.S * sizeof(uint32_t), ws.stream>>>(
+        pages, page_fill, list, po_bm, work, total, t, counts);
     RS_LAUNCH_CHECK();
   }
 }

@@ -6,22 +6,21 @@
 // atomics/s) while a shared-memory histogram of <= 4096 bins takes 0.20 ms at
 // 5.3 TB/s.  So the Cartesian grid is split as outer x inner: the leading
 // digits pick one of B outer buckets and the trailing digits one of S inner
-// cells (10^6 = 1000 x 1000):
+// cells (10^6 = 100 x 10^4):
 //
-//   K1 tile_partition  one CTA per 8192-key tile: map each key to its cell,
-//                      counting-sort the tile by outer bucket in shared
-//                      memory and write the inner digits (uint16) back to
-//                      the tile's own slot, fully coalesced; per-(bucket,
-//                      tile) counts and in-tile starts go to two small
-//                      tables; max / flags / overflow fused               R4 + W2
-//   scan               exclusive scan of the bucket-major [B][T] counts
-//   work list          each bucket cut into groups of ~target keys
-//   K2 inner_gather    one CTA per group: gathers the bucket's runs (~80
-//                      keys each) from consecutive tiles, shared histogram
-//                      over the S inner cells, one flush into the dense
-//                      count grid                                        R2
+//   K1 page_partition  persistent CTAs stream tiles of 4096 keys: map each
+//                      key to its cell, counting-sort the tile by outer
+//                      bucket in shared memory and append each bucket's
+//                      run of inner digits (uint16) to that bucket's current
+//                      2 KB page in the CTA's private page region; pages are
+//                      taken from a shared-memory counter (no global
+//                      atomics, no pre-pass); max / flags / overflow fused  R4 + W2
+//   page lists         per-(bucket, CTA) page counts scanned bucket-major,
+//                      page ids listed per bucket
+//   K2 page_count      one CTA per group of a bucket's pages: streams whole
+//                      pages, shared histogram over the S inner cells, one
+//                      flush into the dense count grid                   R2
 // after which the occupancy scan and the load-balanced emit run unchanged.
-// No histogram pre-pass is needed: each tile sorts only itself.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -33,11 +32,12 @@
 
 namespace rsb {
 
-constexpr int kTlThreads = 512;
+constexpr int kTlThreads = 256;
 constexpr int kTlPerThread = 16;
-constexpr int kTlTile = kTlThreads * kTlPerThread;  // 8192 keys per tile
-constexpr uint32_t kTlMaxBuckets = 4096;            // outer buckets
+constexpr int kTlTile = kTlThreads * kTlPerThread;  // 4096 keys per tile
+constexpr uint32_t kTlMaxBuckets = 1024;            // outer buckets
 constexpr uint32_t kTlMaxInner = 16384;             // inner cells (smem hist <= 64 KB)
+constexpr uint32_t kPage = 1024;                    // inner digits per page (2 KB)
 constexpr int kGatherThreads = 256;
 
 struct TwoLevel {
@@ -47,7 +47,9 @@ struct TwoLevel {
   unsigned long long magic;  // bucket = (cell * magic) >> shift, exact for cell < 2^32
   uint32_t shift;
   uint32_t T;                // tiles = ceil(n / kTlTile)
-  uint64_t target;           // keys per K2 group
+  uint32_t G;                // persistent partition CTAs
+  uint32_t pages_per_cta;    // page region of one CTA
+  uint32_t group_pages;      // pages per K2 work item
 };
 
 __device__ __forceinline__ uint32_t tl_bucket(uint32_t cell, const TwoLevel& t) {
@@ -141,106 +143,164 @@ __global__ void __launch_bounds__(kThreads) k_exscan_u32(const uint32_t* __restr
 }
 
 // ------------------------------------------------------------- K1
-// Shared layout (kTilePartitionSmem(B)): s_cnt[B+1] counts -> starts,
-// s_low[kTlTile] inner digits in bucket order.
-__host__ __device__ constexpr size_t kTilePartitionSmem(uint32_t B) {
-  return (((size_t)B + 1) * 4 + 15) / 16 * 16 + (size_t)kTlTile * 2;
+// Dynamic shared layout (kPagePartitionSmem(B)): s_cnt[B+1] tile counts ->
+// starts, s_page[B] current page per bucket, s_fill[B] its fill, s_np[B]
+// pages opened per bucket, s_low[kTlTile] staged inner digits.
+__host__ __device__ constexpr size_t kPagePartitionOffset(uint32_t B) {
+  return (((size_t)B + 1) * 4 + (size_t)B * 12 + 15) / 16 * 16;
+}
+__host__ __device__ constexpr size_t kPagePartitionSmem(uint32_t B) {
+  return kPagePartitionOffset(B) + (size_t)kTlTile * 2;
 }
 
 template <class Map>
-__global__ void __launch_bounds__(kTlThreads) k_tile_partition(const typename Map::In* __restrict__ in, uint64_t n,
+__global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Map::In* __restrict__ in, uint64_t n,
                                                                Map map, TwoLevel t, bool aligned,
-                                                               uint16_t* __restrict__ lows,       // [T][kTlTile]
-                                                               uint32_t* __restrict__ cnt_bm,     // [B][T]
-                                                               uint16_t* __restrict__ start_tm,   // [T][B]
+                                                               uint16_t* __restrict__ pages,        // [G*ppc][kPage]
+                                                               uint16_t* __restrict__ page_bucket,  // [G*ppc]
+                                                               uint16_t* __restrict__ page_fill,    // [G*ppc]
+                                                               uint32_t* __restrict__ pc_bm,        // [B][G]
                                                                DevStats* st) {
   using In = typename Map::In;
   extern __shared__ __align__(16) unsigned char tl_smem[];
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(tl_smem);
-  uint16_t* s_low = reinterpret_cast<uint16_t*>(tl_smem + (((size_t)t.B + 1) * 4 + 15) / 16 * 16);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(tl_smem);  // [B+1]
+  uint32_t* s_page = s_cnt + t.B + 1;                       // [B]
+  uint32_t* s_fill = s_page + t.B;                          // [B]
+  uint32_t* s_np = s_fill + t.B;                            // [B]
+  uint16_t* s_low = reinterpret_cast<uint16_t*>(tl_smem + kPagePartitionOffset(t.B));
   __shared__ uint32_t s_scan[kTlThreads / 32];
+  __shared__ uint32_t s_next;  // next free page of this CTA's region
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t tile = blockIdx.x;
-  const uint64_t base = (uint64_t)tile * kTlTile;
-  const uint64_t end = base + kTlTile < n ? base + kTlTile : n;
-  for (uint32_t b = threadIdx.x; b <= t.B; b += blockDim.x) s_cnt[b] = 0;
-  __syncthreads();
+  const uint32_t page0 = blockIdx.x * t.pages_per_cta;
+  for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) {
+    s_page[b] = 0xffffffffu;
+    s_fill[b] = kPage;  // "full": the first key of a bucket opens a page
+    s_np[b] = 0;
+  }
+  if (threadIdx.x == 0) s_next = 0;
   unsigned long long mx = 0;
   unsigned flags = 0, ovf = 0;
-  uint32_t pk[kTlPerThread];  // bucket << 16 | rank   (0xffffffff = not counted)
-  uint16_t lo[kTlPerThread];
+  const uint32_t per = (t.B + kTlThreads - 1) / kTlThreads;
+  In cur[4][4], nxt[4][4];
+  uint32_t tile = blockIdx.x;
+  if (tile < t.T) {
 #pragma unroll
-  for (int q = 0; q < kTlPerThread / 4; ++q) {
-    const uint64_t i0 = base + q * (kTlThreads * 4) + threadIdx.x * 4;
-    In v[4];
-    Load4<In>::run(in, i0, end, aligned, v);
+    for (int q = 0; q < 4; ++q)
+      Load4<In>::run(in, (uint64_t)tile * kTlTile + q * 1024 + threadIdx.x * 4, n, aligned, cur[q]);
+  }
+  for (; tile < t.T; tile += gridDim.x) {
+    const uint64_t base = (uint64_t)tile * kTlTile;
+    const uint32_t nt = tile + gridDim.x;
+    if (nt < t.T) {  // software pipeline: the next tile's loads are in flight
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      pk[q * 4 + e] = 0xffffffffu;
-      lo[q * 4 + e] = 0;
-      if (i0 + e < end) {
-        const unsigned long long k = map(v[e], flags);
-        mx = k > mx ? k : mx;
-        if (k < t.cells) {
-          const uint32_t b = tl_bucket(static_cast<uint32_t>(k), t);
-          lo[q * 4 + e] = static_cast<uint16_t>(static_cast<uint32_t>(k) - b * t.S);
-          pk[q * 4 + e] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
-        } else {
-          ovf = 1;
+      for (int q = 0; q < 4; ++q)
+        Load4<In>::run(in, (uint64_t)nt * kTlTile + q * 1024 + threadIdx.x * 4, n, aligned, nxt[q]);
+    }
+    for (uint32_t b = threadIdx.x; b <= t.B; b += blockDim.x) s_cnt[b] = 0;
+    __syncthreads();
+    uint32_t pk[kTlPerThread];  // bucket << 16 | rank in tile (0xffffffff: not counted)
+    uint32_t lo2[kTlPerThread / 2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i0 = base + q * 1024 + threadIdx.x * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        uint32_t l = 0;
+        pk[q * 4 + e] = 0xffffffffu;
+        if (i0 + e < n) {
+          const unsigned long long kk = map(cur[q][e], flags);
+          mx = kk > mx ? kk : mx;
+          if (kk < t.cells) {
+            const uint32_t b = tl_bucket(static_cast<uint32_t>(kk), t);
+            l = static_cast<uint32_t>(kk) - b * t.S;
+            pk[q * 4 + e] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
+          } else {
+            ovf = 1;
+          }
+        }
+        if (e & 1) lo2[(q * 4 + e) >> 1] |= l << 16;
+        else lo2[(q * 4 + e) >> 1] = l;
+      }
+    }
+    __syncthreads();
+    {  // exclusive scan of s_cnt over buckets; s_cnt[B] = staged keys
+      uint32_t sum = 0;
+      const uint32_t b0 = threadIdx.x * per;
+      for (uint32_t j = 0; j < per; ++j)
+        if (b0 + j < t.B) sum += s_cnt[b0 + j];
+      uint32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) s_scan[warp] = inc;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t r = 0;
+        for (int w = 0; w < kTlThreads / 32; ++w) {
+          const uint32_t c = s_scan[w];
+          s_scan[w] = r;
+          r += c;
+        }
+        s_cnt[t.B] = r;
+      }
+      __syncthreads();
+      uint32_t run = s_scan[warp] + inc - sum;
+      for (uint32_t j = 0; j < per; ++j) {
+        if (b0 + j < t.B) {
+          const uint32_t c = s_cnt[b0 + j];
+          s_cnt[b0 + j] = run;
+          run += c;
         }
       }
     }
-  }
-  __syncthreads();
-  // counts out (bucket-major for the scan), then exclusive scan in place
-  const uint32_t per = (t.B + kTlThreads - 1) / kTlThreads;
-  const uint32_t b0 = threadIdx.x * per;
-  uint32_t sum = 0;
-  for (uint32_t j = 0; j < per; ++j) {
-    const uint32_t b = b0 + j;
-    if (b < t.B) {
-      const uint32_t c = s_cnt[b];
-      cnt_bm[(uint64_t)b * t.T + tile] = c;
-      sum += c;
-    }
-  }
-  uint32_t inc = sum;
+    __syncthreads();
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += y;
-  }
-  if (lane == 31) s_scan[warp] = inc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t r = 0;
-    for (int w = 0; w < kTlThreads / 32; ++w) {
-      const uint32_t c = s_scan[w];
-      s_scan[w] = r;
-      r += c;
+    for (int j = 0; j < kTlPerThread; ++j)
+      if (pk[j] != 0xffffffffu)
+        s_low[s_cnt[pk[j] >> 16] + (pk[j] & 0xffffu)] = static_cast<uint16_t>(lo2[j >> 1] >> ((j & 1) * 16));
+    __syncthreads();
+    // append each bucket's run to its current page (one warp per bucket)
+    for (uint32_t b = warp; b < t.B; b += kTlThreads / 32) {
+      const uint32_t s = s_cnt[b], len = s_cnt[b + 1] - s;
+      if (len == 0) continue;
+      uint32_t fill = s_fill[b], pg = s_page[b];
+      uint32_t done = 0;
+      while (done < len) {
+        if (fill == kPage) {  // close the full page, open a new one
+          uint32_t np = 0;
+          if (lane == 0) {
+            np = atomicAdd(&s_next, 1u);
+            if (pg != 0xffffffffu) page_fill[page0 + pg] = static_cast<uint16_t>(kPage);
+            page_bucket[page0 + np] = static_cast<uint16_t>(b);
+            s_np[b] += 1;
+          }
+          pg = __shfl_sync(0xffffffffu, np, 0);
+          fill = 0;
+        }
+        const uint32_t take = min(len - done, kPage - fill);
+        uint16_t* dst = pages + ((uint64_t)(page0 + pg) * kPage + fill);
+        for (uint32_t i = lane; i < take; i += 32) dst[i] = s_low[s + done + i];
+        fill += take;
+        done += take;
+      }
+      if (lane == 0) {
+        s_fill[b] = fill;
+        s_page[b] = pg;
+      }
     }
-  }
-  __syncthreads();
-  uint32_t run = s_scan[warp] + inc - sum;
-  for (uint32_t j = 0; j < per; ++j) {
-    const uint32_t b = b0 + j;
-    if (b < t.B) {
-      const uint32_t c = s_cnt[b];
-      s_cnt[b] = run;
-      start_tm[(uint64_t)tile * t.B + b] = static_cast<uint16_t>(run);
-      run += c;
-    }
-  }
-  __syncthreads();
 #pragma unroll
-  for (int j = 0; j < kTlPerThread; ++j)
-    if (pk[j] != 0xffffffffu) s_low[s_cnt[pk[j] >> 16] + (pk[j] & 0xffffu)] = lo[j];
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cur[q][e] = nxt[q][e];
+    __syncthreads();
+  }
   __syncthreads();
-  // the whole tile slot, 16-byte stores (entries past the counted keys are
-  // never read: K2 reads exactly each bucket's run)
-  uint4* dst = reinterpret_cast<uint4*>(lows + base);
-  const uint4* src = reinterpret_cast<const uint4*>(s_low);
-  for (uint32_t i = threadIdx.x; i < kTlTile / 8; i += blockDim.x) __stcs(dst + i, src[i]);
+  for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) {
+    if (s_page[b] != 0xffffffffu) page_fill[page0 + s_page[b]] = static_cast<uint16_t>(s_fill[b]);
+    pc_bm[(uint64_t)b * t.G + blockIdx.x] = s_np[b];
+  }
   warp_max_to(mx, &st->max_key);
   flags = warp_or(flags | (ovf ? 0x80000000u : 0u));
   if ((threadIdx.x & 31) == 0 && flags) {
@@ -249,27 +309,42 @@ __global__ void __launch_bounds__(kTlThreads) k_tile_partition(const typename Ma
   }
 }
 
-// ------------------------------------------------------ K2 work list
-// groups[b] = ceil(total_b / target); work_start = exclusive scan (one CTA,
-// B <= 4096).  off_bm is the exclusive scan of cnt_bm, so bucket b's keys
-// are [off_bm[b*T], off_bm[(b+1)*T]) in bucket-major order.
-__global__ void k_work_list(const uint32_t* __restrict__ off_bm, const unsigned long long* total, TwoLevel t,
-                            uint32_t* __restrict__ work_start) {
-  __shared__ uint32_t s_w[1024];
-  const uint32_t per = (t.B + blockDim.x - 1) / blockDim.x;
-  uint32_t g[8];
-  uint32_t sum = 0;
-  for (uint32_t j = 0; j < per && j < 8; ++j) {
-    const uint32_t b = threadIdx.x * per + j;
-    g[j] = 0;
-    if (b < t.B) {
-      const unsigned long long lo = off_bm[(uint64_t)b * t.T];
-      const unsigned long long hi = (b + 1 < t.B) ? off_bm[(uint64_t)(b + 1) * t.T] : *total;
-      g[j] = static_cast<uint32_t>((hi - lo + t.target - 1) / t.target);
-    }
-    sum += g[j];
+// Page list grouped by bucket: CTA c walks its used pages (allocated densely
+// from 0) and places page p of bucket b at list[po_bm[b][c] + rank].
+__global__ void k_page_list(const uint16_t* __restrict__ page_bucket, const uint32_t* __restrict__ po_bm,
+                            const uint32_t* __restrict__ pc_bm, TwoLevel t, uint32_t* __restrict__ list) {
+  extern __shared__ uint32_t s_cur[];  // [B]
+  __shared__ uint32_t s_used;
+  const uint32_t c = blockIdx.x;
+  if (threadIdx.x == 0) s_used = 0;
+  __syncthreads();
+  uint32_t used = 0;
+  for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) {
+    s_cur[b] = po_bm[(uint64_t)b * t.G + c];
+    used += pc_bm[(uint64_t)b * t.G + c];
   }
-  s_w[threadIdx.x] = sum;
+  atomicAdd(&s_used, used);
+  __syncthreads();
+  const uint32_t page0 = c * t.pages_per_cta;
+  for (uint32_t p = threadIdx.x; p < s_used; p += blockDim.x) {
+    const uint32_t b = page_bucket[page0 + p];
+    list[atomicAdd(&s_cur[b], 1u)] = page0 + p;
+  }
+}
+
+// Work list: bucket b owns list entries [po_bm[b*G], po_bm[(b+1)*G]), cut
+// into groups of group_pages; work_start = exclusive scan of group counts.
+__global__ void k_page_work(const uint32_t* __restrict__ po_bm, const unsigned long long* total, TwoLevel t,
+                            uint32_t* __restrict__ work_start) {
+  __shared__ uint32_t s_w[kTlMaxBuckets];
+  const uint32_t b = threadIdx.x;
+  uint32_t g = 0;
+  if (b < t.B) {
+    const uint32_t lo = po_bm[(uint64_t)b * t.G];
+    const uint32_t hi = (b + 1 < t.B) ? po_bm[(uint64_t)(b + 1) * t.G] : static_cast<uint32_t>(*total);
+    g = (hi - lo + t.group_pages - 1) / t.group_pages;
+  }
+  s_w[threadIdx.x] = g;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t r = 0;
@@ -281,29 +356,22 @@ __global__ void k_work_list(const uint32_t* __restrict__ off_bm, const unsigned 
     work_start[t.B] = r;
   }
   __syncthreads();
-  uint32_t run = s_w[threadIdx.x];
-  for (uint32_t j = 0; j < per && j < 8; ++j) {
-    const uint32_t b = threadIdx.x * per + j;
-    if (b < t.B) work_start[b] = run;
-    run += g[j];
-  }
+  if (b < t.B) work_start[b] = s_w[b];
 }
 
 // --------------------------------------------------------------- K2
-// CTA w -> bucket b (work_start[b] <= w < work_start[b+1]), group g = w -
-// work_start[b], bucket-local key range [g*target, (g+1)*target).  Tiles are
-// found by binary search over off_bm[b][*]; each warp walks tiles and its
-// lanes count the run's inner digits into the shared histogram.
-__global__ void __launch_bounds__(kGatherThreads) k_inner_gather(const uint16_t* __restrict__ lows,
-                                                                 const uint32_t* __restrict__ off_bm,
-                                                                 const uint32_t* __restrict__ cnt_bm,
-                                                                 const uint16_t* __restrict__ start_tm,
-                                                                 const uint32_t* __restrict__ work_start,
-                                                                 const unsigned long long* total, TwoLevel t,
-                                                                 uint32_t* __restrict__ counts) {
+// CTA w -> bucket b (work_start[b] <= w < work_start[b+1]) and its group of
+// pages; streams the pages as a flat range of 16-byte slots (128 per page),
+// shared histogram over the S inner cells, one flush into the grid.
+__global__ void __launch_bounds__(kGatherThreads) k_page_count(const uint16_t* __restrict__ pages,
+                                                               const uint16_t* __restrict__ page_fill,
+                                                               const uint32_t* __restrict__ list,
+                                                               const uint32_t* __restrict__ po_bm,
+                                                               const uint32_t* __restrict__ work_start,
+                                                               const unsigned long long* total, TwoLevel t,
+                                                               uint32_t* __restrict__ counts) {
   extern __shared__ uint32_t s_c[];  // [S]
-  __shared__ uint32_t s_b, s_t0, s_t1;
-  __shared__ unsigned long long s_k0, s_k1;
+  __shared__ uint32_t s_b, s_p0, s_p1;
   const uint32_t w = blockIdx.x;
   if (w >= work_start[t.B]) return;
   if (threadIdx.x == 0) {
@@ -314,50 +382,32 @@ __global__ void __launch_bounds__(kGatherThreads) k_inner_gather(const uint16_t*
       else hi = mid;
     }
     const uint32_t b = lo;
-    const uint32_t g = w - work_start[b];
-    const uint32_t* row = off_bm + (uint64_t)b * t.T;
-    const unsigned long long bstart = row[0];
-    const unsigned long long bend = (b + 1 < t.B) ? off_bm[(uint64_t)(b + 1) * t.T] : *total;
-    unsigned long long k0 = bstart + (unsigned long long)g * t.target;
-    unsigned long long k1 = k0 + t.target < bend ? k0 + t.target : bend;
-    // first tile whose run ends after k0: last t with row[t] <= k0
-    uint32_t a = 0, z = t.T;
-    while (z - a > 1) {
-      const uint32_t mid = (a + z) >> 1;
-      if (row[mid] <= k0) a = mid;
-      else z = mid;
-    }
-    uint32_t c = a, e = t.T;  // first t with row[t] >= k1
-    while (c < e) {
-      const uint32_t mid = (c + e) >> 1;
-      if (row[mid] >= k1) e = mid;
-      else c = mid + 1;
-    }
+    const uint32_t first = po_bm[(uint64_t)b * t.G];
+    const uint32_t last = (b + 1 < t.B) ? po_bm[(uint64_t)(b + 1) * t.G] : static_cast<uint32_t>(*total);
+    const uint32_t p0 = first + (w - work_start[b]) * t.group_pages;
     s_b = b;
-    s_t0 = a;
-    s_t1 = c;
-    s_k0 = k0;
-    s_k1 = k1;
+    s_p0 = p0;
+    s_p1 = p0 + t.group_pages < last ? p0 + t.group_pages : last;
   }
   for (uint32_t i = threadIdx.x; i < t.S; i += blockDim.x) s_c[i] = 0;
   __syncthreads();
-  const uint32_t b = s_b;
-  const unsigned long long k0 = s_k0, k1 = s_k1;
-  const uint32_t* row = off_bm + (uint64_t)b * t.T;
-  const uint32_t* crow = cnt_bm + (uint64_t)b * t.T;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t tt = s_t0 + warp; tt < s_t1; tt += kGatherThreads / 32) {
-    const unsigned long long r0 = row[tt];
-    const unsigned long long r1 = r0 + crow[tt];
-    const unsigned long long a = r0 > k0 ? r0 : k0;
-    const unsigned long long z = r1 < k1 ? r1 : k1;
-    if (a >= z) continue;
-    const uint16_t* src = lows + (uint64_t)tt * kTlTile + start_tm[(uint64_t)tt * t.B + b] + (a - r0);
-    const uint32_t len = static_cast<uint32_t>(z - a);
-    for (uint32_t i = lane; i < len; i += 32) atomicAdd(&s_c[src[i]], 1u);
+  const uint32_t np = s_p1 - s_p0;
+  constexpr uint32_t kSlots = kPage / 8;
+  for (uint32_t s = threadIdx.x; s < np * kSlots; s += blockDim.x) {
+    const uint32_t pi = s / kSlots, q = s % kSlots;
+    const uint32_t page = list[s_p0 + pi];
+    const uint32_t fill = page_fill[page];
+    if (q * 8 >= fill) continue;
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(pages + (uint64_t)page * kPage) + q);
+    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (q * 8 + 2 * j < fill) atomicAdd(&s_c[ws[j] & 0xffffu], 1u);
+      if (q * 8 + 2 * j + 1 < fill) atomicAdd(&s_c[ws[j] >> 16], 1u);
+    }
   }
   __syncthreads();
-  const unsigned long long cb = (unsigned long long)b * t.S;
+  const unsigned long long cb = (unsigned long long)s_b * t.S;
   for (uint32_t c = threadIdx.x; c < t.S; c += blockDim.x)
     if (s_c[c] && cb + c < t.cells) atomicAdd(&counts[cb + c], s_c[c]);
 }
