@@ -277,6 +277,9 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
   }
   RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
   const uint64_t max_groups = P / t.group_pages + t.B + 1;
+  if (t.S * sizeof(uint32_t) > 48 * 1024)
+    RS_CUDA(cudaFuncSetAttribute(k_page_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(t.S * sizeof(uint32_t))));
   {
     PassTimer pt_(RS_PASS_COUNT, ws.stream);
     k_page_count<<<static_cast<unsigned>(max_groups), kGatherThreads, t.S * sizeof(uint32_t), ws.stream>>>(

@@ -147,10 +147,10 @@ __global__ void __launch_bounds__(kThreads) k_exscan_u32(const uint32_t* __restr
 // starts, s_page[B] current page per bucket, s_fill[B] its fill, s_np[B]
 // pages opened per bucket, s_low[kTlTile] staged inner digits.
 __host__ __device__ constexpr size_t kPagePartitionOffset(uint32_t B) {
-  return (((size_t)B + 1) * 4 + (size_t)B * 12 + 15) / 16 * 16;
+  return (((size_t)B + 1) * 4 + (size_t)B * 24 + 15) / 16 * 16;
 }
 __host__ __device__ constexpr size_t kPagePartitionSmem(uint32_t B) {
-  return kPagePartitionOffset(B) + (size_t)kTlTile * 2;
+  return kPagePartitionOffset(B) + (size_t)kTlTile * 4;  // s_low + s_bkt
 }
 
 template <class Map>
@@ -167,7 +167,11 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
   uint32_t* s_page = s_cnt + t.B + 1;                       // [B]
   uint32_t* s_fill = s_page + t.B;                          // [B]
   uint32_t* s_np = s_fill + t.B;                            // [B]
+  uint32_t* s_pa = s_np + t.B;                              // [B] page of the run's first key
+  uint32_t* s_fa = s_pa + t.B;                              // [B] its slot in that page
+  uint32_t* s_pb = s_fa + t.B;                              // [B] first continuation page
   uint16_t* s_low = reinterpret_cast<uint16_t*>(tl_smem + kPagePartitionOffset(t.B));
+  uint16_t* s_bkt = s_low + kTlTile;
   __shared__ uint32_t s_scan[kTlThreads / 32];
   __shared__ uint32_t s_next;  // next free page of this CTA's region
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -257,38 +261,54 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kTlPerThread; ++j)
-      if (pk[j] != 0xffffffffu)
-        s_low[s_cnt[pk[j] >> 16] + (pk[j] & 0xffffu)] = static_cast<uint16_t>(lo2[j >> 1] >> ((j & 1) * 16));
-    __syncthreads();
-    // append each bucket's run to its current page (one warp per bucket)
-    for (uint32_t b = warp; b < t.B; b += kTlThreads / 32) {
-      const uint32_t s = s_cnt[b], len = s_cnt[b + 1] - s;
+    for (int j = 0; j < kTlPerThread; ++j) {
+      if (pk[j] != 0xffffffffu) {
+        const uint32_t pos = s_cnt[pk[j] >> 16] + (pk[j] & 0xffffu);
+        s_low[pos] = static_cast<uint16_t>(lo2[j >> 1] >> ((j & 1) * 16));
+        s_bkt[pos] = static_cast<uint16_t>(pk[j] >> 16);
+      }
+    }
+    // page bookkeeping, one thread per bucket: a run that does not fit the
+    // current page spills into freshly allocated consecutive pages
+    for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) {
+      const uint32_t len = s_cnt[b + 1] - s_cnt[b];
       if (len == 0) continue;
       uint32_t fill = s_fill[b], pg = s_page[b];
-      uint32_t done = 0;
-      while (done < len) {
-        if (fill == kPage) {  // close the full page, open a new one
-          uint32_t np = 0;
-          if (lane == 0) {
-            np = atomicAdd(&s_next, 1u);
-            if (pg != 0xffffffffu) page_fill[page0 + pg] = static_cast<uint16_t>(kPage);
-            page_bucket[page0 + np] = static_cast<uint16_t>(b);
-            s_np[b] += 1;
-          }
-          pg = __shfl_sync(0xffffffffu, np, 0);
-          fill = 0;
+      const uint32_t room = (pg == 0xffffffffu) ? 0u : kPage - fill;
+      uint32_t pa = pg, fa = fill, pb = 0;
+      if (len > room) {
+        const uint32_t extra = (len - room + kPage - 1) / kPage;
+        const uint32_t first = atomicAdd(&s_next, extra);
+        for (uint32_t j = 0; j < extra; ++j) page_bucket[page0 + first + j] = static_cast<uint16_t>(b);
+        for (uint32_t j = 0; j + 1 < extra; ++j) page_fill[page0 + first + j] = static_cast<uint16_t>(kPage);
+        if (pg != 0xffffffffu) page_fill[page0 + pg] = static_cast<uint16_t>(kPage);
+        s_np[b] += extra;
+        if (room == 0) {
+          pa = first;
+          fa = 0;
+          pb = first + 1;
+        } else {
+          pb = first;
         }
-        const uint32_t take = min(len - done, kPage - fill);
-        uint16_t* dst = pages + ((uint64_t)(page0 + pg) * kPage + fill);
-        for (uint32_t i = lane; i < take; i += 32) dst[i] = s_low[s + done + i];
-        fill += take;
-        done += take;
+        pg = first + extra - 1;
+        fill = len - room - (extra - 1) * kPage;
+      } else {
+        fill += len;
       }
-      if (lane == 0) {
-        s_fill[b] = fill;
-        s_page[b] = pg;
-      }
+      s_fill[b] = fill;
+      s_page[b] = pg;
+      s_pa[b] = pa;
+      s_fa[b] = fa;
+      s_pb[b] = pb;
+    }
+    __syncthreads();
+    // element-parallel copy of the staged runs into their pages
+    const uint32_t staged = s_cnt[t.B];
+    for (uint32_t i = threadIdx.x; i < staged; i += blockDim.x) {
+      const uint32_t b = s_bkt[i];
+      const uint32_t slot = s_fa[b] + (i - s_cnt[b]);
+      const uint32_t page = slot < kPage ? s_pa[b] : s_pb[b] + (slot - kPage) / kPage;
+      pages[(uint64_t)(page0 + page) * kPage + (slot & (kPage - 1))] = s_low[i];
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
