@@ -776,7 +776,7 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
     }
     if (!chars || !out) fail(RS_INVALID_ARGUMENT, "null device pointer");
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
-    auto* tab = ws.get<uint8_t>(kSlotMisc, sizeof(StrTable));
+    auto* tab = ws.get<uint8_t>(kSlotAlphabet, sizeof(StrTable));
     RS_CUDA(cudaMemcpyAsync(tab, &t, sizeof(StrTable), cudaMemcpyHostToDevice, ws.stream));
     const auto* d_ord = reinterpret_cast<const uint16_t*>(tab);
     const auto* d_sym = tab + offsetof(StrTable, sym);

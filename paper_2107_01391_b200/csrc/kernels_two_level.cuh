@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kThreads) k_exscan_u32(const uint32_t* __restr
 // starts, s_page[B] current page per bucket, s_fill[B] its fill, s_np[B]
 // pages opened per bucket, s_low[kTlTile] staged inner digits.
 __host__ __device__ constexpr size_t kPagePartitionOffset(uint32_t B) {
-  return (((size_t)B + 1) * 4 + (size_t)B * 24 + 15) / 16 * 16;
+  return (((size_t)B + 1) * 4 + (size_t)B * 12 + 15) / 16 * 16 + (size_t)B * 16;
 }
 __host__ __device__ constexpr size_t kPagePartitionSmem(uint32_t B) {
   return kPagePartitionOffset(B) + (size_t)kTlTile * 4;  // s_low + s_bkt
@@ -167,15 +167,16 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
   uint32_t* s_page = s_cnt + t.B + 1;                       // [B]
   uint32_t* s_fill = s_page + t.B;                          // [B]
   uint32_t* s_np = s_fill + t.B;                            // [B]
-  uint32_t* s_pa = s_np + t.B;                              // [B] page of the run's first key
-  uint32_t* s_fa = s_pa + t.B;                              // [B] its slot in that page
-  uint32_t* s_pb = s_fa + t.B;                              // [B] first continuation page
+  // per bucket, this tile: {run start in staging, dest of rank r < thr = A + r,
+  // else Bv + r, thr} (dest = index into the CTA's page region)
+  uint4* s_dst = reinterpret_cast<uint4*>(tl_smem + (((size_t)t.B + 1) * 4 + (size_t)t.B * 12 + 15) / 16 * 16);
   uint16_t* s_low = reinterpret_cast<uint16_t*>(tl_smem + kPagePartitionOffset(t.B));
   uint16_t* s_bkt = s_low + kTlTile;
   __shared__ uint32_t s_scan[kTlThreads / 32];
   __shared__ uint32_t s_next;  // next free page of this CTA's region
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t page0 = blockIdx.x * t.pages_per_cta;
+  uint16_t* my_pages = pages + (uint64_t)page0 * kPage;
   for (uint32_t b = threadIdx.x; b < t.B; b += blockDim.x) {
     s_page[b] = 0xffffffffu;
     s_fill[b] = kPage;  // "full": the first key of a bucket opens a page
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
     __syncthreads();
     uint32_t pk[kTlPerThread];  // bucket << 16 | rank in tile (0xffffffff: not counted)
     uint32_t lo2[kTlPerThread / 2];
+    const bool full = base + kTlTile <= n;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint64_t i0 = base + q * 1024 + threadIdx.x * 4;
@@ -211,7 +213,7 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
       for (int e = 0; e < 4; ++e) {
         uint32_t l = 0;
         pk[q * 4 + e] = 0xffffffffu;
-        if (i0 + e < n) {
+        if (full || i0 + e < n) {
           const unsigned long long kk = map(cur[q][e], flags);
           mx = kk > mx ? kk : mx;
           if (kk < t.cells) {
@@ -297,18 +299,18 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
       }
       s_fill[b] = fill;
       s_page[b] = pg;
-      s_pa[b] = pa;
-      s_fa[b] = fa;
-      s_pb[b] = pb;
+      // continuation pages are consecutive, so rank r >= kPage - fa lands at
+      // (pb - 1) * kPage + fa + r
+      s_dst[b] = make_uint4(s_cnt[b], pa * kPage + fa, (pb - 1) * kPage + fa, kPage - fa);
     }
     __syncthreads();
     // element-parallel copy of the staged runs into their pages
     const uint32_t staged = s_cnt[t.B];
+#pragma unroll 4
     for (uint32_t i = threadIdx.x; i < staged; i += blockDim.x) {
-      const uint32_t b = s_bkt[i];
-      const uint32_t slot = s_fa[b] + (i - s_cnt[b]);
-      const uint32_t page = slot < kPage ? s_pa[b] : s_pb[b] + (slot - kPage) / kPage;
-      pages[(uint64_t)(page0 + page) * kPage + (slot & (kPage - 1))] = s_low[i];
+      const uint4 d = s_dst[s_bkt[i]];
+      const uint32_t r = i - d.x;
+      my_pages[(r < d.w ? d.y : d.z) + r] = s_low[i];
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)

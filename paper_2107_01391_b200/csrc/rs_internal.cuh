@@ -162,6 +162,7 @@ enum Slot : int {
   kSlotLows = 15,       // partitioned inner digits (uint16)
   kSlotDesc2 = 16,      // look-back descriptors of the second scan
   kSlotScratch = 17,
+  kSlotAlphabet = 18,   // string ordinal / symbol tables
 };
 
 }  // namespace rsb
