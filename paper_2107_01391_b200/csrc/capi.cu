@@ -422,13 +422,13 @@ unsigned long long magic_div(uint64_t d) { return ~0ull / d + 1ull; }  // ceil(2
 
 KvPass kv_pass(uint32_t g, uint32_t digits, uint64_t n) {
   KvPass p{};
-  if (!div_magic32(pow10u(3 * g), p.magic_div, p.shift_div)) {  // 10^9: 64-bit high product
-    p.magic_div = magic_div(pow10u(3 * g));
+  if (!div_magic32(pow10u(2 * g), p.magic_div, p.shift_div)) {  // no 32-bit magic: 64-bit high product
+    p.magic_div = magic_div(pow10u(2 * g));
     p.shift_div = 64;
   }
-  div_magic32(1000, p.magic_1000, p.shift_1000);
-  const uint32_t rem = digits - 3 * g;
-  p.bins = rem >= 3 ? 1000u : static_cast<uint32_t>(pow10u(rem));
+  div_magic32(100, p.magic_1000, p.shift_1000);
+  const uint32_t rem = digits - 2 * g;
+  p.bins = rem >= 2 ? 100u : static_cast<uint32_t>(pow10u(rem));
   const uint64_t tiles = (n + kKvTile - 1) / kKvTile;
   uint64_t G = (uint64_t)sm_count() * 3;
   if (G > tiles) G = tiles ? tiles : 1;
@@ -439,7 +439,7 @@ KvPass kv_pass(uint32_t g, uint32_t digits, uint64_t n) {
 
 void kv_sort(Workspace& ws, const uint32_t* keys, const uint32_t* vals, uint64_t n, uint32_t digits,
              uint32_t* keys_out, uint32_t* vals_out) {
-  const uint32_t passes = (digits + 2) / 3;
+  const uint32_t passes = (digits + 1) / 2;
   reset_stats(ws);
   uint32_t* tk = ws.get<uint32_t>(kSlotTmpKeys, n);
   uint32_t* tv = ws.get<uint32_t>(kSlotTmpVals, n);

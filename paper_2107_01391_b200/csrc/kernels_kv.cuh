@@ -3,16 +3,18 @@
 // The reference has no record API; its stable order is rsort's
 // originals_by_key (rsort.cpp:133-145) == baselines::radix_sort_lsd_by
 // (baselines.hpp:24-46), which makes base-10 LSD passes.  Here a pass takes a
-// group of three decimal digits (radix 1000: a 10x10x10 sub-grid of the
-// Cartesian count space), so a 6-digit key needs two stable passes instead of
-// six.  Stable order is unique, so the output is bit-identical to the
-// reference's for any stable schedule.
+// pair of decimal digits (radix 100: a 10x10 sub-grid of the Cartesian count
+// space), so a 6-digit key needs three stable passes instead of six.  (Triples
+// — radix 1000, two passes — measured 6 ms per pass on B200: the per-tile
+// work over 1000 digit bins and 4-record write runs dominated.)  Stable order
+// is unique, so the output is bit-identical to the reference's for any stable
+// schedule.
 //
 // Per pass (reduce-then-scan, deterministic):
 //   k_kv_chunk_hist     per-CTA digit counts over a contiguous chunk      R4
 //   exscan              [bins][G] -> each CTA's start in every digit run
 //   k_kv_chunk_scatter  the CTA walks its chunk tile by tile in order; each
-//                       warp ranks its records stably with 10 ballots over
+//                       warp ranks its records stably with 7 ballots over
 //                       the digit bits (no __match_any_sync, which measured
 //                       ~10x slower on B200), the tile is staged in shared
 //                       memory in digit order and written so consecutive
@@ -30,9 +32,9 @@ namespace rsb {
 constexpr int kKvThreads = 256;
 constexpr int kKvItems = 16;                    // records per thread per tile
 constexpr int kKvTile = kKvThreads * kKvItems;  // 4096 records
-constexpr int kKvBins = 1000;                   // three decimal digits
-constexpr int kKvBits = 10;                     // 1000 < 2^10
-constexpr int kKvMaxPasses = 4;                 // 10-digit uint32 keys
+constexpr int kKvBins = 100;                    // two decimal digits
+constexpr int kKvBits = 7;                      // 100 < 2^7
+constexpr int kKvMaxPasses = 5;                 // 10-digit uint32 keys
 constexpr int kKvWarps = kKvThreads / 32;
 constexpr size_t kKvSmemBytes = kKvWarps * kKvBins * 2  // s_wh
                                 + kKvBins * 4 * 3        // s_cnt, s_start, s_cur
@@ -41,10 +43,10 @@ constexpr size_t kKvSmemBytes = kKvWarps * kKvBins * 2  // s_wh
                                 + 64 * 4;
 
 struct KvPass {
-  unsigned long long magic_div;   // floor(k / 10^(3*pass)) = (k * magic_div) >> shift_div
-  unsigned long long magic_1000;  // floor(q / 1000) = (q * magic_1000) >> shift_1000
+  unsigned long long magic_div;   // floor(k / 10^(2*pass)) = (k * magic_div) >> shift_div
+  unsigned long long magic_1000;  // floor(q / 100) = (q * magic_1000) >> shift_1000
   uint32_t shift_div, shift_1000;
-  uint32_t bins;                  // 1000, or 10^(remaining digits) on the top pass
+  uint32_t bins;                  // 100, or 10 on a top pass with one digit left
   uint64_t chunk;                 // records per CTA (multiple of kKvTile)
   uint32_t G;                     // CTAs
 };
@@ -53,7 +55,7 @@ __device__ __forceinline__ uint32_t kv_digit(uint32_t key, const KvPass& p) {
   const uint32_t q = p.shift_div == 64
                          ? static_cast<uint32_t>(__umul64hi(static_cast<unsigned long long>(key), p.magic_div))
                          : static_cast<uint32_t>((static_cast<unsigned long long>(key) * p.magic_div) >> p.shift_div);
-  return q - 1000u * static_cast<uint32_t>((static_cast<unsigned long long>(q) * p.magic_1000) >> p.shift_1000);
+  return q - 100u * static_cast<uint32_t>((static_cast<unsigned long long>(q) * p.magic_1000) >> p.shift_1000);
 }
 
 __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __restrict__ keys, uint64_t n,
@@ -164,40 +166,23 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_scatter(const uint32_t*
       s_cnt[b] = run;
     }
     __syncthreads();
-    // tile-local exclusive scan over digits (4 per thread)
-    {
-      uint32_t loc[4], sum = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t b = threadIdx.x * 4 + q;
-        loc[q] = b < p.bins ? s_cnt[b] : 0u;
-        sum += loc[q];
-      }
-      uint32_t inc = sum;
+    // tile-local exclusive scan over digits (warp 0..3, one digit per lane)
+    if (threadIdx.x < 128) {
+      const uint32_t b = threadIdx.x;
+      const uint32_t c = b < p.bins ? s_cnt[b] : 0u;
+      uint32_t inc = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += y;
       }
       if (lane == 31) s_scan[warp] = inc;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t r = 0;
-        for (int w = 0; w < kKvWarps; ++w) {
-          const uint32_t c = s_scan[w];
-          s_scan[w] = r;
-          r += c;
-        }
-        s_total = r;
-      }
-      __syncthreads();
-      uint32_t run = s_scan[warp] + inc - sum;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t b = threadIdx.x * 4 + q;
-        if (b < p.bins) s_start[b] = run;
-        run += loc[q];
-      }
+      __syncwarp();
+      asm volatile("bar.sync 1, 128;");
+      uint32_t before = 0;
+      for (int w = 0; w < warp; ++w) before += s_scan[w];
+      if (b < p.bins) s_start[b] = before + inc - c;
+      if (b == 127) s_total = before + inc;
     }
     __syncthreads();
 #pragma unroll
