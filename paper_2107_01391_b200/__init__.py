@@ -98,10 +98,12 @@ def _cuda_tensor(t, dtypes, what):
 
 
 # ----------------------------------------------------------- device API
-def sort_u32(keys, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits: int = 0, out=None):
+def sort_u32(keys, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits: int = 0, out=None, msd: bool = False):
     """sort_integers for uint32 keys held in an int32/uint32 CUDA tensor.
 
-    Returns ``(sorted, report)``; ``sorted`` has the input's dtype."""
+    Returns ``(sorted, report)``; ``sorted`` has the input's dtype.  With
+    ``msd=True`` a key space above ``max_cells`` is split by MSD bucket passes
+    instead of raising cell_budget_exceeded."""
     torch = _torch()
     keys = _cuda_tensor(keys, (torch.int32, torch.uint32), "keys")
     n = keys.numel()
@@ -109,8 +111,8 @@ def sort_u32(keys, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits: int = 0,
         out = torch.empty_like(keys)
     rep = RsReport()
     lib = _lib.load()
-    _check(lib.rs_sort_u32(_ptr(keys), n, _ptr(out), out.numel(), ctypes.byref(_opts(max_cells, key_digits)),
-                           ctypes.byref(rep), _stream()))
+    _check(lib.rs_sort_u32(_ptr(keys), n, _ptr(out), out.numel(),
+                           ctypes.byref(_opts(max_cells, key_digits, msd)), ctypes.byref(rep), _stream()))
     return out, _report(rep)
 
 

@@ -18,6 +18,7 @@
 #include "kernels_kv.cuh"
 #include "kernels_two_level.cuh"
 #include "kernels_msd.cuh"
+#include "kernels_msd_engine.cuh"
 #include "recsort_b200.h"
 #include "rs_internal.cuh"
 
@@ -381,11 +382,14 @@ void grid_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, u
 
 uint64_t pow10u(uint32_t e) { return checked_pow(10, e); }
 
+void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t* out);
+
 // Shared driver for the decimal-integer paths (u32 and i64).
 template <class Map, class Out, class K>
 void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, const K* sorted,
                   uint64_t out_capacity, const rs_options* opt, rs_report* report,
-                  cudaStream_t stream, uint32_t max_digits) {
+                  cudaStream_t stream, uint32_t max_digits,
+                  void (*msd_u32)(Workspace&, const typename Map::In*, uint64_t, const K*) = nullptr) {
   ensure_device();
   const uint64_t budget = budget_of(opt);
   if (n > 0 && (!in || !sorted)) fail(RS_INVALID_ARGUMENT, "null device pointer");
@@ -400,6 +404,14 @@ void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, cons
   uint32_t digits = hint;
   if (!hinted) {
     digits = digit_count(device_max(ws, in, n, map));
+  }
+  if (msd_u32 && opt && opt->msd && pow10u(digits) > budget) {
+    // wide keys: MSD bucket passes + per-bucket grids
+    if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
+    msd_u32(ws, in, n, sorted);
+    const uint32_t d = static_cast<uint32_t>(ws.h_stats->report_digits);
+    if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{10, d, d}};
+    return;
   }
   make_key_spec(10, digits, digits, budget);  // budget gate before the grid exists
   if (out_capacity < n)
@@ -568,6 +580,115 @@ struct OutStr {
   }
 };
 
+
+// ------------------------------------------------------------ MSD engine
+// Segmented MSD over 8-bit digit sub-grids (kernels_msd_engine.cuh).  Levels
+// run until every segment became a leaf; each level synchronises once to
+// size the next one.  Leaves write the final output through `emit`.
+template <class Load, class Emit>
+void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emit) {
+  using K = typename Load::Key;
+  if (n == 0) return;
+  if (n >= 0xFFFFFFFFull) fail(RS_INVALID_ARGUMENT, "the MSD path sorts fewer than 2^32 keys per call");
+  K* buf[2] = {ws.get<K>(kSlotTmpKeys, n), ws.get<K>(kSlotTmpVals, n)};
+  const uint64_t cap = std::min<uint64_t>(n, 1ull << 26) + 256;
+  auto* segs_a = ws.get<MsdSeg>(kSlotCtaHist, cap);
+  auto* segs_b = ws.get<MsdSeg>(kSlotCtaOff, cap);
+  auto* leaf_grid = ws.get<MsdSeg>(kSlotBucketStart, cap);
+  auto* leaf_small = ws.get<MsdSeg>(kSlotLows, cap);
+  auto* leaf_copy = ws.get<MsdSeg>(kSlotTmpKeys2, cap);
+  auto* cnt = ws.get<unsigned>(kSlotScratch, 8);
+  auto* total = reinterpret_cast<unsigned long long*>(cnt + 4);
+  MsdSeg first{0, static_cast<uint32_t>(n), 0, 0};
+  RS_CUDA(cudaMemcpyAsync(segs_a, &first, sizeof(MsdSeg), cudaMemcpyHostToDevice, ws.stream));
+  uint32_t nseg = 1;
+  uint32_t shift = key_bits > kMsdDigitBits ? key_bits - kMsdDigitBits : 0;
+  MsdSeg* segs_in = segs_a;
+  MsdSeg* segs_out = segs_b;
+  for (int level = 0; nseg > 0; ++level) {
+    // chunks of every open segment
+    auto* ccount = ws.get<uint32_t>(kSlotMisc, 2ull * nseg + 2);
+    uint32_t* cstart = ccount + nseg + 1;
+    k_msd_chunk_counts<<<(nseg + 255) / 256, 256, 0, ws.stream>>>(segs_in, nseg, ccount);
+    RS_LAUNCH_CHECK();
+    exscan_u32(ws, ccount, nseg, cstart, total);
+    k_msd_chunk_assign<<<(nseg + 255) / 256, 256, 0, ws.stream>>>(segs_in, nseg, ccount, cstart);
+    RS_LAUNCH_CHECK();
+    unsigned long long nchunks = 0;
+    RS_CUDA(cudaMemcpyAsync(&nchunks, total, sizeof(nchunks), cudaMemcpyDeviceToHost, ws.stream));
+    RS_CUDA(cudaStreamSynchronize(ws.stream));
+    auto* chunk_seg = ws.get<uint32_t>(kSlotTileFirst, nchunks);
+    auto* table = ws.get<uint32_t>(kSlotCounts, nchunks * kMsdBins);
+    auto* off = ws.get<uint32_t>(kSlotOccEnd, nchunks * kMsdBins);
+    k_msd_chunks<<<nseg, 256, 0, ws.stream>>>(segs_in, nseg, chunk_seg);
+    RS_LAUNCH_CHECK();
+    K* dst = buf[level & 1];
+    {
+      PassTimer pt_(RS_PASS_MSD_HIST, ws.stream);
+      if (level == 0) k_msd_hist<<<nchunks, kMsdThreads, 0, ws.stream>>>(load0, segs_in, chunk_seg, shift, table);
+      else k_msd_hist<<<nchunks, kMsdThreads, 0, ws.stream>>>(LoadKeys<K>{buf[(level - 1) & 1]}, segs_in,
+                                                              chunk_seg, shift, table);
+      RS_LAUNCH_CHECK();
+    }
+    exscan_u32(ws, table, nchunks * kMsdBins, off, total);
+    {
+      PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
+      if (level == 0) k_msd_scatter<<<nchunks, kMsdThreads, 0, ws.stream>>>(load0, segs_in, chunk_seg, shift, off, dst);
+      else k_msd_scatter<<<nchunks, kMsdThreads, 0, ws.stream>>>(LoadKeys<K>{buf[(level - 1) & 1]}, segs_in,
+                                                                 chunk_seg, shift, off, dst);
+      RS_LAUNCH_CHECK();
+    }
+    RS_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned), ws.stream));
+    MsdLists L{segs_out, leaf_grid, leaf_small, leaf_copy, cnt};
+    const unsigned long long pairs = (unsigned long long)nseg * kMsdBins;
+    k_msd_classify<<<static_cast<unsigned>((pairs + 255) / 256), 256, 0, ws.stream>>>(segs_in, nseg, off, shift, L);
+    RS_LAUNCH_CHECK();
+    unsigned h[4] = {};
+    RS_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, ws.stream));
+    RS_CUDA(cudaStreamSynchronize(ws.stream));
+    if ((uint64_t)h[0] > cap || (uint64_t)h[1] > cap || (uint64_t)h[2] > cap || (uint64_t)h[3] > cap)
+      fail(RS_CUDA_ERROR, "MSD segment list overflow");
+    {
+      PassTimer pt_(RS_PASS_BUCKET, ws.stream, (h[1] ? 1 : 0) + (h[2] ? 1 : 0) + (h[3] ? 1 : 0));
+      if (h[3]) k_leaf_copy<K, Emit><<<h[3], 256, 0, ws.stream>>>(dst, leaf_copy, emit);
+      if (h[1]) {
+        const size_t smem = ((1u << shift) + 1) / 2 * sizeof(uint32_t);
+        RS_CUDA(cudaFuncSetAttribute(k_leaf_grid<K, Emit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        k_leaf_grid<K, Emit><<<h[1], kMsdThreads, smem, ws.stream>>>(dst, leaf_grid, shift, emit);
+      }
+      if (h[2]) k_leaf_bitonic<K, Emit><<<h[2], kMsdThreads, 0, ws.stream>>>(dst, leaf_small, emit);
+      RS_LAUNCH_CHECK();
+    }
+    nseg = h[0];
+    std::swap(segs_in, segs_out);
+    if (shift == 0 && nseg) fail(RS_CUDA_ERROR, "MSD: segments left after the last digit");
+    shift = shift > kMsdDigitBits ? shift - kMsdDigitBits : 0;
+  }
+}
+void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t* out) {
+  reset_stats(ws);
+  msd_sort(ws, LoadKeys<uint32_t>{in}, n, 32, EmitKey<uint32_t>{const_cast<uint32_t*>(out)});
+  {
+    PassTimer pt_(RS_PASS_REPORT, ws.stream);
+    k_report<uint32_t><<<1, 32, 0, ws.stream>>>(out, n, 10, 0, 0, 0, ws.stats);
+    RS_LAUNCH_CHECK();
+  }
+  pull_stats(ws);
+}
+
+void msd_sort_str(Workspace& ws, const uint8_t* chars, uint64_t n, uint32_t width, uint32_t w, uint32_t radix,
+                  const uint16_t* d_ord, const uint8_t* d_sym, uint8_t* out) {
+  reset_stats(ws);
+  msd_sort(ws, LoadStr{chars, width, d_ord}, n, 5 * width, EmitStr{out, width, d_sym});
+  {
+    PassTimer pt_(RS_PASS_REPORT, ws.stream);
+    k_report_recs<<<1, 32, 0, ws.stream>>>(out, n, width, w, radix, d_ord, ws.stats);
+    RS_LAUNCH_CHECK();
+  }
+  pull_stats(ws);
+}
+
 }  // namespace rsb
 
 using namespace rsb;
@@ -646,7 +767,7 @@ rs_status rs_sort_u32(const uint32_t* keys, uint64_t n, uint32_t* out, uint64_t 
   return guarded([&] {
     OutU32 o{out, 0u, aligned16(out)};
     integer_sort(keys, n, MapU32{}, o, out, out_capacity, opt, report,
-                 static_cast<cudaStream_t>(stream), 10);
+                 static_cast<cudaStream_t>(stream), 10, &msd_u32_entry);
   });
 }
 
@@ -813,7 +934,9 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
       return;
     }
     if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
-    msd_sort_str(ws, keys, n, t.radix, w, out, width, d_sym, report);
+    if (t.radix > 32) fail(RS_INVALID_ARGUMENT, "the MSD string path packs 5-bit ordinals: at most 31 symbols");
+    msd_sort_str(ws, chars, n, width, w, t.radix, d_ord, d_sym, out);
+    if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{t.radix, w, w}};
   });
 }
 
@@ -999,9 +1122,3 @@ rs_status rs_emit_u32(const uint32_t* counts, uint64_t cells, uint64_t cell_lo, 
 
 }  // extern "C"
 
-namespace rsb {
-void msd_sort_str(Workspace&, const unsigned long long*, uint64_t, uint32_t, uint32_t, uint8_t*,
-                  uint32_t, const uint8_t*, rs_report*) {
-  fail(RS_CELL_BUDGET_EXCEEDED, "MSD string path not built yet");
-}
-}  // namespace rsb

@@ -11,7 +11,7 @@
 
 namespace rsb {
 
-constexpr int kMsdThreads = 256;
+constexpr int kMsdThreads = 256;  // also used by kernels_msd_engine.cuh
 constexpr uint32_t kMsdSmemBuckets = 12288;
 
 // Histogram of bucket = key / divisor (magic-number division, exact for
@@ -118,9 +118,5 @@ __global__ void __launch_bounds__(kMsdThreads) k_part_scatter(const uint32_t* __
   }
 }
 
-struct Workspace;
-void msd_sort_str(Workspace& ws, const unsigned long long* keys, uint64_t n, uint32_t radix,
-                  uint32_t digits, uint8_t* out, uint32_t width, const uint8_t* d_sym,
-                  rs_report* report);
 
 }  // namespace rsb

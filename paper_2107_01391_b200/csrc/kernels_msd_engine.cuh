@@ -1,0 +1,430 @@
+// kernels_msd_engine.cuh — MSD bucket passes for keys too wide for one grid
+// (the reference raises cell_budget_exceeded instead,
+// key_model.cpp:72-76).
+//
+// Keys are 32- or 64-bit integers whose order is the sort order (uint32
+// keys; fixed-width strings packed 5 bits per symbol ordinal, which keeps
+// lexicographic order because every ordinal < 32).  Each level splits every
+// open segment by its next 8-bit digit — a 256-cell sub-grid of the
+// Cartesian space:
+//   k_msd_hist     per (segment, chunk) digit counts, layout per segment
+//                  [digit][chunk]                                    R
+//   exscan         ONE global look-back scan over all segments' tables:
+//                  entry (s, d, c) minus entry (s, 0, 0) is the key's
+//                  offset inside segment s
+//   k_msd_scatter  tiles staged in shared memory by digit, runs written to
+//                  the other buffer at their final positions           R + W
+//   k_msd_classify each (segment, digit) run becomes a leaf or a segment
+//                  of the next level
+// Leaves (no key leaves its final position again):
+//   k_leaf_grid    dense leaves (remaining bits <= 16): the recombinant
+//                  step itself — a shared-memory count grid over the
+//                  remaining 2^bits cells, scan, run-length emit         R + W
+//   k_leaf_bitonic small sparse leaves (<= 2048 keys): shared bitonic sort R + W
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels_grid.cuh"
+#include "kernels_msd.cuh"
+#include "rs_internal.cuh"
+
+namespace rsb {
+
+constexpr int kMsdDigitBits = 8;
+constexpr int kMsdBins = 1 << kMsdDigitBits;
+constexpr int kMsdTile = 4096;          // keys per scatter tile
+constexpr uint32_t kMsdChunk = 65536;   // keys per (segment, chunk) work item
+constexpr uint32_t kLeafSmall = 2048;   // bitonic leaf capacity
+constexpr int kLeafGridBits = 16;       // count-grid leaf: <= 2^16 cells (u16 pairs, 128 KB)
+
+struct MsdSeg {
+  unsigned long long start;  // position in the array (final position)
+  uint32_t size;
+  uint32_t chunk0;           // first chunk of this segment in the level's chunk list
+  uint32_t nchunks;
+};
+
+// ------------------------------------------------------------- loaders
+// Level 0 reads the caller's input through a loader; deeper levels read keys
+// from the ping-pong buffers.
+template <class K>
+struct LoadKeys {
+  using Key = K;
+  const K* p;
+  __device__ __forceinline__ K operator()(unsigned long long i) const { return __ldcs(p + i); }
+};
+
+// Fixed-width records -> packed key (5 bits per ordinal, pad ordinal 0,
+// first symbol most significant).  bad |= symbol outside the alphabet.
+struct LoadStr {
+  using Key = unsigned long long;
+  const uint8_t* recs;
+  uint32_t width;
+  const uint16_t* ord;  // device table (256 entries)
+  __device__ __forceinline__ unsigned long long operator()(unsigned long long i) const {
+    const uint8_t* r = recs + i * width;
+    unsigned long long k = 0;
+    bool ended = false;
+    for (uint32_t j = 0; j < width; ++j) {
+      uint32_t o = 0;
+      if (!ended) {
+        const uint8_t c = r[j];
+        if (c == 0) ended = true;
+        else o = __ldg(ord + c);
+      }
+      k = (k << 5) | o;
+    }
+    return k;
+  }
+};
+
+// ------------------------------------------------------------- emitters
+template <class K>
+struct EmitKey {
+  K* out;
+  __device__ __forceinline__ void operator()(unsigned long long pos, K key) const { out[pos] = key; }
+};
+
+// packed key -> record bytes (key_to_string, key_model.cpp:249-263: pad
+// ordinals become NUL bytes)
+struct EmitStr {
+  uint8_t* out;
+  uint32_t width;
+  const uint8_t* sym;  // device: ordinal -> byte, sym[0] = 0
+  __device__ __forceinline__ void operator()(unsigned long long pos, unsigned long long key) const {
+    uint8_t* r = out + pos * width;
+    for (int j = (int)width - 1; j >= 0; --j) {
+      r[j] = sym[key & 31u];
+      key >>= 5;
+    }
+  }
+};
+
+// ------------------------------------------------------------- level
+// chunk -> (segment) map: chunk_seg[c] = s
+__global__ void k_msd_chunks(const MsdSeg* __restrict__ segs, uint32_t nseg, uint32_t* __restrict__ chunk_seg) {
+  const uint32_t s = blockIdx.x;
+  if (s >= nseg) return;
+  const MsdSeg g = segs[s];
+  for (uint32_t c = threadIdx.x; c < g.nchunks; c += blockDim.x) chunk_seg[g.chunk0 + c] = s;
+}
+
+template <class Load>
+__global__ void __launch_bounds__(kMsdThreads) k_msd_hist(Load ld, const MsdSeg* __restrict__ segs,
+                                                          const uint32_t* __restrict__ chunk_seg, uint32_t shift,
+                                                          uint32_t* __restrict__ table) {
+  __shared__ uint32_t s_h[kMsdBins];
+  const uint32_t c = blockIdx.x;
+  const MsdSeg g = segs[chunk_seg[c]];
+  const uint32_t ci = c - g.chunk0;
+  for (int b = threadIdx.x; b < kMsdBins; b += blockDim.x) s_h[b] = 0;
+  __syncthreads();
+  const unsigned long long a = g.start + (unsigned long long)ci * kMsdChunk;
+  const uint32_t len = min(kMsdChunk, g.size - ci * kMsdChunk);
+  for (uint32_t i = threadIdx.x; i < len; i += blockDim.x)
+    atomicAdd(&s_h[(uint32_t)(ld(a + i) >> shift) & (kMsdBins - 1)], 1u);
+  __syncthreads();
+  uint32_t* t = table + (unsigned long long)g.chunk0 * kMsdBins;  // segment table [digit][chunk]
+  for (int b = threadIdx.x; b < kMsdBins; b += blockDim.x) t[(unsigned long long)b * g.nchunks + ci] = s_h[b];
+}
+
+template <class Load>
+__global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdSeg* __restrict__ segs,
+                                                             const uint32_t* __restrict__ chunk_seg, uint32_t shift,
+                                                             const uint32_t* __restrict__ off,
+                                                             typename Load::Key* __restrict__ dst) {
+  using K = typename Load::Key;
+  __shared__ uint32_t s_cur[kMsdBins];
+  __shared__ uint32_t s_cnt[kMsdBins + 1];
+  __shared__ K s_key[kMsdTile];
+  __shared__ uint8_t s_dig[kMsdTile];
+  __shared__ uint32_t s_scan[kMsdThreads / 32];
+  const uint32_t c = blockIdx.x;
+  const MsdSeg g = segs[chunk_seg[c]];
+  const uint32_t ci = c - g.chunk0;
+  const uint32_t* t = off + (unsigned long long)g.chunk0 * kMsdBins;
+  const uint32_t base0 = t[0];
+  for (int b = threadIdx.x; b < kMsdBins; b += blockDim.x) s_cur[b] = t[(unsigned long long)b * g.nchunks + ci] - base0;
+  const unsigned long long a = g.start + (unsigned long long)ci * kMsdChunk;
+  const uint32_t len = min(kMsdChunk, g.size - ci * kMsdChunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t t0 = 0; t0 < len; t0 += kMsdTile) {
+    const uint32_t tl = min((uint32_t)kMsdTile, len - t0);
+    for (int b = threadIdx.x; b <= kMsdBins; b += blockDim.x) s_cnt[b] = 0;
+    __syncthreads();
+    K k[kMsdTile / kMsdThreads];
+    uint32_t rk[kMsdTile / kMsdThreads];
+#pragma unroll
+    for (int j = 0; j < kMsdTile / kMsdThreads; ++j) {
+      const uint32_t i = t0 + j * kMsdThreads + threadIdx.x;
+      rk[j] = 0xffffffffu;
+      if (i < t0 + tl) {
+        k[j] = ld(a + i);
+        const uint32_t d = (uint32_t)(k[j] >> shift) & (kMsdBins - 1);
+        rk[j] = (d << 16) | atomicAdd(&s_cnt[d], 1u);
+      }
+    }
+    __syncthreads();
+    {  // exclusive scan of 256 counts, one per thread
+      const uint32_t v = s_cnt[threadIdx.x];
+      uint32_t inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) s_scan[warp] = inc;
+      __syncthreads();
+      uint32_t before = 0;
+      for (int w = 0; w < warp; ++w) before += s_scan[w];
+      __syncthreads();
+      s_cnt[threadIdx.x] = before + inc - v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kMsdTile / kMsdThreads; ++j) {
+      if (rk[j] != 0xffffffffu) {
+        const uint32_t d = rk[j] >> 16;
+        const uint32_t pos = s_cnt[d] + (rk[j] & 0xffffu);
+        s_key[pos] = k[j];
+        s_dig[pos] = static_cast<uint8_t>(d);
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < tl; i += blockDim.x) {
+      const uint32_t d = s_dig[i];
+      dst[g.start + s_cur[d] + (i - s_cnt[d])] = s_key[i];
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kMsdBins; b += blockDim.x) {
+      const uint32_t end = (b + 1 < kMsdBins) ? s_cnt[b + 1] : tl;
+      s_cur[b] += end - s_cnt[b];
+    }
+    __syncthreads();
+  }
+}
+
+// Leaf / next-segment lists (device counters in cnt[0..3]: next, grid,
+// small, copy).  Thread per (segment, digit).
+struct MsdLists {
+  MsdSeg* next;
+  MsdSeg* leaf_grid;
+  MsdSeg* leaf_small;
+  MsdSeg* leaf_copy;
+  unsigned* cnt;  // [4]
+};
+
+__global__ void k_msd_classify(const MsdSeg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ off,
+                               uint32_t rem_bits, MsdLists L) {
+  const unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t s = static_cast<uint32_t>(idx / kMsdBins);
+  const uint32_t d = static_cast<uint32_t>(idx % kMsdBins);
+  if (s >= nseg) return;
+  const MsdSeg g = segs[s];
+  const uint32_t* t = off + (unsigned long long)g.chunk0 * kMsdBins;
+  const uint32_t lo = t[(unsigned long long)d * g.nchunks] - t[0];
+  const uint32_t hi = (d + 1 < kMsdBins) ? t[(unsigned long long)(d + 1) * g.nchunks] - t[0] : g.size;
+  const uint32_t size = hi - lo;
+  if (size == 0) return;
+  const MsdSeg sub{g.start + lo, size, 0, 0};
+  // rem_bits = bits below this level's digit
+  if (rem_bits == 0 || size == 1) {
+    L.leaf_copy[atomicAdd(&L.cnt[3], 1u)] = sub;
+  } else if (rem_bits <= kLeafGridBits && size >= (1u << rem_bits) / 16 && size <= 65535u) {
+    L.leaf_grid[atomicAdd(&L.cnt[1], 1u)] = sub;
+  } else if (size <= kLeafSmall) {
+    L.leaf_small[atomicAdd(&L.cnt[2], 1u)] = sub;
+  } else {
+    L.next[atomicAdd(&L.cnt[0], 1u)] = sub;
+  }
+}
+
+// Fill chunk0 / nchunks of a segment list (exclusive scan of chunk counts).
+__global__ void k_msd_chunk_counts(const MsdSeg* __restrict__ segs, uint32_t nseg, uint32_t* __restrict__ counts) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nseg) counts[s] = (segs[s].size + kMsdChunk - 1) / kMsdChunk;
+}
+__global__ void k_msd_chunk_assign(MsdSeg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ counts,
+                                   const uint32_t* __restrict__ starts) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nseg) {
+    segs[s].chunk0 = starts[s];
+    segs[s].nchunks = counts[s];
+  }
+}
+
+// ------------------------------------------------------------- leaves
+template <class K, class Emit>
+__global__ void k_leaf_copy(const K* __restrict__ src, const MsdSeg* __restrict__ segs, Emit emit) {
+  const MsdSeg g = segs[blockIdx.x];
+  for (uint32_t i = threadIdx.x; i < g.size; i += blockDim.x) emit(g.start + i, src[g.start + i]);
+}
+
+// The recombinant step on a leaf: every key of the segment shares the bits
+// above rem_bits, so a count grid over the 2^rem_bits remaining cells sorts
+// it.  Counters are uint16 pairs in 32-bit words (segments hold < 65536
+// keys), grid <= 2^16 cells = 128 KB.
+template <class K, class Emit>
+__global__ void __launch_bounds__(kMsdThreads) k_leaf_grid(const K* __restrict__ src, const MsdSeg* __restrict__ segs,
+                                                           uint32_t rem_bits, Emit emit) {
+  extern __shared__ uint32_t s_w[];  // 2^rem_bits / 2 words
+  __shared__ uint32_t s_scan[kMsdThreads / 32];
+  const MsdSeg g = segs[blockIdx.x];
+  const uint32_t cells = 1u << rem_bits;
+  const uint32_t words = (cells + 1) / 2;
+  const K mask = (K(1) << rem_bits) - 1;
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) s_w[i] = 0;
+  __syncthreads();
+  const K prefix = src[g.start] & ~mask;
+  for (uint32_t i = threadIdx.x; i < g.size; i += blockDim.x) {
+    const uint32_t cell = static_cast<uint32_t>(src[g.start + i] & mask);
+    atomicAdd(&s_w[cell >> 1], 1u << ((cell & 1) * 16));
+  }
+  __syncthreads();
+  // exclusive scan over cells: each thread owns a contiguous run of words
+  const uint32_t per = (words + kMsdThreads - 1) / kMsdThreads;
+  const uint32_t w0 = threadIdx.x * per;
+  uint32_t sum = 0;
+  for (uint32_t j = 0; j < per; ++j)
+    if (w0 + j < words) sum += (s_w[w0 + j] & 0xffffu) + (s_w[w0 + j] >> 16);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_scan[warp] = inc;
+  __syncthreads();
+  uint32_t run = inc - sum;
+  for (int w = 0; w < warp; ++w) run += s_scan[w];
+  // emit this thread's cells in order (runs are short: a leaf is dense but
+  // has < 65536 keys over its cells)
+  for (uint32_t j = 0; j < per; ++j) {
+    const uint32_t wi = w0 + j;
+    if (wi >= words) break;
+    const uint32_t w = s_w[wi];
+    const uint32_t c0 = w & 0xffffu, c1 = w >> 16;
+    for (uint32_t q = 0; q < c0; ++q) emit(g.start + run + q, prefix | K(2 * wi));
+    run += c0;
+    for (uint32_t q = 0; q < c1; ++q) emit(g.start + run + q, prefix | K(2 * wi + 1));
+    run += c1;
+  }
+}
+
+// Small sparse leaf: shared bitonic sort of <= 2048 keys (padded with the
+// maximum key), then emit.
+template <class K, class Emit>
+__global__ void __launch_bounds__(kMsdThreads) k_leaf_bitonic(const K* __restrict__ src, const MsdSeg* __restrict__ segs,
+                                                              Emit emit) {
+  __shared__ K s[kLeafSmall];
+  const MsdSeg g = segs[blockIdx.x];
+  uint32_t n2 = 1;
+  while (n2 < g.size) n2 <<= 1;
+  for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) s[i] = i < g.size ? src[g.start + i] : ~K(0);
+  __syncthreads();
+  for (uint32_t k = 2; k <= n2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const K a = s[i], b = s[ixj];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            s[i] = b;
+            s[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < g.size; i += blockDim.x) emit(g.start + i, s[i]);
+}
+
+// ------------------------------------------------------------- report
+// Single-grid report for packed string keys: row = first
+// ordinal; span = last - first suffix (in base `radix`) within the row.
+__device__ __forceinline__ unsigned long long packed_to_radix(unsigned long long key, uint32_t width, uint32_t w,
+                                                              uint32_t radix) {
+  // key holds `width` 5-bit ordinals; the reference key uses the first w
+  unsigned long long v = 0;
+  for (uint32_t j = 0; j < w; ++j) v = v * radix + ((key >> (5 * (width - 1 - j))) & 31u);
+  return v;
+}
+
+__global__ void k_report_packed(const unsigned long long* __restrict__ sorted, uint64_t n, uint32_t width, uint32_t w,
+                                uint32_t radix, DevStats* st) {
+  unsigned long long span = 0;
+  const unsigned long long mod = d_pow(radix, w - 1);
+  for (uint32_t r = threadIdx.x; r < radix; r += blockDim.x) {
+    // keys with first ordinal r: [r << 5(width-1), (r+1) << 5(width-1))
+    const unsigned long long lo_key = (unsigned long long)r << (5 * (width - 1));
+    const unsigned long long hi_key = (unsigned long long)(r + 1) << (5 * (width - 1));
+    uint64_t a = 0, b = n;
+    while (a < b) {
+      const uint64_t mid = (a + b) >> 1;
+      if (sorted[mid] >= lo_key) b = mid;
+      else a = mid + 1;
+    }
+    uint64_t c = a, e = n;
+    while (c < e) {
+      const uint64_t mid = (c + e) >> 1;
+      if (sorted[mid] >= hi_key) e = mid;
+      else c = mid + 1;
+    }
+    if (a < c)
+      span += packed_to_radix(sorted[c - 1], width, w, radix) % mod -
+              packed_to_radix(sorted[a], width, w, radix) % mod + 1;
+  }
+  for (int o = 16; o > 0; o >>= 1) span += __shfl_xor_sync(0xffffffffu, span, o);
+  if (threadIdx.x == 0) {
+    st->cells_traversed = span;
+    st->report_digits = w;
+  }
+}
+
+// Same report read directly off sorted fixed-width records: row = ordinal of
+// the first byte, suffix = base-radix value of bytes 1..w-1 (pad = 0).
+__device__ __forceinline__ uint32_t rec_ord(const uint8_t* r, uint32_t j, uint32_t width, const uint16_t* ord) {
+  for (uint32_t q = 0; q < j; ++q)
+    if (r[q] == 0) return 0;
+  return j < width && r[j] ? ord[r[j]] : 0;
+}
+
+__global__ void k_report_recs(const uint8_t* __restrict__ recs, uint64_t n, uint32_t width, uint32_t w,
+                              uint32_t radix, const uint16_t* __restrict__ ord, DevStats* st) {
+  unsigned long long span = 0;
+  for (uint32_t r = threadIdx.x; r < radix; r += blockDim.x) {
+    uint64_t a = 0, b = n;  // first record with first ordinal >= r
+    while (a < b) {
+      const uint64_t mid = (a + b) >> 1;
+      if (rec_ord(recs + mid * width, 0, width, ord) >= r) b = mid;
+      else a = mid + 1;
+    }
+    uint64_t c = a, e = n;  // first record with first ordinal >= r+1
+    while (c < e) {
+      const uint64_t mid = (c + e) >> 1;
+      if (rec_ord(recs + mid * width, 0, width, ord) >= r + 1) e = mid;
+      else c = mid + 1;
+    }
+    if (a < c) {
+      unsigned long long lo = 0, hi = 0;
+      for (uint32_t j = 1; j < w; ++j) {
+        lo = lo * radix + rec_ord(recs + a * width, j, width, ord);
+        hi = hi * radix + rec_ord(recs + (c - 1) * width, j, width, ord);
+      }
+      span += hi - lo + 1;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) span += __shfl_xor_sync(0xffffffffu, span, o);
+  if (threadIdx.x == 0) {
+    st->cells_traversed = span;
+    st->report_digits = w;
+  }
+}
+
+}  // namespace rsb

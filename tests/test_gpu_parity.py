@@ -295,3 +295,63 @@ def rs_seed(cfg):
     from oracle import Oracle
 
     return Oracle().config_seed(cfg)
+
+
+# ------------------------------------------------- MSD (wide keys, A17)
+@pytest.mark.parametrize("n,bound", [(1 << 22, 0), (300_001, 0), (1 << 20, 10**9), (5000, 0)])
+def test_msd_u32_vs_oracle(rs, oracle, n, bound):
+    keys = oracle.gen_u32(oracle.config_seed(5), 0, n, bound)
+    want = np.sort(keys)
+    out, rep = rs.sort_u32(_t(keys.view(np.int32)), msd=True)
+    assert np.array_equal(_np_u32(out), want)
+    d = len(str(int(want[-1])))
+    assert _rep(rep) == oracle.report_from_sorted(want.astype(np.uint64), 10, d)
+
+
+def test_msd_u32_skew_and_duplicates(rs, oracle):
+    keys = np.concatenate([np.full(200_000, 4_000_000_000, dtype=np.uint32),
+                           oracle.gen_u32(8, 0, 100_000, 0), np.arange(70_000, dtype=np.uint32) * 7,
+                           np.full(70_000, 123, dtype=np.uint32)])
+    out, _ = rs.sort_u32(_t(keys.view(np.int32)), msd=True)
+    assert np.array_equal(_np_u32(out), np.sort(keys))
+
+
+def test_msd_strings_vs_oracle(rs, oracle, golden):
+    recs = oracle.gen_str_cfg4(oracle.config_seed(4), 0, 1 << 20)
+    want, wrep = oracle.sort_fixed_strings(recs)
+    out, rep = rs.sort_fixed_str(_t(recs), msd=True)
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert _rep(rep) == wrep
+    out, _ = rs.sort_fixed_str(_t(golden["cfg4_recs"]), msd=True)
+    assert np.array_equal(out.cpu().numpy(), golden["cfg4_sorted"])
+
+
+def test_msd_strings_variable_length(rs, oracle):
+    recs = oracle.gen_str_cfg4(17, 0, 200_000)
+    lens = oracle.gen_u32(18, 0, 200_000, 9)
+    for i, l in enumerate(lens):
+        recs[i, l:] = 0
+    want, wrep = oracle.sort_fixed_strings(recs)
+    out, rep = rs.sort_fixed_str(_t(recs), msd=True)
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert _rep(rep) == wrep
+
+
+def test_cfg5_full_size_properties(rs):
+    """2^31 full-range uint32 keys (BASELINE cfg5 on one GPU): sorted, and
+    the same multiset by order-independent hashes."""
+    import torch
+
+    n = 1 << 31
+    keys = gen_u32_device(rs, rs_seed(5), n, 0)
+    out, rep = rs.sort_u32(keys, msd=True)
+    assert rep.written == n and rep.spec.total_digits == 10
+    a = keys.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    b = out.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    assert bool((b[1:] >= b[:-1]).all())
+    for mul in (0x9E3779B1, 0x85EBCA77):
+        ha = ((a * mul) & 0xFFFFFFFF).sum()
+        hb = ((b * mul) & 0xFFFFFFFF).sum()
+        assert int(ha) == int(hb)
+    del a, b, out, keys
+    torch.cuda.empty_cache()
