@@ -1,0 +1,111 @@
+"""Multi-GPU host logic (paper_2107_01391_b200/dist.py) on CPU:
+world-size-2 gloo process groups with the device phases replaced by
+test-only numpy stand-ins.  What is exercised is exactly the product's
+collective / splitter / range logic: the grid all-reduce, the contiguous cell
+ranges per rank, the MSD bucket splitters, the all-to-all exchange and the
+concatenation property (rank outputs in rank order == the sorted input)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2107_01391_b200.dist import bucket_splitters, cell_ranges, range_partition_sort, sharded_grid_sort
+
+
+class NumpyOps:
+    """Test-only stand-ins for GpuOps (the product always uses the CUDA library)."""
+
+    def count(self, keys, cells):
+        return torch.from_numpy(np.bincount(keys.numpy().astype(np.int64), minlength=cells).astype(np.int32))
+
+    def emit(self, counts, lo, hi, n_out):
+        c = counts.numpy()[lo:hi].astype(np.int64)
+        out = np.repeat(np.arange(lo, hi, dtype=np.int64), c).astype(np.int32)
+        assert out.size == n_out
+        return torch.from_numpy(out)
+
+    def bucket_hist(self, keys, divisor, buckets):
+        b = (keys.numpy().view(np.uint32).astype(np.int64) // divisor)
+        return torch.from_numpy(np.bincount(b, minlength=buckets).astype(np.int64))
+
+    def partition(self, keys, divisor, bounds):
+        k = keys.numpy().view(np.uint32).astype(np.int64)
+        part = np.searchsorted(np.asarray(bounds[1:-1]), k // divisor, side="right")
+        order = np.argsort(part, kind="stable")
+        return torch.from_numpy(keys.numpy()[order].copy()), np.bincount(part, minlength=len(bounds) - 1).tolist()
+
+    def sort(self, keys, key_digits=0):
+        return torch.from_numpy(np.sort(keys.numpy().view(np.uint32)).view(np.int32))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, mode, shared):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        keys = shared["keys"]
+        n = keys.numel()
+        mine = keys[rank * n // world:(rank + 1) * n // world].clone()
+        if mode == "grid":
+            out = sharded_grid_sort(mine, shared["cells"], ops=NumpyOps())
+        else:
+            out = range_partition_sort(mine, shared["divisor"], shared["buckets"], ops=NumpyOps())
+        torch.save(out, shared["dir"] + f"/out{rank}.pt")
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(mode, keys, tmp_path, **kw):
+    world = 2
+    shared = {"keys": keys, "dir": str(tmp_path), **kw}
+    mp.spawn(_worker, args=(world, _free_port(), mode, shared), nprocs=world, join=True)
+    return [torch.load(str(tmp_path) + f"/out{r}.pt") for r in range(world)]
+
+
+def test_cell_ranges_balance_and_cover():
+    counts = torch.tensor([5, 0, 0, 7, 1, 1, 0, 9, 2, 3])
+    prefix = torch.cumsum(counts, 0)
+    for world in (1, 2, 3, 4, 8):
+        r = cell_ranges(prefix, world)
+        assert r[0][0] == 0 and r[-1][1] == counts.numel()
+        assert all(a[1] == b[0] for a, b in zip(r, r[1:]))  # contiguous, cuts on cell boundaries
+    r = cell_ranges(prefix, 2)
+    left = int(counts[r[0][0]:r[0][1]].sum())
+    assert abs(left - (28 - left)) <= 9  # never splits a cell; within one cell of balance
+
+
+def test_bucket_splitters_cover_all_buckets():
+    hist = torch.tensor([0, 100, 3, 3, 3, 200, 0, 50])
+    b = bucket_splitters(hist, 4)
+    assert b[0] == 0 and b[-1] == hist.numel() and len(b) == 5
+    assert all(x <= y for x, y in zip(b, b[1:]))
+
+
+def test_sharded_grid_sort_gloo(tmp_path):
+    rng = np.random.default_rng(3)
+    keys = torch.from_numpy(rng.integers(0, 10**5, 200_001).astype(np.int32))
+    outs = _run("grid", keys, tmp_path, cells=10**5)
+    got = np.concatenate([o.numpy() for o in outs])
+    assert np.array_equal(got, np.sort(keys.numpy()))
+    # the rank slices are contiguous cell ranges and roughly balanced
+    assert abs(outs[0].numel() - outs[1].numel()) < 200_001 // 10
+
+
+def test_range_partition_sort_gloo(tmp_path):
+    rng = np.random.default_rng(4)
+    keys = torch.from_numpy(rng.integers(0, 2**32, 100_003, dtype=np.uint64).astype(np.uint32).view(np.int32))
+    outs = _run("range", keys, tmp_path, divisor=10**7, buckets=430)
+    got = np.concatenate([o.numpy().view(np.uint32) for o in outs])
+    assert np.array_equal(got, np.sort(keys.numpy().view(np.uint32)))
