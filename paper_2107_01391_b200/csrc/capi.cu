@@ -655,7 +655,7 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
         const size_t smem = ((1u << shift) + 1) / 2 * sizeof(uint32_t);
         RS_CUDA(cudaFuncSetAttribute(k_leaf_grid<K, Emit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-        k_leaf_grid<K, Emit><<<h[1], kMsdThreads, smem, ws.stream>>>(dst, leaf_grid, shift, emit);
+        k_leaf_grid<K, Emit><<<h[1], kLeafGridThreads, smem, ws.stream>>>(dst, leaf_grid, shift, emit);
       }
       if (h[2]) k_leaf_bitonic<K, Emit><<<h[2], kMsdThreads, 0, ws.stream>>>(dst, leaf_small, emit);
       RS_LAUNCH_CHECK();

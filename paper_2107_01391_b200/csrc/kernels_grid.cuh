@@ -86,11 +86,14 @@ __device__ __forceinline__ void count_cell_global(uint32_t* __restrict__ counts,
 // outside the spec, hashing.cpp:31-34).
 struct MapU32 {
   using In = uint32_t;
+  using Key = uint32_t;  // mapped keys fit 32 bits: the partition works in 32-bit arithmetic
   __device__ __forceinline__ unsigned long long operator()(uint32_t k, unsigned&) const { return k; }
+  __device__ __forceinline__ uint32_t key32(uint32_t k, unsigned&) const { return k; }
 };
 
 struct MapI64 {
   using In = int64_t;
+  using Key = unsigned long long;
   __device__ __forceinline__ unsigned long long operator()(int64_t v, unsigned& flags) const {
     if (v < 0) {
       flags |= kFlagNegative;
@@ -102,6 +105,7 @@ struct MapI64 {
 
 struct MapU64 {
   using In = unsigned long long;
+  using Key = unsigned long long;
   __device__ __forceinline__ unsigned long long operator()(unsigned long long v, unsigned&) const { return v; }
 };
 
@@ -119,6 +123,7 @@ struct MapU64 {
 // rounded, so every "rounds to x" test is exact.
 struct MapF64 {
   using In = double;
+  using Key = unsigned long long;
   double P;      // 10^scale
   double P2;     // 2 * 10^scale
   double limit;  // 2^53 / 100

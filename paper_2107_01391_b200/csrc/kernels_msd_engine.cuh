@@ -39,6 +39,7 @@ constexpr int kMsdTile = 4096;          // keys per scatter tile
 constexpr uint32_t kMsdChunk = 65536;   // keys per (segment, chunk) work item
 constexpr uint32_t kLeafSmall = 2048;   // bitonic leaf capacity
 constexpr int kLeafGridBits = 16;       // count-grid leaf: <= 2^16 cells (u16 pairs, 128 KB)
+constexpr int kLeafGridThreads = 1024;  // one 128 KB CTA per SM: 32 warps to hide latency
 
 struct MsdSeg {
   unsigned long long start;  // position in the array (final position)
@@ -268,10 +269,11 @@ __global__ void k_leaf_copy(const K* __restrict__ src, const MsdSeg* __restrict_
 // it.  Counters are uint16 pairs in 32-bit words (segments hold < 65536
 // keys), grid <= 2^16 cells = 128 KB.
 template <class K, class Emit>
-__global__ void __launch_bounds__(kMsdThreads) k_leaf_grid(const K* __restrict__ src, const MsdSeg* __restrict__ segs,
-                                                           uint32_t rem_bits, Emit emit) {
+__global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restrict__ src,
+                                                                const MsdSeg* __restrict__ segs, uint32_t rem_bits,
+                                                                Emit emit) {
   extern __shared__ uint32_t s_w[];  // 2^rem_bits / 2 words
-  __shared__ uint32_t s_scan[kMsdThreads / 32];
+  __shared__ uint32_t s_scan[kLeafGridThreads / 32];
   const MsdSeg g = segs[blockIdx.x];
   const uint32_t cells = 1u << rem_bits;
   const uint32_t words = (cells + 1) / 2;
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(kMsdThreads) k_leaf_grid(const K* __restrict__
   }
   __syncthreads();
   // exclusive scan over cells: each thread owns a contiguous run of words
-  const uint32_t per = (words + kMsdThreads - 1) / kMsdThreads;
+  const uint32_t per = (words + kLeafGridThreads - 1) / kLeafGridThreads;
   const uint32_t w0 = threadIdx.x * per;
   uint32_t sum = 0;
   for (uint32_t j = 0; j < per; ++j)

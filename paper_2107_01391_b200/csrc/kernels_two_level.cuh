@@ -150,7 +150,7 @@ __host__ __device__ constexpr size_t kPagePartitionOffset(uint32_t B) {
   return (((size_t)B + 1) * 4 + (size_t)B * 12 + 15) / 16 * 16 + (size_t)B * 16;
 }
 __host__ __device__ constexpr size_t kPagePartitionSmem(uint32_t B) {
-  return kPagePartitionOffset(B) + (size_t)kTlTile * 4;  // s_low + s_bkt
+  return kPagePartitionOffset(B) + (size_t)kTlTile * 4;  // staged (bucket << 16 | inner digit)
 }
 
 template <class Map>
@@ -170,8 +170,7 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
   // per bucket, this tile: {run start in staging, dest of rank r < thr = A + r,
   // else Bv + r, thr} (dest = index into the CTA's page region)
   uint4* s_dst = reinterpret_cast<uint4*>(tl_smem + (((size_t)t.B + 1) * 4 + (size_t)t.B * 12 + 15) / 16 * 16);
-  uint16_t* s_low = reinterpret_cast<uint16_t*>(tl_smem + kPagePartitionOffset(t.B));
-  uint16_t* s_bkt = s_low + kTlTile;
+  uint32_t* s_stage = reinterpret_cast<uint32_t*>(tl_smem + kPagePartitionOffset(t.B));
   __shared__ uint32_t s_scan[kTlThreads / 32];
   __shared__ uint32_t s_next;  // next free page of this CTA's region
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -184,6 +183,8 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
   }
   if (threadIdx.x == 0) s_next = 0;
   unsigned long long mx = 0;
+  uint32_t mx32 = 0;
+  const uint32_t cells32 = t.cells > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(t.cells);
   unsigned flags = 0, ovf = 0;
   const uint32_t per = (t.B + kTlThreads - 1) / kTlThreads;
   In cur[4][4], nxt[4][4];
@@ -214,14 +215,27 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
         uint32_t l = 0;
         pk[q * 4 + e] = 0xffffffffu;
         if (full || i0 + e < n) {
-          const unsigned long long kk = map(cur[q][e], flags);
-          mx = kk > mx ? kk : mx;
-          if (kk < t.cells) {
-            const uint32_t b = tl_bucket(static_cast<uint32_t>(kk), t);
-            l = static_cast<uint32_t>(kk) - b * t.S;
-            pk[q * 4 + e] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
+          if constexpr (sizeof(typename Map::Key) == 4) {
+            // 32-bit keys: compares, max and bucket math stay 32-bit
+            const uint32_t kk = map.key32(cur[q][e], flags);
+            mx32 = kk > mx32 ? kk : mx32;
+            if (kk < cells32) {
+              const uint32_t b = tl_bucket(kk, t);
+              l = kk - b * t.S;
+              pk[q * 4 + e] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
+            } else {
+              ovf = 1;
+            }
           } else {
-            ovf = 1;
+            const unsigned long long kk = map(cur[q][e], flags);
+            mx = kk > mx ? kk : mx;
+            if (kk < t.cells) {
+              const uint32_t b = tl_bucket(static_cast<uint32_t>(kk), t);
+              l = static_cast<uint32_t>(kk) - b * t.S;
+              pk[q * 4 + e] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
+            } else {
+              ovf = 1;
+            }
           }
         }
         if (e & 1) lo2[(q * 4 + e) >> 1] |= l << 16;
@@ -265,9 +279,8 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
 #pragma unroll
     for (int j = 0; j < kTlPerThread; ++j) {
       if (pk[j] != 0xffffffffu) {
-        const uint32_t pos = s_cnt[pk[j] >> 16] + (pk[j] & 0xffffu);
-        s_low[pos] = static_cast<uint16_t>(lo2[j >> 1] >> ((j & 1) * 16));
-        s_bkt[pos] = static_cast<uint16_t>(pk[j] >> 16);
+        const uint32_t b = pk[j] >> 16;
+        s_stage[s_cnt[b] + (pk[j] & 0xffffu)] = (b << 16) | ((lo2[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
       }
     }
     // page bookkeeping, one thread per bucket: a run that does not fit the
@@ -308,9 +321,10 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
     const uint32_t staged = s_cnt[t.B];
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < staged; i += blockDim.x) {
-      const uint4 d = s_dst[s_bkt[i]];
+      const uint32_t w = s_stage[i];
+      const uint4 d = s_dst[w >> 16];
       const uint32_t r = i - d.x;
-      my_pages[(r < d.w ? d.y : d.z) + r] = s_low[i];
+      my_pages[(r < d.w ? d.y : d.z) + r] = static_cast<uint16_t>(w);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -323,7 +337,7 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
     if (s_page[b] != 0xffffffffu) page_fill[page0 + s_page[b]] = static_cast<uint16_t>(s_fill[b]);
     pc_bm[(uint64_t)b * t.G + blockIdx.x] = s_np[b];
   }
-  warp_max_to(mx, &st->max_key);
+  warp_max_to(mx > mx32 ? mx : mx32, &st->max_key);
   flags = warp_or(flags | (ovf ? 0x80000000u : 0u));
   if ((threadIdx.x & 31) == 0 && flags) {
     if (flags & 0x7fffffffu) atomicOr(&st->flags, flags & 0x7fffffffu);
