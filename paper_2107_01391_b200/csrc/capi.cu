@@ -474,7 +474,8 @@ void kv_sort(Workspace& ws, const uint32_t* keys, const uint32_t* vals, uint64_t
     uint32_t* dv = to_out ? vals_out : tv;
     {
       PassTimer pt_(RS_PASS_KV_HIST, ws.stream);
-      k_kv_chunk_hist<<<p.G, kKvThreads, 0, ws.stream>>>(sk, n, p, aligned16(sk), hist, ws.stats);
+      RS_CUDA(cudaMemsetAsync(hist, 0, bg * sizeof(uint32_t), ws.stream));
+      k_kv_chunk_hist<<<p.G * kKvHistSplit, kKvThreads, 0, ws.stream>>>(sk, n, p, aligned16(sk), hist, ws.stats);
       RS_LAUNCH_CHECK();
     }
     exscan_u32(ws, hist, bg, off, total);
@@ -597,8 +598,9 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
   auto* leaf_grid = ws.get<MsdSeg>(kSlotBucketStart, cap);
   auto* leaf_small = ws.get<MsdSeg>(kSlotLows, cap);
   auto* leaf_copy = ws.get<MsdSeg>(kSlotTmpKeys2, cap);
+  auto* leaf_warp = ws.get<MsdSeg>(kSlotTmpVals2, cap);
   auto* cnt = ws.get<unsigned>(kSlotScratch, 8);
-  auto* total = reinterpret_cast<unsigned long long*>(cnt + 4);
+  auto* total = reinterpret_cast<unsigned long long*>(cnt + 6);
   MsdSeg first{0, static_cast<uint32_t>(n), 0, 0};
   RS_CUDA(cudaMemcpyAsync(segs_a, &first, sizeof(MsdSeg), cudaMemcpyHostToDevice, ws.stream));
   uint32_t nseg = 1;
@@ -638,18 +640,22 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
                                                                  chunk_seg, shift, off, dst);
       RS_LAUNCH_CHECK();
     }
-    RS_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned), ws.stream));
-    MsdLists L{segs_out, leaf_grid, leaf_small, leaf_copy, cnt};
+    RS_CUDA(cudaMemsetAsync(cnt, 0, 5 * sizeof(unsigned), ws.stream));
+    MsdLists L{segs_out, leaf_grid, leaf_small, leaf_copy, leaf_warp, cnt};
     const unsigned long long pairs = (unsigned long long)nseg * kMsdBins;
     k_msd_classify<<<static_cast<unsigned>((pairs + 255) / 256), 256, 0, ws.stream>>>(segs_in, nseg, off, shift, L);
     RS_LAUNCH_CHECK();
-    unsigned h[4] = {};
+    unsigned h[5] = {};
     RS_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, ws.stream));
     RS_CUDA(cudaStreamSynchronize(ws.stream));
-    if ((uint64_t)h[0] > cap || (uint64_t)h[1] > cap || (uint64_t)h[2] > cap || (uint64_t)h[3] > cap)
-      fail(RS_CUDA_ERROR, "MSD segment list overflow");
+    for (unsigned v : h)
+      if ((uint64_t)v > cap) fail(RS_CUDA_ERROR, "MSD segment list overflow");
     {
-      PassTimer pt_(RS_PASS_BUCKET, ws.stream, (h[1] ? 1 : 0) + (h[2] ? 1 : 0) + (h[3] ? 1 : 0));
+      PassTimer pt_(RS_PASS_BUCKET, ws.stream, (h[1] ? 1 : 0) + (h[2] ? 1 : 0) + (h[3] ? 1 : 0) + (h[4] ? 1 : 0));
+      if (h[4]) {
+        const unsigned blocks = std::min<unsigned>((h[4] + 7) / 8, sm_count() * 16);
+        k_leaf_warp<K, Emit><<<blocks, kMsdThreads, 0, ws.stream>>>(dst, leaf_warp, h[4], emit);
+      }
       if (h[3]) k_leaf_copy<K, Emit><<<h[3], 256, 0, ws.stream>>>(dst, leaf_copy, emit);
       if (h[1]) {
         const size_t smem = ((1u << shift) + 1) / 2 * sizeof(uint32_t);

@@ -58,6 +58,9 @@ __device__ __forceinline__ uint32_t kv_digit(uint32_t key, const KvPass& p) {
   return q - 100u * static_cast<uint32_t>((static_cast<unsigned long long>(q) * p.magic_1000) >> p.shift_1000);
 }
 
+// grid = G x kKvHistSplit: CTA (c, s) counts sub-range s of chunk c and adds
+// its counts into hist[d][c] (zeroed by the host).
+constexpr int kKvHistSplit = 4;
 __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __restrict__ keys, uint64_t n,
                                                               KvPass p, bool aligned,
                                                               uint32_t* __restrict__ hist,  // [bins][G]
@@ -65,8 +68,11 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __
   __shared__ uint32_t s_h[kKvBins];
   for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) s_h[b] = 0;
   __syncthreads();
-  const uint64_t c0 = (uint64_t)blockIdx.x * p.chunk;
-  const uint64_t c1 = c0 + p.chunk < n ? c0 + p.chunk : n;
+  const uint32_t c = blockIdx.x / kKvHistSplit, sub = blockIdx.x % kKvHistSplit;
+  const uint64_t span = p.chunk / kKvHistSplit;  // chunk is a multiple of kKvTile
+  const uint64_t cend = (uint64_t)c * p.chunk + p.chunk < n ? (uint64_t)c * p.chunk + p.chunk : n;
+  const uint64_t c0 = (uint64_t)c * p.chunk + sub * span;
+  const uint64_t c1 = sub + 1 == kKvHistSplit ? cend : (c0 + span < cend ? c0 + span : cend);
   unsigned long long mx = 0;
   for (uint64_t base = c0; base < c1; base += kKvTile) {
 #pragma unroll
@@ -89,7 +95,8 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __
     }
   }
   __syncthreads();
-  for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) hist[(uint64_t)b * p.G + blockIdx.x] = s_h[b];
+  for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x)
+    if (s_h[b]) atomicAdd(&hist[(uint64_t)b * p.G + c], s_h[b]);
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long w = __shfl_xor_sync(0xffffffffu, mx, o);
     mx = w > mx ? w : mx;

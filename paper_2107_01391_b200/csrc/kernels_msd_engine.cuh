@@ -37,7 +37,8 @@ constexpr int kMsdDigitBits = 8;
 constexpr int kMsdBins = 1 << kMsdDigitBits;
 constexpr int kMsdTile = 4096;          // keys per scatter tile
 constexpr uint32_t kMsdChunk = 65536;   // keys per (segment, chunk) work item
-constexpr uint32_t kLeafSmall = 2048;   // bitonic leaf capacity
+constexpr uint32_t kLeafSmall = 2048;   // shared bitonic leaf capacity
+constexpr uint32_t kLeafWarp = 32;      // warp (register) bitonic leaf capacity
 constexpr int kLeafGridBits = 16;       // count-grid leaf: <= 2^16 cells (u16 pairs, 128 KB)
 constexpr int kLeafGridThreads = 1024;  // one 128 KB CTA per SM: 32 warps to hide latency
 
@@ -215,7 +216,8 @@ struct MsdLists {
   MsdSeg* leaf_grid;
   MsdSeg* leaf_small;
   MsdSeg* leaf_copy;
-  unsigned* cnt;  // [4]
+  MsdSeg* leaf_warp;
+  unsigned* cnt;  // [5]: next, grid, small, copy, warp
 };
 
 __global__ void k_msd_classify(const MsdSeg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ off,
@@ -235,11 +237,13 @@ __global__ void k_msd_classify(const MsdSeg* __restrict__ segs, uint32_t nseg, c
   if (rem_bits == 0 || size == 1) {
     L.leaf_copy[atomicAdd(&L.cnt[3], 1u)] = sub;
   } else if (rem_bits <= kLeafGridBits && size >= (1u << rem_bits) / 16 && size <= 65535u) {
-    L.leaf_grid[atomicAdd(&L.cnt[1], 1u)] = sub;
-  } else if (size <= kLeafSmall) {
-    L.leaf_small[atomicAdd(&L.cnt[2], 1u)] = sub;
+    L.leaf_grid[atomicAdd(&L.cnt[1], 1u)] = sub;  // dense: the count grid
+  } else if (size <= kLeafWarp) {
+    L.leaf_warp[atomicAdd(&L.cnt[4], 1u)] = sub;  // tiny: one warp, registers
+  } else if (size <= kLeafSmall && rem_bits <= kMsdDigitBits) {
+    L.leaf_small[atomicAdd(&L.cnt[2], 1u)] = sub;  // last digit: shared bitonic
   } else {
-    L.next[atomicAdd(&L.cnt[0], 1u)] = sub;
+    L.next[atomicAdd(&L.cnt[0], 1u)] = sub;  // split by the next 8-bit digit
   }
 }
 
@@ -345,6 +349,30 @@ __global__ void __launch_bounds__(kMsdThreads) k_leaf_bitonic(const K* __restric
     }
   }
   for (uint32_t i = threadIdx.x; i < g.size; i += blockDim.x) emit(g.start + i, s[i]);
+}
+
+// Tiny leaves (<= 32 keys): one warp per segment, lane i holds key i, a
+// register bitonic network over shuffles; warps stride over the list.
+template <class K, class Emit>
+__global__ void __launch_bounds__(kMsdThreads) k_leaf_warp(const K* __restrict__ src, const MsdSeg* __restrict__ segs,
+                                                           uint32_t nseg, Emit emit) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x / 32);
+  for (uint32_t s = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); s < nseg; s += nw) {
+    const MsdSeg g = segs[s];
+    K v = lane < g.size ? src[g.start + lane] : ~K(0);
+#pragma unroll
+    for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        const K o = __shfl_xor_sync(0xffffffffu, v, j);
+        const bool up = (lane & k) == 0;
+        const bool lower = (lane & j) == 0;
+        v = (lower == up) ? (v < o ? v : o) : (v < o ? o : v);
+      }
+    }
+    if (lane < g.size) emit(g.start + lane, v);
+  }
 }
 
 // ------------------------------------------------------------- report
