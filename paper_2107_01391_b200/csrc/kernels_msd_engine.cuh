@@ -57,6 +57,30 @@ struct LoadKeys {
   using Key = K;
   const K* p;
   __device__ __forceinline__ K operator()(unsigned long long i) const { return __ldcs(p + i); }
+  // A tile of up to kMsdTile keys at a: 16-byte vectors when a is aligned
+  // (thread t takes elements 4t..4t+3 of each 1024-element quarter), else
+  // element j*256+t.  Order inside a tile is irrelevant to the partition.
+  __device__ __forceinline__ void load16(unsigned long long a, uint32_t tl, K (&k)[kMsdTile / kMsdThreads]) {
+    vec_ = (sizeof(K) == 4) && ((reinterpret_cast<uintptr_t>(p + a) & 15) == 0) && tl == kMsdTile;
+    if (vec_) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 w = __ldcs(reinterpret_cast<const uint4*>(p + a) + q * kMsdThreads + threadIdx.x);
+        k[4 * q] = static_cast<K>(w.x); k[4 * q + 1] = static_cast<K>(w.y);
+        k[4 * q + 2] = static_cast<K>(w.z); k[4 * q + 3] = static_cast<K>(w.w);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kMsdTile / kMsdThreads; ++j) {
+        const uint32_t i = j * kMsdThreads + threadIdx.x;
+        k[j] = i < tl ? __ldcs(p + a + i) : K(0);
+      }
+    }
+  }
+  __device__ __forceinline__ bool valid(int j, uint32_t tl) const {
+    return vec_ || (uint32_t)(j * kMsdThreads + threadIdx.x) < tl;
+  }
+  bool vec_ = false;
 };
 
 // Fixed-width records -> packed key (5 bits per ordinal, pad ordinal 0,
@@ -66,6 +90,14 @@ struct LoadStr {
   const uint8_t* recs;
   uint32_t width;
   const uint16_t* ord;  // device table (256 entries)
+  __device__ __forceinline__ void load16(unsigned long long a, uint32_t tl, Key (&k)[kMsdTile / kMsdThreads]) const {
+#pragma unroll
+    for (int j = 0; j < kMsdTile / kMsdThreads; ++j) {
+      const uint32_t i = j * kMsdThreads + threadIdx.x;
+      k[j] = i < tl ? (*this)(a + i) : 0ull;
+    }
+  }
+  __device__ __forceinline__ bool valid(int j, uint32_t tl) const { return (uint32_t)(j * kMsdThreads + threadIdx.x) < tl; }
   __device__ __forceinline__ unsigned long long operator()(unsigned long long i) const {
     const uint8_t* r = recs + i * width;
     unsigned long long k = 0;
@@ -139,10 +171,11 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdS
                                                              const uint32_t* __restrict__ off,
                                                              typename Load::Key* __restrict__ dst) {
   using K = typename Load::Key;
-  __shared__ uint32_t s_cur[kMsdBins];
-  __shared__ uint32_t s_cnt[kMsdBins + 1];
+  constexpr int kPer = kMsdTile / kMsdThreads;  // 16 keys per thread per tile
+  __shared__ uint32_t s_base[kMsdBins];  // segment-relative destination of this tile's digit run, minus its start
+  __shared__ uint32_t s_cur[kMsdBins];   // running segment-relative cursor per digit
+  __shared__ uint32_t s_cnt[kMsdBins];
   __shared__ K s_key[kMsdTile];
-  __shared__ uint8_t s_dig[kMsdTile];
   __shared__ uint32_t s_scan[kMsdThreads / 32];
   const uint32_t c = blockIdx.x;
   const MsdSeg g = segs[chunk_seg[c]];
@@ -152,19 +185,19 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdS
   for (int b = threadIdx.x; b < kMsdBins; b += blockDim.x) s_cur[b] = t[(unsigned long long)b * g.nchunks + ci] - base0;
   const unsigned long long a = g.start + (unsigned long long)ci * kMsdChunk;
   const uint32_t len = min(kMsdChunk, g.size - ci * kMsdChunk);
+  K* seg_dst = dst + g.start;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t t0 = 0; t0 < len; t0 += kMsdTile) {
     const uint32_t tl = min((uint32_t)kMsdTile, len - t0);
-    for (int b = threadIdx.x; b <= kMsdBins; b += blockDim.x) s_cnt[b] = 0;
+    s_cnt[threadIdx.x] = 0;
     __syncthreads();
-    K k[kMsdTile / kMsdThreads];
-    uint32_t rk[kMsdTile / kMsdThreads];
+    K k[kPer];
+    uint32_t rk[kPer];
+    ld.load16(a + t0, tl, k);  // element j*kMsdThreads + threadIdx.x (or a permutation of the tile)
 #pragma unroll
-    for (int j = 0; j < kMsdTile / kMsdThreads; ++j) {
-      const uint32_t i = t0 + j * kMsdThreads + threadIdx.x;
+    for (int j = 0; j < kPer; ++j) {
       rk[j] = 0xffffffffu;
-      if (i < t0 + tl) {
-        k[j] = ld(a + i);
+      if (ld.valid(j, tl)) {
         const uint32_t d = (uint32_t)(k[j] >> shift) & (kMsdBins - 1);
         rk[j] = (d << 16) | atomicAdd(&s_cnt[d], 1u);
       }
@@ -181,29 +214,22 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdS
       if (lane == 31) s_scan[warp] = inc;
       __syncthreads();
       uint32_t before = 0;
-      for (int w = 0; w < warp; ++w) before += s_scan[w];
-      __syncthreads();
-      s_cnt[threadIdx.x] = before + inc - v;
+#pragma unroll
+      for (int w = 0; w < kMsdThreads / 32; ++w) before += w < warp ? s_scan[w] : 0u;
+      const uint32_t start = before + inc - v;
+      s_base[threadIdx.x] = s_cur[threadIdx.x] - start;
+      s_cur[threadIdx.x] += v;
+      s_cnt[threadIdx.x] = start;
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kMsdTile / kMsdThreads; ++j) {
-      if (rk[j] != 0xffffffffu) {
-        const uint32_t d = rk[j] >> 16;
-        const uint32_t pos = s_cnt[d] + (rk[j] & 0xffffu);
-        s_key[pos] = k[j];
-        s_dig[pos] = static_cast<uint8_t>(d);
-      }
-    }
+    for (int j = 0; j < kPer; ++j)
+      if (rk[j] != 0xffffffffu) s_key[s_cnt[rk[j] >> 16] + (rk[j] & 0xffffu)] = k[j];
     __syncthreads();
+#pragma unroll 4
     for (uint32_t i = threadIdx.x; i < tl; i += blockDim.x) {
-      const uint32_t d = s_dig[i];
-      dst[g.start + s_cur[d] + (i - s_cnt[d])] = s_key[i];
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < kMsdBins; b += blockDim.x) {
-      const uint32_t end = (b + 1 < kMsdBins) ? s_cnt[b + 1] : tl;
-      s_cur[b] += end - s_cnt[b];
+      const K key = s_key[i];
+      seg_dst[s_base[(uint32_t)(key >> shift) & (kMsdBins - 1)] + i] = key;
     }
     __syncthreads();
   }

@@ -37,6 +37,14 @@ def main():
         rs._check(lib.rs_gen_f64_cfg3(o.config_seed(3), 0, n, rs._ptr(cdf), cdf.numel(), rs._ptr(x), rs._stream()))
         for _ in range(2):
             rs.sort_f64(x, 3, key_digits=6)
+    if "--cfg5" in sys.argv:
+        del keys, out
+        torch.cuda.empty_cache()
+        n5 = 1 << 31
+        k5 = torch.empty(n5, dtype=torch.int32, device="cuda")
+        rs._check(lib.rs_gen_u32(o.config_seed(5), 0, n5, 0, rs._ptr(k5), rs._stream()))
+        o5 = torch.empty_like(k5)
+        rs.sort_u32(k5, out=o5, msd=True)
     torch.cuda.synchronize()
     print("ok", rep)
 
