@@ -658,7 +658,7 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
       }
       if (h[3]) k_leaf_copy<K, Emit><<<h[3], 256, 0, ws.stream>>>(dst, leaf_copy, emit);
       if (h[1]) {
-        const size_t smem = ((1u << shift) + 1) / 2 * sizeof(uint32_t);
+        const size_t smem = leaf_grid_words(shift) * sizeof(uint32_t);
         RS_CUDA(cudaFuncSetAttribute(k_leaf_grid<K, Emit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
         k_leaf_grid<K, Emit><<<h[1], kLeafGridThreads, smem, ws.stream>>>(dst, leaf_grid, shift, emit);

@@ -191,6 +191,12 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_scatter(const uint32_t*
       if (b < p.bins) s_start[b] = before + inc - c;
       if (b == 127) s_total = before + inc;
     }
+    // s_cnt[b] becomes this tile's destination base: dest(i) = s_cnt[b] + i
+    for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) {
+      const uint32_t c = s_cnt[b];
+      s_cnt[b] = s_cur[b] - s_start[b];
+      s_cur[b] += c;
+    }
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kKvItems; ++j) {
@@ -198,19 +204,17 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_scatter(const uint32_t*
         const uint32_t pos = s_start[d[j]] + wh[d[j]] + rank[j];
         s_keys[pos] = k[j];
         s_vals[pos] = v[j];
-        s_dig[pos] = static_cast<uint16_t>(d[j]);
       }
     }
     __syncthreads();
     const uint32_t total = s_total;
+#pragma unroll 4
     for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
-      const uint32_t b = s_dig[i];
-      const uint32_t g = s_cur[b] + (i - s_start[b]);
-      keys_out[g] = s_keys[i];
+      const uint32_t key = s_keys[i];
+      const uint32_t g = s_cnt[kv_digit(key, p)] + i;
+      keys_out[g] = key;
       vals_out[g] = s_vals[i];
     }
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) s_cur[b] += s_cnt[b];
     for (int i = threadIdx.x; i < kKvWarps * kKvBins; i += blockDim.x) s_wh[i] = 0;
     __syncthreads();
   }

@@ -297,31 +297,44 @@ __global__ void k_leaf_copy(const K* __restrict__ src, const MsdSeg* __restrict_
 // The recombinant step on a leaf: every key of the segment shares the bits
 // above rem_bits, so a count grid over the 2^rem_bits remaining cells sorts
 // it.  Counters are uint16 pairs in 32-bit words (segments hold < 65536
-// keys), grid <= 2^16 cells = 128 KB.
+// keys); word w lives at w + w/32 so that threads scanning 32 consecutive
+// words each hit distinct banks.  Grid <= 2^16 cells = 132 KB.
+__host__ __device__ constexpr uint32_t leaf_grid_words(uint32_t rem_bits) {
+  const uint32_t words = ((1u << rem_bits) + 1) / 2;
+  return words + words / 32 + 1;
+}
+
 template <class K, class Emit>
 __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restrict__ src,
                                                                 const MsdSeg* __restrict__ segs, uint32_t rem_bits,
                                                                 Emit emit) {
-  extern __shared__ uint32_t s_w[];  // 2^rem_bits / 2 words
+  extern __shared__ uint32_t s_w[];
   __shared__ uint32_t s_scan[kLeafGridThreads / 32];
   const MsdSeg g = segs[blockIdx.x];
   const uint32_t cells = 1u << rem_bits;
   const uint32_t words = (cells + 1) / 2;
+  const uint32_t phys = leaf_grid_words(rem_bits);
   const K mask = (K(1) << rem_bits) - 1;
-  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) s_w[i] = 0;
+  for (uint32_t i = threadIdx.x; i < phys; i += blockDim.x) s_w[i] = 0;
   __syncthreads();
   const K prefix = src[g.start] & ~mask;
   for (uint32_t i = threadIdx.x; i < g.size; i += blockDim.x) {
     const uint32_t cell = static_cast<uint32_t>(src[g.start + i] & mask);
-    atomicAdd(&s_w[cell >> 1], 1u << ((cell & 1) * 16));
+    const uint32_t w = cell >> 1;
+    atomicAdd(&s_w[w + (w >> 5)], 1u << ((cell & 1) * 16));
   }
   __syncthreads();
   // exclusive scan over cells: each thread owns a contiguous run of words
   const uint32_t per = (words + kLeafGridThreads - 1) / kLeafGridThreads;
   const uint32_t w0 = threadIdx.x * per;
   uint32_t sum = 0;
-  for (uint32_t j = 0; j < per; ++j)
-    if (w0 + j < words) sum += (s_w[w0 + j] & 0xffffu) + (s_w[w0 + j] >> 16);
+  for (uint32_t j = 0; j < per; ++j) {
+    const uint32_t w = w0 + j;
+    if (w < words) {
+      const uint32_t v = s_w[w + (w >> 5)];
+      sum += (v & 0xffffu) + (v >> 16);
+    }
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t inc = sum;
 #pragma unroll
@@ -333,13 +346,12 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   __syncthreads();
   uint32_t run = inc - sum;
   for (int w = 0; w < warp; ++w) run += s_scan[w];
-  // emit this thread's cells in order (runs are short: a leaf is dense but
-  // has < 65536 keys over its cells)
+  // emit this thread's cells in order
   for (uint32_t j = 0; j < per; ++j) {
     const uint32_t wi = w0 + j;
     if (wi >= words) break;
-    const uint32_t w = s_w[wi];
-    const uint32_t c0 = w & 0xffffu, c1 = w >> 16;
+    const uint32_t v = s_w[wi + (wi >> 5)];
+    const uint32_t c0 = v & 0xffffu, c1 = v >> 16;
     for (uint32_t q = 0; q < c0; ++q) emit(g.start + run + q, prefix | K(2 * wi));
     run += c0;
     for (uint32_t q = 0; q < c1; ++q) emit(g.start + run + q, prefix | K(2 * wi + 1));
