@@ -442,7 +442,14 @@ KvPass kv_pass(uint32_t g, uint32_t digits, uint64_t n) {
   const uint32_t rem = digits - 2 * g;
   p.bins = rem >= 2 ? 100u : static_cast<uint32_t>(pow10u(rem));
   const uint64_t tiles = (n + kKvTile - 1) / kKvTile;
-  uint64_t G = (uint64_t)sm_count() * 3;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_kv_chunk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kKvSmemBytes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kv_chunk_scatter, kKvThreads, kKvSmemBytes);
+    if (per_sm < 1) per_sm = 1;
+  }
+  uint64_t G = (uint64_t)sm_count() * per_sm;  // one persistent wave
   if (G > tiles) G = tiles ? tiles : 1;
   p.chunk = ((tiles + G - 1) / G) * kKvTile;
   p.G = static_cast<uint32_t>((n + p.chunk - 1) / p.chunk);
@@ -481,7 +488,8 @@ void kv_sort(Workspace& ws, const uint32_t* keys, const uint32_t* vals, uint64_t
     exscan_u32(ws, hist, bg, off, total);
     {
       PassTimer pt_(RS_PASS_KV_SCATTER, ws.stream);
-      k_kv_chunk_scatter<<<p.G, kKvThreads, kKvSmemBytes, ws.stream>>>(sk, sv, dk, dv, n, p, off);
+      k_kv_chunk_scatter<<<p.G, kKvThreads, kKvSmemBytes, ws.stream>>>(sk, sv, dk, dv, n, p, off,
+                                                                        aligned16(sk) && aligned16(sv));
       RS_LAUNCH_CHECK();
     }
     sk = dk;

@@ -13,7 +13,9 @@
 // Per pass (reduce-then-scan, deterministic):
 //   k_kv_chunk_hist     per-CTA digit counts over a contiguous chunk      R4
 //   exscan              [bins][G] -> each CTA's start in every digit run
-//   k_kv_chunk_scatter  the CTA walks its chunk tile by tile in order; each
+//   k_kv_chunk_scatter  the CTA walks its chunk tile by tile in order (tiles
+//                       double-buffered in shared memory by 1D TMA bulk
+//                       copies, cp.async.bulk + mbarrier); each
 //                       warp ranks its records stably with 7 ballots over
 //                       the digit bits (no __match_any_sync, which measured
 //                       ~10x slower on B200), the tile is staged in shared
@@ -25,6 +27,7 @@
 
 #include <cstdint>
 
+#include "bulk_copy.cuh"
 #include "rs_internal.cuh"
 
 namespace rsb {
@@ -36,11 +39,6 @@ constexpr int kKvBins = 100;                    // two decimal digits
 constexpr int kKvBits = 7;                      // 100 < 2^7
 constexpr int kKvMaxPasses = 5;                 // 10-digit uint32 keys
 constexpr int kKvWarps = kKvThreads / 32;
-constexpr size_t kKvSmemBytes = kKvWarps * kKvBins * 2  // s_wh
-                                + kKvBins * 4 * 3        // s_cnt, s_start, s_cur
-                                + kKvTile * 4 * 2        // s_keys, s_vals
-                                + kKvTile * 2            // s_dig
-                                + 64 * 4;
 
 struct KvPass {
   unsigned long long magic_div;   // floor(k / 10^(2*pass)) = (k * magic_div) >> shift_div
@@ -104,21 +102,28 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __
   if ((threadIdx.x & 31) == 0 && mx) atomicMax(&st->max_key, mx);
 }
 
-__global__ void __launch_bounds__(kKvThreads) k_kv_chunk_scatter(const uint32_t* __restrict__ keys_in,
+// Shared layout: two input buffers of one tile (keys then values, 32 KB
+// each) filled by 1D TMA bulk copies one tile ahead; after a tile's records
+// are in registers its buffer becomes that tile's output staging.
+constexpr size_t kKvSmemBytes = 2 * (size_t)kKvTile * 8  // s_in[2] (keys | vals)
+                                + kKvWarps * kKvBins * 2  // s_wh
+                                + kKvBins * 4 * 3;        // s_cnt, s_start, s_cur
+
+__global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32_t* __restrict__ keys_in,
                                                                  const uint32_t* __restrict__ vals_in,
                                                                  uint32_t* __restrict__ keys_out,
                                                                  uint32_t* __restrict__ vals_out, uint64_t n,
-                                                                 KvPass p, const uint32_t* __restrict__ off) {
-  extern __shared__ __align__(16) unsigned char kv_smem[];
-  uint32_t* s_keys = reinterpret_cast<uint32_t*>(kv_smem);  // [kKvTile]
-  uint32_t* s_vals = s_keys + kKvTile;                      // [kKvTile]
-  uint32_t* s_cnt = s_vals + kKvTile;                       // [kKvBins]
-  uint32_t* s_start = s_cnt + kKvBins;                      // [kKvBins]
-  uint32_t* s_cur = s_start + kKvBins;                      // [kKvBins]
-  uint16_t* s_wh = reinterpret_cast<uint16_t*>(s_cur + kKvBins);  // [kKvWarps][kKvBins]
-  uint16_t* s_dig = s_wh + kKvWarps * kKvBins;                    // [kKvTile]
+                                                                 KvPass p, const uint32_t* __restrict__ off,
+                                                                 bool bulk_ok) {
+  extern __shared__ __align__(128) unsigned char kv_smem[];
+  uint32_t* s_in = reinterpret_cast<uint32_t*>(kv_smem);              // [2][2][kKvTile]
+  uint16_t* s_wh = reinterpret_cast<uint16_t*>(s_in + 4 * kKvTile);   // [kKvWarps][kKvBins]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_wh + kKvWarps * kKvBins);
+  uint32_t* s_start = s_cnt + kKvBins;
+  uint32_t* s_cur = s_start + kKvBins;
   __shared__ uint32_t s_scan[kKvWarps];
   __shared__ uint32_t s_total;
+  __shared__ __align__(8) unsigned long long s_bar[2];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
@@ -127,22 +132,53 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_scatter(const uint32_t*
   const uint64_t c0 = (uint64_t)blockIdx.x * p.chunk;
   const uint64_t c1 = c0 + p.chunk < n ? c0 + p.chunk : n;
   uint16_t* wh = s_wh + warp * kKvBins;
+  // a tile can be bulk-loaded when it is full and the inputs are 16-byte aligned
+  auto full_tile = [&](uint64_t t0) { return bulk_ok && t0 + kKvTile <= c1; };
+  auto issue = [&](uint64_t t0, int buf) {  // one thread
+    fence_proxy_async_smem();
+    mbar_expect_tx(&s_bar[buf], 2 * kKvTile * 4);
+    bulk_g2s(s_in + buf * 2 * kKvTile, keys_in + t0, kKvTile * 4, &s_bar[buf]);
+    bulk_g2s(s_in + buf * 2 * kKvTile + kKvTile, vals_in + t0, kKvTile * 4, &s_bar[buf]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
   __syncthreads();
-
-  for (uint64_t t0 = c0; t0 < c1; t0 += kKvTile) {
-    // striped load: record t0 + warp*512 + j*32 + lane (input order =
+  if (threadIdx.x == 0 && c0 < c1 && full_tile(c0)) issue(c0, 0);
+  unsigned phase[2] = {0, 0};
+  int buf = 0;
+  for (uint64_t t0 = c0; t0 < c1; t0 += kKvTile, buf ^= 1) {
+    const uint64_t nt = t0 + kKvTile;
+    if (threadIdx.x == 0 && nt < c1 && full_tile(nt)) issue(nt, buf ^ 1);
+    uint32_t* in_k = s_in + buf * 2 * kKvTile;
+    uint32_t* in_v = in_k + kKvTile;
+    // striped order: record t0 + warp*512 + j*32 + lane (input order =
     // warp-major, then j, then lane)
     uint32_t k[kKvItems], v[kKvItems], rank[kKvItems];
     uint32_t d[kKvItems];
+    if (full_tile(t0)) {
+      mbar_wait(&s_bar[buf], phase[buf]);
+      phase[buf] ^= 1;
 #pragma unroll
-    for (int j = 0; j < kKvItems; ++j) {
-      const uint64_t i = t0 + warp * (kKvItems * 32) + j * 32 + lane;
-      const bool ok = i < c1;
-      k[j] = ok ? __ldcs(keys_in + i) : 0u;
-      v[j] = ok ? __ldcs(vals_in + i) : 0u;
-      d[j] = ok ? kv_digit(k[j], p) : 0xffffu;
+      for (int j = 0; j < kKvItems; ++j) {
+        const uint32_t i = warp * (kKvItems * 32) + j * 32 + lane;
+        k[j] = in_k[i];
+        v[j] = in_v[i];
+        d[j] = kv_digit(k[j], p);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kKvItems; ++j) {
+        const uint64_t i = t0 + warp * (kKvItems * 32) + j * 32 + lane;
+        const bool ok = i < c1;
+        k[j] = ok ? __ldcs(keys_in + i) : 0u;
+        v[j] = ok ? __ldcs(vals_in + i) : 0u;
+        d[j] = ok ? kv_digit(k[j], p) : 0xffffu;
+      }
     }
-    // stable warp ranks: peers = lanes with the same digit, from 10 ballots
+    // stable warp ranks: peers = lanes with the same digit, from 7 ballots
 #pragma unroll
     for (int j = 0; j < kKvItems; ++j) {
       const bool ok = d[j] != 0xffffu;
@@ -173,7 +209,7 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_scatter(const uint32_t*
       s_cnt[b] = run;
     }
     __syncthreads();
-    // tile-local exclusive scan over digits (warp 0..3, one digit per lane)
+    // tile-local exclusive scan over digits (warps 0..3, one digit per lane)
     if (threadIdx.x < 128) {
       const uint32_t b = threadIdx.x;
       const uint32_t c = b < p.bins ? s_cnt[b] : 0u;
@@ -188,32 +224,32 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_scatter(const uint32_t*
       asm volatile("bar.sync 1, 128;");
       uint32_t before = 0;
       for (int w = 0; w < warp; ++w) before += s_scan[w];
-      if (b < p.bins) s_start[b] = before + inc - c;
+      if (b < p.bins) {
+        const uint32_t start = before + inc - c;
+        s_start[b] = start;
+        s_cnt[b] = s_cur[b] - start;  // this tile's destination base: dest(i) = s_cnt[b] + i
+        s_cur[b] += c;
+      }
       if (b == 127) s_total = before + inc;
     }
-    // s_cnt[b] becomes this tile's destination base: dest(i) = s_cnt[b] + i
-    for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) {
-      const uint32_t c = s_cnt[b];
-      s_cnt[b] = s_cur[b] - s_start[b];
-      s_cur[b] += c;
-    }
     __syncthreads();
+    // stage in digit order into this tile's (consumed) input buffer
 #pragma unroll
     for (int j = 0; j < kKvItems; ++j) {
       if (d[j] != 0xffffu) {
         const uint32_t pos = s_start[d[j]] + wh[d[j]] + rank[j];
-        s_keys[pos] = k[j];
-        s_vals[pos] = v[j];
+        in_k[pos] = k[j];
+        in_v[pos] = v[j];
       }
     }
     __syncthreads();
     const uint32_t total = s_total;
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
-      const uint32_t key = s_keys[i];
+      const uint32_t key = in_k[i];
       const uint32_t g = s_cnt[kv_digit(key, p)] + i;
       keys_out[g] = key;
-      vals_out[g] = s_vals[i];
+      vals_out[g] = in_v[i];
     }
     for (int i = threadIdx.x; i < kKvWarps * kKvBins; i += blockDim.x) s_wh[i] = 0;
     __syncthreads();
