@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kThreads) k_exscan_u32(const uint32_t* __restr
 // starts, s_page[B] current page per bucket, s_fill[B] its fill, s_np[B]
 // pages opened per bucket, s_low[kTlTile] staged inner digits.
 __host__ __device__ constexpr size_t kPagePartitionOffset(uint32_t B) {
-  return (((size_t)B + 1) * 4 + (size_t)B * 12 + 15) / 16 * 16 + (size_t)B * 16;
+  return (((size_t)B + 2) * 4 + (size_t)B * 12 + 15) / 16 * 16 + (size_t)B * 16;
 }
 __host__ __device__ constexpr size_t kPagePartitionSmem(uint32_t B) {
   return kPagePartitionOffset(B) + (size_t)kTlTile * 4;  // staged (bucket << 16 | inner digit)
@@ -163,13 +163,13 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
                                                                DevStats* st) {
   using In = typename Map::In;
   extern __shared__ __align__(16) unsigned char tl_smem[];
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(tl_smem);  // [B+1]
-  uint32_t* s_page = s_cnt + t.B + 1;                       // [B]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(tl_smem);  // [B+2]: buckets, staged total, dummy
+  uint32_t* s_page = s_cnt + t.B + 2;                       // [B]
   uint32_t* s_fill = s_page + t.B;                          // [B]
   uint32_t* s_np = s_fill + t.B;                            // [B]
   // per bucket, this tile: {run start in staging, dest of rank r < thr = A + r,
   // else Bv + r, thr} (dest = index into the CTA's page region)
-  uint4* s_dst = reinterpret_cast<uint4*>(tl_smem + (((size_t)t.B + 1) * 4 + (size_t)t.B * 12 + 15) / 16 * 16);
+  uint4* s_dst = reinterpret_cast<uint4*>(tl_smem + (((size_t)t.B + 2) * 4 + (size_t)t.B * 12 + 15) / 16 * 16);
   uint32_t* s_stage = reinterpret_cast<uint32_t*>(tl_smem + kPagePartitionOffset(t.B));
   __shared__ uint32_t s_scan[kTlThreads / 32];
   __shared__ uint32_t s_next;  // next free page of this CTA's region
@@ -202,44 +202,42 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
       for (int q = 0; q < 4; ++q)
         Load4<In>::run(in, (uint64_t)nt * kTlTile + q * 1024 + threadIdx.x * 4, n, aligned, nxt[q]);
     }
-    for (uint32_t b = threadIdx.x; b <= t.B; b += blockDim.x) s_cnt[b] = 0;
+    for (uint32_t b = threadIdx.x; b <= t.B + 1; b += blockDim.x) s_cnt[b] = 0;
     __syncthreads();
-    uint32_t pk[kTlPerThread];  // bucket << 16 | rank in tile (0xffffffff: not counted)
+    // Branch-free key loop: keys that are past the end or outside the grid
+    // are counted in the dummy bin B+1 and never staged.
+    uint32_t pk[kTlPerThread];  // bucket << 16 | rank in tile
     uint32_t lo2[kTlPerThread / 2];
     const bool full = base + kTlTile <= n;
+    const uint32_t dummy = t.B + 1;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint64_t i0 = base + q * 1024 + threadIdx.x * 4;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        uint32_t l = 0;
-        pk[q * 4 + e] = 0xffffffffu;
-        if (full || i0 + e < n) {
-          if constexpr (sizeof(typename Map::Key) == 4) {
-            // 32-bit keys: compares, max and bucket math stay 32-bit
-            const uint32_t kk = map.key32(cur[q][e], flags);
-            mx32 = kk > mx32 ? kk : mx32;
-            if (kk < cells32) {
-              const uint32_t b = tl_bucket(kk, t);
-              l = kk - b * t.S;
-              pk[q * 4 + e] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
-            } else {
-              ovf = 1;
-            }
-          } else {
-            const unsigned long long kk = map(cur[q][e], flags);
-            mx = kk > mx ? kk : mx;
-            if (kk < t.cells) {
-              const uint32_t b = tl_bucket(static_cast<uint32_t>(kk), t);
-              l = static_cast<uint32_t>(kk) - b * t.S;
-              pk[q * 4 + e] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
-            } else {
-              ovf = 1;
-            }
-          }
+        const bool ok = full || i0 + e < n;
+        uint32_t b, l;
+        if constexpr (sizeof(typename Map::Key) == 4) {
+          // 32-bit keys: compares, max and bucket math stay 32-bit
+          const uint32_t kk = map.key32(cur[q][e], flags);
+          const bool in = ok && kk < cells32;
+          ovf |= ok && !in;
+          mx32 = (ok && kk > mx32) ? kk : mx32;
+          const uint32_t bk = tl_bucket(kk, t);
+          b = in ? bk : dummy;
+          l = kk - bk * t.S;
+        } else {
+          const unsigned long long kk = ok ? map(cur[q][e], flags) : 0ull;
+          const bool in = ok && kk < t.cells;
+          ovf |= ok && !in;
+          mx = (ok && kk > mx) ? kk : mx;
+          const uint32_t bk = tl_bucket(static_cast<uint32_t>(kk), t);
+          b = in ? bk : dummy;
+          l = static_cast<uint32_t>(kk) - bk * t.S;
         }
-        if (e & 1) lo2[(q * 4 + e) >> 1] |= l << 16;
-        else lo2[(q * 4 + e) >> 1] = l;
+        pk[q * 4 + e] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
+        if (e & 1) lo2[(q * 4 + e) >> 1] |= (l & 0xffffu) << 16;
+        else lo2[(q * 4 + e) >> 1] = l & 0xffffu;
       }
     }
     __syncthreads();
@@ -278,10 +276,9 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kTlPerThread; ++j) {
-      if (pk[j] != 0xffffffffu) {
-        const uint32_t b = pk[j] >> 16;
+      const uint32_t b = pk[j] >> 16;
+      if (b != dummy)
         s_stage[s_cnt[b] + (pk[j] & 0xffffu)] = (b << 16) | ((lo2[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
-      }
     }
     // page bookkeeping, one thread per bucket: a run that does not fit the
     // current page spills into freshly allocated consecutive pages
