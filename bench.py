@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-kv", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the multi-GPU sharded-grid path even at N=1 (one-rank NCCL group)")
     ap.add_argument("--no-clock-window", action="store_true",
                     help="skip the untimed steps around the timed region (for ncu launch lists)")
     args = ap.parse_args()
@@ -204,8 +206,11 @@ def main():
     from paper_2107_01391_b200 import dist as rsd
 
     torch.cuda.set_device(local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    use_dist = world > 1 or args.dist
+    if use_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
     lib = rs._lib.load()
     stream = rs._stream
 
@@ -220,7 +225,7 @@ def main():
     rep = rs.RsReport()
 
     def step():
-        if world == 1:
+        if not use_dist:
             rs._check(lib.rs_sort_u32(rs._ptr(keys), n, rs._ptr(out), n, ctypes.byref(opts), ctypes.byref(rep),
                                       stream()))
         else:
@@ -242,7 +247,7 @@ def main():
         while time.perf_counter() < t_end:
             step()
         torch.cuda.synchronize()
-        if world > 1:
+        if use_dist:
             dist.barrier()
         launches0 = lib.rs_launch_count()
         ev0.record()
@@ -255,10 +260,10 @@ def main():
         while time.perf_counter() < t_end:
             step()
         torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
+    if use_dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -271,13 +276,13 @@ def main():
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": "cfg2 (BASELINE configs[1]): 2^28 uint32 keys/GPU uniform in [0,10^6), key-only, "
                                "6-digit 10^6-cell grid", "keys_per_gpu": n, "key_digits_declared": KEY_DIGITS,
-                   "parallelism": f"shard{world}" if world > 1 else "single",
+                   "parallelism": f"shard{world}" if use_dist else "single",
                    "l2": "inputs (1 GiB) larger than L2 (126 MB); no flush"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
 
-    if rank == 0 and world == 1:
+    if rank == 0 and not use_dist:
         # per-pass device time with CUDA events on the library's stream
         lib.rs_profile_enable(1)
         lib.rs_profile_reset()
@@ -361,7 +366,7 @@ def main():
 
     if rank == 0:
         print(json.dumps(result), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 

@@ -227,13 +227,20 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
           b = in ? bk : dummy;
           l = kk - bk * t.S;
         } else {
-          const unsigned long long kk = ok ? map(cur[q][e], flags) : 0ull;
-          const bool in = ok && kk < t.cells;
-          ovf |= ok && !in;
-          mx = (ok && kk > mx) ? kk : mx;
-          const uint32_t bk = tl_bucket(static_cast<uint32_t>(kk), t);
-          b = in ? bk : dummy;
-          l = static_cast<uint32_t>(kk) - bk * t.S;
+          // 64-bit mapped keys (float64 / int64 mappers are heavy): branch so
+          // the mapper and bucket math only run for real keys
+          b = dummy;
+          l = 0;
+          if (ok) {
+            const unsigned long long kk = map(cur[q][e], flags);
+            mx = kk > mx ? kk : mx;
+            if (kk < t.cells) {
+              b = tl_bucket(static_cast<uint32_t>(kk), t);
+              l = static_cast<uint32_t>(kk) - b * t.S;
+            } else {
+              ovf = 1;
+            }
+          }
         }
         pk[q * 4 + e] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
         if (e & 1) lo2[(q * 4 + e) >> 1] |= (l & 0xffffu) << 16;

@@ -355,3 +355,57 @@ def test_cfg5_full_size_properties(rs):
         assert int(ha) == int(hb)
     del a, b, out, keys
     torch.cuda.empty_cache()
+
+
+# ------------------------------------- multi-GPU device phases (1-rank NCCL)
+def test_dist_paths_on_device_nccl(rs, oracle):
+    """The sharded-grid and range-partition orchestration of dist.py with the
+    real device phases (rs_count_u32 / rs_emit_u32 / rs_bucket_hist_u32 /
+    rs_partition_u32) over a one-rank NCCL group."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2107_01391_b200.dist import range_partition_sort, sharded_grid_sort
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        keys = oracle.gen_u32(21, 0, 1 << 22, 10**6)
+        out = sharded_grid_sort(_t(keys.view(np.int32)), 10**6)
+        assert np.array_equal(_np_u32(out), np.sort(keys))
+        wide = oracle.gen_u32(22, 0, 1 << 21, 0)
+        out = range_partition_sort(_t(wide.view(np.int32)), 10**7, 430)
+        assert np.array_equal(_np_u32(out), np.sort(wide))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_partition_phase_api(rs, oracle):
+    import torch
+
+    lib = rs._lib.load()
+    keys = oracle.gen_u32(23, 0, 300_001, 0)
+    d = _t(keys.view(np.int32))
+    hist = torch.zeros(430, dtype=torch.int64, device="cuda")
+    rs._check(lib.rs_bucket_hist_u32(rs._ptr(d), d.numel(), 10**7, rs._ptr(hist), 430, rs._stream()))
+    assert np.array_equal(hist.cpu().numpy(), np.bincount(keys.astype(np.int64) // 10**7, minlength=430))
+    bounds = [0, 100, 250, 430]
+    out = torch.empty_like(d)
+    hb = (ctypes.c_uint32 * 4)(*bounds)
+    hc = (ctypes.c_uint64 * 3)()
+    rs._check(lib.rs_partition_u32(rs._ptr(d), d.numel(), 10**7, hb, 3, rs._ptr(out), hc, rs._stream()))
+    got = _np_u32(out)
+    part = np.searchsorted(np.array(bounds[1:-1]), keys.astype(np.int64) // 10**7, side="right")
+    assert list(hc) == np.bincount(part, minlength=3).tolist()
+    start = 0
+    for p in range(3):
+        seg = got[start:start + hc[p]]
+        assert np.array_equal(np.sort(seg), np.sort(keys[part == p]))
+        start += hc[p]
