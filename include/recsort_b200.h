@@ -177,8 +177,9 @@ rs_status rs_sort_u32_kv_host(const uint32_t* h_keys, const uint32_t* h_vals,
 
 /* ---- phase API (multi-GPU orchestration) -------------------- */
 /* Count uint32 keys into a caller-owned grid of `cells` uint32 counters
- * (zeroed by the caller or accumulate=1 to add).  Keys >= cells are not
- * counted; h_max receives the maximum key (host pointer, synchronises). */
+ * (overwritten; the same counting pass as rs_sort_u32).  Keys >= cells are
+ * not counted; h_max, if not NULL, receives the maximum key (host pointer;
+ * the call then synchronises). */
 rs_status rs_count_u32(const uint32_t* keys, uint64_t n, uint32_t* counts,
                        uint64_t cells, uint32_t* h_max, void* stream);
 /* Emit the run-length expansion of cells [cell_lo, cell_hi) of a (globally

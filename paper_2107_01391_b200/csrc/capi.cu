@@ -1072,18 +1072,7 @@ rs_status rs_count_u32(const uint32_t* keys, uint64_t n, uint32_t* counts, uint6
     if (cells == 0 || cells > 0xFFFFFFFFull) fail(RS_INVALID_ARGUMENT, "cells out of range");
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
     reset_stats(ws);
-    if (n > 0) {
-      PassTimer pt_(RS_PASS_COUNT, ws.stream);
-      if (cells <= kSmemCellsMax) {
-        const unsigned grid = stream_grid(n, static_cast<int>(cells * 8 > 8192 ? cells * 8 : 8192), 4);
-        k_count_smem<MapU32><<<grid, kThreads, cells * 4, ws.stream>>>(keys, n, MapU32{}, counts,
-                                                                       cells, ws.stats);
-      } else {
-        k_count_global<MapU32, true><<<stream_grid(n, kThreads * 8, 8), kThreads, 0, ws.stream>>>(
-            keys, n, MapU32{}, counts, cells, ws.stats);
-      }
-      RS_LAUNCH_CHECK();
-    }
+    count_pass(ws, keys, n, MapU32{}, cells, counts);  // same counting pass as rs_sort_u32
     if (h_max) {
       pull_stats(ws);
       *h_max = static_cast<uint32_t>(ws.h_stats->max_key);

@@ -100,7 +100,7 @@ class GpuOps:
     def sort(self, keys: torch.Tensor, key_digits: int = 0) -> torch.Tensor:
         from . import sort_u32
 
-        return sort_u32(keys, key_digits=key_digits, max_cells=10**10)[0]
+        return sort_u32(keys, key_digits=key_digits, msd=True)[0]
 
 
 def sharded_grid_sort(keys: torch.Tensor, cells: int, ops=None, group=None) -> torch.Tensor:
