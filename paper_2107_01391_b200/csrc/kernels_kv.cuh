@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __
 // are in registers its buffer becomes that tile's output staging.
 constexpr size_t kKvSmemBytes = 2 * (size_t)kKvTile * 8  // s_in[2] (keys | vals)
                                 + kKvWarps * kKvBins * 2  // s_wh
-                                + kKvBins * 4 * 3;        // s_cnt, s_start, s_cur
+                                + kKvBins * 4 * 3         // s_cnt, s_start, s_cur
+                                + kKvTile;                // s_dig
 
 __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32_t* __restrict__ keys_in,
                                                                  const uint32_t* __restrict__ vals_in,
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_wh + kKvWarps * kKvBins);
   uint32_t* s_start = s_cnt + kKvBins;
   uint32_t* s_cur = s_start + kKvBins;
+  uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_cur + kKvBins);  // [kKvTile]
   __shared__ uint32_t s_scan[kKvWarps];
   __shared__ uint32_t s_total;
   __shared__ __align__(8) unsigned long long s_bar[2];
@@ -233,23 +235,25 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
       if (b == 127) s_total = before + inc;
     }
     __syncthreads();
-    // stage in digit order into this tile's (consumed) input buffer
+    // stage (key | value) in digit order into this tile's consumed input
+    // buffer, and the digit as one byte
+    unsigned long long* stage = reinterpret_cast<unsigned long long*>(in_k);
 #pragma unroll
     for (int j = 0; j < kKvItems; ++j) {
       if (d[j] != 0xffffu) {
         const uint32_t pos = s_start[d[j]] + wh[d[j]] + rank[j];
-        in_k[pos] = k[j];
-        in_v[pos] = v[j];
+        stage[pos] = (static_cast<unsigned long long>(v[j]) << 32) | k[j];
+        s_dig[pos] = static_cast<uint8_t>(d[j]);
       }
     }
     __syncthreads();
     const uint32_t total = s_total;
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
-      const uint32_t key = in_k[i];
-      const uint32_t g = s_cnt[kv_digit(key, p)] + i;
-      keys_out[g] = key;
-      vals_out[g] = in_v[i];
+      const unsigned long long kv = stage[i];
+      const uint32_t g = s_cnt[s_dig[i]] + i;
+      keys_out[g] = static_cast<uint32_t>(kv);
+      vals_out[g] = static_cast<uint32_t>(kv >> 32);
     }
     for (int i = threadIdx.x; i < kKvWarps * kKvBins; i += blockDim.x) s_wh[i] = 0;
     __syncthreads();
