@@ -63,11 +63,8 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __
                                                               KvPass p, bool aligned,
                                                               uint32_t* __restrict__ hist,  // [bins][G]
                                                               DevStats* st) {
-  // one copy of the histogram per lane, interleaved so lane l always hits
-  // bank l: no same-address conflicts inside a warp (100 bins would collide)
-  __shared__ uint32_t s_h[kKvBins * 32];
-  const uint32_t lane = threadIdx.x & 31;
-  for (uint32_t b = threadIdx.x; b < kKvBins * 32; b += blockDim.x) s_h[b] = 0;
+  __shared__ uint32_t s_h[kKvBins];
+  for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) s_h[b] = 0;
   __syncthreads();
   const uint32_t c = blockIdx.x / kKvHistSplit, sub = blockIdx.x % kKvHistSplit;
   const uint64_t span = p.chunk / kKvHistSplit;  // chunk is a multiple of kKvTile
@@ -90,18 +87,14 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __
       for (int e = 0; e < 4; ++e) {
         if (i0 + e < c1) {
           mx = v[e] > mx ? v[e] : mx;
-          atomicAdd(&s_h[kv_digit(v[e], p) * 32 + lane], 1u);
+          atomicAdd(&s_h[kv_digit(v[e], p)], 1u);
         }
       }
     }
   }
   __syncthreads();
-  for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x) {
-    uint32_t sum = 0;
-#pragma unroll 8
-    for (int l = 0; l < 32; ++l) sum += s_h[b * 32 + ((l + b) & 31)];
-    if (sum) atomicAdd(&hist[(uint64_t)b * p.G + c], sum);
-  }
+  for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x)
+    if (s_h[b]) atomicAdd(&hist[(uint64_t)b * p.G + c], s_h[b]);
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long w = __shfl_xor_sync(0xffffffffu, mx, o);
     mx = w > mx ? w : mx;

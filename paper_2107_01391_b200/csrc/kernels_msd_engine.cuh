@@ -150,26 +150,19 @@ template <class Load>
 __global__ void __launch_bounds__(kMsdThreads) k_msd_hist(Load ld, const MsdSeg* __restrict__ segs,
                                                           const uint32_t* __restrict__ chunk_seg, uint32_t shift,
                                                           uint32_t* __restrict__ table) {
-  // per-lane histogram copies (bin*32 + lane): no same-address conflicts in a warp
-  __shared__ uint32_t s_h[kMsdBins * 32];
-  const uint32_t lane = threadIdx.x & 31;
+  __shared__ uint32_t s_h[kMsdBins];
   const uint32_t c = blockIdx.x;
   const MsdSeg g = segs[chunk_seg[c]];
   const uint32_t ci = c - g.chunk0;
-  for (int b = threadIdx.x; b < kMsdBins * 32; b += blockDim.x) s_h[b] = 0;
+  for (int b = threadIdx.x; b < kMsdBins; b += blockDim.x) s_h[b] = 0;
   __syncthreads();
   const unsigned long long a = g.start + (unsigned long long)ci * kMsdChunk;
   const uint32_t len = min(kMsdChunk, g.size - ci * kMsdChunk);
   for (uint32_t i = threadIdx.x; i < len; i += blockDim.x)
-    atomicAdd(&s_h[((uint32_t)(ld(a + i) >> shift) & (kMsdBins - 1)) * 32 + lane], 1u);
+    atomicAdd(&s_h[(uint32_t)(ld(a + i) >> shift) & (kMsdBins - 1)], 1u);
   __syncthreads();
   uint32_t* t = table + (unsigned long long)g.chunk0 * kMsdBins;  // segment table [digit][chunk]
-  for (int b = threadIdx.x; b < kMsdBins; b += blockDim.x) {
-    uint32_t sum = 0;
-#pragma unroll 8
-    for (int l = 0; l < 32; ++l) sum += s_h[b * 32 + ((l + b) & 31)];
-    t[(unsigned long long)b * g.nchunks + ci] = sum;
-  }
+  for (int b = threadIdx.x; b < kMsdBins; b += blockDim.x) t[(unsigned long long)b * g.nchunks + ci] = s_h[b];
 }
 
 template <class Load>
