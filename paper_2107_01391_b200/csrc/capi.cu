@@ -402,7 +402,11 @@ void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, cons
   const uint32_t hint = opt ? opt->key_digits : 0;
   const bool hinted = hint >= 1 && hint <= max_digits && pow10u(hint) <= budget;
   uint32_t digits = hint;
-  if (!hinted) {
+  // a declared width already above the budget goes to the MSD path without
+  // the max pass (the MSD sort does not need the geometry up front)
+  const bool msd_declared = msd_u32 && opt && opt->msd && hint >= 1 && hint <= max_digits &&
+                            pow10u(hint) > budget;
+  if (!hinted && !msd_declared) {
     digits = digit_count(device_max(ws, in, n, map));
   }
   if (msd_u32 && opt && opt->msd && pow10u(digits) > budget) {

@@ -346,16 +346,30 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   __syncthreads();
   uint32_t run = inc - sum;
   for (int w = 0; w < warp; ++w) run += s_scan[w];
-  // emit this thread's cells in order
-  for (uint32_t j = 0; j < per; ++j) {
-    const uint32_t wi = w0 + j;
-    if (wi >= words) break;
-    const uint32_t v = s_w[wi + (wi >> 5)];
-    const uint32_t c0 = v & 0xffffu, c1 = v >> 16;
-    for (uint32_t q = 0; q < c0; ++q) emit(g.start + run + q, prefix | K(2 * wi));
-    run += c0;
-    for (uint32_t q = 0; q < c1; ++q) emit(g.start + run + q, prefix | K(2 * wi + 1));
-    run += c1;
+  // Emit warp-cooperatively: the warp's 32 threads own a contiguous range of
+  // cells and hence a contiguous output range starting at lane 0's offset.
+  // Lanes take 32 consecutive cells at a time and write consecutive
+  // positions (coalesced), instead of each thread streaming its own run.
+  uint32_t out = __shfl_sync(0xffffffffu, run, 0);
+  const uint32_t c_begin = warp * 32 * per * 2;
+  const uint32_t c_end = min(cells, c_begin + 32 * per * 2);
+  for (uint32_t c0 = c_begin; c0 < c_end; c0 += 32) {
+    const uint32_t c = c0 + lane;
+    uint32_t cnt = 0;
+    if (c < c_end) {
+      const uint32_t w = c >> 1;
+      const uint32_t v = s_w[w + (w >> 5)];
+      cnt = (c & 1) ? (v >> 16) : (v & 0xffffu);
+    }
+    uint32_t inc2 = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc2, o);
+      if (lane >= o) inc2 += y;
+    }
+    const uint32_t at = out + inc2 - cnt;
+    for (uint32_t q = 0; q < cnt; ++q) emit(g.start + at + q, prefix | K(c));
+    out += __shfl_sync(0xffffffffu, inc2, 31);
   }
 }
 
