@@ -318,10 +318,25 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   for (uint32_t i = threadIdx.x; i < phys; i += blockDim.x) s_w[i] = 0;
   __syncthreads();
   const K prefix = src[g.start] & ~mask;
-  for (uint32_t i = threadIdx.x; i < g.size; i += blockDim.x) {
-    const uint32_t cell = static_cast<uint32_t>(src[g.start + i] & mask);
-    const uint32_t w = cell >> 1;
-    atomicAdd(&s_w[w + (w >> 5)], 1u << ((cell & 1) * 16));
+  {  // four independent loads in flight before the atomics
+    const K* sp = src + g.start;
+    uint32_t i = threadIdx.x;
+    for (; i + 3 * kLeafGridThreads < g.size; i += 4 * kLeafGridThreads) {
+      K v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(sp + i + u * kLeafGridThreads);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t cell = static_cast<uint32_t>(v[u] & mask);
+        const uint32_t w = cell >> 1;
+        atomicAdd(&s_w[w + (w >> 5)], 1u << ((cell & 1) * 16));
+      }
+    }
+    for (; i < g.size; i += kLeafGridThreads) {
+      const uint32_t cell = static_cast<uint32_t>(sp[i] & mask);
+      const uint32_t w = cell >> 1;
+      atomicAdd(&s_w[w + (w >> 5)], 1u << ((cell & 1) * 16));
+    }
   }
   __syncthreads();
   // exclusive scan over cells: each thread owns a contiguous run of words
@@ -351,24 +366,21 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   // Lanes take 32 consecutive cells at a time and write consecutive
   // positions (coalesced), instead of each thread streaming its own run.
   uint32_t out = __shfl_sync(0xffffffffu, run, 0);
-  const uint32_t c_begin = warp * 32 * per * 2;
-  const uint32_t c_end = min(cells, c_begin + 32 * per * 2);
-  for (uint32_t c0 = c_begin; c0 < c_end; c0 += 32) {
-    const uint32_t c = c0 + lane;
-    uint32_t cnt = 0;
-    if (c < c_end) {
-      const uint32_t w = c >> 1;
-      const uint32_t v = s_w[w + (w >> 5)];
-      cnt = (c & 1) ? (v >> 16) : (v & 0xffffu);
-    }
-    uint32_t inc2 = cnt;
+  const uint32_t w_begin = warp * 32 * per;                 // first counter word of this warp
+  const uint32_t w_end = min(words, w_begin + 32 * per);
+  for (uint32_t w0 = w_begin; w0 < w_end; w0 += 32) {       // lane: one word = two cells
+    const uint32_t w = w0 + lane;
+    const uint32_t v = w < w_end ? s_w[w + (w >> 5)] : 0u;
+    const uint32_t c0 = v & 0xffffu, c1 = v >> 16;
+    uint32_t inc2 = c0 + c1;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, inc2, o);
       if (lane >= o) inc2 += y;
     }
-    const uint32_t at = out + inc2 - cnt;
-    for (uint32_t q = 0; q < cnt; ++q) emit(g.start + at + q, prefix | K(c));
+    const uint32_t at = out + inc2 - c0 - c1;
+    for (uint32_t q = 0; q < c0; ++q) emit(g.start + at + q, prefix | K(2 * w));
+    for (uint32_t q = 0; q < c1; ++q) emit(g.start + at + c0 + q, prefix | K(2 * w + 1));
     out += __shfl_sync(0xffffffffu, inc2, 31);
   }
 }
