@@ -640,7 +640,7 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
     {
       PassTimer pt_(RS_PASS_MSD_HIST, ws.stream);
       if (level == 0) k_msd_hist<<<nchunks, kMsdThreads, 0, ws.stream>>>(load0, segs_in, chunk_seg, shift, table);
-      else k_msd_hist<<<nchunks, kMsdThreads, 0, ws.stream>>>(LoadKeys<K>{buf[(level - 1) & 1]}, segs_in,
+      else k_msd_hist<<<nchunks, kMsdThreads, 0, ws.stream>>>(LoadKeys<K>{buf[(level - 1) & 1], n}, segs_in,
                                                               chunk_seg, shift, table);
       RS_LAUNCH_CHECK();
     }
@@ -648,7 +648,7 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
     {
       PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
       if (level == 0) k_msd_scatter<<<nchunks, kMsdThreads, 0, ws.stream>>>(load0, segs_in, chunk_seg, shift, off, dst);
-      else k_msd_scatter<<<nchunks, kMsdThreads, 0, ws.stream>>>(LoadKeys<K>{buf[(level - 1) & 1]}, segs_in,
+      else k_msd_scatter<<<nchunks, kMsdThreads, 0, ws.stream>>>(LoadKeys<K>{buf[(level - 1) & 1], n}, segs_in,
                                                                  chunk_seg, shift, off, dst);
       RS_LAUNCH_CHECK();
     }
@@ -686,7 +686,7 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
 }
 void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t* out) {
   reset_stats(ws);
-  msd_sort(ws, LoadKeys<uint32_t>{in}, n, 32, EmitKey<uint32_t>{const_cast<uint32_t*>(out)});
+  msd_sort(ws, LoadKeys<uint32_t>{in, n}, n, 32, EmitKey<uint32_t>{const_cast<uint32_t*>(out)});
   {
     PassTimer pt_(RS_PASS_REPORT, ws.stream);
     k_report<uint32_t><<<1, 32, 0, ws.stream>>>(out, n, 10, 0, 0, 0, ws.stats);

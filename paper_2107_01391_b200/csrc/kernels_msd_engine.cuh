@@ -26,9 +26,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels_grid.cuh"
 #include "kernels_msd.cuh"
+#include "bulk_copy.cuh"
 #include "rs_internal.cuh"
 
 namespace rsb {
@@ -56,6 +58,7 @@ template <class K>
 struct LoadKeys {
   using Key = K;
   const K* p;
+  unsigned long long n_total;  // readable elements at p (bulk copies never read past them)
   __device__ __forceinline__ K operator()(unsigned long long i) const { return __ldcs(p + i); }
   // A tile of up to kMsdTile keys at a: 16-byte vectors when a is aligned
   // (thread t takes elements 4t..4t+3 of each 1024-element quarter), else
@@ -171,12 +174,17 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdS
                                                              const uint32_t* __restrict__ off,
                                                              typename Load::Key* __restrict__ dst) {
   using K = typename Load::Key;
+  // uint32 keys: tiles double-buffered by 1D TMA bulk copies (an aligned
+  // superset of the tile, the offset skipped in shared memory); the consumed
+  // buffer is reused as the output staging
+  constexpr bool kBulk = std::is_same<Load, LoadKeys<uint32_t>>::value;
   constexpr int kPer = kMsdTile / kMsdThreads;  // 16 keys per thread per tile
   __shared__ uint32_t s_base[kMsdBins];  // segment-relative destination of this tile's digit run, minus its start
   __shared__ uint32_t s_cur[kMsdBins];   // running segment-relative cursor per digit
   __shared__ uint32_t s_cnt[kMsdBins];
-  __shared__ K s_key[kMsdTile];
+  __shared__ __align__(16) K s_buf[kBulk ? 2 : 1][kMsdTile + 4];
   __shared__ uint32_t s_scan[kMsdThreads / 32];
+  __shared__ __align__(8) unsigned long long s_bar[2];
   const uint32_t c = blockIdx.x;
   const MsdSeg g = segs[chunk_seg[c]];
   const uint32_t ci = c - g.chunk0;
@@ -185,19 +193,84 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdS
   for (int b = threadIdx.x; b < kMsdBins; b += blockDim.x) s_cur[b] = t[(unsigned long long)b * g.nchunks + ci] - base0;
   const unsigned long long a = g.start + (unsigned long long)ci * kMsdChunk;
   const uint32_t len = min(kMsdChunk, g.size - ci * kMsdChunk);
+  const uint32_t ntiles = (len + kMsdTile - 1) / kMsdTile;
   K* seg_dst = dst + g.start;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t t0 = 0; t0 < len; t0 += kMsdTile) {
+  // tile u of this chunk: aligned superset [a+u*T - mis, ...) of round-up size
+  auto tile_geo = [&](uint32_t u, uint32_t& mis, uint32_t& bytes, bool& ok) {
+    if constexpr (kBulk) {
+      const unsigned long long e0 = a + (unsigned long long)u * kMsdTile;
+      const uint32_t tl = min((uint32_t)kMsdTile, len - u * kMsdTile);
+      mis = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(ld.p + e0) & 15) / sizeof(K));
+      bytes = ((tl + mis) * (uint32_t)sizeof(K) + 15) & ~15u;
+      ok = e0 - mis + bytes / sizeof(K) <= ld.n_total;
+    } else {
+      mis = bytes = 0;
+      ok = false;
+    }
+  };
+  unsigned phase[2] = {0, 0};
+  if constexpr (kBulk) {
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar[0], 1);
+      mbar_init(&s_bar[1], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t mis, bytes;
+      bool ok;
+      tile_geo(0, mis, bytes, ok);
+      if (ok) {
+        if constexpr (kBulk) {
+          mbar_expect_tx(&s_bar[0], bytes);
+          bulk_g2s(&s_buf[0][0], ld.p + a - mis, bytes, &s_bar[0]);
+        }
+      }
+    }
+  }
+  for (uint32_t u = 0; u < ntiles; ++u) {
+    const uint32_t t0 = u * kMsdTile;
     const uint32_t tl = min((uint32_t)kMsdTile, len - t0);
+    const int buf = kBulk ? (u & 1) : 0;
     s_cnt[threadIdx.x] = 0;
+    if constexpr (kBulk) {
+      if (threadIdx.x == 0 && u + 1 < ntiles) {
+        uint32_t mis, bytes;
+        bool ok;
+        tile_geo(u + 1, mis, bytes, ok);
+        if (ok) {
+          if constexpr (kBulk) {
+            fence_proxy_async_smem();
+            mbar_expect_tx(&s_bar[buf ^ 1], bytes);
+            bulk_g2s(&s_buf[buf ^ 1][0], ld.p + a + t0 + kMsdTile - mis, bytes, &s_bar[buf ^ 1]);
+          }
+        }
+      }
+    }
     __syncthreads();
     K k[kPer];
     uint32_t rk[kPer];
-    ld.load16(a + t0, tl, k);  // element j*kMsdThreads + threadIdx.x (or a permutation of the tile)
+    bool bulk_tile = false;
+    if constexpr (kBulk) {
+      uint32_t mis, bytes;
+      tile_geo(u, mis, bytes, bulk_tile);
+      if (bulk_tile) {
+        mbar_wait(&s_bar[buf], phase[buf]);
+        phase[buf] ^= 1;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+          const uint32_t i = j * kMsdThreads + threadIdx.x;
+          k[j] = i < tl ? s_buf[buf][mis + i] : K(0);
+        }
+      }
+    }
+    if (!bulk_tile) ld.load16(a + t0, tl, k);  // element j*kMsdThreads + threadIdx.x (or a permutation)
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
       rk[j] = 0xffffffffu;
-      if (ld.valid(j, tl)) {
+      const bool valid = bulk_tile ? (uint32_t)(j * kMsdThreads + threadIdx.x) < tl : ld.valid(j, tl);
+      if (valid) {
         const uint32_t d = (uint32_t)(k[j] >> shift) & (kMsdBins - 1);
         rk[j] = (d << 16) | atomicAdd(&s_cnt[d], 1u);
       }
@@ -222,13 +295,14 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdS
       s_cnt[threadIdx.x] = start;
     }
     __syncthreads();
+    K* stage = &s_buf[buf][0];
 #pragma unroll
     for (int j = 0; j < kPer; ++j)
-      if (rk[j] != 0xffffffffu) s_key[s_cnt[rk[j] >> 16] + (rk[j] & 0xffffu)] = k[j];
+      if (rk[j] != 0xffffffffu) stage[s_cnt[rk[j] >> 16] + (rk[j] & 0xffffu)] = k[j];
     __syncthreads();
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < tl; i += blockDim.x) {
-      const K key = s_key[i];
+      const K key = stage[i];
       seg_dst[s_base[(uint32_t)(key >> shift) & (kMsdBins - 1)] + i] = key;
     }
     __syncthreads();
