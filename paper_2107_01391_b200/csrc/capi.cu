@@ -11,6 +11,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -231,8 +232,9 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
   if (!div_magic32(S, t.magic, t.shift)) return false;
   t.T = static_cast<uint32_t>((n + kTlTile - 1) / kTlTile);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_page_partition<MapU32>, kTlThreads,
-                                                kPagePartitionSmem(t.B));
+  cudaFuncSetAttribute(k_page_partition_u32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kPageU32Smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_page_partition_u32, kTlThreads, kPageU32Smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t G = (uint64_t)sm_count() * per_sm;  // one persistent wave
   if (G > t.T) G = t.T;
@@ -264,10 +266,25 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
                                  static_cast<int>(smem)));
   {
     PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
+    if constexpr (std::is_same<Map, MapU32>::value) {
+      if (al && t.B <= 256) {  // TMA-fed specialisation
+        static bool attr = false;
+        if (!attr) {
+          RS_CUDA(cudaFuncSetAttribute(k_page_partition_u32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kPageU32Smem)));
+          attr = true;
+        }
+        k_page_partition_u32<<<t.G, kTlThreads, kPageU32Smem, ws.stream>>>(in, n, t, pages, page_bucket, page_fill,
+                                                                           pc_bm, ws.stats);
+        RS_LAUNCH_CHECK();
+        goto partitioned;
+      }
+    }
     k_page_partition<Map><<<t.G, kTlThreads, smem, ws.stream>>>(in, n, map, t, al, pages, page_bucket,
                                                                 page_fill, pc_bm, ws.stats);
     RS_LAUNCH_CHECK();
   }
+partitioned:
   exscan_u32(ws, pc_bm, bg, po_bm, total);
   {
     PassTimer pt_(RS_PASS_SCAN, ws.stream, 2);

@@ -27,6 +27,7 @@
 
 #include <cstdint>
 
+#include "bulk_copy.cuh"
 #include "kernels_grid.cuh"
 #include "rs_internal.cuh"
 
@@ -347,6 +348,180 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
     if (flags & 0x7fffffffu) atomicOr(&st->flags, flags & 0x7fffffffu);
     if (flags & 0x80000000u) atomicOr(&st->overflow, 1u);
   }
+}
+
+
+// ---------------------------------------------------------- K1 (uint32)
+// Specialised partition for uint32 keys when B <= 256 and the input is
+// 16-byte aligned: tiles arrive by 1D TMA bulk copies one tile ahead
+// (double buffer), one thread per bucket does the scan and the page
+// bookkeeping in the same step, and the counters are cleared inside the copy
+// phase.  Same output as k_page_partition<MapU32>.
+constexpr size_t kPageU32Smem = 2 * (size_t)kTlTile * 4  // s_in[2]
+                                + (size_t)kTlTile * 4    // s_stage
+                                + 256 * 16               // s_dst
+                                + 258 * 4 * 4;           // s_cnt, s_page, s_fill, s_np
+
+__global__ void __launch_bounds__(kTlThreads, 3) k_page_partition_u32(const uint32_t* __restrict__ in, uint64_t n,
+                                                                   TwoLevel t,
+                                                                   uint16_t* __restrict__ pages,
+                                                                   uint16_t* __restrict__ page_bucket,
+                                                                   uint16_t* __restrict__ page_fill,
+                                                                   uint32_t* __restrict__ pc_bm,
+                                                                   DevStats* st) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint32_t* s_in = reinterpret_cast<uint32_t*>(sm);             // [2][kTlTile]
+  uint32_t* s_stage = s_in + 2 * kTlTile;                        // [kTlTile]
+  uint4* s_dst = reinterpret_cast<uint4*>(s_stage + kTlTile);   // [256]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_dst + 256);   // [258]: buckets, total, dummy
+  uint32_t* s_page = s_cnt + 258;
+  uint32_t* s_fill = s_page + 258;
+  uint32_t* s_np = s_fill + 258;
+  __shared__ uint32_t s_scan[kTlThreads / 32];
+  __shared__ uint32_t s_next;
+  __shared__ __align__(8) unsigned long long s_bar[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t B = t.B, dummy = t.B + 1;
+  const uint32_t cells32 = static_cast<uint32_t>(t.cells);
+  const uint32_t page0 = blockIdx.x * t.pages_per_cta;
+  uint16_t* my_pages = pages + (uint64_t)page0 * kPage;
+  const uint32_t full_tiles = static_cast<uint32_t>(n / kTlTile);
+  if (threadIdx.x < 258) {
+    s_cnt[threadIdx.x] = 0;
+    s_page[threadIdx.x] = 0xffffffffu;
+    s_fill[threadIdx.x] = kPage;
+    s_np[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) {
+    s_next = 0;
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t tile, int b) {  // one thread
+    fence_proxy_async_smem();
+    mbar_expect_tx(&s_bar[b], kTlTile * 4);
+    bulk_g2s(s_in + b * kTlTile, in + (uint64_t)tile * kTlTile, kTlTile * 4, &s_bar[b]);
+  };
+  if (threadIdx.x == 0 && blockIdx.x < full_tiles) issue(blockIdx.x, 0);
+  uint32_t mx = 0;
+  unsigned ovf = 0;
+  unsigned phase[2] = {0, 0};
+  int buf = 0;
+  for (uint32_t tile = blockIdx.x; tile < t.T; tile += gridDim.x, buf ^= 1) {
+    const uint32_t nt = tile + gridDim.x;
+    if (threadIdx.x == 0 && nt < full_tiles) issue(nt, buf ^ 1);
+    const bool full = tile < full_tiles;
+    uint32_t key[kTlPerThread];
+    if (full) {
+      mbar_wait(&s_bar[buf], phase[buf]);
+      phase[buf] ^= 1;
+      const uint4* src = reinterpret_cast<const uint4*>(s_in + buf * kTlTile);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 v = src[q * kTlThreads + threadIdx.x];
+        key[4 * q] = v.x; key[4 * q + 1] = v.y; key[4 * q + 2] = v.z; key[4 * q + 3] = v.w;
+      }
+    } else {
+      const uint64_t base = (uint64_t)tile * kTlTile;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint64_t i = base + q * 1024 + threadIdx.x * 4 + e;
+          key[4 * q + e] = i < n ? in[i] : 0xffffffffu;  // past the end: dummy bin
+        }
+    }
+    const uint64_t base = (uint64_t)tile * kTlTile;
+    uint32_t pk[kTlPerThread], lo2[kTlPerThread / 2];
+#pragma unroll
+    for (int j = 0; j < kTlPerThread; ++j) {
+      const uint32_t kk = key[j];
+      const bool ok = full || base + (j >> 2) * 1024 + threadIdx.x * 4 + (j & 3) < n;
+      const bool ing = ok && kk < cells32;
+      ovf |= ok && !ing;
+      mx = (ok && kk > mx) ? kk : mx;
+      const uint32_t bk = tl_bucket(kk, t);
+      const uint32_t b = ing ? bk : dummy;
+      pk[j] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
+      const uint32_t l = (kk - bk * t.S) & 0xffffu;
+      if (j & 1) lo2[j >> 1] |= l << 16;
+      else lo2[j >> 1] = l;
+    }
+    __syncthreads();
+    // one thread per bucket: exclusive scan + page bookkeeping
+    {
+      const uint32_t b = threadIdx.x;
+      const uint32_t len = b < B ? s_cnt[b] : 0u;
+      uint32_t inc = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) s_scan[warp] = inc;
+      __syncthreads();
+      uint32_t before = 0;
+#pragma unroll
+      for (int w = 0; w < kTlThreads / 32; ++w) before += w < warp ? s_scan[w] : 0u;
+      const uint32_t start = before + inc - len;
+      if (b == kTlThreads - 1) s_cnt[B] = before + inc;  // staged keys
+      if (b < B && len) {
+        uint32_t fill = s_fill[b], pg = s_page[b];
+        const uint32_t room = (pg == 0xffffffffu) ? 0u : kPage - fill;
+        uint32_t pa = pg, fa = fill, pb = 0;
+        if (len > room) {
+          const uint32_t extra = (len - room + kPage - 1) / kPage;
+          const uint32_t first = atomicAdd(&s_next, extra);
+          for (uint32_t j = 0; j < extra; ++j) page_bucket[page0 + first + j] = static_cast<uint16_t>(b);
+          for (uint32_t j = 0; j + 1 < extra; ++j) page_fill[page0 + first + j] = static_cast<uint16_t>(kPage);
+          if (pg != 0xffffffffu) page_fill[page0 + pg] = static_cast<uint16_t>(kPage);
+          s_np[b] += extra;
+          if (room == 0) {
+            pa = first;
+            fa = 0;
+            pb = first + 1;
+          } else {
+            pb = first;
+          }
+          pg = first + extra - 1;
+          fill = len - room - (extra - 1) * kPage;
+        } else {
+          fill += len;
+        }
+        s_fill[b] = fill;
+        s_page[b] = pg;
+        s_dst[b] = make_uint4(start, pa * kPage + fa, (pb - 1) * kPage + fa, kPage - fa);
+      }
+      __syncwarp();
+      if (b < B) s_cnt[b] = start;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kTlPerThread; ++j) {
+      const uint32_t b = pk[j] >> 16;
+      if (b != dummy) s_stage[s_cnt[b] + (pk[j] & 0xffffu)] = (b << 16) | ((lo2[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
+    }
+    __syncthreads();
+    const uint32_t staged = s_cnt[B];
+    if (threadIdx.x < 258) s_cnt[threadIdx.x] = 0;  // ready for the next tile (read again only after a barrier)
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < staged; i += kTlThreads) {
+      const uint32_t w = s_stage[i];
+      const uint4 d = s_dst[w >> 16];
+      const uint32_t r = i - d.x;
+      my_pages[(r < d.w ? d.y : d.z) + r] = static_cast<uint16_t>(w);
+    }
+    __syncthreads();
+  }
+  for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
+    if (s_page[b] != 0xffffffffu) page_fill[page0 + s_page[b]] = static_cast<uint16_t>(s_fill[b]);
+    pc_bm[(uint64_t)b * t.G + blockIdx.x] = s_np[b];
+  }
+  warp_max_to(mx, &st->max_key);
+  const unsigned f = warp_or(ovf ? 1u : 0u);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(&st->overflow, 1u);
 }
 
 // Page list grouped by bucket: CTA c walks its used pages (allocated densely
