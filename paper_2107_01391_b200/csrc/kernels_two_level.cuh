@@ -498,14 +498,16 @@ __global__ void __launch_bounds__(kTlThreads, 3) k_page_partition_u32(const uint
       if (b < B) s_cnt[b] = start;
     }
     __syncthreads();
+    const uint32_t staged = s_cnt[B];
 #pragma unroll
     for (int j = 0; j < kTlPerThread; ++j) {
       const uint32_t b = pk[j] >> 16;
       if (b != dummy) s_stage[s_cnt[b] + (pk[j] & 0xffffu)] = (b << 16) | ((lo2[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
     }
     __syncthreads();
-    const uint32_t staged = s_cnt[B];
-    if (threadIdx.x < 258) s_cnt[threadIdx.x] = 0;  // ready for the next tile (read again only after a barrier)
+    // every read of the counters is behind the barrier above: clear them for
+    // the next tile (its atomics come after the barrier closing this tile)
+    for (uint32_t b = threadIdx.x; b < B + 2; b += kTlThreads) s_cnt[b] = 0;
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < staged; i += kTlThreads) {
       const uint32_t w = s_stage[i];
