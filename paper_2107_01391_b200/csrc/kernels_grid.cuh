@@ -149,10 +149,16 @@ struct MapF64 {
     double f = floor(p);
     if (p == f && err < 0.0) f -= 1.0;
     const unsigned long long m = static_cast<unsigned long long>(f);
-    if (static_cast<double>(m) / P == x) return m;
-    if (static_cast<double>(m + 1) / P == x) return m + 1;
-    if (static_cast<double>(2 * m + 1) / P2 == x) return m + 1;
-    const double fr = p - f;  // exact
+    const double fr = p - f;  // exact, in [0, 1]
+    // The reals that round to x span < 0.02 in units of 1/P and |err| is far
+    // below 0.001, so an integer (or half-integer) candidate can only round
+    // to x when p lies within 0.02 of it: test only the nearest candidate.
+    if (fr < 0.02 || fr > 0.98) {
+      const unsigned long long c = fr < 0.5 ? m : m + 1;
+      if (static_cast<double>(c) / P == x) return c;
+    } else if (fr > 0.48 && fr < 0.52) {
+      if (static_cast<double>(2 * m + 1) / P2 == x) return m + 1;
+    }
     const bool up = fr > 0.5 || (fr == 0.5 && err > 0.0);
     return up ? m + 1 : m;
   }

@@ -29,13 +29,14 @@ def kernel_f64(x: float, scale: int):
     if p == f and err < 0.0:
         f -= 1.0
     m = int(f)
-    if float(m) / P == x:
-        return m
-    if float(m + 1) / P == x:
-        return m + 1
-    if float(2 * m + 1) / P2 == x:
-        return m + 1
     fr = p - f
+    if fr < 0.02 or fr > 0.98:
+        c = m if fr < 0.5 else m + 1
+        if float(c) / P == x:
+            return c
+    elif 0.48 < fr < 0.52:
+        if float(2 * m + 1) / P2 == x:
+            return m + 1
     up = fr > 0.5 or (fr == 0.5 and err > 0.0)
     return m + 1 if up else m
 
