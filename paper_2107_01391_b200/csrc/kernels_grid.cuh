@@ -121,21 +121,6 @@ struct MapU64 {
 //    half-up result is decided by x*P versus m+1/2, exactly.
 // IEEE division of two exact doubles (m < 2^53, P <= 10^15) is correctly
 // rounded, so every "rounds to x" test is exact.
-// fl(num / den) == x for positive normal x, exact integers num < 2^53 and
-// den <= 2*10^15: true iff |num - x*den| <= den*ulp(x)/2 (ties to even).  The
-// residual comes from one fma (one rounding), so only a band of relative
-// width 2^-50 around the tie is ambiguous; there the IEEE division decides.
-__device__ __forceinline__ bool rounds_to(double num, double den, double x) {
-  const double r = fabs(fma(-x, den, num));
-  const long long bits = __double_as_longlong(x);
-  const int e = static_cast<int>((bits >> 52) & 0x7ff);  // biased exponent, x normal
-  const double half_ulp = __longlong_as_double(static_cast<long long>(e - 53) << 52);  // 2^(E-53)
-  const double h = den * half_ulp;
-  if (r < h * (1.0 - 0x1.0p-50)) return true;
-  if (r > h * (1.0 + 0x1.0p-50)) return false;
-  return num / den == x;
-}
-
 struct MapF64 {
   using In = double;
   using Key = unsigned long long;
@@ -170,9 +155,9 @@ struct MapF64 {
     // to x when p lies within 0.02 of it: test only the nearest candidate.
     if (fr < 0.02 || fr > 0.98) {
       const unsigned long long c = fr < 0.5 ? m : m + 1;
-      if (rounds_to(static_cast<double>(c), P, x)) return c;
+      if (static_cast<double>(c) / P == x) return c;
     } else if (fr > 0.48 && fr < 0.52) {
-      if (rounds_to(static_cast<double>(2 * m + 1), P2, x)) return m + 1;
+      if (static_cast<double>(2 * m + 1) / P2 == x) return m + 1;
     }
     const bool up = fr > 0.5 || (fr == 0.5 && err > 0.0);
     return up ? m + 1 : m;
