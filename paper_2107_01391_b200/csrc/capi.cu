@@ -628,6 +628,7 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
   auto* leaf_small = ws.get<MsdSeg>(kSlotLows, cap);
   auto* leaf_copy = ws.get<MsdSeg>(kSlotTmpKeys2, cap);
   auto* leaf_warp = ws.get<MsdSeg>(kSlotTmpVals2, cap);
+  auto* leaf_thread = ws.get<MsdSeg>(kSlotExtra1, cap);
   auto* cnt = ws.get<unsigned>(kSlotScratch, 8);
   auto* total = reinterpret_cast<unsigned long long*>(cnt + 6);
   MsdSeg first{0, static_cast<uint32_t>(n), 0, 0};
@@ -669,18 +670,23 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
                                                                  chunk_seg, shift, off, dst);
       RS_LAUNCH_CHECK();
     }
-    RS_CUDA(cudaMemsetAsync(cnt, 0, 5 * sizeof(unsigned), ws.stream));
-    MsdLists L{segs_out, leaf_grid, leaf_small, leaf_copy, leaf_warp, cnt};
+    RS_CUDA(cudaMemsetAsync(cnt, 0, 6 * sizeof(unsigned), ws.stream));
+    MsdLists L{segs_out, leaf_grid, leaf_small, leaf_copy, leaf_warp, leaf_thread, cnt};
     const unsigned long long pairs = (unsigned long long)nseg * kMsdBins;
     k_msd_classify<<<static_cast<unsigned>((pairs + 255) / 256), 256, 0, ws.stream>>>(segs_in, nseg, off, shift, L);
     RS_LAUNCH_CHECK();
-    unsigned h[5] = {};
+    unsigned h[6] = {};
     RS_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, ws.stream));
     RS_CUDA(cudaStreamSynchronize(ws.stream));
     for (unsigned v : h)
       if ((uint64_t)v > cap) fail(RS_CUDA_ERROR, "MSD segment list overflow");
     {
-      PassTimer pt_(RS_PASS_BUCKET, ws.stream, (h[1] ? 1 : 0) + (h[2] ? 1 : 0) + (h[3] ? 1 : 0) + (h[4] ? 1 : 0));
+      PassTimer pt_(RS_PASS_BUCKET, ws.stream,
+                    (h[1] ? 1 : 0) + (h[2] ? 1 : 0) + (h[3] ? 1 : 0) + (h[4] ? 1 : 0) + (h[5] ? 1 : 0));
+      if (h[5]) {
+        const unsigned blocks = std::min<unsigned>((h[5] + kMsdThreads - 1) / kMsdThreads, sm_count() * 16);
+        k_leaf_thread<K, Emit><<<blocks, kMsdThreads, 0, ws.stream>>>(dst, leaf_thread, h[5], emit);
+      }
       if (h[4]) {
         const unsigned blocks = std::min<unsigned>((h[4] + 7) / 8, sm_count() * 16);
         k_leaf_warp<K, Emit><<<blocks, kMsdThreads, 0, ws.stream>>>(dst, leaf_warp, h[4], emit);
@@ -715,7 +721,9 @@ void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t
 void msd_sort_str(Workspace& ws, const uint8_t* chars, uint64_t n, uint32_t width, uint32_t w, uint32_t radix,
                   const uint16_t* d_ord, const uint8_t* d_sym, uint8_t* out) {
   reset_stats(ws);
-  msd_sort(ws, LoadStr{chars, width, d_ord}, n, 5 * width, EmitStr{out, width, d_sym});
+  LoadStr ld{chars, width, d_ord};
+  ld.w8 = width == 8 && (reinterpret_cast<uintptr_t>(chars) & 7) == 0;
+  msd_sort(ws, ld, n, 5 * width, EmitStr{out, width, d_sym});
   {
     PassTimer pt_(RS_PASS_REPORT, ws.stream);
     k_report_recs<<<1, 32, 0, ws.stream>>>(out, n, width, w, radix, d_ord, ws.stats);

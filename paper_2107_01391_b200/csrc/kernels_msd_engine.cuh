@@ -41,6 +41,7 @@ constexpr int kMsdTile = 4096;          // keys per scatter tile
 constexpr uint32_t kMsdChunk = 65536;   // keys per (segment, chunk) work item
 constexpr uint32_t kLeafSmall = 2048;   // shared bitonic leaf capacity
 constexpr uint32_t kLeafWarp = 32;      // warp (register) bitonic leaf capacity
+constexpr uint32_t kLeafThread = 16;    // one thread, insertion sort in registers
 constexpr int kLeafGridBits = 16;       // count-grid leaf: <= 2^16 cells (u16 pairs, 128 KB)
 constexpr int kLeafGridThreads = 1024;  // one 128 KB CTA per SM: 32 warps to hide latency
 
@@ -101,7 +102,21 @@ struct LoadStr {
     }
   }
   __device__ __forceinline__ bool valid(int j, uint32_t tl) const { return (uint32_t)(j * kMsdThreads + threadIdx.x) < tl; }
+  bool w8 = false;       // 8-byte records at an 8-byte aligned base: one 64-bit load each
   __device__ __forceinline__ unsigned long long operator()(unsigned long long i) const {
+    if (w8) {
+      const unsigned long long w = __ldcs(reinterpret_cast<const unsigned long long*>(recs) + i);
+      unsigned long long k = 0;
+      bool ended = false;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t c = static_cast<uint32_t>(w >> (8 * j)) & 0xffu;
+        ended |= c == 0;
+        const uint32_t o = ended ? 0u : __ldg(ord + c);
+        k = (k << 5) | o;
+      }
+      return k;
+    }
     const uint8_t* r = recs + i * width;
     unsigned long long k = 0;
     bool ended = false;
@@ -317,7 +332,8 @@ struct MsdLists {
   MsdSeg* leaf_small;
   MsdSeg* leaf_copy;
   MsdSeg* leaf_warp;
-  unsigned* cnt;  // [5]: next, grid, small, copy, warp
+  MsdSeg* leaf_thread;
+  unsigned* cnt;  // [6]: next, grid, small, copy, warp, thread
 };
 
 __global__ void k_msd_classify(const MsdSeg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ off,
@@ -338,8 +354,10 @@ __global__ void k_msd_classify(const MsdSeg* __restrict__ segs, uint32_t nseg, c
     L.leaf_copy[atomicAdd(&L.cnt[3], 1u)] = sub;
   } else if (rem_bits <= kLeafGridBits && size >= (1u << rem_bits) / 16 && size <= 65535u) {
     L.leaf_grid[atomicAdd(&L.cnt[1], 1u)] = sub;  // dense: the count grid
+  } else if (size <= kLeafThread) {
+    L.leaf_thread[atomicAdd(&L.cnt[5], 1u)] = sub;  // tiny: one thread, registers
   } else if (size <= kLeafWarp) {
-    L.leaf_warp[atomicAdd(&L.cnt[4], 1u)] = sub;  // tiny: one warp, registers
+    L.leaf_warp[atomicAdd(&L.cnt[4], 1u)] = sub;  // small: one warp, registers
   } else if (size <= kLeafSmall && rem_bits <= kMsdDigitBits) {
     L.leaf_small[atomicAdd(&L.cnt[2], 1u)] = sub;  // last digit: shared bitonic
   } else {
@@ -510,6 +528,32 @@ __global__ void __launch_bounds__(kMsdThreads) k_leaf_warp(const K* __restrict__
       }
     }
     if (lane < g.size) emit(g.start + lane, v);
+  }
+}
+
+// Tiny leaves (<= 16 keys): one thread per segment, insertion sort in
+// registers (fully unrolled, so the array stays in registers).
+template <class K, class Emit>
+__global__ void __launch_bounds__(kMsdThreads) k_leaf_thread(const K* __restrict__ src, const MsdSeg* __restrict__ segs,
+                                                             uint32_t nseg, Emit emit) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += stride) {
+    const MsdSeg g = segs[s];
+    K v[kLeafThread];
+#pragma unroll
+    for (uint32_t i = 0; i < kLeafThread; ++i) v[i] = i < g.size ? src[g.start + i] : ~K(0);
+#pragma unroll
+    for (uint32_t i = 1; i < kLeafThread; ++i) {
+#pragma unroll
+      for (uint32_t j = i; j > 0; --j) {  // compare-exchange down: a sorting network
+        const K a = v[j - 1], b = v[j];
+        v[j - 1] = a < b ? a : b;
+        v[j] = a < b ? b : a;
+      }
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < kLeafThread; ++i)
+      if (i < g.size) emit(g.start + i, v[i]);
   }
 }
 
