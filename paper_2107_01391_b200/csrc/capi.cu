@@ -140,6 +140,16 @@ int sm_count() {
   return sms;
 }
 
+size_t smem_optin() {  // opt-in dynamic shared memory per block
+  static size_t b = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v > 0 ? static_cast<size_t>(v) : static_cast<size_t>(232448);
+  }();
+  return b;
+}
+
 // Persistent-style grid for streaming passes: up to `per_sm` CTAs per SM,
 // never more than there are 16-byte vectors to read.
 unsigned stream_grid(uint64_t n_elems, int elems_per_cta, int per_sm = 8) {
@@ -229,7 +239,7 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
   t.cells = cells;
   t.S = static_cast<uint32_t>(S);
   t.B = static_cast<uint32_t>((cells + S - 1) / S);
-  if (!div_magic32(S, t.magic, t.shift)) return false;
+  if (!div_magic32(S, t.magic, t.shift) || t.shift < 32) return false;  // S == 1: never (cells > smem grid)
   t.T = static_cast<uint32_t>((n + kTlTile - 1) / kTlTile);
   int per_sm = 0;
   cudaFuncSetAttribute(k_page_partition_u32, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -586,6 +596,69 @@ __global__ void __launch_bounds__(kThreads) k_str_keys(const uint8_t* __restrict
   if ((threadIdx.x & 31) == 0 && mxlen) atomicMax(&st->max_key, mxlen);
 }
 
+
+// Width (longest string) and symbol validation only, for the MSD path: no key
+// written; 8-byte records read as two 16-byte loads per thread per round.
+__global__ void __launch_bounds__(kThreads) k_str_scan(const uint8_t* __restrict__ recs, uint64_t n, uint32_t width,
+                                                       bool w8, const uint16_t* __restrict__ ord_g, DevStats* st) {
+  __shared__ uint16_t ord[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) ord[i] = ord_g[i];
+  __syncthreads();
+  unsigned bad = 0;
+  unsigned long long mxlen = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  auto scan8 = [&](unsigned long long w) {
+    uint32_t len = 0;
+    bool ended = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t c = static_cast<uint32_t>(w >> (8 * j)) & 0xffu;
+      ended |= c == 0;
+      if (!ended) {
+        ++len;
+        bad |= ord[c] == 0;
+      }
+    }
+    mxlen = len > mxlen ? len : mxlen;
+  };
+  if (w8) {
+    const auto* r2 = reinterpret_cast<const ulonglong2*>(recs);
+    const uint64_t pairs = n >> 1;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + stride < pairs; i += 2 * stride) {
+      const ulonglong2 a = __ldcs(r2 + i), b = __ldcs(r2 + i + stride);
+      scan8(a.x), scan8(a.y), scan8(b.x), scan8(b.y);
+    }
+    if (i < pairs) {
+      const ulonglong2 a = __ldcs(r2 + i);
+      scan8(a.x), scan8(a.y);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+      scan8(reinterpret_cast<const unsigned long long*>(recs)[n - 1]);
+  } else {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      uint32_t len = 0;
+      bool ended = false;
+      const uint8_t* r = recs + i * width;
+      for (uint32_t j = 0; j < width && !ended; ++j) {
+        const uint8_t c = r[j];
+        if (c == 0) ended = true;
+        else {
+          ++len;
+          bad |= ord[c] == 0;
+        }
+      }
+      mxlen = len > mxlen ? len : mxlen;
+    }
+  }
+  if (bad) atomicOr(&st->flags, 8u);
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, mxlen, o);
+    mxlen = w > mxlen ? w : mxlen;
+  }
+  if ((threadIdx.x & 31) == 0 && mxlen) atomicMax(&st->max_key, mxlen);
+}
+
 // Emit writer for strings: key -> record bytes (key_to_string,
 // key_model.cpp:249-263; pad ordinals become NUL bytes).
 struct OutStr {
@@ -693,10 +766,13 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
       }
       if (h[3]) k_leaf_copy<K, Emit><<<h[3], 256, 0, ws.stream>>>(dst, leaf_copy, emit);
       if (h[1]) {
-        const size_t smem = leaf_grid_words(shift) * sizeof(uint32_t);
+        // grid + uint16 staging for segments up to `lcap` keys (the rest: run-length emit)
+        const size_t grid_b = leaf_grid_words(shift) * sizeof(uint32_t);
+        const size_t smem = std::min<size_t>(grid_b + 2 * 65536, smem_optin() - 1024);
+        const uint32_t lcap = static_cast<uint32_t>(std::min<size_t>((smem - grid_b) / 2, 65535));
         RS_CUDA(cudaFuncSetAttribute(k_leaf_grid<K, Emit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-        k_leaf_grid<K, Emit><<<h[1], kLeafGridThreads, smem, ws.stream>>>(dst, leaf_grid, shift, emit);
+        k_leaf_grid<K, Emit><<<h[1], kLeafGridThreads, smem, ws.stream>>>(dst, leaf_grid, shift, lcap, emit);
       }
       if (h[2]) k_leaf_bitonic<K, Emit><<<h[2], kMsdThreads, 0, ws.stream>>>(dst, leaf_small, emit);
       RS_LAUNCH_CHECK();
@@ -944,13 +1020,12 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
     RS_CUDA(cudaMemcpyAsync(tab, &t, sizeof(StrTable), cudaMemcpyHostToDevice, ws.stream));
     const auto* d_ord = reinterpret_cast<const uint16_t*>(tab);
     const auto* d_sym = tab + offsetof(StrTable, sym);
-    auto* keys = ws.get<unsigned long long>(kSlotMapped, n);
-    // width of the data = longest string (key_model.cpp:228-230)
+    // width of the data = longest string (key_model.cpp:228-230), symbols checked
     reset_stats(ws);
     {
       PassTimer pt_(RS_PASS_OTHER, ws.stream);
-      k_str_keys<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, width,
-                                                                                t.radix, d_ord, keys, ws.stats);
+      const bool w8 = width == 8 && (reinterpret_cast<uintptr_t>(chars) & 15) == 0;
+      k_str_scan<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w8, d_ord, ws.stats);
       RS_LAUNCH_CHECK();
     }
     pull_stats(ws);
@@ -963,13 +1038,12 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
     if (!msd || total_cells <= budget) {
       const rs_key_spec spec = make_key_spec(t.radix, w, w, budget);
       if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
-      if (w != width) {  // re-key at the data width
-        {
-          PassTimer pt_(RS_PASS_OTHER, ws.stream);
-          k_str_keys<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w, t.radix,
-                                                                                    d_ord, keys, ws.stats);
-          RS_LAUNCH_CHECK();
-        }
+      auto* keys = ws.get<unsigned long long>(kSlotMapped, n);
+      {  // base-radix keys at the data width
+        PassTimer pt_(RS_PASS_OTHER, ws.stream);
+        k_str_keys<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w, t.radix,
+                                                                                  d_ord, keys, ws.stats);
+        RS_LAUNCH_CHECK();
       }
       OutStr o{out, width, w, t.radix, d_sym, 0ull};
       grid_sort(ws, keys, n, MapU64{}, total_cells, o, keys, t.radix, w, 0);

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
   }
   __syncthreads();
   if (threadIdx.x == 0 && c0 < c1 && full_tile(c0)) issue(c0, 0);
-  unsigned phase[2] = {0, 0};
+  unsigned phase = 0;  // bit b: parity of buffer b's barrier
   int buf = 0;
   for (uint64_t t0 = c0; t0 < c1; t0 += kKvTile, buf ^= 1) {
     const uint64_t nt = t0 + kKvTile;
@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
     uint32_t k[kKvItems], v[kKvItems], rank[kKvItems];
     uint32_t d[kKvItems];
     if (full_tile(t0)) {
-      mbar_wait(&s_bar[buf], phase[buf]);
-      phase[buf] ^= 1;
+      mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
 #pragma unroll
       for (int j = 0; j < kKvItems; ++j) {
         const uint32_t i = warp * (kKvItems * 32) + j * 32 + lane;

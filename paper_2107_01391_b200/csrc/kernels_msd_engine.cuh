@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_hist(Load ld, const MsdSeg*
 }
 
 template <class Load>
-__global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdSeg* __restrict__ segs,
+__global__ void __launch_bounds__(kMsdThreads, 4) k_msd_scatter(Load ld, const MsdSeg* __restrict__ segs,
                                                              const uint32_t* __restrict__ chunk_seg, uint32_t shift,
                                                              const uint32_t* __restrict__ off,
                                                              typename Load::Key* __restrict__ dst) {
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdS
       ok = false;
     }
   };
-  unsigned phase[2] = {0, 0};
+  unsigned phase = 0;  // bit b: parity of buffer b's barrier
   if constexpr (kBulk) {
     if (threadIdx.x == 0) {
       mbar_init(&s_bar[0], 1);
@@ -265,14 +265,14 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdS
     }
     __syncthreads();
     K k[kPer];
-    uint32_t rk[kPer];
+    uint32_t rk2[kPer / 2];  // ranks in the tile (< 4096), two per word; 0xffff = no key
     bool bulk_tile = false;
     if constexpr (kBulk) {
       uint32_t mis, bytes;
       tile_geo(u, mis, bytes, bulk_tile);
       if (bulk_tile) {
-        mbar_wait(&s_bar[buf], phase[buf]);
-        phase[buf] ^= 1;
+        mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
+        phase ^= 1u << buf;
 #pragma unroll
         for (int j = 0; j < kPer; ++j) {
           const uint32_t i = j * kMsdThreads + threadIdx.x;
@@ -283,12 +283,11 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdS
     if (!bulk_tile) ld.load16(a + t0, tl, k);  // element j*kMsdThreads + threadIdx.x (or a permutation)
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
-      rk[j] = 0xffffffffu;
+      uint32_t r = 0xffffu;
       const bool valid = bulk_tile ? (uint32_t)(j * kMsdThreads + threadIdx.x) < tl : ld.valid(j, tl);
-      if (valid) {
-        const uint32_t d = (uint32_t)(k[j] >> shift) & (kMsdBins - 1);
-        rk[j] = (d << 16) | atomicAdd(&s_cnt[d], 1u);
-      }
+      if (valid) r = atomicAdd(&s_cnt[(uint32_t)(k[j] >> shift) & (kMsdBins - 1)], 1u);
+      if (j & 1) rk2[j >> 1] |= r << 16;
+      else rk2[j >> 1] = r;
     }
     __syncthreads();
     {  // exclusive scan of 256 counts, one per thread
@@ -312,8 +311,10 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_scatter(Load ld, const MsdS
     __syncthreads();
     K* stage = &s_buf[buf][0];
 #pragma unroll
-    for (int j = 0; j < kPer; ++j)
-      if (rk[j] != 0xffffffffu) stage[s_cnt[rk[j] >> 16] + (rk[j] & 0xffffu)] = k[j];
+    for (int j = 0; j < kPer; ++j) {
+      const uint32_t r = (rk2[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+      if (r != 0xffffu) stage[s_cnt[(uint32_t)(k[j] >> shift) & (kMsdBins - 1)] + r] = k[j];
+    }
     __syncthreads();
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < tl; i += blockDim.x) {
@@ -389,47 +390,59 @@ __global__ void k_leaf_copy(const K* __restrict__ src, const MsdSeg* __restrict_
 // The recombinant step on a leaf: every key of the segment shares the bits
 // above rem_bits, so a count grid over the 2^rem_bits remaining cells sorts
 // it.  Counters are uint16 pairs in 32-bit words (segments hold < 65536
-// keys); word w lives at w + w/32 so that threads scanning 32 consecutive
-// words each hit distinct banks.  Grid <= 2^16 cells = 132 KB.
-__host__ __device__ constexpr uint32_t leaf_grid_words(uint32_t rem_bits) {
-  const uint32_t words = ((1u << rem_bits) + 1) / 2;
-  return words + words / 32 + 1;
-}
+// keys); word w lives at w ^ ((w >> 5) & 31) so that threads scanning 32
+// consecutive words each hit distinct banks.  Grid <= 2^16 cells = 128 KB.
+//
+// Segments up to `cap` keys (the shared memory left after the grid, as
+// uint16 cells) are finished by a counting-sort scatter inside shared
+// memory: counts become exclusive offsets in place, each key (re-read from
+// L2) takes its rank with one returning shared atomic and drops its cell
+// into the staging array, which is then written out in order — one coalesced
+// store per key.  Larger segments walk the grid (run-length emit).
+__host__ __device__ constexpr uint32_t leaf_grid_words(uint32_t rem_bits) { return ((1u << rem_bits) + 1) / 2; }
+__device__ __forceinline__ uint32_t leaf_gw(uint32_t w) { return w ^ ((w >> 5) & 31u); }
 
 template <class K, class Emit>
 __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restrict__ src,
                                                                 const MsdSeg* __restrict__ segs, uint32_t rem_bits,
-                                                                Emit emit) {
+                                                                uint32_t cap, Emit emit) {
   extern __shared__ uint32_t s_w[];
   __shared__ uint32_t s_scan[kLeafGridThreads / 32];
   const MsdSeg g = segs[blockIdx.x];
   const uint32_t cells = 1u << rem_bits;
   const uint32_t words = (cells + 1) / 2;
-  const uint32_t phys = leaf_grid_words(rem_bits);
+  uint16_t* s_out = reinterpret_cast<uint16_t*>(s_w + words);
+  const bool scatter = g.size <= cap;
   const K mask = (K(1) << rem_bits) - 1;
-  for (uint32_t i = threadIdx.x; i < phys; i += blockDim.x) s_w[i] = 0;
+  // One CTA per SM: the first batch of keys is in flight while the grid is
+  // zeroed, later batches keep kB loads per thread outstanding.
+  constexpr int kB = sizeof(K) == 4 ? 16 : 8;
+  const K* sp = src + g.start;
+  const K prefix = sp[0] & ~mask;
+  K v[kB];
+  auto load = [&](uint32_t i, bool last_use) {
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const uint32_t e = i + u * kLeafGridThreads;
+      v[u] = e < g.size ? (last_use ? __ldcs(sp + e) : __ldcg(sp + e)) : K(0);
+    }
+  };
+  uint32_t i = threadIdx.x;
+  load(i, !scatter);
+  for (uint32_t z = threadIdx.x; z < words; z += blockDim.x) s_w[z] = 0;
   __syncthreads();
-  const K prefix = src[g.start] & ~mask;
-  {  // four independent loads in flight before the atomics
-    const K* sp = src + g.start;
-    uint32_t i = threadIdx.x;
-    for (; i + 3 * kLeafGridThreads < g.size; i += 4 * kLeafGridThreads) {
-      K v[4];
+  for (;;) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldcs(sp + i + u * kLeafGridThreads);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kB; ++u)
+      if (i + u * kLeafGridThreads < g.size) {
         const uint32_t cell = static_cast<uint32_t>(v[u] & mask);
-        const uint32_t w = cell >> 1;
-        atomicAdd(&s_w[w + (w >> 5)], 1u << ((cell & 1) * 16));
+        atomicAdd(&s_w[leaf_gw(cell >> 1)], 1u << ((cell & 1) * 16));
       }
-    }
-    for (; i < g.size; i += kLeafGridThreads) {
-      const uint32_t cell = static_cast<uint32_t>(sp[i] & mask);
-      const uint32_t w = cell >> 1;
-      atomicAdd(&s_w[w + (w >> 5)], 1u << ((cell & 1) * 16));
-    }
+    i += kB * kLeafGridThreads;
+    if (i >= g.size) break;
+    load(i, !scatter);
   }
+  if (scatter) load(threadIdx.x, true);  // the rank pass re-reads the segment (L2)
   __syncthreads();
   // exclusive scan over cells: each thread owns a contiguous run of words
   const uint32_t per = (words + kLeafGridThreads - 1) / kLeafGridThreads;
@@ -438,8 +451,8 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   for (uint32_t j = 0; j < per; ++j) {
     const uint32_t w = w0 + j;
     if (w < words) {
-      const uint32_t v = s_w[w + (w >> 5)];
-      sum += (v & 0xffffu) + (v >> 16);
+      const uint32_t x = s_w[leaf_gw(w)];
+      sum += (x & 0xffffu) + (x >> 16);
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -453,6 +466,34 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   __syncthreads();
   uint32_t run = inc - sum;
   for (int w = 0; w < warp; ++w) run += s_scan[w];
+  if (scatter) {
+    for (uint32_t j = 0; j < per; ++j) {  // counts -> exclusive offsets (< 65536: no carry between halves)
+      const uint32_t w = w0 + j;
+      if (w < words) {
+        const uint32_t x = s_w[leaf_gw(w)];
+        const uint32_t c0 = x & 0xffffu, c1 = x >> 16;
+        s_w[leaf_gw(w)] = run | ((run + c0) << 16);
+        run += c0 + c1;
+      }
+    }
+    __syncthreads();
+    for (i = threadIdx.x;;) {
+#pragma unroll
+      for (int u = 0; u < kB; ++u)
+        if (i + u * kLeafGridThreads < g.size) {
+          const uint32_t cell = static_cast<uint32_t>(v[u] & mask);
+          const uint32_t sh = (cell & 1) * 16;
+          const uint32_t old = atomicAdd(&s_w[leaf_gw(cell >> 1)], 1u << sh);
+          s_out[(old >> sh) & 0xffffu] = static_cast<uint16_t>(cell);
+        }
+      i += kB * kLeafGridThreads;
+      if (i >= g.size) break;
+      load(i, true);
+    }
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < g.size; p += kLeafGridThreads) emit(g.start + p, prefix | K(s_out[p]));
+    return;
+  }
   // Emit warp-cooperatively: the warp's 32 threads own a contiguous range of
   // cells and hence a contiguous output range starting at lane 0's offset.
   // Lanes take 32 consecutive cells at a time and write consecutive
@@ -460,10 +501,10 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   uint32_t out = __shfl_sync(0xffffffffu, run, 0);
   const uint32_t w_begin = warp * 32 * per;                 // first counter word of this warp
   const uint32_t w_end = min(words, w_begin + 32 * per);
-  for (uint32_t w0 = w_begin; w0 < w_end; w0 += 32) {       // lane: one word = two cells
-    const uint32_t w = w0 + lane;
-    const uint32_t v = w < w_end ? s_w[w + (w >> 5)] : 0u;
-    const uint32_t c0 = v & 0xffffu, c1 = v >> 16;
+  for (uint32_t wb = w_begin; wb < w_end; wb += 32) {       // lane: one word = two cells
+    const uint32_t w = wb + lane;
+    const uint32_t x = w < w_end ? s_w[leaf_gw(w)] : 0u;
+    const uint32_t c0 = x & 0xffffu, c1 = x >> 16;
     uint32_t inc2 = c0 + c1;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "bulk_copy.cuh"
 #include "kernels_grid.cuh"
@@ -406,8 +407,8 @@ __global__ void __launch_bounds__(kTlThreads, 3) k_page_partition_u32(const uint
   };
   if (threadIdx.x == 0 && blockIdx.x < full_tiles) issue(blockIdx.x, 0);
   uint32_t mx = 0;
-  unsigned ovf = 0;
-  unsigned phase[2] = {0, 0};
+  const uint32_t magic32 = static_cast<uint32_t>(t.magic), shift32 = t.shift - 32;
+  unsigned phase = 0;  // bit b: parity of buffer b's barrier
   int buf = 0;
   for (uint32_t tile = blockIdx.x; tile < t.T; tile += gridDim.x, buf ^= 1) {
     const uint32_t nt = tile + gridDim.x;
@@ -415,8 +416,8 @@ __global__ void __launch_bounds__(kTlThreads, 3) k_page_partition_u32(const uint
     const bool full = tile < full_tiles;
     uint32_t key[kTlPerThread];
     if (full) {
-      mbar_wait(&s_bar[buf], phase[buf]);
-      phase[buf] ^= 1;
+      mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
       const uint4* src = reinterpret_cast<const uint4*>(s_in + buf * kTlTile);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -435,20 +436,26 @@ __global__ void __launch_bounds__(kTlThreads, 3) k_page_partition_u32(const uint
     }
     const uint64_t base = (uint64_t)tile * kTlTile;
     uint32_t pk[kTlPerThread], lo2[kTlPerThread / 2];
+    // bucket = floor(kk / S) as one 32-bit high product (magic < 2^32,
+    // shift >= 32); keys outside the grid count in the dummy bin B+1 and
+    // raise the overflow flag through the running max (checked at the end)
+    auto rank = [&](auto full_tile) {
 #pragma unroll
-    for (int j = 0; j < kTlPerThread; ++j) {
-      const uint32_t kk = key[j];
-      const bool ok = full || base + (j >> 2) * 1024 + threadIdx.x * 4 + (j & 3) < n;
-      const bool ing = ok && kk < cells32;
-      ovf |= ok && !ing;
-      mx = (ok && kk > mx) ? kk : mx;
-      const uint32_t bk = tl_bucket(kk, t);
-      const uint32_t b = ing ? bk : dummy;
-      pk[j] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
-      const uint32_t l = (kk - bk * t.S) & 0xffffu;
-      if (j & 1) lo2[j >> 1] |= l << 16;
-      else lo2[j >> 1] = l;
-    }
+      for (int j = 0; j < kTlPerThread; ++j) {
+        const uint32_t kk = key[j];
+        bool ok = true;
+        if constexpr (!decltype(full_tile)::value) ok = base + (j >> 2) * 1024 + threadIdx.x * 4 + (j & 3) < n;
+        mx = (ok && kk > mx) ? kk : mx;
+        const uint32_t bk = __umulhi(kk, magic32) >> shift32;
+        const uint32_t b = (ok && kk < cells32) ? bk : dummy;
+        pk[j] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
+        const uint32_t l = (kk - bk * t.S) & 0xffffu;
+        if (j & 1) lo2[j >> 1] |= l << 16;
+        else lo2[j >> 1] = l;
+      }
+    };
+    if (full) rank(std::true_type{});
+    else rank(std::false_type{});
     __syncthreads();
     // one thread per bucket: exclusive scan + page bookkeeping
     {
@@ -522,7 +529,7 @@ __global__ void __launch_bounds__(kTlThreads, 3) k_page_partition_u32(const uint
     pc_bm[(uint64_t)b * t.G + blockIdx.x] = s_np[b];
   }
   warp_max_to(mx, &st->max_key);
-  const unsigned f = warp_or(ovf ? 1u : 0u);
+  const unsigned f = warp_or(mx >= cells32 ? 1u : 0u);
   if ((threadIdx.x & 31) == 0 && f) atomicOr(&st->overflow, 1u);
 }
 

@@ -316,6 +316,22 @@ def test_msd_u32_skew_and_duplicates(rs, oracle):
     assert np.array_equal(_np_u32(out), np.sort(keys))
 
 
+def test_msd_count_grid_leaf_modes(rs, oracle):
+    """16-bit count-grid leaves on both sides of the shared-memory staging
+    capacity (~50K keys: scatter below, run-length emit above), a segment at
+    the 65535-key limit, and one cell holding a whole segment."""
+    parts = []
+    for hi, size in [(3, 30_000), (9, 49_000), (11, 52_000), (12, 60_000), (200, 65_535), (201, 40_000)]:
+        low = oracle.gen_u32(1000 + hi, 0, size, 1 << 16)
+        parts.append((np.uint32(hi) << np.uint32(16)) | low)
+    parts.append(np.full(45_000, (77 << 16) | 5, dtype=np.uint32))   # one cell, scatter mode
+    parts.append(np.full(61_000, (78 << 16) | 65535, dtype=np.uint32))  # one cell, emit mode
+    keys = np.concatenate(parts)
+    keys = keys[np.argsort(oracle.gen_u32(99, 0, keys.size, 0), kind="stable")]
+    out, _ = rs.sort_u32(_t(keys.view(np.int32)), msd=True)
+    assert np.array_equal(_np_u32(out), np.sort(keys))
+
+
 def test_msd_strings_vs_oracle(rs, oracle, golden):
     recs = oracle.gen_str_cfg4(oracle.config_seed(4), 0, 1 << 20)
     want, wrep = oracle.sort_fixed_strings(recs)
