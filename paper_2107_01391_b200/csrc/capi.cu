@@ -250,9 +250,11 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
   if (G > t.T) G = t.T;
   t.G = static_cast<uint32_t>(G);
   const uint64_t tiles_per = (t.T + G - 1) / G;
-  t.pages_per_cta = static_cast<uint32_t>(tiles_per * (kTlTile / kPage) + t.B);
+  // entries per tile <= kTlTile + 7 pads per bucket run (uint32 partition),
+  // plus one partly filled page per bucket
+  t.pages_per_cta = static_cast<uint32_t>((tiles_per * (kTlTile + 7ull * t.B) + kPage - 1) / kPage + t.B);
   // groups of ~16*S keys keep the per-group flush of S counters small
-  t.group_pages = static_cast<uint32_t>(std::max<uint64_t>(128, 16ull * S / kPage));
+  t.group_pages = static_cast<uint32_t>(std::min<uint64_t>(kMaxGroupPages, std::max<uint64_t>(128, 16ull * S / kPage)));
   return true;
 }
 

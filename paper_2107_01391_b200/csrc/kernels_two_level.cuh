@@ -40,7 +40,9 @@ constexpr int kTlTile = kTlThreads * kTlPerThread;  // 4096 keys per tile
 constexpr uint32_t kTlMaxBuckets = 1024;            // outer buckets
 constexpr uint32_t kTlMaxInner = 16384;             // inner cells (smem hist <= 64 KB)
 constexpr uint32_t kPage = 1024;                    // inner digits per page (2 KB)
+constexpr uint16_t kPagePad = 0xffff;               // padding entry (inner digits are < 16384)
 constexpr int kGatherThreads = 256;
+constexpr uint32_t kMaxGroupPages = 256;            // pages per page-count work item (16 * S / kPage <= 256)
 
 struct TwoLevel {
   unsigned long long cells;  // grid size C
@@ -358,12 +360,11 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
 // (double buffer), one thread per bucket does the scan and the page
 // bookkeeping in the same step, and the counters are cleared inside the copy
 // phase.  Same output as k_page_partition<MapU32>.
-constexpr size_t kPageU32Smem = 2 * (size_t)kTlTile * 4  // s_in[2]
-                                + (size_t)kTlTile * 4    // s_stage
+constexpr size_t kPageU32Smem = 2 * (size_t)kTlTile * 4  // s_in[2]; the consumed buffer stages the tile
                                 + 256 * 16               // s_dst
                                 + 258 * 4 * 4;           // s_cnt, s_page, s_fill, s_np
 
-__global__ void __launch_bounds__(kTlThreads, 3) k_page_partition_u32(const uint32_t* __restrict__ in, uint64_t n,
+__global__ void __launch_bounds__(kTlThreads, 4) k_page_partition_u32(const uint32_t* __restrict__ in, uint64_t n,
                                                                    TwoLevel t,
                                                                    uint16_t* __restrict__ pages,
                                                                    uint16_t* __restrict__ page_bucket,
@@ -372,8 +373,7 @@ __global__ void __launch_bounds__(kTlThreads, 3) k_page_partition_u32(const uint
                                                                    DevStats* st) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint32_t* s_in = reinterpret_cast<uint32_t*>(sm);             // [2][kTlTile]
-  uint32_t* s_stage = s_in + 2 * kTlTile;                        // [kTlTile]
-  uint4* s_dst = reinterpret_cast<uint4*>(s_stage + kTlTile);   // [256]
+  uint4* s_dst = reinterpret_cast<uint4*>(s_in + 2 * kTlTile);  // [256]
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_dst + 256);   // [258]: buckets, total, dummy
   uint32_t* s_page = s_cnt + 258;
   uint32_t* s_fill = s_page + 258;
@@ -457,11 +457,16 @@ __global__ void __launch_bounds__(kTlThreads, 3) k_page_partition_u32(const uint
     if (full) rank(std::true_type{});
     else rank(std::false_type{});
     __syncthreads();
-    // one thread per bucket: exclusive scan + page bookkeeping
+    // One thread per bucket: exclusive scan of the runs padded to 8 entries
+    // (16 bytes) + page bookkeeping.  Pages fill in 8-entry units, so every
+    // run and every page split stays 16-byte aligned for the bulk stores.
+    uint16_t* stage = reinterpret_cast<uint16_t*>(s_in + buf * kTlTile);  // keys are in registers
+    const uint32_t b = threadIdx.x;
+    const uint32_t len = b < B ? s_cnt[b] : 0u;
+    const uint32_t plen = (len + 7) & ~7u;
+    uint32_t start, dst_a = 0, dst_b = 0, thr = 0;
     {
-      const uint32_t b = threadIdx.x;
-      const uint32_t len = b < B ? s_cnt[b] : 0u;
-      uint32_t inc = len;
+      uint32_t inc = plen;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
@@ -472,14 +477,13 @@ __global__ void __launch_bounds__(kTlThreads, 3) k_page_partition_u32(const uint
       uint32_t before = 0;
 #pragma unroll
       for (int w = 0; w < kTlThreads / 32; ++w) before += w < warp ? s_scan[w] : 0u;
-      const uint32_t start = before + inc - len;
-      if (b == kTlThreads - 1) s_cnt[B] = before + inc;  // staged keys
+      start = before + inc - plen;
       if (b < B && len) {
         uint32_t fill = s_fill[b], pg = s_page[b];
         const uint32_t room = (pg == 0xffffffffu) ? 0u : kPage - fill;
         uint32_t pa = pg, fa = fill, pb = 0;
-        if (len > room) {
-          const uint32_t extra = (len - room + kPage - 1) / kPage;
+        if (plen > room) {
+          const uint32_t extra = (plen - room + kPage - 1) / kPage;
           const uint32_t first = atomicAdd(&s_next, extra);
           for (uint32_t j = 0; j < extra; ++j) page_bucket[page0 + first + j] = static_cast<uint16_t>(b);
           for (uint32_t j = 0; j + 1 < extra; ++j) page_fill[page0 + first + j] = static_cast<uint16_t>(kPage);
@@ -493,34 +497,40 @@ __global__ void __launch_bounds__(kTlThreads, 3) k_page_partition_u32(const uint
             pb = first;
           }
           pg = first + extra - 1;
-          fill = len - room - (extra - 1) * kPage;
+          fill = plen - room - (extra - 1) * kPage;
         } else {
-          fill += len;
+          fill += plen;
         }
         s_fill[b] = fill;
         s_page[b] = pg;
-        s_dst[b] = make_uint4(start, pa * kPage + fa, (pb - 1) * kPage + fa, kPage - fa);
+        dst_a = pa * kPage + fa;  // ranks < thr: the current page
+        dst_b = pb * kPage;       // the rest: consecutive fresh pages
+        thr = kPage - fa;
+        for (uint32_t r = len; r < plen; ++r) stage[start + r] = kPagePad;
       }
       __syncwarp();
       if (b < B) s_cnt[b] = start;
     }
     __syncthreads();
-    const uint32_t staged = s_cnt[B];
+    {  // branch-free: all 16 run starts are read up front (the dummy bin's counter is a valid read)
+      uint32_t pos[kTlPerThread];
 #pragma unroll
-    for (int j = 0; j < kTlPerThread; ++j) {
-      const uint32_t b = pk[j] >> 16;
-      if (b != dummy) s_stage[s_cnt[b] + (pk[j] & 0xffffu)] = (b << 16) | ((lo2[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
+      for (int j = 0; j < kTlPerThread; ++j) pos[j] = s_cnt[pk[j] >> 16] + (pk[j] & 0xffffu);
+#pragma unroll
+      for (int j = 0; j < kTlPerThread; ++j)
+        if ((pk[j] >> 16) != dummy) stage[pos[j]] = static_cast<uint16_t>(lo2[j >> 1] >> ((j & 1) * 16));
     }
+    fence_proxy_async_smem();  // staged entries -> visible to the bulk stores
     __syncthreads();
     // every read of the counters is behind the barrier above: clear them for
     // the next tile (its atomics come after the barrier closing this tile)
-    for (uint32_t b = threadIdx.x; b < B + 2; b += kTlThreads) s_cnt[b] = 0;
-#pragma unroll 4
-    for (uint32_t i = threadIdx.x; i < staged; i += kTlThreads) {
-      const uint32_t w = s_stage[i];
-      const uint4 d = s_dst[w >> 16];
-      const uint32_t r = i - d.x;
-      my_pages[(r < d.w ? d.y : d.z) + r] = static_cast<uint16_t>(w);
+    for (uint32_t i = threadIdx.x; i < B + 2; i += kTlThreads) s_cnt[i] = 0;
+    if (b < B && len) {  // the run, as one or two TMA bulk stores
+      const uint32_t n1 = plen < thr ? plen : thr;
+      bulk_s2g(my_pages + dst_a, stage + start, n1 * 2);
+      if (plen > n1) bulk_s2g(my_pages + dst_b, stage + start + n1, (plen - n1) * 2);
+      bulk_commit();
+      bulk_wait_read();  // the buffer takes a later tile's load
     }
     __syncthreads();
   }
@@ -596,6 +606,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_page_count(const uint16_t* _
                                                                uint32_t* __restrict__ counts) {
   extern __shared__ uint32_t s_c[];  // [S]
   __shared__ uint32_t s_b, s_p0, s_p1;
+  __shared__ uint32_t s_pg[kMaxGroupPages], s_fl[kMaxGroupPages];  // the group's pages and fills
   const uint32_t w = blockIdx.x;
   if (w >= work_start[t.B]) return;
   if (threadIdx.x == 0) {
@@ -615,19 +626,38 @@ __global__ void __launch_bounds__(kGatherThreads) k_page_count(const uint16_t* _
   }
   for (uint32_t i = threadIdx.x; i < t.S; i += blockDim.x) s_c[i] = 0;
   __syncthreads();
-  const uint32_t np = s_p1 - s_p0;
+  const uint32_t np = s_p1 - s_p0;  // <= kMaxGroupPages
+  for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+    const uint32_t page = list[s_p0 + i];
+    s_pg[i] = page;
+    s_fl[i] = page_fill[page];
+  }
+  __syncthreads();
+  // 16-byte slots (8 entries); four independent loads in flight per thread
   constexpr uint32_t kSlots = kPage / 8;
-  for (uint32_t s = threadIdx.x; s < np * kSlots; s += blockDim.x) {
-    const uint32_t pi = s / kSlots, q = s % kSlots;
-    const uint32_t page = list[s_p0 + pi];
-    const uint32_t fill = page_fill[page];
-    if (q * 8 >= fill) continue;
-    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(pages + (uint64_t)page * kPage) + q);
-    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+  constexpr int kU = 4;
+  const uint32_t nslots = np * kSlots;
+  for (uint32_t s0 = threadIdx.x; s0 < nslots; s0 += kU * kGatherThreads) {
+    uint4 v[kU];
+    uint32_t lim[kU];  // valid entries in the slot
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (q * 8 + 2 * j < fill) atomicAdd(&s_c[ws[j] & 0xffffu], 1u);
-      if (q * 8 + 2 * j + 1 < fill) atomicAdd(&s_c[ws[j] >> 16], 1u);
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t s = s0 + u * kGatherThreads;
+      const uint32_t pi = s / kSlots, q = s % kSlots;
+      const uint32_t fill = s < nslots ? s_fl[pi] : 0u;
+      lim[u] = fill > q * 8 ? min(fill - q * 8, 8u) : 0u;
+      v[u] = lim[u] ? __ldcs(reinterpret_cast<const uint4*>(pages + (uint64_t)s_pg[pi] * kPage) + q)
+                    : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t ws[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t e0 = ws[j] & 0xffffu, e1 = ws[j] >> 16;
+        if (2 * j < lim[u] && e0 != kPagePad) atomicAdd(&s_c[e0], 1u);
+        if (2 * j + 1 < lim[u] && e1 != kPagePad) atomicAdd(&s_c[e1], 1u);
+      }
     }
   }
   __syncthreads();
