@@ -140,6 +140,9 @@ int sm_count() {
   return sms;
 }
 
+// k_report: one warp per leading digit, at most 32 warps
+unsigned report_threads(uint32_t radix) { return 32u * (radix < 32 ? (radix ? radix : 1) : 32); }
+
 size_t smem_optin() {  // opt-in dynamic shared memory per block
   static size_t b = [] {
     int dev = 0, v = 0;
@@ -358,17 +361,15 @@ void scan_pass(Workspace& ws, const uint32_t* counts, uint64_t cells, uint64_t n
   auto* occ_end = ws.get<unsigned long long>(kSlotOccEnd, cells);
   RS_CUDA(cudaMemsetAsync(desc, 0, 2ull * tiles * sizeof(unsigned long long), ws.stream));
   RS_CUDA(cudaMemsetAsync(&ws.stats->tile_counter, 0, sizeof(unsigned), ws.stream));
-  {
-    PassTimer pt_(RS_PASS_SCAN, ws.stream);
-    k_scan_cells<<<tiles, kThreads, 0, ws.stream>>>(counts, cells, occ_cell, occ_end, desc, desc + tiles,
-                                                     tiles, ws.stats);
-    RS_LAUNCH_CHECK();
-  }
   const uint32_t etiles = static_cast<uint32_t>((n + kEmitTile - 1) / kEmitTile);
   auto* tile_first = ws.get<uint32_t>(kSlotTileFirst, etiles + 1ull);
   {
-    PassTimer pt_(RS_PASS_SCAN, ws.stream);
-    k_tile_first<<<(etiles + 1 + 255) / 256, 256, 0, ws.stream>>>(occ_end, ws.stats, n, etiles, tile_first);
+    PassTimer pt_(RS_PASS_SCAN, ws.stream, 2);  // k_scan_cells + k_fill_spans
+    auto* spans = ws.get<uint4>(kSlotSpans, etiles / 3 + 1ull);  // a long span covers >= 3 tiles
+    k_scan_cells<<<tiles, kThreads, 0, ws.stream>>>(counts, cells, occ_cell, occ_end, desc, desc + tiles,
+                                                     tiles, ws.stats, etiles, tile_first, spans);
+    RS_LAUNCH_CHECK();
+    k_fill_spans<<<sm_count() * 4, kThreads, 0, ws.stream>>>(spans, ws.stats, tile_first);
     RS_LAUNCH_CHECK();
   }
 }
@@ -402,7 +403,7 @@ void grid_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, u
   (void)sorted;
   {
     PassTimer pt_(RS_PASS_REPORT, ws.stream);
-    k_report<uint32_t><<<1, 32, 0, ws.stream>>>(static_cast<const uint32_t*>(ws.buf[kSlotOccCell]), 0,
+    k_report<uint32_t><<<1, report_threads(radix), 0, ws.stream>>>(static_cast<const uint32_t*>(ws.buf[kSlotOccCell]), 0,
                                                 radix, total_digits, frac_digits, 0, ws.stats, true);
     RS_LAUNCH_CHECK();
   }
@@ -530,7 +531,7 @@ void kv_sort(Workspace& ws, const uint32_t* keys, const uint32_t* vals, uint64_t
   }
   {
     PassTimer pt_(RS_PASS_REPORT, ws.stream);
-    k_report<uint32_t><<<1, 32, 0, ws.stream>>>(keys_out, n, 10, 0, 0, 0, ws.stats);
+    k_report<uint32_t><<<1, report_threads(10), 0, ws.stream>>>(keys_out, n, 10, 0, 0, 0, ws.stats);
     RS_LAUNCH_CHECK();
   }
   pull_stats(ws);
@@ -790,7 +791,7 @@ void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t
   msd_sort(ws, LoadKeys<uint32_t>{in, n}, n, 32, EmitKey<uint32_t>{const_cast<uint32_t*>(out)});
   {
     PassTimer pt_(RS_PASS_REPORT, ws.stream);
-    k_report<uint32_t><<<1, 32, 0, ws.stream>>>(out, n, 10, 0, 0, 0, ws.stats);
+    k_report<uint32_t><<<1, report_threads(10), 0, ws.stream>>>(out, n, 10, 0, 0, 0, ws.stats);
     RS_LAUNCH_CHECK();
   }
   pull_stats(ws);
@@ -1205,7 +1206,7 @@ rs_status rs_emit_u32(const uint32_t* counts, uint64_t cells, uint64_t cell_lo, 
       {
         PassTimer pt_(RS_PASS_SCAN, ws.stream);
         k_scan_cells<<<tiles, kThreads, 0, ws.stream>>>(counts + cell_lo, span, occ_cell, occ_end, desc,
-                                                         desc + tiles, tiles, ws.stats);
+                                                         desc + tiles, tiles, ws.stats, 0, nullptr, nullptr);
         RS_LAUNCH_CHECK();
       }
       pull_stats(ws);

@@ -300,17 +300,29 @@ constexpr unsigned long long kDescAgg = 1ull << 62;
 constexpr unsigned long long kDescPre = 2ull << 62;
 constexpr unsigned long long kDescVal = (1ull << 62) - 1;
 
-__device__ __forceinline__ unsigned long long lookback(volatile unsigned long long* desc, uint32_t tile) {
+// Exclusive prefix of `tile` from its predecessors' descriptors, called by a
+// whole warp: lane l reads descriptor tile-1-l, so one window of 32
+// predecessors costs one round trip; the window's aggregates are summed up to
+// the nearest inclusive prefix, else the warp moves 32 tiles back.
+__device__ __forceinline__ unsigned long long warp_lookback(volatile unsigned long long* desc, uint32_t tile) {
+  const int lane = threadIdx.x & 31;
   unsigned long long prefix = 0;
-  for (int64_t i = (int64_t)tile - 1; i >= 0; --i) {
-    unsigned long long d;
-    do {
-      d = desc[i];
-    } while ((d >> 62) == 0);
-    prefix += d & kDescVal;
-    if ((d >> 62) == 2) break;
+  for (int64_t base = (int64_t)tile - 1;; base -= 32) {
+    const int64_t i = base - lane;
+    unsigned long long d = kDescPre;  // before tile 0: an empty inclusive prefix
+    if (i >= 0) {
+      do {
+        d = desc[i];
+      } while ((d >> 62) == 0);
+    }
+    const unsigned pre = __ballot_sync(0xffffffffu, (d >> 62) == 2);
+    const int stop = pre ? __ffs(pre) - 1 : 31;
+    unsigned long long v = lane <= stop ? (d & kDescVal) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    prefix += v;
+    if (pre) return prefix;
   }
-  return prefix;
 }
 
 __global__ void __launch_bounds__(kThreads) k_scan_cells(const uint32_t* __restrict__ counts,
@@ -319,7 +331,9 @@ __global__ void __launch_bounds__(kThreads) k_scan_cells(const uint32_t* __restr
                                                          unsigned long long* __restrict__ occ_end,
                                                          unsigned long long* desc_occ,
                                                          unsigned long long* desc_sum,
-                                                         uint32_t num_tiles, DevStats* st) {
+                                                         uint32_t num_tiles, DevStats* st,
+                                                         uint32_t etiles, uint32_t* __restrict__ tile_first,
+                                                         uint4* __restrict__ spans) {
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_wocc[kThreads / 32], s_wsum[kThreads / 32];
   __shared__ unsigned long long s_pocc, s_psum;
@@ -364,51 +378,84 @@ __global__ void __launch_bounds__(kThreads) k_scan_cells(const uint32_t* __restr
     s_wsum[warp] = isum;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long ro = 0, rs = 0;
-    for (int w = 0; w < kThreads / 32; ++w) {
-      const unsigned long long a = s_wocc[w], b = s_wsum[w];
-      s_wocc[w] = ro;
-      s_wsum[w] = rs;
-      ro += a;
-      rs += b;
-    }
-    volatile unsigned long long* vo = desc_occ;
-    volatile unsigned long long* vs = desc_sum;
-    unsigned long long po = 0, ps = 0;
+  // tile totals (every thread; the warp sums are in shared memory)
+  unsigned long long ro = 0, rs = 0, bo = 0, bs = 0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) {
+    const unsigned long long a = s_wocc[w], b = s_wsum[w];
+    bo += w < warp ? a : 0ull;
+    bs += w < warp ? b : 0ull;
+    ro += a;
+    rs += b;
+  }
+  // warp 0 chains the occupied count, warp 1 the key sum
+  if (warp < 2) {
+    volatile unsigned long long* vd = warp == 0 ? desc_occ : desc_sum;
+    const unsigned long long r = warp == 0 ? ro : rs;
+    unsigned long long p = 0;
     if (tile == 0) {
-      vo[0] = kDescPre | ro;
-      vs[0] = kDescPre | rs;
+      if (lane == 0) vd[0] = kDescPre | r;
     } else {
-      vo[tile] = kDescAgg | ro;
-      vs[tile] = kDescAgg | rs;
-      po = lookback(vo, tile);
-      ps = lookback(vs, tile);
-      vo[tile] = kDescPre | (po + ro);
-      vs[tile] = kDescPre | (ps + rs);
+      if (lane == 0) vd[tile] = kDescAgg | r;
+      p = warp_lookback(vd, tile);
+      if (lane == 0) vd[tile] = kDescPre | (p + r);
     }
-    s_pocc = po;
-    s_psum = ps;
-    if (tile == num_tiles - 1) {
-      st->n_occupied = po + ro;
-      st->total = ps + rs;
+    if (lane == 0) {
+      if (warp == 0) s_pocc = p;
+      else s_psum = p;
     }
   }
   __syncthreads();
-  unsigned long long pos = s_pocc + s_wocc[warp] + (iocc - occ);
-  unsigned long long run = s_psum + s_wsum[warp] + (isum - sum);
+  const unsigned long long m = s_pocc + ro, total = s_psum + rs;
+  if (tile == num_tiles - 1 && threadIdx.x == 0) {
+    st->n_occupied = m;
+    st->total = total;
+  }
+  unsigned long long pos = s_pocc + bo + (iocc - occ);
+  unsigned long long run = s_psum + bs + (isum - sum);
+  // emit tile e starts at output position e*kEmitTile: the occupied cell
+  // whose key run holds that position starts the tile (tile_first[e]).  A
+  // cell spanning one or two tiles is written by its thread; longer spans
+  // (hot cells, all in one scan tile under skew) go to a list that
+  // k_fill_spans spreads over the whole GPU.
 #pragma unroll
   for (int k = 0; k < kScanPerThread; ++k) {
     if (c[k]) {
-      run += c[k];
       occ_cell[pos] = static_cast<uint32_t>(c0 + k);
+      if (tile_first) {
+        const unsigned long long e0 = (run + kEmitTile - 1) / kEmitTile;
+        unsigned long long e1 = (run + c[k] + kEmitTile - 1) / kEmitTile;
+        e1 = e1 < etiles ? e1 : etiles;
+        if (e1 > e0 + 2) {
+          spans[atomicAdd(&st->long_spans, 1u)] =
+              make_uint4(static_cast<uint32_t>(e0), static_cast<uint32_t>(e1), static_cast<uint32_t>(pos), 0u);
+        } else {
+          for (unsigned long long e = e0; e < e1; ++e) tile_first[e] = static_cast<uint32_t>(pos);
+        }
+      }
+      run += c[k];
       occ_end[pos] = run;
       ++pos;
     }
   }
+  // sentinels: tiles past the counted keys (keys outside the grid) and entry etiles
+  if (tile_first && tile == num_tiles - 1)
+    for (unsigned long long e = (total + kEmitTile - 1) / kEmitTile + threadIdx.x; e <= etiles; e += blockDim.x)
+      tile_first[e] = static_cast<uint32_t>(m);
 }
 
-// First occupied-cell index of every emit tile: tile_first[t] = first j with
+// tile_first over the long spans listed by k_scan_cells (disjoint tile
+// ranges, at most etiles/3 of them): one CTA per span, threads over tiles.
+__global__ void k_fill_spans(const uint4* __restrict__ spans, const DevStats* st, uint32_t* __restrict__ tile_first) {
+  const uint32_t count = st->long_spans;
+  for (uint32_t s = blockIdx.x; s < count; s += gridDim.x) {
+    const uint4 u = spans[s];
+    for (uint32_t e = u.x + threadIdx.x; e < u.y; e += blockDim.x) tile_first[e] = u.z;
+  }
+}
+
+// First occupied-cell index of every emit tile when the key total is only
+// known after the scan (rs_emit_u32; grid sorts fill it inside k_scan_cells): tile_first[t] = first j with
 // occ_end[j] > t*kEmitTile (t = 0..tiles; entry `tiles` is the sentinel M).
 __global__ void k_tile_first(const unsigned long long* __restrict__ occ_end, const DevStats* st,
                              uint64_t n, uint32_t tiles, uint32_t* __restrict__ tile_first) {
@@ -561,27 +608,42 @@ __global__ void k_report(const K* __restrict__ sorted, uint64_t n, uint32_t radi
   const uint32_t digits =
       total_digits ? total_digits : d_digit_count(top / d_pow(10, frac_digits)) + frac_digits;
   const unsigned long long mod = d_pow(radix, digits - 1);
+  // one warp per leading digit (row): the row's first and last keys by two
+  // warp-cooperative searches (32 probes per round trip)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  auto lower_bound = [&](uint64_t a, uint64_t b, unsigned long long key) {  // first i in [a,b) with sorted[i] >= key
+    while (b - a > 32) {
+      const uint64_t step = (b - a) / 32;
+      const uint64_t idx = a + (uint64_t)(lane + 1) * step;
+      const bool ge = idx < b ? (unsigned long long)sorted[idx] + key_add >= key : true;
+      const unsigned m = __ballot_sync(0xffffffffu, ge);
+      if (m == 0) {
+        a = a + 32 * step + 1;
+      } else {
+        const int f = __ffs(m) - 1;
+        b = a + (uint64_t)(f + 1) * step;
+        a = f > 0 ? a + (uint64_t)f * step + 1 : a;
+      }
+    }
+    const uint64_t idx = a + lane;
+    const bool ge = idx < b ? (unsigned long long)sorted[idx] + key_add >= key : true;
+    const unsigned m = __ballot_sync(0xffffffffu, ge);
+    return m ? a + (uint64_t)(__ffs(m) - 1) : b;
+  };
   unsigned long long span = 0;
-  for (uint32_t r = threadIdx.x; r < radix; r += blockDim.x) {
+  for (uint32_t r = warp; r < radix; r += nwarps) {
     const unsigned long long lo_key = (unsigned long long)r * mod;
-    const unsigned long long hi_key = lo_key + mod;
-    uint64_t a = 0, b = n;
-    while (a < b) {  // first >= lo_key
-      const uint64_t mid = (a + b) >> 1;
-      if ((unsigned long long)sorted[mid] + key_add >= lo_key) b = mid;
-      else a = mid + 1;
-    }
-    uint64_t c = a, d = n;
-    while (c < d) {  // first >= hi_key
-      const uint64_t mid = (c + d) >> 1;
-      if ((unsigned long long)sorted[mid] + key_add >= hi_key) d = mid;
-      else c = mid + 1;
-    }
-    if (a < c) span += (unsigned long long)sorted[c - 1] - (unsigned long long)sorted[a] + 1;
+    const uint64_t a = lower_bound(0, n, lo_key);
+    const uint64_t c = lower_bound(a, n, lo_key + mod);
+    if (a < c && lane == 0) span += (unsigned long long)sorted[c - 1] - (unsigned long long)sorted[a] + 1;
   }
-  for (int o = 16; o > 0; o >>= 1) span += __shfl_xor_sync(0xffffffffu, span, o);
+  __shared__ unsigned long long s_span[32];
+  if (lane == 0) s_span[warp] = span;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    st->cells_traversed = span;
+    unsigned long long total = 0;
+    for (int w = 0; w < nwarps; ++w) total += s_span[w];
+    st->cells_traversed = total;
     st->report_digits = digits;
   }
 }

@@ -118,27 +118,29 @@ __global__ void __launch_bounds__(kThreads) k_exscan_u32(const uint32_t* __restr
   }
   if (lane == 31) s_w[warp] = inc;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long r = 0;
-    for (int w = 0; w < kThreads / 32; ++w) {
-      const unsigned long long c = s_w[w];
-      s_w[w] = r;
-      r += c;
-    }
+  unsigned long long r = 0, before = 0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) {
+    before += w < warp ? s_w[w] : 0ull;
+    r += s_w[w];
+  }
+  if (warp == 0) {
     volatile unsigned long long* vd = desc;
     unsigned long long p = 0;
     if (tile == 0) {
-      vd[0] = kDescPre | r;
+      if (lane == 0) vd[0] = kDescPre | r;
     } else {
-      vd[tile] = kDescAgg | r;
-      p = lookback(vd, tile);
-      vd[tile] = kDescPre | (p + r);
+      if (lane == 0) vd[tile] = kDescAgg | r;
+      p = warp_lookback(vd, tile);
+      if (lane == 0) vd[tile] = kDescPre | (p + r);
     }
-    s_prefix = p;
-    if (tile == num_tiles - 1) *total = p + r;
+    if (lane == 0) {
+      s_prefix = p;
+      if (tile == num_tiles - 1) *total = p + r;
+    }
   }
   __syncthreads();
-  unsigned long long run = s_prefix + s_w[warp] + inc - sum;
+  unsigned long long run = s_prefix + before + inc - sum;
 #pragma unroll
   for (int k = 0; k < kScanPerThread; ++k) {
     if (i0 + k < count) out[i0 + k] = static_cast<uint32_t>(run);

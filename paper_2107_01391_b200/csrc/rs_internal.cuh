@@ -98,7 +98,7 @@ struct DevStats {
   unsigned int overflow;         // a key fell outside the grid
   unsigned int flags;            // bit0 negative, bit1 non-finite, bit2 out-of-domain
   unsigned int tile_counter;     // dynamic tile ids for the look-back scan
-  unsigned int pad;
+  unsigned int long_spans;        // hot cells spanning >= 3 emit tiles (k_scan_cells -> k_fill_spans)
   unsigned long long cells_traversed;  // report (per-row spans)
   unsigned long long report_digits;    // total_digits found by the report kernel
 };
@@ -110,7 +110,7 @@ enum : unsigned { kFlagNegative = 1u, kFlagNonFinite = 2u, kFlagDomain = 4u };
 struct Workspace {
   int device = -1;
   cudaStream_t stream = nullptr;
-  static constexpr int kSlots = 20;
+  static constexpr int kSlots = 21;
   void* buf[kSlots] = {};
   size_t cap[kSlots] = {};
   DevStats* stats = nullptr;   // device
@@ -164,6 +164,7 @@ enum Slot : int {
   kSlotScratch = 17,
   kSlotAlphabet = 18,   // string ordinal / symbol tables
   kSlotExtra1 = 19,     // MSD thread-leaf list
+  kSlotSpans = 20,      // long emit-tile spans of hot cells
 };
 
 }  // namespace rsb
