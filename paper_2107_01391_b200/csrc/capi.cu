@@ -233,6 +233,7 @@ bool div_magic32(uint64_t d, unsigned long long& magic, uint32_t& shift) {
 // (10^6 = 100 x 10^4).  Few outer buckets keep each tile's bucket runs long
 // (~40 keys per 4096-key tile); 10^4 inner counters (40 KB) still fit a
 // shared histogram.
+template <class Map>
 bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
   if (cells <= kSmemCellsMax || cells > 0xFFFFFFFFull || n >= 0x7FFFFFFFull * 16) return false;
   uint64_t B = (cells + 9999) / 10000;
@@ -244,11 +245,13 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
   t.B = static_cast<uint32_t>((cells + S - 1) / S);
   if (!div_magic32(S, t.magic, t.shift) || t.shift < 32) return false;  // S == 1: never (cells > smem grid)
   t.T = static_cast<uint32_t>((n + kTlTile - 1) / kTlTile);
-  int per_sm = 0;
-  cudaFuncSetAttribute(k_page_partition_u32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(kPageU32Smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_page_partition_u32, kTlThreads, kPageU32Smem);
-  if (per_sm < 1) per_sm = 1;
+  static const int per_sm = [] {  // once per mapper (one device type per process)
+    int b = 0;
+    cudaFuncSetAttribute(k_page_partition_tma<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(page_tma_smem<Map>()));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_page_partition_tma<Map>, kTlThreads, page_tma_smem<Map>());
+    return b < 1 ? 1 : b;
+  }();
   uint64_t G = (uint64_t)sm_count() * per_sm;  // one persistent wave
   if (G > t.T) G = t.T;
   t.G = static_cast<uint32_t>(G);
@@ -281,25 +284,15 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
                                  static_cast<int>(smem)));
   {
     PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
-    if constexpr (std::is_same<Map, MapU32>::value) {
-      if (al && t.B <= 256) {  // TMA-fed specialisation
-        static bool attr = false;
-        if (!attr) {
-          RS_CUDA(cudaFuncSetAttribute(k_page_partition_u32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kPageU32Smem)));
-          attr = true;
-        }
-        k_page_partition_u32<<<t.G, kTlThreads, kPageU32Smem, ws.stream>>>(in, n, t, pages, page_bucket, page_fill,
-                                                                           pc_bm, ws.stats);
-        RS_LAUNCH_CHECK();
-        goto partitioned;
-      }
+    if (al && t.B <= 256) {  // TMA-fed tiles, bulk-stored pages
+      k_page_partition_tma<Map><<<t.G, kTlThreads, page_tma_smem<Map>(), ws.stream>>>(
+          in, n, map, t, pages, page_bucket, page_fill, pc_bm, ws.stats);
+    } else {
+      k_page_partition<Map><<<t.G, kTlThreads, smem, ws.stream>>>(in, n, map, t, al, pages, page_bucket,
+                                                                  page_fill, pc_bm, ws.stats);
     }
-    k_page_partition<Map><<<t.G, kTlThreads, smem, ws.stream>>>(in, n, map, t, al, pages, page_bucket,
-                                                                page_fill, pc_bm, ws.stats);
     RS_LAUNCH_CHECK();
   }
-partitioned:
   exscan_u32(ws, pc_bm, bg, po_bm, total);
   {
     PassTimer pt_(RS_PASS_SCAN, ws.stream, 2);
@@ -332,7 +325,7 @@ void count_pass(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, 
     return;
   }
   TwoLevel t{};
-  if (plan_two_level(cells, n, t)) {
+  if (plan_two_level<Map>(cells, n, t)) {
     two_level_count(ws, in, n, map, t, counts);
     return;
   }

@@ -356,27 +356,36 @@ __global__ void __launch_bounds__(kTlThreads) k_page_partition(const typename Ma
 }
 
 
-// ---------------------------------------------------------- K1 (uint32)
-// Specialised partition for uint32 keys when B <= 256 and the input is
-// 16-byte aligned: tiles arrive by 1D TMA bulk copies one tile ahead
-// (double buffer), one thread per bucket does the scan and the page
-// bookkeeping in the same step, and the counters are cleared inside the copy
-// phase.  Same output as k_page_partition<MapU32>.
-constexpr size_t kPageU32Smem = 2 * (size_t)kTlTile * 4  // s_in[2]; the consumed buffer stages the tile
-                                + 256 * 16               // s_dst
-                                + 258 * 4 * 4;           // s_cnt, s_page, s_fill, s_np
+// ------------------------------------------------------- K1 (TMA-fed)
+// Partition for 16-byte aligned inputs with B <= 256: tiles of 4096 inputs
+// arrive by 1D TMA bulk copies one tile ahead (double buffer); each key is
+// mapped straight from the shared tile (uint32 keys: four 16-byte vectors
+// per thread; 8-byte inputs: one element per thread per step, so only the
+// 32-bit cells stay in registers).  One thread per bucket scans and keeps
+// the page bookkeeping; the tile is staged by bucket in the consumed input
+// buffer, each bucket run padded to 16 bytes, and written to its page(s) by
+// TMA bulk stores.  Same page contents as k_page_partition<Map> (plus pad
+// entries, skipped by k_page_count).
+template <class Map>
+__host__ __device__ constexpr size_t page_tma_smem() {
+  return 2 * (size_t)kTlTile * sizeof(typename Map::In)  // s_in[2]; the consumed buffer stages the tile
+         + 256 * 16                                      // s_run: this tile's run geometry per bucket
+         + 258 * 4 * 4;                                  // s_cnt, s_page, s_fill, s_np
+}
+template <class Map>
+constexpr int page_tma_min_blocks() { return sizeof(typename Map::In) == 4 ? 4 : 2; }
 
-__global__ void __launch_bounds__(kTlThreads, 4) k_page_partition_u32(const uint32_t* __restrict__ in, uint64_t n,
-                                                                   TwoLevel t,
-                                                                   uint16_t* __restrict__ pages,
-                                                                   uint16_t* __restrict__ page_bucket,
-                                                                   uint16_t* __restrict__ page_fill,
-                                                                   uint32_t* __restrict__ pc_bm,
-                                                                   DevStats* st) {
+template <class Map>
+__global__ void __launch_bounds__(kTlThreads, page_tma_min_blocks<Map>())
+    k_page_partition_tma(const typename Map::In* __restrict__ in, uint64_t n, Map map, TwoLevel t,
+                         uint16_t* __restrict__ pages, uint16_t* __restrict__ page_bucket,
+                         uint16_t* __restrict__ page_fill, uint32_t* __restrict__ pc_bm, DevStats* st) {
+  using In = typename Map::In;
+  constexpr bool k32 = sizeof(In) == 4;
   extern __shared__ __align__(128) unsigned char sm[];
-  uint32_t* s_in = reinterpret_cast<uint32_t*>(sm);             // [2][kTlTile]
-  uint4* s_dst = reinterpret_cast<uint4*>(s_in + 2 * kTlTile);  // [256]
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_dst + 256);   // [258]: buckets, total, dummy
+  In* s_in = reinterpret_cast<In*>(sm);                         // [2][kTlTile]
+  uint4* s_run = reinterpret_cast<uint4*>(s_in + 2 * kTlTile);       // [256]: start, plen, dst_a, dst_b
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_run + 256);        // [258]: buckets, total, dummy
   uint32_t* s_page = s_cnt + 258;
   uint32_t* s_fill = s_page + 258;
   uint32_t* s_np = s_fill + 258;
@@ -404,52 +413,69 @@ __global__ void __launch_bounds__(kTlThreads, 4) k_page_partition_u32(const uint
   __syncthreads();
   auto issue = [&](uint32_t tile, int b) {  // one thread
     fence_proxy_async_smem();
-    mbar_expect_tx(&s_bar[b], kTlTile * 4);
-    bulk_g2s(s_in + b * kTlTile, in + (uint64_t)tile * kTlTile, kTlTile * 4, &s_bar[b]);
+    mbar_expect_tx(&s_bar[b], kTlTile * sizeof(In));
+    bulk_g2s(s_in + b * kTlTile, in + (uint64_t)tile * kTlTile, kTlTile * sizeof(In), &s_bar[b]);
   };
   if (threadIdx.x == 0 && blockIdx.x < full_tiles) issue(blockIdx.x, 0);
-  uint32_t mx = 0;
+  uint32_t mx32 = 0;
+  unsigned long long mx64 = 0;
+  unsigned flags = 0;
   const uint32_t magic32 = static_cast<uint32_t>(t.magic), shift32 = t.shift - 32;
   unsigned phase = 0;  // bit b: parity of buffer b's barrier
   int buf = 0;
+  // element of the tile handled by (thread, j): 16-byte vectors for uint32
+  auto elem = [&](int j) -> uint32_t {
+    return k32 ? (uint32_t)((j >> 2) * 1024 + threadIdx.x * 4 + (j & 3)) : (uint32_t)(j * kTlThreads + threadIdx.x);
+  };
   for (uint32_t tile = blockIdx.x; tile < t.T; tile += gridDim.x, buf ^= 1) {
     const uint32_t nt = tile + gridDim.x;
     if (threadIdx.x == 0 && nt < full_tiles) issue(nt, buf ^ 1);
     const bool full = tile < full_tiles;
-    uint32_t key[kTlPerThread];
+    uint32_t kreg[k32 ? kTlPerThread : 1];
     if (full) {
       mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
       phase ^= 1u << buf;
-      const uint4* src = reinterpret_cast<const uint4*>(s_in + buf * kTlTile);
+      if constexpr (k32) {
+        const uint4* src = reinterpret_cast<const uint4*>(s_in + buf * kTlTile);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 v = src[q * kTlThreads + threadIdx.x];
-        key[4 * q] = v.x; key[4 * q + 1] = v.y; key[4 * q + 2] = v.z; key[4 * q + 3] = v.w;
-      }
-    } else {
-      const uint64_t base = (uint64_t)tile * kTlTile;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint64_t i = base + q * 1024 + threadIdx.x * 4 + e;
-          key[4 * q + e] = i < n ? in[i] : 0xffffffffu;  // past the end: dummy bin
+        for (int q = 0; q < 4; ++q) {
+          const uint4 v = src[q * kTlThreads + threadIdx.x];
+          kreg[4 * q] = v.x; kreg[4 * q + 1] = v.y; kreg[4 * q + 2] = v.z; kreg[4 * q + 3] = v.w;
         }
+      }
     }
-    const uint64_t base = (uint64_t)tile * kTlTile;
     uint32_t pk[kTlPerThread], lo2[kTlPerThread / 2];
-    // bucket = floor(kk / S) as one 32-bit high product (magic < 2^32,
+    // bucket = floor(cell / S) as one 32-bit high product (magic < 2^32,
     // shift >= 32); keys outside the grid count in the dummy bin B+1 and
     // raise the overflow flag through the running max (checked at the end)
     auto rank = [&](auto full_tile) {
+      constexpr bool kFull = decltype(full_tile)::value;
 #pragma unroll
       for (int j = 0; j < kTlPerThread; ++j) {
-        const uint32_t kk = key[j];
         bool ok = true;
-        if constexpr (!decltype(full_tile)::value) ok = base + (j >> 2) * 1024 + threadIdx.x * 4 + (j & 3) < n;
-        mx = (ok && kk > mx) ? kk : mx;
+        In v;
+        if constexpr (kFull) {
+          if constexpr (k32) v = static_cast<In>(kreg[j]);
+          else v = s_in[buf * kTlTile + elem(j)];
+        } else {
+          const uint64_t i = (uint64_t)tile * kTlTile + elem(j);
+          ok = i < n;
+          v = ok ? in[i] : In{};
+        }
+        uint32_t kk;
+        bool ing;
+        if constexpr (k32) {
+          kk = map.key32(v, flags);
+          mx32 = (ok && kk > mx32) ? kk : mx32;
+          ing = ok && kk < cells32;
+        } else {
+          const unsigned long long k64 = ok ? map(v, flags) : 0ull;
+          mx64 = k64 > mx64 ? k64 : mx64;
+          ing = ok && k64 < t.cells;
+          kk = static_cast<uint32_t>(k64);
+        }
         const uint32_t bk = __umulhi(kk, magic32) >> shift32;
-        const uint32_t b = (ok && kk < cells32) ? bk : dummy;
+        const uint32_t b = ing ? bk : dummy;
         pk[j] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
         const uint32_t l = (kk - bk * t.S) & 0xffffu;
         if (j & 1) lo2[j >> 1] |= l << 16;
@@ -462,12 +488,12 @@ __global__ void __launch_bounds__(kTlThreads, 4) k_page_partition_u32(const uint
     // One thread per bucket: exclusive scan of the runs padded to 8 entries
     // (16 bytes) + page bookkeeping.  Pages fill in 8-entry units, so every
     // run and every page split stays 16-byte aligned for the bulk stores.
-    uint16_t* stage = reinterpret_cast<uint16_t*>(s_in + buf * kTlTile);  // keys are in registers
+    uint16_t* stage = reinterpret_cast<uint16_t*>(s_in + buf * kTlTile);  // the tile was consumed above
     const uint32_t b = threadIdx.x;
     const uint32_t len = b < B ? s_cnt[b] : 0u;
     const uint32_t plen = (len + 7) & ~7u;
-    uint32_t start, dst_a = 0, dst_b = 0, thr = 0;
     {
+      uint32_t start;
       uint32_t inc = plen;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -505,9 +531,10 @@ __global__ void __launch_bounds__(kTlThreads, 4) k_page_partition_u32(const uint
         }
         s_fill[b] = fill;
         s_page[b] = pg;
-        dst_a = pa * kPage + fa;  // ranks < thr: the current page
-        dst_b = pb * kPage;       // the rest: consecutive fresh pages
-        thr = kPage - fa;
+        // ranks < kPage - fa: the current page at pa*kPage + fa; the rest:
+        // consecutive fresh pages from pb*kPage (parked in shared memory
+        // across the staging step, which needs the registers)
+        s_run[b] = make_uint4(start, plen, pa * kPage + fa, pb * kPage);
         for (uint32_t r = len; r < plen; ++r) stage[start + r] = kPagePad;
       }
       __syncwarp();
@@ -528,9 +555,11 @@ __global__ void __launch_bounds__(kTlThreads, 4) k_page_partition_u32(const uint
     // the next tile (its atomics come after the barrier closing this tile)
     for (uint32_t i = threadIdx.x; i < B + 2; i += kTlThreads) s_cnt[i] = 0;
     if (b < B && len) {  // the run, as one or two TMA bulk stores
-      const uint32_t n1 = plen < thr ? plen : thr;
-      bulk_s2g(my_pages + dst_a, stage + start, n1 * 2);
-      if (plen > n1) bulk_s2g(my_pages + dst_b, stage + start + n1, (plen - n1) * 2);
+      const uint4 r = s_run[b];  // start, plen, dst_a, dst_b
+      const uint32_t thr = kPage - (r.z & (kPage - 1));
+      const uint32_t n1 = r.y < thr ? r.y : thr;
+      bulk_s2g(my_pages + r.z, stage + r.x, n1 * 2);
+      if (r.y > n1) bulk_s2g(my_pages + r.w, stage + r.x + n1, (r.y - n1) * 2);
       bulk_commit();
       bulk_wait_read();  // the buffer takes a later tile's load
     }
@@ -540,9 +569,13 @@ __global__ void __launch_bounds__(kTlThreads, 4) k_page_partition_u32(const uint
     if (s_page[b] != 0xffffffffu) page_fill[page0 + s_page[b]] = static_cast<uint16_t>(s_fill[b]);
     pc_bm[(uint64_t)b * t.G + blockIdx.x] = s_np[b];
   }
+  const unsigned long long mx = k32 ? (unsigned long long)mx32 : mx64;
   warp_max_to(mx, &st->max_key);
-  const unsigned f = warp_or(mx >= cells32 ? 1u : 0u);
-  if ((threadIdx.x & 31) == 0 && f) atomicOr(&st->overflow, 1u);
+  flags = warp_or(flags | (mx >= t.cells ? 0x80000000u : 0u));
+  if ((threadIdx.x & 31) == 0 && flags) {
+    if (flags & 0x7fffffffu) atomicOr(&st->flags, flags & 0x7fffffffu);
+    if (flags & 0x80000000u) atomicOr(&st->overflow, 1u);
+  }
 }
 
 // Page list grouped by bucket: CTA c walks its used pages (allocated densely
