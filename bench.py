@@ -294,10 +294,10 @@ def main():
         lib.rs_profile_read(ms_arr, ln_arr)
         lib.rs_profile_enable(0)
         # algorithmic bytes per pass of the two-level plan (csrc/kernels_two_level.cuh):
-        # outer hist R4, outer scatter R4 + W2 (uint16 inner digit), inner count
-        # R2, emit W4; the scans touch only the grid (10^6 cells) and the
-        # [100][G] per-CTA histograms.
-        algo_bytes = {"msd_hist": 4 * n, "msd_scatter": 6 * n, "count": 2 * n, "emit": 4 * n,
+        # partition R4 + W2 (keys in, uint16 inner digits out to pages), page
+        # count R2, emit W4; the scans touch only the grid (10^6 cells) and the
+        # [100][G] per-CTA page counts.  (msd_* entries: the MSD engine.)
+        algo_bytes = {"msd_hist": 4 * n, "msd_scatter": 8 * n, "partition": 6 * n, "count": 2 * n, "emit": 4 * n,
                       "scan": KEY_BOUND * 4 + KEY_BOUND * 12, "report": 0}
         passes = {}
         for i in range(rs._lib.RS_NUM_PASSES):

@@ -102,7 +102,7 @@ enum {
   RS_PASS_MAX = 0, RS_PASS_COUNT = 1, RS_PASS_SCAN = 2, RS_PASS_EMIT = 3,
   RS_PASS_REPORT = 4, RS_PASS_KV_HIST = 5, RS_PASS_KV_SCATTER = 6,
   RS_PASS_MSD_HIST = 7, RS_PASS_MSD_SCATTER = 8, RS_PASS_BUCKET = 9,
-  RS_PASS_COPY = 10, RS_PASS_OTHER = 11, RS_NUM_PASSES = 12
+  RS_PASS_COPY = 10, RS_PASS_OTHER = 11, RS_PASS_PARTITION = 12, RS_NUM_PASSES = 13
 };
 uint64_t rs_launch_count(void);
 void rs_profile_enable(int on);

@@ -34,7 +34,7 @@ STATUS_NAMES = {
 }
 RS_OK = 0
 DEFAULT_CELL_BUDGET = 100_000_000  # key_model.hpp:16
-RS_NUM_PASSES = 12
+RS_NUM_PASSES = 13
 
 
 class RsKeySpec(ctypes.Structure):

@@ -283,7 +283,7 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
     RS_CUDA(cudaFuncSetAttribute(k_page_partition<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   {
-    PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
+    PassTimer pt_(RS_PASS_PARTITION, ws.stream);
     if (al && t.B <= 256) {  // TMA-fed tiles, bulk-stored pages
       k_page_partition_tma<Map><<<t.G, kTlThreads, page_tma_smem<Map>(), ws.stream>>>(
           in, n, map, t, pages, page_bucket, page_fill, pc_bm, ws.stats);
@@ -857,8 +857,9 @@ int rs_profile_read(double* h_ms, uint64_t* h_launches) {
   return RS_NUM_PASSES;
 }
 const char* rs_pass_name(int pass) {
-  static const char* names[RS_NUM_PASSES] = {"max", "count", "scan", "emit", "report", "kv_hist",
-                                             "kv_scatter", "msd_hist", "msd_scatter", "bucket", "copy", "other"};
+  static const char* names[RS_NUM_PASSES] = {"max",      "count",       "scan",   "emit", "report",
+                                             "kv_hist",  "kv_scatter",  "msd_hist", "msd_scatter",
+                                             "bucket",   "copy",        "other",  "partition"};
   return (pass >= 0 && pass < RS_NUM_PASSES) ? names[pass] : "unknown";
 }
 
