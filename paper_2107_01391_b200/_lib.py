@@ -11,7 +11,7 @@ import os
 from ctypes import POINTER, c_char_p, c_int, c_uint32, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librecsort_b200.so")
+LIB_PATH = os.environ.get("RS_LIB_PATH") or os.path.join(HERE, "librecsort_b200.so")  # override: A/B timing only
 
 # rs_status, in recsort::errc order + 1 (proj/include/recsort/error.hpp:10-23)
 STATUS_NAMES = {

@@ -658,6 +658,7 @@ __global__ void __launch_bounds__(kThreads) k_str_scan(const uint8_t* __restrict
 // Emit writer for strings: key -> record bytes (key_to_string,
 // key_model.cpp:249-263; pad ordinals become NUL bytes).
 struct OutStr {
+  static constexpr int kWordBytes = 0;  // records
   uint8_t* out;
   uint32_t width, digits, radix;
   const uint8_t* sym;  // device: ordinal -> byte, sym[0] = 0
@@ -676,6 +677,9 @@ struct OutStr {
   __device__ __forceinline__ void put4(uint64_t p, const uint32_t (&c)[4], uint64_t end) const {
     for (int e = 0; e < 4; ++e)
       if (p + e < end) put_key(p + e, base + c[e]);
+  }
+  __device__ __forceinline__ void put4_full(uint64_t p, const uint32_t (&c)[4]) const {
+    for (int e = 0; e < 4; ++e) put_key(p + e, base + c[e]);
   }
 };
 

@@ -479,10 +479,19 @@ __global__ void k_tile_first(const unsigned long long* __restrict__ occ_end, con
 // ----------------------------------------------------------- K4: emit
 // Output writers: positions p..p+3 receive key values v[0..3].
 struct OutU32 {
+  static constexpr int kWordBytes = 4;
   uint32_t* out;
   uint32_t base;
   bool aligned;
   __device__ __forceinline__ void put1(uint64_t p, uint32_t c) const { out[p] = c + base; }
+  // p..p+3 inside the output
+  __device__ __forceinline__ void put4_full(uint64_t p, const uint32_t (&c)[4]) const {
+    if (aligned) {
+      __stcs(reinterpret_cast<uint4*>(out + p), make_uint4(c[0] + base, c[1] + base, c[2] + base, c[3] + base));
+    } else {
+      for (int e = 0; e < 4; ++e) out[p + e] = c[e] + base;
+    }
+  }
   __device__ __forceinline__ void put4(uint64_t p, const uint32_t (&c)[4], uint64_t end) const {
     if (aligned && p + 4 <= end) {
       __stcs(reinterpret_cast<uint4*>(out + p), make_uint4(c[0] + base, c[1] + base, c[2] + base, c[3] + base));
@@ -494,10 +503,19 @@ struct OutU32 {
 };
 
 struct OutU64 {
+  static constexpr int kWordBytes = 8;
   unsigned long long* out;
   unsigned long long base;
   bool aligned;
   __device__ __forceinline__ void put1(uint64_t p, uint32_t c) const { out[p] = c + base; }
+  __device__ __forceinline__ void put4_full(uint64_t p, const uint32_t (&c)[4]) const {
+    if (aligned) {
+      __stcs(reinterpret_cast<ulonglong2*>(out + p), make_ulonglong2(c[0] + base, c[1] + base));
+      __stcs(reinterpret_cast<ulonglong2*>(out + p + 2), make_ulonglong2(c[2] + base, c[3] + base));
+    } else {
+      for (int e = 0; e < 4; ++e) out[p + e] = c[e] + base;
+    }
+  }
   __device__ __forceinline__ void put4(uint64_t p, const uint32_t (&c)[4], uint64_t end) const {
     if (aligned && p + 4 <= end) {
       __stcs(reinterpret_cast<ulonglong2*>(out + p), make_ulonglong2(c[0] + base, c[1] + base));
@@ -547,6 +565,10 @@ __global__ void __launch_bounds__(kThreads) k_emit(const uint32_t* __restrict__ 
     s_end[k] = static_cast<uint32_t>(e < (unsigned long long)kEmitTile ? e : kEmitTile);
     s_cell[k] = occ_cell[j0 + k];
   }
+  if (threadIdx.x == 0) {  // sentinel: every position lies before it
+    s_end[cnt] = 0xffffffffu;
+    s_cell[cnt] = 0;
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kPerWarp = kEmitTile / (kThreads / 32);  // 1024
@@ -561,25 +583,62 @@ __global__ void __launch_bounds__(kThreads) k_emit(const uint32_t* __restrict__ 
     }
     k = lo < cnt ? lo : cnt - 1;
   }
+  const bool full = pend - p0 == (uint64_t)kEmitTile;
+  if constexpr (Out::kWordBytes == 4) {
+    // 4-byte outputs: the current cell's run end and id stay in registers
+    // across groups (long runs cost no shared loads).  Every occupied cell
+    // holds >= 1 key, so one position further is at most one cell further:
+    // a group that crosses run ends needs no loops.
+    uint32_t ek = s_end[k], ck = s_cell[k];
 #pragma unroll
-  for (int g = 0; g < kPerWarp / 128; ++g) {
-    const uint32_t rel = warp * kPerWarp + g * 128 + lane * 4;  // position - p0
-    const uint64_t base = p0 + rel;
-    if (base >= pend) break;
-    while (k + 1 < cnt && s_end[k] <= rel) ++k;
-    uint32_t v[4];
-    const uint32_t c = s_cell[k];
-    if (s_end[k] >= rel + 4 || k + 1 == cnt) {  // the four positions share a cell
-      v[0] = v[1] = v[2] = v[3] = c;
-    } else {
-      uint32_t kk = k;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        while (kk + 1 < cnt && s_end[kk] <= rel + e) ++kk;
-        v[e] = s_cell[kk];
+    for (int g = 0; g < kPerWarp / 128; ++g) {
+      const uint32_t rel = warp * kPerWarp + g * 128 + lane * 4;  // position - p0
+      if (!full && p0 + rel >= pend) break;
+      while (ek <= rel) {
+        ++k;
+        ek = s_end[k];
+        ck = s_cell[k];
       }
+      uint32_t v[4];
+      v[0] = v[1] = v[2] = v[3] = ck;
+      if (ek < rel + 4) {  // a run ends inside the group
+        uint32_t kk = k, e_kk = ek;
+#pragma unroll
+        for (int e = 1; e < 4; ++e) {
+          if (e_kk <= rel + e) {
+            ++kk;
+            e_kk = s_end[kk];
+          }
+          v[e] = s_cell[kk];
+        }
+      }
+      if (full) out.put4_full(p0 + rel, v);
+      else out.put4(p0 + rel, v, pend);
     }
-    out.put4(base, v, pend);
+  } else {
+    // wider outputs (64-bit keys, records): the store stream, not the walk,
+    // sets the pace (measured: the tighter walk above floods the store queue
+    // and starves the next CTAs' setup loads)
+#pragma unroll
+    for (int g = 0; g < kPerWarp / 128; ++g) {
+      const uint32_t rel = warp * kPerWarp + g * 128 + lane * 4;
+      const uint64_t base = p0 + rel;
+      if (base >= pend) break;
+      while (k + 1 < cnt && s_end[k] <= rel) ++k;  // single-cell tiles (hot cells) skip the load
+      uint32_t v[4];
+      const uint32_t c = s_cell[k];
+      if (s_end[k] >= rel + 4 || k + 1 == cnt) {  // the four positions share a cell
+        v[0] = v[1] = v[2] = v[3] = c;
+      } else {
+        uint32_t kk = k;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          while (kk + 1 < cnt && s_end[kk] <= rel + e) ++kk;
+          v[e] = s_cell[kk];
+        }
+      }
+      out.put4(base, v, pend);
+    }
   }
 }
 
