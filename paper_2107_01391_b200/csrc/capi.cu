@@ -701,7 +701,7 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
   auto* leaf_small = ws.get<MsdSeg>(kSlotLows, cap);
   auto* leaf_copy = ws.get<MsdSeg>(kSlotTmpKeys2, cap);
   auto* leaf_warp = ws.get<MsdSeg>(kSlotTmpVals2, cap);
-  auto* leaf_thread = ws.get<MsdSeg>(kSlotExtra1, cap);
+  auto* leaf_radix = ws.get<MsdSeg>(kSlotExtra1, cap);
   auto* cnt = ws.get<unsigned>(kSlotScratch, 8);
   auto* total = reinterpret_cast<unsigned long long*>(cnt + 6);
   MsdSeg first{0, static_cast<uint32_t>(n), 0, 0};
@@ -744,7 +744,7 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
       RS_LAUNCH_CHECK();
     }
     RS_CUDA(cudaMemsetAsync(cnt, 0, 6 * sizeof(unsigned), ws.stream));
-    MsdLists L{segs_out, leaf_grid, leaf_small, leaf_copy, leaf_warp, leaf_thread, cnt};
+    MsdLists L{segs_out, leaf_grid, leaf_small, leaf_copy, leaf_warp, leaf_radix, cnt};
     const unsigned long long pairs = (unsigned long long)nseg * kMsdBins;
     k_msd_classify<<<static_cast<unsigned>((pairs + 255) / 256), 256, 0, ws.stream>>>(segs_in, nseg, off, shift, L);
     RS_LAUNCH_CHECK();
@@ -757,8 +757,11 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
       PassTimer pt_(RS_PASS_BUCKET, ws.stream,
                     (h[1] ? 1 : 0) + (h[2] ? 1 : 0) + (h[3] ? 1 : 0) + (h[4] ? 1 : 0) + (h[5] ? 1 : 0));
       if (h[5]) {
-        const unsigned blocks = std::min<unsigned>((h[5] + kMsdThreads - 1) / kMsdThreads, sm_count() * 16);
-        k_leaf_thread<K, Emit><<<blocks, kMsdThreads, 0, ws.stream>>>(dst, leaf_thread, h[5], emit);
+        static const bool attr = (cudaFuncSetAttribute(k_leaf_radix<K, Emit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(leaf_radix_smem<K>())), true);
+        (void)attr;
+        k_leaf_radix<K, Emit><<<h[5], kLeafRadixThreads, leaf_radix_smem<K>(), ws.stream>>>(dst, leaf_radix, shift,
+                                                                                             emit);
       }
       if (h[4]) {
         const unsigned blocks = std::min<unsigned>((h[4] + 7) / 8, sm_count() * 16);
@@ -795,11 +798,15 @@ void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t
 }
 
 void msd_sort_str(Workspace& ws, const uint8_t* chars, uint64_t n, uint32_t width, uint32_t w, uint32_t radix,
-                  const uint16_t* d_ord, const uint8_t* d_sym, uint8_t* out) {
+                  const uint16_t* d_ord, const uint8_t* d_sym, uint8_t* out, int lin) {
   reset_stats(ws);
   LoadStr ld{chars, width, d_ord};
   ld.w8 = width == 8 && (reinterpret_cast<uintptr_t>(chars) & 7) == 0;
-  msd_sort(ws, ld, n, 5 * width, EmitStr{out, width, d_sym});
+  ld.lin = lin;
+  EmitStr em{out, width, d_sym};
+  em.lin = lin;
+  em.w8 = width == 8 && (reinterpret_cast<uintptr_t>(out) & 7) == 0;
+  msd_sort(ws, ld, n, 5 * width, em);
   {
     PassTimer pt_(RS_PASS_REPORT, ws.stream);
     k_report_recs<<<1, 32, 0, ws.stream>>>(out, n, width, w, radix, d_ord, ws.stats);
@@ -1053,7 +1060,12 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
     }
     if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
     if (t.radix > 32) fail(RS_INVALID_ARGUMENT, "the MSD string path packs 5-bit ordinals: at most 31 symbols");
-    msd_sort_str(ws, chars, n, width, w, t.radix, d_ord, d_sym, out);
+    // contiguous alphabet (e.g. 'a'..'z'): ordinal <-> byte is arithmetic
+    int lin = static_cast<int>(static_cast<unsigned char>(alpha[0])) - 1;
+    for (size_t i = 1; i < alen; ++i)
+      if (static_cast<unsigned char>(alpha[i]) != static_cast<unsigned char>(alpha[0]) + i) lin = -1;
+    if (static_cast<unsigned char>(alpha[0]) == 0) lin = -1;
+    msd_sort_str(ws, chars, n, width, w, t.radix, d_ord, d_sym, out, lin);
     if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{t.radix, w, w}};
   });
 }

@@ -41,7 +41,8 @@ constexpr int kMsdTile = 4096;          // keys per scatter tile
 constexpr uint32_t kMsdChunk = 65536;   // keys per (segment, chunk) work item
 constexpr uint32_t kLeafSmall = 2048;   // shared bitonic leaf capacity
 constexpr uint32_t kLeafWarp = 32;      // warp (register) bitonic leaf capacity
-constexpr uint32_t kLeafThread = 0;     // thread leaves off: a 16-wide network per 4-key segment measured slower than warp leaves
+constexpr uint32_t kLeafRadixMax = 4096;  // shared-memory LSD leaf: <= 4096 keys, <= 24 remaining bits
+constexpr int kLeafRadixThreads = 256;
 constexpr int kLeafGridBits = 16;       // count-grid leaf: <= 2^16 cells (u16 pairs, 128 KB)
 constexpr int kLeafGridThreads = 1024;  // one 128 KB CTA per SM: 32 warps to hide latency
 
@@ -103,6 +104,10 @@ struct LoadStr {
   }
   __device__ __forceinline__ bool valid(int j, uint32_t tl) const { return (uint32_t)(j * kMsdThreads + threadIdx.x) < tl; }
   bool w8 = false;       // 8-byte records at an 8-byte aligned base: one 64-bit load each
+  int lin = -1;          // contiguous alphabet: ordinal = byte - lin (symbols validated by k_str_scan)
+  __device__ __forceinline__ uint32_t ord_of(uint32_t c) const {
+    return lin >= 0 ? c - static_cast<uint32_t>(lin) : __ldg(ord + c);
+  }
   __device__ __forceinline__ unsigned long long operator()(unsigned long long i) const {
     if (w8) {
       const unsigned long long w = __ldcs(reinterpret_cast<const unsigned long long*>(recs) + i);
@@ -112,7 +117,7 @@ struct LoadStr {
       for (int j = 0; j < 8; ++j) {
         const uint32_t c = static_cast<uint32_t>(w >> (8 * j)) & 0xffu;
         ended |= c == 0;
-        const uint32_t o = ended ? 0u : __ldg(ord + c);
+        const uint32_t o = ended ? 0u : ord_of(c);
         k = (k << 5) | o;
       }
       return k;
@@ -125,7 +130,7 @@ struct LoadStr {
       if (!ended) {
         const uint8_t c = r[j];
         if (c == 0) ended = true;
-        else o = __ldg(ord + c);
+        else o = ord_of(c);
       }
       k = (k << 5) | o;
     }
@@ -146,10 +151,22 @@ struct EmitStr {
   uint8_t* out;
   uint32_t width;
   const uint8_t* sym;  // device: ordinal -> byte, sym[0] = 0
+  int lin = -1;        // contiguous alphabet: byte = ordinal + lin (no table lookups)
+  bool w8 = false;     // 8-byte records at an 8-byte aligned base: one 64-bit store each
+  __device__ __forceinline__ uint32_t byte_of(uint32_t o) const {
+    return lin >= 0 ? (o ? o + static_cast<uint32_t>(lin) : 0u) : sym[o];
+  }
   __device__ __forceinline__ void operator()(unsigned long long pos, unsigned long long key) const {
+    if (w8) {
+      unsigned long long w = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w |= static_cast<unsigned long long>(byte_of((key >> (5 * (7 - j))) & 31u)) << (8 * j);
+      reinterpret_cast<unsigned long long*>(out)[pos] = w;
+      return;
+    }
     uint8_t* r = out + pos * width;
     for (int j = (int)width - 1; j >= 0; --j) {
-      r[j] = sym[key & 31u];
+      r[j] = static_cast<uint8_t>(byte_of(key & 31u));
       key >>= 5;
     }
   }
@@ -333,8 +350,8 @@ struct MsdLists {
   MsdSeg* leaf_small;
   MsdSeg* leaf_copy;
   MsdSeg* leaf_warp;
-  MsdSeg* leaf_thread;
-  unsigned* cnt;  // [6]: next, grid, small, copy, warp, thread
+  MsdSeg* leaf_radix;
+  unsigned* cnt;  // [6]: next, grid, small, copy, warp, radix
 };
 
 __global__ void k_msd_classify(const MsdSeg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ off,
@@ -355,12 +372,12 @@ __global__ void k_msd_classify(const MsdSeg* __restrict__ segs, uint32_t nseg, c
     L.leaf_copy[atomicAdd(&L.cnt[3], 1u)] = sub;
   } else if (rem_bits <= kLeafGridBits && size >= (1u << rem_bits) / 16 && size <= 65535u) {
     L.leaf_grid[atomicAdd(&L.cnt[1], 1u)] = sub;  // dense: the count grid
-  } else if (size <= kLeafThread) {
-    L.leaf_thread[atomicAdd(&L.cnt[5], 1u)] = sub;  // tiny: one thread, registers
   } else if (size <= kLeafWarp) {
     L.leaf_warp[atomicAdd(&L.cnt[4], 1u)] = sub;  // small: one warp, registers
   } else if (size <= kLeafSmall && rem_bits <= kMsdDigitBits) {
     L.leaf_small[atomicAdd(&L.cnt[2], 1u)] = sub;  // last digit: shared bitonic
+  } else if (size <= kLeafRadixMax && rem_bits <= 3 * kMsdDigitBits) {
+    L.leaf_radix[atomicAdd(&L.cnt[5], 1u)] = sub;  // mid-size: shared-memory LSD passes
   } else {
     L.next[atomicAdd(&L.cnt[0], 1u)] = sub;  // split by the next 8-bit digit
   }
@@ -572,30 +589,104 @@ __global__ void __launch_bounds__(kMsdThreads) k_leaf_warp(const K* __restrict__
   }
 }
 
-// Tiny leaves (<= 16 keys): one thread per segment, insertion sort in
-// registers (fully unrolled, so the array stays in registers).
+// Mid-size leaves (<= kLeafRadixMax keys, <= 24 remaining bits): one CTA
+// loads the segment into shared memory and sorts it by the remaining bits
+// with stable 8-bit LSD passes, then writes it once.  Ranking: each warp owns
+// a contiguous range of the segment and takes it 32 keys at a time; the
+// lanes sharing a digit are found with 8 ballots, counted per (digit, warp),
+// and one exclusive scan over the [digit][warp] table gives every group its
+// place — the order inside a digit is (warp, group, lane), i.e. the input
+// order, so the passes are stable.
+template <class K>
+__host__ __device__ constexpr size_t leaf_radix_smem() {
+  return 2 * (size_t)kLeafRadixMax * sizeof(K) + 256 * (kLeafRadixThreads / 32) * sizeof(uint32_t);
+}
+
 template <class K, class Emit>
-__global__ void __launch_bounds__(kMsdThreads) k_leaf_thread(const K* __restrict__ src, const MsdSeg* __restrict__ segs,
-                                                             uint32_t nseg, Emit emit) {
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += stride) {
-    const MsdSeg g = segs[s];
-    K v[16];
+__global__ void __launch_bounds__(kLeafRadixThreads) k_leaf_radix(const K* __restrict__ src,
+                                                                  const MsdSeg* __restrict__ segs, uint32_t rem_bits,
+                                                                  Emit emit) {
+  constexpr int kW = kLeafRadixThreads / 32;
+  extern __shared__ __align__(16) unsigned char lr_smem[];
+  K* in = reinterpret_cast<K*>(lr_smem);
+  K* out = in + kLeafRadixMax;
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(out + kLeafRadixMax);  // [kW warps][256 digits] (digit -> bank)
+  __shared__ uint32_t s_part[kLeafRadixThreads / 32];
+  const MsdSeg g = segs[blockIdx.x];
+  const uint32_t n = g.size;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) in[i] = src[g.start + i];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t per = (n + kW * 32 - 1) / (kW * 32) * 32;  // contiguous range per warp, in groups of 32
+  const uint32_t w0 = warp * per, w1 = min(n, w0 + per);
+  const unsigned lt = (1u << lane) - 1;
+  auto peers_of = [&](uint32_t d, bool v) {  // valid lanes with the same digit
+    unsigned m = __ballot_sync(0xffffffffu, v);
 #pragma unroll
-    for (uint32_t i = 0; i < 16; ++i) v[i] = i < g.size ? src[g.start + i] : ~K(0);
+    for (int b = 0; b < 8; ++b) {
+      const unsigned x = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      m &= ((d >> b) & 1u) ? x : ~x;
+    }
+    return m;
+  };
+  for (uint32_t sh = 0; sh < rem_bits; sh += 8) {
+    for (uint32_t i = threadIdx.x; i < 256 * kW; i += blockDim.x) s_cnt[i] = 0;
+    __syncthreads();
+    for (uint32_t base = w0; base < w1; base += 32) {  // counts per (digit, warp)
+      const uint32_t i = base + lane;
+      const bool v = i < w1;
+      const uint32_t d = v ? static_cast<uint32_t>(in[i] >> sh) & 255u : 0u;
+      const unsigned pm = peers_of(d, v);
+      if (v && (pm & lt) == 0) s_cnt[warp * 256 + d] += __popc(pm);
+      __syncwarp();
+    }
+    __syncthreads();
+    {  // exclusive scan in (digit, warp) order: thread t takes digits t*kPer/kW ..
+      constexpr int kPer = 256 * kW / kLeafRadixThreads;
+      auto at = [&](int j) -> uint32_t& {  // j-th entry in (digit, warp) order
+        const uint32_t e = threadIdx.x * kPer + j;
+        return s_cnt[(e % kW) * 256 + e / kW];
+      };
+      uint32_t v[kPer], sum = 0;
 #pragma unroll
-    for (uint32_t i = 1; i < 16; ++i) {
+      for (int j = 0; j < kPer; ++j) {
+        v[j] = at(j);
+        sum += v[j];
+      }
+      uint32_t inc = sum;
 #pragma unroll
-      for (uint32_t j = i; j > 0; --j) {  // compare-exchange down: a sorting network
-        const K a = v[j - 1], b = v[j];
-        v[j - 1] = a < b ? a : b;
-        v[j] = a < b ? b : a;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) s_part[warp] = inc;
+      __syncthreads();
+      uint32_t run = inc - sum;
+      for (int w = 0; w < warp; ++w) run += s_part[w];
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        at(j) = run;
+        run += v[j];
       }
     }
-#pragma unroll
-    for (uint32_t i = 0; i < 16; ++i)
-      if (i < g.size) emit(g.start + i, v[i]);
+    __syncthreads();
+    for (uint32_t base = w0; base < w1; base += 32) {  // stable scatter
+      const uint32_t i = base + lane;
+      const bool v = i < w1;
+      const K key = v ? in[i] : K(0);
+      const uint32_t d = static_cast<uint32_t>(key >> sh) & 255u;
+      const unsigned pm = peers_of(d, v);
+      const uint32_t pos = v ? s_cnt[warp * 256 + d] + __popc(pm & lt) : 0u;
+      __syncwarp();
+      if (v && (pm & lt) == 0) s_cnt[warp * 256 + d] += __popc(pm);
+      __syncwarp();
+      if (v) out[pos] = key;
+    }
+    __syncthreads();
+    K* t = in;
+    in = out;
+    out = t;
   }
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) emit(g.start + i, in[i]);
 }
 
 // ------------------------------------------------------------- report

@@ -163,7 +163,7 @@ enum Slot : int {
   kSlotDesc2 = 16,      // look-back descriptors of the second scan
   kSlotScratch = 17,
   kSlotAlphabet = 18,   // string ordinal / symbol tables
-  kSlotExtra1 = 19,     // MSD thread-leaf list
+  kSlotExtra1 = 19,     // MSD radix-leaf list
   kSlotSpans = 20,      // long emit-tile spans of hot cells
 };
 

@@ -342,6 +342,28 @@ def test_msd_strings_vs_oracle(rs, oracle, golden):
     assert np.array_equal(out.cpu().numpy(), golden["cfg4_sorted"])
 
 
+@pytest.mark.parametrize("alphabet,width", [("zyxwvutsrqponmlkjihgfedcba", 8),   # table path (not contiguous)
+                                            ("abcdefghijklmnopqrstuvwxyz", 7),   # contiguous, unpacked stores
+                                            ("0123456789", 8)])                  # contiguous, other base
+def test_msd_strings_alphabets(rs, oracle, alphabet, width):
+    n = 150_000
+    pick = oracle.gen_u32(31 + width, 0, n * width, len(alphabet)).reshape(n, width)
+    recs = np.frombuffer(alphabet.encode(), dtype=np.uint8)[pick]
+    recs[::7, width - 2:] = 0  # some shorter strings
+    # reference order = alphabet ordinals (strings_to_keys, key_model.cpp:190-247),
+    # not byte order: key = sum ord_i * radix^(w-1-i), pad ordinal 0
+    ords = np.zeros(256, dtype=np.uint64)
+    ords[np.frombuffer(alphabet.encode(), dtype=np.uint8)] = np.arange(1, len(alphabet) + 1, dtype=np.uint64)
+    radix = len(alphabet) + 1
+    keys = np.zeros(n, dtype=np.uint64)
+    for i in range(width):
+        keys = keys * np.uint64(radix) + ords[recs[:, i]]
+    order = np.argsort(keys, kind="stable")
+    out, rep = rs.sort_fixed_str(_t(np.ascontiguousarray(recs)), alphabet=alphabet, msd=True)
+    assert np.array_equal(out.cpu().numpy(), recs[order])
+    assert _rep(rep) == oracle.report_from_sorted(keys[order], radix, width)
+
+
 def test_msd_strings_variable_length(rs, oracle):
     recs = oracle.gen_str_cfg4(17, 0, 200_000)
     lens = oracle.gen_u32(18, 0, 200_000, 9)
