@@ -593,10 +593,13 @@ __global__ void __launch_bounds__(kThreads) k_str_keys(const uint8_t* __restrict
 }
 
 
-// Width (longest string) and symbol validation only, for the MSD path: no key
-// written; 8-byte records read as two 16-byte loads per thread per round.
+// Width (longest string) and symbol validation for the MSD path, optionally
+// writing each record's packed key (5 bits per ordinal, first symbol most
+// significant, pad 0 — the MSD key order); 8-byte records read as two
+// 16-byte loads per thread per round.
 __global__ void __launch_bounds__(kThreads) k_str_scan(const uint8_t* __restrict__ recs, uint64_t n, uint32_t width,
-                                                       bool w8, const uint16_t* __restrict__ ord_g, DevStats* st) {
+                                                       bool w8, const uint16_t* __restrict__ ord_g, DevStats* st,
+                                                       unsigned long long* __restrict__ packed) {
   __shared__ uint16_t ord[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) ord[i] = ord_g[i];
   __syncthreads();
@@ -606,45 +609,62 @@ __global__ void __launch_bounds__(kThreads) k_str_scan(const uint8_t* __restrict
   auto scan8 = [&](unsigned long long w) {
     uint32_t len = 0;
     bool ended = false;
+    unsigned long long k = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t c = static_cast<uint32_t>(w >> (8 * j)) & 0xffu;
       ended |= c == 0;
-      if (!ended) {
-        ++len;
-        bad |= ord[c] == 0;
-      }
+      const uint32_t o = ended ? 0u : ord[c];
+      len += ended ? 0u : 1u;
+      bad |= !ended && o == 0;
+      k = (k << 5) | o;
     }
     mxlen = len > mxlen ? len : mxlen;
+    return k;
   };
   if (w8) {
     const auto* r2 = reinterpret_cast<const ulonglong2*>(recs);
+    auto* p2 = reinterpret_cast<ulonglong2*>(packed);
     const uint64_t pairs = n >> 1;
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; i + stride < pairs; i += 2 * stride) {
       const ulonglong2 a = __ldcs(r2 + i), b = __ldcs(r2 + i + stride);
-      scan8(a.x), scan8(a.y), scan8(b.x), scan8(b.y);
+      const ulonglong2 ka = make_ulonglong2(scan8(a.x), scan8(a.y)), kb = make_ulonglong2(scan8(b.x), scan8(b.y));
+      if (packed) {
+        p2[i] = ka;
+        p2[i + stride] = kb;
+      }
     }
     if (i < pairs) {
       const ulonglong2 a = __ldcs(r2 + i);
-      scan8(a.x), scan8(a.y);
+      const ulonglong2 ka = make_ulonglong2(scan8(a.x), scan8(a.y));
+      if (packed) p2[i] = ka;
     }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
-      scan8(reinterpret_cast<const unsigned long long*>(recs)[n - 1]);
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const unsigned long long k = scan8(reinterpret_cast<const unsigned long long*>(recs)[n - 1]);
+      if (packed) packed[n - 1] = k;
+    }
   } else {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
       uint32_t len = 0;
       bool ended = false;
+      unsigned long long k = 0;
       const uint8_t* r = recs + i * width;
-      for (uint32_t j = 0; j < width && !ended; ++j) {
-        const uint8_t c = r[j];
-        if (c == 0) ended = true;
-        else {
-          ++len;
-          bad |= ord[c] == 0;
+      for (uint32_t j = 0; j < width; ++j) {
+        uint32_t o = 0;
+        if (!ended) {
+          const uint8_t c = r[j];
+          if (c == 0) ended = true;
+          else {
+            ++len;
+            o = ord[c];
+            bad |= o == 0;
+          }
         }
+        k = (k << 5) | o;
       }
       mxlen = len > mxlen ? len : mxlen;
+      if (packed) packed[i] = k;
     }
   }
   if (bad) atomicOr(&st->flags, 8u);
@@ -702,7 +722,7 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
   auto* leaf_copy = ws.get<MsdSeg>(kSlotTmpKeys2, cap);
   auto* leaf_warp = ws.get<MsdSeg>(kSlotTmpVals2, cap);
   auto* leaf_radix = ws.get<MsdSeg>(kSlotExtra1, cap);
-  auto* cnt = ws.get<unsigned>(kSlotScratch, 8);
+  auto* cnt = ws.get<unsigned>(kSlotScratch, 10);  // [0..5] list counts, [6..7] u64 total, [8] largest radix leaf
   auto* total = reinterpret_cast<unsigned long long*>(cnt + 6);
   MsdSeg first{0, static_cast<uint32_t>(n), 0, 0};
   RS_CUDA(cudaMemcpyAsync(segs_a, &first, sizeof(MsdSeg), cudaMemcpyHostToDevice, ws.stream));
@@ -744,24 +764,26 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
       RS_LAUNCH_CHECK();
     }
     RS_CUDA(cudaMemsetAsync(cnt, 0, 6 * sizeof(unsigned), ws.stream));
-    MsdLists L{segs_out, leaf_grid, leaf_small, leaf_copy, leaf_warp, leaf_radix, cnt};
+    RS_CUDA(cudaMemsetAsync(cnt + 8, 0, sizeof(unsigned), ws.stream));
+    MsdLists L{segs_out, leaf_grid, leaf_small, leaf_copy, leaf_warp, leaf_radix, cnt, cnt + 8};
     const unsigned long long pairs = (unsigned long long)nseg * kMsdBins;
     k_msd_classify<<<static_cast<unsigned>((pairs + 255) / 256), 256, 0, ws.stream>>>(segs_in, nseg, off, shift, L);
     RS_LAUNCH_CHECK();
-    unsigned h[6] = {};
+    unsigned h[9] = {};
     RS_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, ws.stream));
     RS_CUDA(cudaStreamSynchronize(ws.stream));
-    for (unsigned v : h)
-      if ((uint64_t)v > cap) fail(RS_CUDA_ERROR, "MSD segment list overflow");
+    for (int i = 0; i < 6; ++i)
+      if ((uint64_t)h[i] > cap) fail(RS_CUDA_ERROR, "MSD segment list overflow");
     {
       PassTimer pt_(RS_PASS_BUCKET, ws.stream,
                     (h[1] ? 1 : 0) + (h[2] ? 1 : 0) + (h[3] ? 1 : 0) + (h[4] ? 1 : 0) + (h[5] ? 1 : 0));
-      if (h[5]) {
+      if (h[5]) {  // buffers sized to the largest leaf of the list
         static const bool attr = (cudaFuncSetAttribute(k_leaf_radix<K, Emit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       static_cast<int>(leaf_radix_smem<K>())), true);
+                                                       static_cast<int>(leaf_radix_smem<K>(kLeafRadixMax))), true);
         (void)attr;
-        k_leaf_radix<K, Emit><<<h[5], kLeafRadixThreads, leaf_radix_smem<K>(), ws.stream>>>(dst, leaf_radix, shift,
-                                                                                             emit);
+        const uint32_t lcap = (h[8] + 15) & ~15u;
+        k_leaf_radix<K, Emit><<<h[5], kLeafRadixThreads, leaf_radix_smem<K>(lcap), ws.stream>>>(dst, leaf_radix, shift,
+                                                                                                 lcap, emit);
       }
       if (h[4]) {
         const unsigned blocks = std::min<unsigned>((h[4] + 7) / 8, sm_count() * 16);
@@ -798,15 +820,20 @@ void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t
 }
 
 void msd_sort_str(Workspace& ws, const uint8_t* chars, uint64_t n, uint32_t width, uint32_t w, uint32_t radix,
-                  const uint16_t* d_ord, const uint8_t* d_sym, uint8_t* out, int lin) {
+                  const uint16_t* d_ord, const uint8_t* d_sym, uint8_t* out, int lin,
+                  const unsigned long long* packed) {
   reset_stats(ws);
-  LoadStr ld{chars, width, d_ord};
-  ld.w8 = width == 8 && (reinterpret_cast<uintptr_t>(chars) & 7) == 0;
-  ld.lin = lin;
   EmitStr em{out, width, d_sym};
   em.lin = lin;
   em.w8 = width == 8 && (reinterpret_cast<uintptr_t>(out) & 7) == 0;
-  msd_sort(ws, ld, n, 5 * width, em);
+  if (packed) {  // keys packed by k_str_scan
+    msd_sort(ws, LoadKeys<unsigned long long>{packed, n}, n, 5 * width, em);
+  } else {
+    LoadStr ld{chars, width, d_ord};
+    ld.w8 = width == 8 && (reinterpret_cast<uintptr_t>(chars) & 7) == 0;
+    ld.lin = lin;
+    msd_sort(ws, ld, n, 5 * width, em);
+  }
   {
     PassTimer pt_(RS_PASS_REPORT, ws.stream);
     k_report_recs<<<1, 32, 0, ws.stream>>>(out, n, width, w, radix, d_ord, ws.stats);
@@ -1028,12 +1055,16 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
     RS_CUDA(cudaMemcpyAsync(tab, &t, sizeof(StrTable), cudaMemcpyHostToDevice, ws.stream));
     const auto* d_ord = reinterpret_cast<const uint16_t*>(tab);
     const auto* d_sym = tab + offsetof(StrTable, sym);
-    // width of the data = longest string (key_model.cpp:228-230), symbols checked
+    // width of the data = longest string (key_model.cpp:228-230), symbols checked;
+    // with msd the same pass packs the keys the MSD levels read
+    const bool want_msd = opt && opt->msd && width <= 12;
+    unsigned long long* packed = want_msd ? ws.get<unsigned long long>(kSlotMisc2, n) : nullptr;
     reset_stats(ws);
     {
       PassTimer pt_(RS_PASS_OTHER, ws.stream);
       const bool w8 = width == 8 && (reinterpret_cast<uintptr_t>(chars) & 15) == 0;
-      k_str_scan<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w8, d_ord, ws.stats);
+      k_str_scan<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w8, d_ord, ws.stats,
+                                                                              packed);
       RS_LAUNCH_CHECK();
     }
     pull_stats(ws);
@@ -1065,7 +1096,7 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
     for (size_t i = 1; i < alen; ++i)
       if (static_cast<unsigned char>(alpha[i]) != static_cast<unsigned char>(alpha[0]) + i) lin = -1;
     if (static_cast<unsigned char>(alpha[0]) == 0) lin = -1;
-    msd_sort_str(ws, chars, n, width, w, t.radix, d_ord, d_sym, out, lin);
+    msd_sort_str(ws, chars, n, width, w, t.radix, d_ord, d_sym, out, lin, packed);
     if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{t.radix, w, w}};
   });
 }

@@ -351,7 +351,8 @@ struct MsdLists {
   MsdSeg* leaf_copy;
   MsdSeg* leaf_warp;
   MsdSeg* leaf_radix;
-  unsigned* cnt;  // [6]: next, grid, small, copy, warp, radix
+  unsigned* cnt;   // [6]: next, grid, small, copy, warp, radix
+  unsigned* rmax;  // largest radix leaf
 };
 
 __global__ void k_msd_classify(const MsdSeg* __restrict__ segs, uint32_t nseg, const uint32_t* __restrict__ off,
@@ -378,6 +379,7 @@ __global__ void k_msd_classify(const MsdSeg* __restrict__ segs, uint32_t nseg, c
     L.leaf_small[atomicAdd(&L.cnt[2], 1u)] = sub;  // last digit: shared bitonic
   } else if (size <= kLeafRadixMax && rem_bits <= 3 * kMsdDigitBits) {
     L.leaf_radix[atomicAdd(&L.cnt[5], 1u)] = sub;  // mid-size: shared-memory LSD passes
+    atomicMax(L.rmax, size);
   } else {
     L.next[atomicAdd(&L.cnt[0], 1u)] = sub;  // split by the next 8-bit digit
   }
@@ -592,59 +594,52 @@ __global__ void __launch_bounds__(kMsdThreads) k_leaf_warp(const K* __restrict__
 // Mid-size leaves (<= kLeafRadixMax keys, <= 24 remaining bits): one CTA
 // loads the segment into shared memory and sorts it by the remaining bits
 // with stable 8-bit LSD passes, then writes it once.  Ranking: each warp owns
-// a contiguous range of the segment and takes it 32 keys at a time; the
-// lanes sharing a digit are found with 8 ballots, counted per (digit, warp),
-// and one exclusive scan over the [digit][warp] table gives every group its
-// place — the order inside a digit is (warp, group, lane), i.e. the input
-// order, so the passes are stable.
+// a contiguous range of the segment; keys are counted per (digit, warp) with
+// shared atomics, one exclusive scan over the table in (digit, warp) order
+// gives every warp its start per digit, and the warp then walks its range 32
+// keys at a time, the lanes sharing a digit found by __match_any_sync — the
+// order inside a digit is (warp, group, lane), i.e. the input order, so the
+// passes are stable.
 template <class K>
-__host__ __device__ constexpr size_t leaf_radix_smem() {
-  return 2 * (size_t)kLeafRadixMax * sizeof(K) + 256 * (kLeafRadixThreads / 32) * sizeof(uint32_t);
+__host__ __device__ constexpr size_t leaf_radix_smem(uint32_t cap) {  // two key buffers + two count tables
+  return 2 * (size_t)cap * sizeof(K) + 2 * 256 * (kLeafRadixThreads / 32) * sizeof(uint32_t);
 }
 
 template <class K, class Emit>
 __global__ void __launch_bounds__(kLeafRadixThreads) k_leaf_radix(const K* __restrict__ src,
                                                                   const MsdSeg* __restrict__ segs, uint32_t rem_bits,
-                                                                  Emit emit) {
+                                                                  uint32_t cap, Emit emit) {
   constexpr int kW = kLeafRadixThreads / 32;
   extern __shared__ __align__(16) unsigned char lr_smem[];
-  K* in = reinterpret_cast<K*>(lr_smem);
-  K* out = in + kLeafRadixMax;
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(out + kLeafRadixMax);  // [kW warps][256 digits] (digit -> bank)
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(lr_smem);  // [2][kW warps][256 digits] (digit -> bank)
+  K* in = reinterpret_cast<K*>(s_cnt + 2 * 256 * kW);
+  K* out = in + cap;
   __shared__ uint32_t s_part[kLeafRadixThreads / 32];
   const MsdSeg g = segs[blockIdx.x];
   const uint32_t n = g.size;
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) in[i] = src[g.start + i];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t per = (n + kW * 32 - 1) / (kW * 32) * 32;  // contiguous range per warp, in groups of 32
   const uint32_t w0 = warp * per, w1 = min(n, w0 + per);
   const unsigned lt = (1u << lane) - 1;
-  auto peers_of = [&](uint32_t d, bool v) {  // valid lanes with the same digit
-    unsigned m = __ballot_sync(0xffffffffu, v);
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const unsigned x = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-      m &= ((d >> b) & 1u) ? x : ~x;
-    }
-    return m;
-  };
-  for (uint32_t sh = 0; sh < rem_bits; sh += 8) {
-    for (uint32_t i = threadIdx.x; i < 256 * kW; i += blockDim.x) s_cnt[i] = 0;
-    __syncthreads();
-    for (uint32_t base = w0; base < w1; base += 32) {  // counts per (digit, warp)
-      const uint32_t i = base + lane;
-      const bool v = i < w1;
-      const uint32_t d = v ? static_cast<uint32_t>(in[i] >> sh) & 255u : 0u;
-      const unsigned pm = peers_of(d, v);
-      if (v && (pm & lt) == 0) s_cnt[warp * 256 + d] += __popc(pm);
-      __syncwarp();
-    }
-    __syncthreads();
-    {  // exclusive scan in (digit, warp) order: thread t takes digits t*kPer/kW ..
+  for (uint32_t i = threadIdx.x; i < 2 * 256 * kW; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  // load, counting the first digit per (warp range, digit)
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const K key = src[g.start + i];
+    in[i] = key;
+    atomicAdd(&s_cnt[(i / per) * 256 + (static_cast<uint32_t>(key) & 255u)], 1u);
+  }
+  __syncthreads();
+  int cur = 0;
+  for (uint32_t sh = 0; sh < rem_bits; sh += 8, cur ^= 1) {
+    uint32_t* cnt = s_cnt + cur * 256 * kW;
+    uint32_t* nxt = s_cnt + (cur ^ 1) * 256 * kW;
+    const bool more = sh + 8 < rem_bits;
+    {  // exclusive scan in (digit, warp) order: thread t takes entries t*kPer ..
       constexpr int kPer = 256 * kW / kLeafRadixThreads;
-      auto at = [&](int j) -> uint32_t& {  // j-th entry in (digit, warp) order
+      auto at = [&](int j) -> uint32_t& {
         const uint32_t e = threadIdx.x * kPer + j;
-        return s_cnt[(e % kW) * 256 + e / kW];
+        return cnt[(e % kW) * 256 + e / kW];
       };
       uint32_t v[kPer], sum = 0;
 #pragma unroll
@@ -669,19 +664,24 @@ __global__ void __launch_bounds__(kLeafRadixThreads) k_leaf_radix(const K* __res
       }
     }
     __syncthreads();
-    for (uint32_t base = w0; base < w1; base += 32) {  // stable scatter
+    for (uint32_t base = w0; base < w1; base += 32) {  // stable scatter; counts the next digit
       const uint32_t i = base + lane;
       const bool v = i < w1;
       const K key = v ? in[i] : K(0);
       const uint32_t d = static_cast<uint32_t>(key >> sh) & 255u;
-      const unsigned pm = peers_of(d, v);
-      const uint32_t pos = v ? s_cnt[warp * 256 + d] + __popc(pm & lt) : 0u;
+      const unsigned pm = __match_any_sync(0xffffffffu, v ? d : 256u + lane);  // same-digit lanes (MATCH)
+      const uint32_t pos = v ? cnt[warp * 256 + d] + __popc(pm & lt) : 0u;
       __syncwarp();
-      if (v && (pm & lt) == 0) s_cnt[warp * 256 + d] += __popc(pm);
+      if (v && (pm & lt) == 0) cnt[warp * 256 + d] += __popc(pm);
       __syncwarp();
-      if (v) out[pos] = key;
+      if (v) {
+        out[pos] = key;
+        if (more) atomicAdd(&nxt[(pos / per) * 256 + (static_cast<uint32_t>(key >> (sh + 8)) & 255u)], 1u);
+      }
     }
     __syncthreads();
+    // this table is next written two passes later (behind the next scan's barriers)
+    for (uint32_t i = threadIdx.x; i < 256 * kW; i += blockDim.x) cnt[i] = 0;
     K* t = in;
     in = out;
     out = t;

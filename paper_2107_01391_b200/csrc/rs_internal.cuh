@@ -110,7 +110,7 @@ enum : unsigned { kFlagNegative = 1u, kFlagNonFinite = 2u, kFlagDomain = 4u };
 struct Workspace {
   int device = -1;
   cudaStream_t stream = nullptr;
-  static constexpr int kSlots = 21;
+  static constexpr int kSlots = 22;
   void* buf[kSlots] = {};
   size_t cap[kSlots] = {};
   DevStats* stats = nullptr;   // device
@@ -165,6 +165,7 @@ enum Slot : int {
   kSlotAlphabet = 18,   // string ordinal / symbol tables
   kSlotExtra1 = 19,     // MSD radix-leaf list
   kSlotSpans = 20,      // long emit-tile spans of hot cells
+  kSlotMisc2 = 21,      // packed string keys (MSD)
 };
 
 }  // namespace rsb

@@ -1,7 +1,7 @@
 """One cfg2 key-only sort and one cfg2 key/value sort (2^28 keys), for ncu
 captures of individual kernels:
 
-    python tools/profile_one.py [--kv] [--f64]
+    python tools/profile_one.py [--kv] [--f64] [--cfg4] [--cfg5]
     ncu --set full -k regex:k_outer_scatter -c 1 -o prof python tools/profile_one.py
 """
 import ctypes
@@ -37,6 +37,13 @@ def main():
         rs._check(lib.rs_gen_f64_cfg3(o.config_seed(3), 0, n, rs._ptr(cdf), cdf.numel(), rs._ptr(x), rs._stream()))
         for _ in range(2):
             rs.sort_f64(x, 3, key_digits=6)
+    if "--cfg4" in sys.argv:
+        n4 = 1 << 26
+        r4 = torch.empty((n4, 8), dtype=torch.uint8, device="cuda")
+        rs._check(lib.rs_gen_str_cfg4(o.config_seed(4), 0, n4, rs._ptr(r4), rs._stream()))
+        for _ in range(2):
+            rs.sort_fixed_str(r4, msd=True)
+        del r4
     if "--cfg5" in sys.argv:
         del keys, out
         torch.cuda.empty_cache()
