@@ -599,7 +599,8 @@ __global__ void __launch_bounds__(kThreads) k_str_keys(const uint8_t* __restrict
 // 16-byte loads per thread per round.
 __global__ void __launch_bounds__(kThreads) k_str_scan(const uint8_t* __restrict__ recs, uint64_t n, uint32_t width,
                                                        bool w8, const uint16_t* __restrict__ ord_g, DevStats* st,
-                                                       unsigned long long* __restrict__ packed) {
+                                                       unsigned long long* __restrict__ packed, int lin,
+                                                       uint32_t alen) {
   __shared__ uint16_t ord[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) ord[i] = ord_g[i];
   __syncthreads();
@@ -614,7 +615,9 @@ __global__ void __launch_bounds__(kThreads) k_str_scan(const uint8_t* __restrict
     for (int j = 0; j < 8; ++j) {
       const uint32_t c = static_cast<uint32_t>(w >> (8 * j)) & 0xffu;
       ended |= c == 0;
-      const uint32_t o = ended ? 0u : ord[c];
+      // contiguous alphabet: ordinal = byte - lin when inside [lin+1, lin+alen], else 0 (bad)
+      const uint32_t lo = c - static_cast<uint32_t>(lin);
+      const uint32_t o = ended ? 0u : (lin >= 0 ? (lo - 1u < alen ? lo : 0u) : ord[c]);
       len += ended ? 0u : 1u;
       bad |= !ended && o == 0;
       k = (k << 5) | o;
@@ -1055,6 +1058,11 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
     RS_CUDA(cudaMemcpyAsync(tab, &t, sizeof(StrTable), cudaMemcpyHostToDevice, ws.stream));
     const auto* d_ord = reinterpret_cast<const uint16_t*>(tab);
     const auto* d_sym = tab + offsetof(StrTable, sym);
+    // contiguous alphabet (e.g. 'a'..'z'): ordinal <-> byte is arithmetic
+    int lin = static_cast<int>(static_cast<unsigned char>(alpha[0])) - 1;
+    for (size_t i = 1; i < alen; ++i)
+      if (static_cast<unsigned char>(alpha[i]) != static_cast<unsigned char>(alpha[0]) + i) lin = -1;
+    if (static_cast<unsigned char>(alpha[0]) == 0) lin = -1;
     // width of the data = longest string (key_model.cpp:228-230), symbols checked;
     // with msd the same pass packs the keys the MSD levels read
     const bool want_msd = opt && opt->msd && width <= 12;
@@ -1064,7 +1072,7 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
       PassTimer pt_(RS_PASS_OTHER, ws.stream);
       const bool w8 = width == 8 && (reinterpret_cast<uintptr_t>(chars) & 15) == 0;
       k_str_scan<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w8, d_ord, ws.stats,
-                                                                              packed);
+                                                                              packed, lin, static_cast<uint32_t>(alen));
       RS_LAUNCH_CHECK();
     }
     pull_stats(ws);
@@ -1091,11 +1099,6 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
     }
     if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
     if (t.radix > 32) fail(RS_INVALID_ARGUMENT, "the MSD string path packs 5-bit ordinals: at most 31 symbols");
-    // contiguous alphabet (e.g. 'a'..'z'): ordinal <-> byte is arithmetic
-    int lin = static_cast<int>(static_cast<unsigned char>(alpha[0])) - 1;
-    for (size_t i = 1; i < alen; ++i)
-      if (static_cast<unsigned char>(alpha[i]) != static_cast<unsigned char>(alpha[0]) + i) lin = -1;
-    if (static_cast<unsigned char>(alpha[0]) == 0) lin = -1;
     msd_sort_str(ws, chars, n, width, w, t.radix, d_ord, d_sym, out, lin, packed);
     if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{t.radix, w, w}};
   });
