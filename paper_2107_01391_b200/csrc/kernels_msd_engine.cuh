@@ -597,9 +597,9 @@ __global__ void __launch_bounds__(kMsdThreads) k_leaf_warp(const K* __restrict__
 // a contiguous range of the segment; keys are counted per (digit, warp) with
 // shared atomics, one exclusive scan over the table in (digit, warp) order
 // gives every warp its start per digit, and the warp then walks its range 32
-// keys at a time, the lanes sharing a digit found by __match_any_sync — the
-// order inside a digit is (warp, group, lane), i.e. the input order, so the
-// passes are stable.
+// keys at a time, the lanes sharing a digit found by 8 ballots (measured
+// faster than __match_any_sync on B200) — the order inside a digit is (warp,
+// group, lane), i.e. the input order, so the passes are stable.
 template <class K>
 __host__ __device__ constexpr size_t leaf_radix_smem(uint32_t cap) {  // two key buffers + two count tables
   return 2 * (size_t)cap * sizeof(K) + 2 * 256 * (kLeafRadixThreads / 32) * sizeof(uint32_t);
@@ -669,7 +669,12 @@ __global__ void __launch_bounds__(kLeafRadixThreads) k_leaf_radix(const K* __res
       const bool v = i < w1;
       const K key = v ? in[i] : K(0);
       const uint32_t d = static_cast<uint32_t>(key >> sh) & 255u;
-      const unsigned pm = __match_any_sync(0xffffffffu, v ? d : 256u + lane);  // same-digit lanes (MATCH)
+      unsigned pm = __ballot_sync(0xffffffffu, v);  // same-digit lanes: 8 ballots
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const unsigned x = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        pm &= ((d >> b) & 1u) ? x : ~x;
+      }
       const uint32_t pos = v ? cnt[warp * 256 + d] + __popc(pm & lt) : 0u;
       __syncwarp();
       if (v && (pm & lt) == 0) cnt[warp * 256 + d] += __popc(pm);
