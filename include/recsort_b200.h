@@ -165,6 +165,28 @@ rs_status rs_sort_keys(const uint64_t* keys, uint64_t n, rs_key_spec spec,
                        uint64_t* out, uint64_t out_capacity,
                        const rs_options* opt, rs_report* report, void* stream);
 
+/* ---- decimal text ------------------------------------ */
+/* sort_decimal_keys (sort.hpp:44-47, sort.cpp:7-14) over a device string
+ * column in Arrow layout: numeral i is chars[offsets[i] .. offsets[i+1]),
+ * offsets has n+1 entries.  Parsing follows parse_decimal
+ * (key_model.cpp:80-105) and normalize_dataset (key_model.cpp:107-133) on the
+ * GPU: the error is that of the first failing numeral (the one the
+ * reference's sequential loop stops at), with the reference's message.
+ * keys_out[n] receive the sorted mantissas at the dataset scale; report->spec
+ * is the dataset KeySpec {10, lambda + scale, lambda}. */
+rs_status rs_sort_decimal_strings(const char* chars, const uint64_t* offsets, uint64_t n,
+                                  uint64_t* keys_out, uint64_t out_capacity,
+                                  const rs_options* opt, rs_report* report, void* stream);
+
+/* format_scaled_decimal (key_model.cpp:170-180) / reconstruct_value for n
+ * keys at `scale` (<= 19), into a device string column: out_offsets[0..n]
+ * (n+1 entries) and out_chars.  *h_chars_needed (host) receives the total
+ * length; RS_BUFFER_TOO_SMALL when it exceeds out_chars_capacity (the
+ * offsets are written either way). */
+rs_status rs_format_decimals(const uint64_t* keys, uint64_t n, uint32_t scale, char* out_chars,
+                             uint64_t out_chars_capacity, uint64_t* out_offsets,
+                             uint64_t* h_chars_needed, void* stream);
+
 /* ---- host-buffer entry points (H2D / sort / D2H inside one call) -------- */
 /* Same semantics as rs_sort_u32 / rs_sort_u32_kv on HOST buffers; the copies
  * are chunked and overlapped with the counting and emit passes. */

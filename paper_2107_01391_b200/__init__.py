@@ -253,33 +253,71 @@ def _digit_count(v: int) -> int:
     return len(str(v)) if v > 0 else 1
 
 
-def sort_decimal_keys(values, max_cells: int = DEFAULT_CELL_BUDGET):
-    """normalize + hash + extract without rendering (sort.cpp:7-14).  The
-    text ingest (normalize_dataset, key_model.cpp:107-133) runs on the host;
-    the count/scan/emit passes run on the GPU through rs_sort_keys."""
+def _string_column(values):
+    """Arrow-style column: concatenated UTF-8 bytes and n+1 uint64 offsets."""
+    import numpy as np
+
+    enc = [v.encode() for v in values]
+    lens = np.fromiter((len(e) for e in enc), dtype=np.uint64, count=len(enc))
+    offsets = np.zeros(len(enc) + 1, dtype=np.uint64)
+    np.cumsum(lens, out=offsets[1:])
+    chars = np.frombuffer(b"".join(enc), dtype=np.uint8)
+    return chars, offsets
+
+
+def sort_decimal_column(chars, offsets, *, max_cells: int = DEFAULT_CELL_BUDGET):
+    """sort_decimal_keys over a CUDA string column (uint8 chars, int64/uint64
+    offsets of n+1 entries): parse + normalize + count + extract on the GPU.
+    Returns (uint64 keys at the dataset scale as an int64 tensor, report)."""
     torch = _torch()
-    parsed = [_parse_decimal(v) for v in values]
-    scale = max((s for _, s in parsed), default=0)
-    max_int = max((m // 10 ** s for m, s in parsed), default=0)
-    lam = _digit_count(max_int)
-    total = lam + scale if parsed else 1
-    lam = lam if parsed else 1
-    cells = 10 ** total
-    if cells > max_cells:
-        raise Error("cell_budget_exceeded", f"key space needs {cells} cells, budget is {max_cells}")
-    spec = KeySpec(10, total, lam)
-    if not parsed:
-        return [], ExtractionReport(0, 0, spec)
-    keys = torch.tensor([m * 10 ** (scale - s) for m, s in parsed], dtype=torch.int64).to(_device())
-    out, rep = sort_keys(keys, spec, max_cells=max_cells)
-    return out.cpu().tolist(), rep
+    chars = _cuda_tensor(chars, (torch.uint8,), "chars")
+    offsets = _cuda_tensor(offsets, (torch.int64,), "offsets")
+    n = offsets.numel() - 1
+    out = torch.empty(max(n, 1), dtype=torch.int64, device=offsets.device)
+    rep = RsReport()
+    _check(_lib.load().rs_sort_decimal_strings(_ptr(chars), _ptr(offsets), n, _ptr(out), n,
+                                               ctypes.byref(_opts(max_cells)), ctypes.byref(rep), _stream()))
+    return out[:n], _report(rep)
+
+
+def format_decimal_column(keys, scale: int):
+    """format_scaled_decimal on the GPU: (uint8 chars, int64 offsets[n+1])."""
+    torch = _torch()
+    keys = _cuda_tensor(keys, (torch.int64,), "keys")
+    n = keys.numel()
+    offsets = torch.empty(n + 1, dtype=torch.int64, device=keys.device)
+    need = ctypes.c_uint64()
+    lib = _lib.load()
+    st = lib.rs_format_decimals(_ptr(keys), n, scale, None, 0, _ptr(offsets), ctypes.byref(need), _stream())
+    if st not in (0, _lib.RS_BUFFER_TOO_SMALL):
+        _check(st)
+    chars = torch.empty(max(need.value, 1), dtype=torch.uint8, device=keys.device)
+    _check(lib.rs_format_decimals(_ptr(keys), n, scale, _ptr(chars), chars.numel(), _ptr(offsets),
+                                  ctypes.byref(need), _stream()))
+    return chars[: need.value], offsets
+
+
+def sort_decimal_keys(values, max_cells: int = DEFAULT_CELL_BUDGET):
+    """normalize + hash + extract without rendering (sort.cpp:7-14); the
+    numerals are parsed on the GPU (rs_sort_decimal_strings)."""
+    torch = _torch()
+    chars, offsets = _string_column(values)
+    keys, rep = sort_decimal_column(torch.from_numpy(chars.copy()).to(_device()),
+                                    torch.from_numpy(offsets.view("int64")).to(_device()), max_cells=max_cells)
+    return [int(k) for k in keys.cpu().numpy().view("uint64")], rep
 
 
 def sort_decimals(values, max_cells: int = DEFAULT_CELL_BUDGET):
     """Sort decimal numerals; returns (sorted padded values, report)
-    (bindings.cpp:48-55 -> sort.cpp:16-27)."""
-    keys, rep = sort_decimal_keys(values, max_cells)
-    return [_format_scaled(k, rep.spec.scale) for k in keys], rep
+    (bindings.cpp:48-55 -> sort.cpp:16-27): parse, sort and render on the GPU."""
+    torch = _torch()
+    chars, offsets = _string_column(values)
+    keys, rep = sort_decimal_column(torch.from_numpy(chars.copy()).to(_device()),
+                                    torch.from_numpy(offsets.view("int64")).to(_device()), max_cells=max_cells)
+    out_chars, out_off = format_decimal_column(keys, rep.spec.scale)
+    text = bytes(out_chars.cpu().numpy())
+    off = out_off.cpu().numpy()
+    return [text[off[i]:off[i + 1]].decode() for i in range(len(off) - 1)], rep
 
 
 def sort_strings(values, alphabet: str = DEFAULT_ALPHABET, max_cells: int = DEFAULT_CELL_BUDGET):
@@ -307,7 +345,8 @@ def sort_strings(values, alphabet: str = DEFAULT_ALPHABET, max_cells: int = DEFA
 
 __all__ = [
     "DEFAULT_CELL_BUDGET", "Error", "ExtractionReport", "KeySpec", "__version__",
-    "sort_integers", "sort_decimals", "sort_decimal_keys", "sort_strings",
+    "sort_integers", "sort_decimals", "sort_decimal_keys", "sort_strings", "sort_decimal_column",
+    "format_decimal_column",
     "sort_u32", "sort_u32_kv", "sort_i64", "sort_f64", "sort_fixed_str", "sort_keys",
     "recombinant_sort",
 ]

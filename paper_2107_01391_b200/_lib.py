@@ -33,6 +33,7 @@ STATUS_NAMES = {
     102: "no_device",
 }
 RS_OK = 0
+RS_BUFFER_TOO_SMALL = 7
 DEFAULT_CELL_BUDGET = 100_000_000  # key_model.hpp:16
 RS_NUM_PASSES = 13
 
@@ -66,6 +67,8 @@ SIGNATURES = {
     "rs_sort_f64": (c_int, [c_void_p, c_uint64, c_uint32, c_void_p, c_uint64, POINTER(RsOptions), POINTER(RsReport), c_void_p]),
     "rs_sort_fixed_str": (c_int, [c_void_p, c_uint64, c_uint32, c_char_p, c_void_p, c_uint64, POINTER(RsOptions), POINTER(RsReport), c_void_p]),
     "rs_sort_keys": (c_int, [c_void_p, c_uint64, RsKeySpec, c_void_p, c_uint64, POINTER(RsOptions), POINTER(RsReport), c_void_p]),
+    "rs_sort_decimal_strings": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_uint64, POINTER(RsOptions), POINTER(RsReport), c_void_p]),
+    "rs_format_decimals": (c_int, [c_void_p, c_uint64, c_uint32, c_void_p, c_uint64, c_void_p, POINTER(c_uint64), c_void_p]),
     "rs_sort_u32_host": (c_int, [c_void_p, c_uint64, c_void_p, POINTER(RsOptions), POINTER(RsReport), c_void_p]),
     "rs_sort_u32_kv_host": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p, POINTER(RsOptions), POINTER(RsReport), c_void_p]),
     "rs_count_u32": (c_int, [c_void_p, c_uint64, c_void_p, c_uint64, POINTER(c_uint32), c_void_p]),

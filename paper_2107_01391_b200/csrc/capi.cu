@@ -20,6 +20,7 @@
 #include "kernels_two_level.cuh"
 #include "kernels_msd.cuh"
 #include "kernels_msd_engine.cuh"
+#include "kernels_decimal.cuh"
 #include "recsort_b200.h"
 #include "rs_internal.cuh"
 
@@ -849,6 +850,34 @@ void msd_sort_str(Workspace& ws, const uint8_t* chars, uint64_t n, uint32_t widt
 
 using namespace rsb;
 
+// ------------------------------------------------------- decimal text
+// Exclusive scan of n uint64 values into out[0..n] (out[n] = total).
+void exscan_u64(Workspace& ws, const unsigned long long* in, uint64_t n, unsigned long long* out) {
+  const uint32_t tiles = static_cast<uint32_t>((n + kScanTile - 1) / kScanTile);
+  auto* desc = ws.get<unsigned long long>(kSlotDesc2, tiles + 1ull);
+  RS_CUDA(cudaMemsetAsync(desc, 0, (tiles + 1ull) * sizeof(unsigned long long), ws.stream));
+  auto* ticket = reinterpret_cast<unsigned*>(desc + tiles);
+  k_exscan_u64<<<tiles, kThreads, 0, ws.stream>>>(in, n, out, desc, ticket, tiles);
+  RS_LAUNCH_CHECK();
+}
+
+// The reference's message for a numeral's first failing check
+// (key_model.cpp:22-34, 38-49, 80-105).
+[[noreturn]] void fail_numeral(uint32_t code, const std::string& text, uint32_t frac_digits) {
+  switch (code) {
+    case kDecEmpty: fail(RS_PARSE_ERROR, "empty numeral");
+    case kDecNegative: fail(RS_NEGATIVE_VALUE, "negative values are not supported: '" + text + "'");
+    case kDecMultiDot: fail(RS_PARSE_ERROR, "multiple decimal points in '" + text + "'");
+    case kDecNoFrac: fail(RS_PARSE_ERROR, "no digits after decimal point in '" + text + "'");
+    case kDecNoDigits: fail(RS_PARSE_ERROR, "no digits in '" + text + "'");
+    case kDecBadChar: fail(RS_PARSE_ERROR, "invalid character in numeral '" + text + "'");
+    case kDecTooLong:
+      fail(RS_CELL_BUDGET_EXCEEDED, "numeral '" + text + "' has more digits than any cell budget admits");
+    default:
+      fail(RS_CELL_BUDGET_EXCEEDED, "key space 10^" + std::to_string(frac_digits) + " overflows 64 bits");
+  }
+}
+
 // =================================================================== C-ABI
 extern "C" {
 
@@ -1270,6 +1299,94 @@ rs_status rs_emit_u32(const uint32_t* counts, uint64_t cells, uint64_t cell_lo, 
       }
     }
     if (h_written) *h_written = written;
+  });
+}
+
+
+rs_status rs_sort_decimal_strings(const char* chars, const uint64_t* offsets, uint64_t n, uint64_t* keys_out,
+                                  uint64_t out_capacity, const rs_options* opt, rs_report* report, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    const uint64_t budget = budget_of(opt);
+    if (n == 0) {
+      if (report) *report = rs_report{0, 0, make_key_spec(10, 1, 1, budget)};
+      return;
+    }
+    if (!offsets || !keys_out || !chars) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    auto* mant = ws.get<unsigned long long>(kSlotMapped, n);
+    auto* own = ws.get<uint8_t>(kSlotTmpKeys, n);
+    auto* ds = reinterpret_cast<DecStats*>(ws.get<uint8_t>(kSlotAlphabet, sizeof(StrTable)));
+    const auto* off = reinterpret_cast<const unsigned long long*>(offsets);
+    RS_CUDA(cudaMemsetAsync(ds, 0, sizeof(DecStats), ws.stream));
+    RS_CUDA(cudaMemsetAsync(&ds->first_error, 0xff, sizeof(unsigned long long), ws.stream));
+    {
+      PassTimer pt_(RS_PASS_OTHER, ws.stream);
+      k_dec_parse<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, off, n, mant, own, ds);
+      RS_LAUNCH_CHECK();
+    }
+    DecStats h{};
+    RS_CUDA(cudaMemcpyAsync(&h, ds, sizeof(h), cudaMemcpyDeviceToHost, ws.stream));
+    RS_CUDA(cudaStreamSynchronize(ws.stream));
+    if (h.first_error != ~0ull) {  // the numeral the reference's loop stops at
+      const uint64_t i = h.first_error >> 8;
+      unsigned long long be[2];
+      RS_CUDA(cudaMemcpy(be, off + i, sizeof(be), cudaMemcpyDeviceToHost));
+      std::string text(be[1] - be[0], '\0');
+      if (!text.empty()) RS_CUDA(cudaMemcpy(text.data(), chars + be[0], text.size(), cudaMemcpyDeviceToHost));
+      const size_t dot = text.find('.');
+      fail_numeral(static_cast<uint32_t>(h.first_error & 0xff), text,
+                   dot == std::string::npos ? 0u : static_cast<uint32_t>(text.size() - dot - 1));
+    }
+    // normalize_dataset (key_model.cpp:107-133): lambda from the largest
+    // integer part, the dataset scale from the longest fraction
+    const uint32_t scale = h.max_scale;
+    const uint32_t lambda = digit_count(h.max_integer);
+    const rs_key_spec spec = make_key_spec(10, lambda + scale, lambda, budget);
+    if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
+    {
+      PassTimer pt_(RS_PASS_OTHER, ws.stream);
+      k_dec_scale<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(mant, own, n, scale);
+      RS_LAUNCH_CHECK();
+    }
+    OutU64 o{reinterpret_cast<unsigned long long*>(keys_out), 0ull, aligned16(keys_out)};
+    grid_sort(ws, mant, n, MapU64{}, checked_pow(10, lambda + scale), o, keys_out, 10, lambda + scale, 0);
+    if (report) *report = rs_report{n, ws.h_stats->cells_traversed, spec};
+  });
+}
+
+rs_status rs_format_decimals(const uint64_t* keys, uint64_t n, uint32_t scale, char* out_chars,
+                             uint64_t out_chars_capacity, uint64_t* out_offsets, uint64_t* h_chars_needed,
+                             void* stream) {
+  return guarded([&] {
+    ensure_device();
+    if (scale > 19) fail(RS_INVALID_ARGUMENT, "scale must be at most 19");
+    if (!out_offsets || (n && !keys)) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    auto* off = reinterpret_cast<unsigned long long*>(out_offsets);
+    unsigned long long total = 0;
+    if (n == 0) {
+      RS_CUDA(cudaMemsetAsync(off, 0, sizeof(unsigned long long), ws.stream));
+    } else {
+      auto* len = ws.get<unsigned long long>(kSlotMapped, n);
+      const auto* k = reinterpret_cast<const unsigned long long*>(keys);
+      PassTimer pt_(RS_PASS_OTHER, ws.stream, 2);
+      k_dec_len<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(k, n, scale, len);
+      RS_LAUNCH_CHECK();
+      exscan_u64(ws, len, n, off);
+      RS_CUDA(cudaMemcpyAsync(&total, off + n, sizeof(total), cudaMemcpyDeviceToHost, ws.stream));
+    }
+    RS_CUDA(cudaStreamSynchronize(ws.stream));
+    if (h_chars_needed) *h_chars_needed = total;
+    if (total > out_chars_capacity) fail(RS_BUFFER_TOO_SMALL, "output character buffer too small");
+    if (n) {
+      if (!out_chars) fail(RS_INVALID_ARGUMENT, "null device pointer");
+      PassTimer pt_(RS_PASS_OTHER, ws.stream);
+      k_dec_format<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(
+          reinterpret_cast<const unsigned long long*>(keys), n, scale, off, out_chars);
+      RS_LAUNCH_CHECK();
+      RS_CUDA(cudaStreamSynchronize(ws.stream));
+    }
   });
 }
 

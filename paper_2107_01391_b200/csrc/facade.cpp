@@ -52,40 +52,6 @@ rs_options opts(const SortOptions& o) { return rs_options{o.max_cells, o.key_dig
 ExtractionReport rep(const rs_report& r) { return ExtractionReport{r.written, r.cells_traversed}; }
 KeySpec spec(const rs_report& r) { return KeySpec{r.spec.radix, r.spec.total_digits, r.spec.integer_digits}; }
 
-// parse_decimal grammar (key_model.cpp:80-105).
-void parse_decimal(const std::string& text, std::uint64_t& mantissa, std::uint32_t& scale) {
-  if (text.empty()) throw Error(errc::parse_error, "empty numeral");
-  if (text.front() == '-') throw Error(errc::negative_value, "negative values are not supported: '" + text + "'");
-  const std::size_t dot = text.find('.');
-  const std::string ip = text.substr(0, dot);
-  const std::string fp = dot == std::string::npos ? std::string{} : text.substr(dot + 1);
-  if (dot != std::string::npos && fp.find('.') != std::string::npos)
-    throw Error(errc::parse_error, "multiple decimal points in '" + text + "'");
-  if (dot != std::string::npos && fp.empty())
-    throw Error(errc::parse_error, "no digits after decimal point in '" + text + "'");
-  if (ip.empty() && fp.empty()) throw Error(errc::parse_error, "no digits in '" + text + "'");
-  std::uint64_t acc = 0;
-  for (const std::string* part : {&ip, &fp})
-    for (char c : *part) {
-      if (c < '0' || c > '9') throw Error(errc::parse_error, "invalid character in numeral '" + text + "'");
-      const std::uint64_t d = static_cast<std::uint64_t>(c - '0');
-      if (acc > (~std::uint64_t{0} - d) / 10)
-        throw Error(errc::cell_budget_exceeded, "numeral '" + text + "' has more digits than any cell budget admits");
-      acc = acc * 10 + d;
-    }
-  mantissa = acc;
-  scale = static_cast<std::uint32_t>(fp.size());
-}
-
-std::uint64_t pow10(std::uint32_t e) {
-  std::uint64_t r = 1;
-  for (std::uint32_t i = 0; i < e; ++i) {
-    if (r > ~std::uint64_t{0} / 10) throw Error(errc::cell_budget_exceeded, "key space overflows 64 bits");
-    r *= 10;
-  }
-  return r;
-}
-
 std::uint32_t digits(std::uint64_t v) {
   std::uint32_t d = 1;
   while (v >= 10) {
@@ -130,50 +96,62 @@ IntegerSortResult sort_integers(std::span<const std::int64_t> values, std::uint6
   return res;
 }
 
-DecimalKeySortResult sort_decimal_keys(std::span<const std::string> values, std::uint64_t max_cells) {
-  // normalize_dataset (key_model.cpp:107-133) on the host, the count grid on the device
-  std::vector<std::uint64_t> mant(values.size());
-  std::vector<std::uint32_t> scales(values.size());
-  std::uint32_t scale = 0;
-  std::uint64_t max_int = 0;
+namespace {
+// The numerals as a device string column (Arrow layout: bytes + n+1 offsets).
+struct DecColumn {
+  DevBuf<char> chars;
+  DevBuf<std::uint64_t> offsets;
+};
+DecColumn upload_column(std::span<const std::string> values) {
+  std::vector<std::uint64_t> off(values.size() + 1, 0);
+  std::string flat;
   for (std::size_t i = 0; i < values.size(); ++i) {
-    parse_decimal(values[i], mant[i], scales[i]);
-    scale = std::max(scale, scales[i]);
-    max_int = std::max(max_int, mant[i] / pow10(scales[i]));
+    flat += values[i];
+    off[i + 1] = flat.size();
   }
-  const std::uint32_t lambda = values.empty() ? 1 : digits(max_int);
-  const std::uint32_t total = values.empty() ? 1 : lambda + scale;
-  rs_key_spec ks{10, total, lambda};
-  for (std::size_t i = 0; i < values.size(); ++i) mant[i] *= pow10(scale - scales[i]);
-  const std::size_t n = mant.size();
-  DevBuf<std::uint64_t> in = upload(mant.data(), n), out(n);
+  return DecColumn{upload(flat.data(), std::max<std::size_t>(flat.size(), 1)), upload(off.data(), off.size())};
+}
+}  // namespace
+
+DecimalKeySortResult sort_decimal_keys(std::span<const std::string> values, std::uint64_t max_cells) {
+  // parse_decimal + normalize_dataset + count + extract, all on the device
+  const std::size_t n = values.size();
+  DecColumn col = upload_column(values);
+  DevBuf<std::uint64_t> out(std::max<std::size_t>(n, 1));
   rs_options o{max_cells, 0, 0};
   rs_report r{};
-  throw_status(rs_sort_keys(in.p, n, ks, out.p, n, &o, &r, nullptr));
+  throw_status(rs_sort_decimal_strings(col.chars.p, col.offsets.p, n, out.p, n, &o, &r, nullptr));
   DecimalKeySortResult res;
   res.keys.resize(n);
   if (n) cuda_ok(cudaMemcpy(res.keys.data(), out.p, n * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
-  res.spec = KeySpec{10, total, lambda};
+  res.spec = spec(r);
   res.report = rep(r);
   return res;
 }
 
 DecimalSortResult sort_decimals(std::span<const std::string> values, std::uint64_t max_cells) {
-  DecimalKeySortResult k = sort_decimal_keys(values, max_cells);
+  // as sort_decimal_keys, then format_scaled_decimal on the device
+  const std::size_t n = values.size();
+  DecColumn col = upload_column(values);
+  DevBuf<std::uint64_t> keys(std::max<std::size_t>(n, 1));
+  rs_options o{max_cells, 0, 0};
+  rs_report r{};
+  throw_status(rs_sort_decimal_strings(col.chars.p, col.offsets.p, n, keys.p, n, &o, &r, nullptr));
   DecimalSortResult res;
-  res.spec = k.spec;
-  res.report = k.report;
-  const std::uint64_t p = pow10(k.spec.scale());
-  for (std::uint64_t key : k.keys) {  // format_scaled_decimal (key_model.cpp:170-180)
-    std::string s = std::to_string(key / p);
-    if (k.spec.scale()) {
-      const std::string frac = std::to_string(key % p);
-      s += '.';
-      s.append(k.spec.scale() - frac.size(), '0');
-      s += frac;
-    }
-    res.values.push_back(std::move(s));
-  }
+  res.spec = spec(r);
+  res.report = rep(r);
+  DevBuf<std::uint64_t> off(n + 1);
+  std::uint64_t need = 0;
+  const rs_status st = rs_format_decimals(keys.p, n, res.spec.scale(), nullptr, 0, off.p, &need, nullptr);
+  if (st != RS_OK && st != RS_BUFFER_TOO_SMALL) throw_status(st);
+  DevBuf<char> chars(std::max<std::uint64_t>(need, 1));
+  throw_status(rs_format_decimals(keys.p, n, res.spec.scale(), chars.p, need, off.p, &need, nullptr));
+  std::string flat(need, '\0');
+  std::vector<std::uint64_t> h_off(n + 1);
+  if (need) cuda_ok(cudaMemcpy(flat.data(), chars.p, need, cudaMemcpyDeviceToHost));
+  cuda_ok(cudaMemcpy(h_off.data(), off.p, (n + 1) * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+  res.values.reserve(n);
+  for (std::size_t i = 0; i < n; ++i) res.values.emplace_back(flat.substr(h_off[i], h_off[i + 1] - h_off[i]));
   return res;
 }
 
