@@ -851,16 +851,6 @@ void msd_sort_str(Workspace& ws, const uint8_t* chars, uint64_t n, uint32_t widt
 using namespace rsb;
 
 // ------------------------------------------------------- decimal text
-// Exclusive scan of n uint64 values into out[0..n] (out[n] = total).
-void exscan_u64(Workspace& ws, const unsigned long long* in, uint64_t n, unsigned long long* out) {
-  const uint32_t tiles = static_cast<uint32_t>((n + kScanTile - 1) / kScanTile);
-  auto* desc = ws.get<unsigned long long>(kSlotDesc2, tiles + 1ull);
-  RS_CUDA(cudaMemsetAsync(desc, 0, (tiles + 1ull) * sizeof(unsigned long long), ws.stream));
-  auto* ticket = reinterpret_cast<unsigned*>(desc + tiles);
-  k_exscan_u64<<<tiles, kThreads, 0, ws.stream>>>(in, n, out, desc, ticket, tiles);
-  RS_LAUNCH_CHECK();
-}
-
 // The reference's message for a numeral's first failing check
 // (key_model.cpp:22-34, 38-49, 80-105).
 [[noreturn]] void fail_numeral(uint32_t code, const std::string& text, uint32_t frac_digits) {
@@ -1368,12 +1358,14 @@ rs_status rs_format_decimals(const uint64_t* keys, uint64_t n, uint32_t scale, c
     if (n == 0) {
       RS_CUDA(cudaMemsetAsync(off, 0, sizeof(unsigned long long), ws.stream));
     } else {
-      auto* len = ws.get<unsigned long long>(kSlotMapped, n);
       const auto* k = reinterpret_cast<const unsigned long long*>(keys);
-      PassTimer pt_(RS_PASS_OTHER, ws.stream, 2);
-      k_dec_len<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(k, n, scale, len);
+      const uint32_t tiles = static_cast<uint32_t>((n + kScanTile - 1) / kScanTile);
+      auto* desc = ws.get<unsigned long long>(kSlotDesc2, tiles + 1ull);
+      RS_CUDA(cudaMemsetAsync(desc, 0, (tiles + 1ull) * sizeof(unsigned long long), ws.stream));
+      PassTimer pt_(RS_PASS_OTHER, ws.stream);
+      k_dec_offsets<<<tiles, kThreads, 0, ws.stream>>>(k, n, scale, off, desc, reinterpret_cast<unsigned*>(desc + tiles),
+                                                       tiles);
       RS_LAUNCH_CHECK();
-      exscan_u64(ws, len, n, off);
       RS_CUDA(cudaMemcpyAsync(&total, off + n, sizeof(total), cudaMemcpyDeviceToHost, ws.stream));
     }
     RS_CUDA(cudaStreamSynchronize(ws.stream));

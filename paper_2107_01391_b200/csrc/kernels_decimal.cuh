@@ -11,7 +11,7 @@
 //                 failing numeral (lowest index, i.e. the one the reference's
 //                 sequential loop stops at) by an atomicMin of (index, code)
 //   k_dec_scale   key = mantissa * 10^(dataset scale - own scale)
-//   k_dec_len     rendered length per key; exclusive scan -> offsets
+//   k_dec_offsets rendered length per key, scanned into the output offsets
 //   k_dec_format  digits written right to left into the output column
 #pragma once
 
@@ -55,64 +55,82 @@ __global__ void __launch_bounds__(kThreads) k_dec_parse(const char* __restrict__
                                                         unsigned long long* __restrict__ mant,
                                                         uint8_t* __restrict__ scale_out, DecStats* ds) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const auto* bytes = reinterpret_cast<const unsigned char*>(chars);
   unsigned long long mx_int = 0;
   uint32_t mx_scale = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const unsigned long long b = offsets[i], e = offsets[i + 1];
-    const uint64_t len = e - b;
-    const char* s = chars + b;
-    uint32_t code = kDecOk;
-    unsigned long long m = 0;
-    uint32_t frac = 0;
+    const unsigned long long b = offsets[i];
+    const uint32_t len = static_cast<uint32_t>(offsets[i + 1] - b);
+    const unsigned char* s = bytes + b;
+    // one sweep: digits counted and accumulated (wrapping), the first dot
+    // (integer part = the value before it), a second dot, other bytes
+    uint32_t dot = 0xffffffffu, ndig = 0;
+    bool second_dot = false, bad = false;
+    unsigned long long m = 0, ip = 0;
+    for (uint32_t j = 0; j < len; ++j) {
+      const uint32_t c = __ldg(s + j);
+      const uint32_t d = c - '0';
+      if (d < 10) {
+        m = m * 10 + d;
+        ++ndig;
+      } else if (c == '.') {
+        second_dot |= dot != 0xffffffffu;
+        if (dot == 0xffffffffu) {
+          dot = j;
+          ip = m;
+        }
+      } else {
+        bad = true;
+      }
+    }
+    if (dot == 0xffffffffu) ip = m;
+    // < 20 digits never overflow 64 bits; otherwise accumulate_digits' exact
+    // rule (key_model.cpp:22-34), digit by digit
+    bool overflow = false;
+    if (ndig >= 20 && !bad) {
+      unsigned long long acc = 0, acc_ip = 0;
+      for (uint32_t j = 0; j < len && !overflow; ++j) {
+        const uint32_t d = __ldg(s + j) - '0';
+        if (d >= 10) continue;
+        if (acc > (~0ull - d) / 10) overflow = true;
+        else acc = acc * 10 + d;
+        if (dot == 0xffffffffu || j < dot) acc_ip = acc;
+      }
+      m = acc;
+      ip = acc_ip;
+    }
+    uint32_t code = kDecOk, frac = 0;
     if (len == 0) {
       code = kDecEmpty;
     } else if (s[0] == '-') {
       code = kDecNegative;
     } else {
-      // one sweep: the dot position, a second dot, non-digits, the mantissa
-      int64_t dot = -1;
-      bool second_dot = false, bad = false, overflow = false;
-      for (uint64_t j = 0; j < len; ++j) {
-        const unsigned c = static_cast<unsigned char>(s[j]);
-        if (c == '.') {
-          if (dot >= 0) second_dot = true;
-          else dot = static_cast<int64_t>(j);
-          continue;
-        }
-        if (c < '0' || c > '9') {
-          bad = true;
-          continue;
-        }
-        const unsigned long long d = c - '0';
-        if (m > (~0ull - d) / 10) overflow = true;  // accumulate_digits (key_model.cpp:22-34)
-        else if (!overflow) m = m * 10 + d;
-      }
-      const uint64_t ilen = dot >= 0 ? static_cast<uint64_t>(dot) : len;
-      const uint64_t flen = dot >= 0 ? len - ilen - 1 : 0;
+      const uint32_t ilen = dot != 0xffffffffu ? dot : len;
+      const uint32_t flen = dot != 0xffffffffu ? len - ilen - 1 : 0;
       if (second_dot) code = kDecMultiDot;
-      else if (dot >= 0 && flen == 0) code = kDecNoFrac;
+      else if (dot != 0xffffffffu && flen == 0) code = kDecNoFrac;
       else if (ilen == 0 && flen == 0) code = kDecNoDigits;
       else if (bad) code = kDecBadChar;
       else if (overflow) code = kDecTooLong;
       else if (flen > 19) code = kDecScaleOverflow;
-      frac = static_cast<uint32_t>(flen);
+      frac = flen;
     }
     if (code != kDecOk) {
       atomicMin(&ds->first_error, (static_cast<unsigned long long>(i) << 8) | code);
       m = 0;
+      ip = 0;
       frac = 0;
     }
     mant[i] = m;
     scale_out[i] = static_cast<uint8_t>(frac);
-    const unsigned long long ip = m / c_pow10[frac];
     mx_int = ip > mx_int ? ip : mx_int;
     mx_scale = frac > mx_scale ? frac : mx_scale;
   }
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long a = __shfl_xor_sync(0xffffffffu, mx_int, o);
-    const uint32_t b = __shfl_xor_sync(0xffffffffu, mx_scale, o);
+    const uint32_t bb = __shfl_xor_sync(0xffffffffu, mx_scale, o);
     mx_int = a > mx_int ? a : mx_int;
-    mx_scale = b > mx_scale ? b : mx_scale;
+    mx_scale = bb > mx_scale ? bb : mx_scale;
   }
   if ((threadIdx.x & 31) == 0) {
     if (mx_int) atomicMax(&ds->max_integer, mx_int);
@@ -134,15 +152,9 @@ __device__ __forceinline__ uint32_t dec_digits(unsigned long long v) {
   return d;
 }
 
-// rendered length of format_scaled_decimal(key, scale)
-__global__ void __launch_bounds__(kThreads) k_dec_len(const unsigned long long* __restrict__ keys, uint64_t n,
-                                                      uint32_t scale, unsigned long long* __restrict__ len) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    len[i] = dec_digits(keys[i] / c_pow10[scale]) + (scale ? 1 + scale : 0);
-}
-
-// to_string(mantissa / p) [ '.' zero-padded(mantissa % p, scale) ]
+// to_string(mantissa / p) [ '.' zero-padded(mantissa % p, scale) ]: digits
+// written right to left from the end of the numeral's slot, the point
+// before the (scale+1)-th digit; 32-bit arithmetic once the value fits.
 __global__ void __launch_bounds__(kThreads) k_dec_format(const unsigned long long* __restrict__ keys, uint64_t n,
                                                          uint32_t scale,
                                                          const unsigned long long* __restrict__ offsets,
@@ -151,34 +163,58 @@ __global__ void __launch_bounds__(kThreads) k_dec_format(const unsigned long lon
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     unsigned long long v = keys[i];
     char* end = out + offsets[i + 1];
-    for (uint32_t j = 0; j < scale; ++j) {  // fractional digits, right to left
-      *--end = static_cast<char>('0' + v % 10);
+    uint32_t j = 0;  // digits written
+    auto emit = [&](uint32_t dg) {
+      if (scale != 0 && j == scale) *--end = '.';
+      *--end = static_cast<char>('0' + dg);
+      ++j;
+    };
+    while (v >> 32) {
+      emit(static_cast<uint32_t>(v % 10));
       v /= 10;
     }
-    if (scale) *--end = '.';
-    do {
-      *--end = static_cast<char>('0' + v % 10);
-      v /= 10;
-    } while (v);
+    uint32_t x = static_cast<uint32_t>(v);
+    do {  // at least scale + 1 digits: a leading 0 before the point
+      emit(x % 10);
+      x /= 10;
+    } while (x != 0 || j <= scale);
   }
 }
 
-// Exclusive scan of n uint64 values (look-back), out[n] = total.
-__global__ void __launch_bounds__(kThreads) k_exscan_u64(const unsigned long long* __restrict__ in, uint64_t count,
-                                                         unsigned long long* __restrict__ out,
-                                                         unsigned long long* desc, unsigned* tile_counter,
-                                                         uint32_t num_tiles) {
+// Offsets of the rendered column: exclusive scan of the rendered lengths of
+// format_scaled_decimal(key, scale) — the integer part key / 10^scale has
+// max(1, digits(key) - scale) digits, so no division — computed while the
+// keys stream in (striped, coalesced); out[n] = total.  Look-back over tiles
+// of 4096 keys.
+__global__ void __launch_bounds__(kThreads) k_dec_offsets(const unsigned long long* __restrict__ keys, uint64_t n,
+                                                          uint32_t scale, unsigned long long* __restrict__ out,
+                                                          unsigned long long* desc, unsigned* tile_counter,
+                                                          uint32_t num_tiles) {
+  __shared__ uint32_t s_len[kScanTile + kScanTile / 32];  // index r at r + r/32: both access orders conflict-free
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_w[kThreads / 32];
   __shared__ unsigned long long s_prefix;
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint64_t i0 = (uint64_t)tile * kScanTile + threadIdx.x * kScanPerThread;
-  unsigned long long v[kScanPerThread], sum = 0;
+  const uint64_t t0 = (uint64_t)tile * kScanTile;
+  const uint32_t extra = scale ? 1 + scale : 0;
+#pragma unroll
+  for (int k = 0; k < kScanPerThread; ++k) {  // striped: consecutive lanes, consecutive keys
+    const uint32_t r = k * kThreads + threadIdx.x;
+    uint32_t l = 0;
+    if (t0 + r < n) {
+      const uint32_t d = dec_digits(keys[t0 + r]);
+      l = (d > scale ? d - scale : 1u) + extra;
+    }
+    s_len[r + (r >> 5)] = l;
+  }
+  __syncthreads();
+  uint32_t v[kScanPerThread], sum = 0;  // blocked: thread t owns entries 16t .. 16t+15
 #pragma unroll
   for (int k = 0; k < kScanPerThread; ++k) {
-    v[k] = (i0 + k < count) ? in[i0 + k] : 0ull;
+    const uint32_t r = threadIdx.x * kScanPerThread + k;
+    v[k] = s_len[r + (r >> 5)];
     sum += v[k];
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -208,15 +244,24 @@ __global__ void __launch_bounds__(kThreads) k_exscan_u64(const unsigned long lon
     }
     if (lane == 0) {
       s_prefix = p;
-      if (tile == num_tiles - 1) out[count] = p + r;
+      if (tile == num_tiles - 1) out[n] = p + r;
     }
   }
   __syncthreads();
-  unsigned long long run = s_prefix + before + inc - sum;
+  // exclusive tile-relative offsets back into shared memory, then striped stores
+  uint32_t run = static_cast<uint32_t>(before + inc - sum);
 #pragma unroll
   for (int k = 0; k < kScanPerThread; ++k) {
-    if (i0 + k < count) out[i0 + k] = run;
+    const uint32_t r = threadIdx.x * kScanPerThread + k;
+    s_len[r + (r >> 5)] = run;
     run += v[k];
+  }
+  __syncthreads();
+  const unsigned long long base = s_prefix;
+#pragma unroll
+  for (int k = 0; k < kScanPerThread; ++k) {
+    const uint32_t rr = k * kThreads + threadIdx.x;
+    if (t0 + rr < n) out[t0 + rr] = base + s_len[rr + (rr >> 5)];
   }
 }
 

@@ -4,7 +4,7 @@ SplitMix64 streams, already resident in HBM; each config is
 timed over K steps with CUDA events after W warm-up steps, with per-pass
 device times from the library's own events.
 
-    python tools/bench_configs.py [--steps 5] [--warmup 2] [--only cfg4]
+    python tools/bench_configs.py [--steps 5] [--warmup 2] [--only cfg4,dec]
 """
 import argparse
 import ctypes
@@ -116,6 +116,37 @@ def main():
         out = torch.empty_like(k)
         ms, l, p = timed(lambda: rs.sort_u32(k, out=out, msd=True, key_digits=10), args.steps, args.warmup)
         record("cfg5_u32_full_msd_1gpu", n, 20, ms, l, p, {"note": "declared 10-digit domain (full uint32)"})
+    if want("dec"):
+        # cfg3's values as decimal text ("k/1000" rendered with 3
+        # fractional digits by rs_format_decimals), parsed + sorted + rendered on the GPU
+        n = 1 << 28
+        k32 = torch.empty(n, dtype=torch.int32, device="cuda")
+        rs._check(lib.rs_gen_u32(o.config_seed(3), 0, n, 10**6, rs._ptr(k32), s()))
+        keys = (k32.to(torch.int64) & 0xFFFFFFFF).contiguous()
+        del k32
+        chars, offsets = rs.format_decimal_column(keys, 3)
+        nbytes = chars.numel()
+        out = torch.empty(n, dtype=torch.int64, device="cuda")
+        rep = rs.RsReport()
+        opts = rs._opts(10**9)
+
+        def parse_sort():
+            rs._check(lib.rs_sort_decimal_strings(rs._ptr(chars), rs._ptr(offsets), n, rs._ptr(out), n,
+                                                  ctypes.byref(opts), ctypes.byref(rep), s()))
+        ms, l, p = timed(parse_sort, args.steps, args.warmup)
+        record("dec_cfg3_text_parse_sort", n, nbytes / n + 8 + 8, ms, l, p,
+               {"text_bytes": nbytes, "note": "numerals k/1000 as text; R chars+offsets, W keys"})
+        need = ctypes.c_uint64()
+        oc = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        oo = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+
+        def render():
+            rs._check(lib.rs_format_decimals(rs._ptr(out), n, 3, rs._ptr(oc), nbytes, rs._ptr(oo),
+                                             ctypes.byref(need), s()))
+        ms, l, p = timed(render, args.steps, args.warmup)
+        record("dec_cfg3_render", n, 8 + nbytes / n + 8, ms, l, p, {"note": "R keys, W chars+offsets"})
+        del chars, offsets, out, oc, oo, keys
+        torch.cuda.empty_cache()
     print(json.dumps(res))
 
 
