@@ -762,8 +762,16 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
     exscan_u32(ws, table, nchunks * kMsdBins, off, total);
     {
       PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
-      if (level == 0) k_msd_scatter<<<nchunks, kMsdThreads, 0, ws.stream>>>(load0, segs_in, chunk_seg, shift, off, dst);
-      else k_msd_scatter<<<nchunks, kMsdThreads, 0, ws.stream>>>(LoadKeys<K>{buf[(level - 1) & 1], n}, segs_in,
+      static const bool attr = (cudaFuncSetAttribute(k_msd_scatter<Load>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     static_cast<int>(msd_scatter_smem<Load>())),
+                                cudaFuncSetAttribute(k_msd_scatter<LoadKeys<K>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     static_cast<int>(msd_scatter_smem<LoadKeys<K>>())),
+                                true);
+      (void)attr;
+      if (level == 0)
+        k_msd_scatter<<<nchunks, kMsdThreads, msd_scatter_smem<Load>(), ws.stream>>>(load0, segs_in, chunk_seg, shift,
+                                                                                      off, dst);
+      else k_msd_scatter<<<nchunks, kMsdThreads, msd_scatter_smem<LoadKeys<K>>(), ws.stream>>>(LoadKeys<K>{buf[(level - 1) & 1], n}, segs_in,
                                                                  chunk_seg, shift, off, dst);
       RS_LAUNCH_CHECK();
     }

@@ -37,7 +37,11 @@ namespace rsb {
 
 constexpr int kMsdDigitBits = 8;
 constexpr int kMsdBins = 1 << kMsdDigitBits;
-constexpr int kMsdTile = 4096;          // keys per scatter tile
+constexpr int kMsdTile = 8192;          // largest scatter tile
+// keys per scatter tile: 32-bit keys 8192 (128-byte digit runs), 64-bit keys
+// 4096 (the 64-bit register tile already costs ~120 registers at 4096)
+template <class K>
+__host__ __device__ constexpr int msd_tile() { return sizeof(K) == 4 ? 8192 : 4096; }
 constexpr uint32_t kMsdChunk = 65536;   // keys per (segment, chunk) work item
 constexpr uint32_t kLeafSmall = 2048;   // shared bitonic leaf capacity
 constexpr uint32_t kLeafWarp = 32;      // warp (register) bitonic leaf capacity
@@ -65,18 +69,19 @@ struct LoadKeys {
   // A tile of up to kMsdTile keys at a: 16-byte vectors when a is aligned
   // (thread t takes elements 4t..4t+3 of each 1024-element quarter), else
   // element j*256+t.  Order inside a tile is irrelevant to the partition.
-  __device__ __forceinline__ void load16(unsigned long long a, uint32_t tl, K (&k)[kMsdTile / kMsdThreads]) {
-    vec_ = (sizeof(K) == 4) && ((reinterpret_cast<uintptr_t>(p + a) & 15) == 0) && tl == kMsdTile;
+  static constexpr int kTile = msd_tile<K>();
+  __device__ __forceinline__ void load16(unsigned long long a, uint32_t tl, K (&k)[kTile / kMsdThreads]) {
+    vec_ = (sizeof(K) == 4) && ((reinterpret_cast<uintptr_t>(p + a) & 15) == 0) && tl == kTile;
     if (vec_) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kTile / (4 * kMsdThreads); ++q) {
         const uint4 w = __ldcs(reinterpret_cast<const uint4*>(p + a) + q * kMsdThreads + threadIdx.x);
         k[4 * q] = static_cast<K>(w.x); k[4 * q + 1] = static_cast<K>(w.y);
         k[4 * q + 2] = static_cast<K>(w.z); k[4 * q + 3] = static_cast<K>(w.w);
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < kMsdTile / kMsdThreads; ++j) {
+      for (int j = 0; j < kTile / kMsdThreads; ++j) {
         const uint32_t i = j * kMsdThreads + threadIdx.x;
         k[j] = i < tl ? __ldcs(p + a + i) : K(0);
       }
@@ -95,9 +100,10 @@ struct LoadStr {
   const uint8_t* recs;
   uint32_t width;
   const uint16_t* ord;  // device table (256 entries)
-  __device__ __forceinline__ void load16(unsigned long long a, uint32_t tl, Key (&k)[kMsdTile / kMsdThreads]) const {
+  static constexpr int kTile = msd_tile<Key>();
+  __device__ __forceinline__ void load16(unsigned long long a, uint32_t tl, Key (&k)[kTile / kMsdThreads]) const {
 #pragma unroll
-    for (int j = 0; j < kMsdTile / kMsdThreads; ++j) {
+    for (int j = 0; j < kTile / kMsdThreads; ++j) {
       const uint32_t i = j * kMsdThreads + threadIdx.x;
       k[j] = i < tl ? (*this)(a + i) : 0ull;
     }
@@ -201,20 +207,30 @@ __global__ void __launch_bounds__(kMsdThreads) k_msd_hist(Load ld, const MsdSeg*
 }
 
 template <class Load>
-__global__ void __launch_bounds__(kMsdThreads, 4) k_msd_scatter(Load ld, const MsdSeg* __restrict__ segs,
+constexpr size_t msd_scatter_smem() {  // tile buffers: two (TMA double buffer) for uint32 keys
+  return (std::is_same<Load, LoadKeys<uint32_t>>::value ? 2 : 1) * (size_t)(msd_tile<typename Load::Key>() + 4) *
+         sizeof(typename Load::Key);
+}
+template <class Load>
+constexpr int msd_scatter_min_blocks() { return sizeof(typename Load::Key) == 4 ? 3 : 4; }
+
+template <class Load>
+__global__ void __launch_bounds__(kMsdThreads, msd_scatter_min_blocks<Load>()) k_msd_scatter(Load ld, const MsdSeg* __restrict__ segs,
                                                              const uint32_t* __restrict__ chunk_seg, uint32_t shift,
                                                              const uint32_t* __restrict__ off,
                                                              typename Load::Key* __restrict__ dst) {
   using K = typename Load::Key;
+  constexpr int kTile = msd_tile<K>();
   // uint32 keys: tiles double-buffered by 1D TMA bulk copies (an aligned
   // superset of the tile, the offset skipped in shared memory); the consumed
   // buffer is reused as the output staging
   constexpr bool kBulk = std::is_same<Load, LoadKeys<uint32_t>>::value;
-  constexpr int kPer = kMsdTile / kMsdThreads;  // 16 keys per thread per tile
+  constexpr int kPer = kTile / kMsdThreads;  // 16 keys per thread per tile
   __shared__ uint32_t s_base[kMsdBins];  // segment-relative destination of this tile's digit run, minus its start
   __shared__ uint32_t s_cur[kMsdBins];   // running segment-relative cursor per digit
   __shared__ uint32_t s_cnt[kMsdBins];
-  __shared__ __align__(16) K s_buf[kBulk ? 2 : 1][kMsdTile + 4];
+  extern __shared__ __align__(16) unsigned char msd_smem[];
+  auto s_buf = reinterpret_cast<K(*)[kTile + 4]>(msd_smem);  // [kBulk ? 2 : 1][kTile + 4]
   __shared__ uint32_t s_scan[kMsdThreads / 32];
   __shared__ __align__(8) unsigned long long s_bar[2];
   const uint32_t c = blockIdx.x;
@@ -225,14 +241,14 @@ __global__ void __launch_bounds__(kMsdThreads, 4) k_msd_scatter(Load ld, const M
   for (int b = threadIdx.x; b < kMsdBins; b += blockDim.x) s_cur[b] = t[(unsigned long long)b * g.nchunks + ci] - base0;
   const unsigned long long a = g.start + (unsigned long long)ci * kMsdChunk;
   const uint32_t len = min(kMsdChunk, g.size - ci * kMsdChunk);
-  const uint32_t ntiles = (len + kMsdTile - 1) / kMsdTile;
+  const uint32_t ntiles = (len + kTile - 1) / kTile;
   K* seg_dst = dst + g.start;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // tile u of this chunk: aligned superset [a+u*T - mis, ...) of round-up size
   auto tile_geo = [&](uint32_t u, uint32_t& mis, uint32_t& bytes, bool& ok) {
     if constexpr (kBulk) {
-      const unsigned long long e0 = a + (unsigned long long)u * kMsdTile;
-      const uint32_t tl = min((uint32_t)kMsdTile, len - u * kMsdTile);
+      const unsigned long long e0 = a + (unsigned long long)u * kTile;
+      const uint32_t tl = min((uint32_t)kTile, len - u * kTile);
       mis = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(ld.p + e0) & 15) / sizeof(K));
       bytes = ((tl + mis) * (uint32_t)sizeof(K) + 15) & ~15u;
       ok = e0 - mis + bytes / sizeof(K) <= ld.n_total;
@@ -262,8 +278,8 @@ __global__ void __launch_bounds__(kMsdThreads, 4) k_msd_scatter(Load ld, const M
     }
   }
   for (uint32_t u = 0; u < ntiles; ++u) {
-    const uint32_t t0 = u * kMsdTile;
-    const uint32_t tl = min((uint32_t)kMsdTile, len - t0);
+    const uint32_t t0 = u * kTile;
+    const uint32_t tl = min((uint32_t)kTile, len - t0);
     const int buf = kBulk ? (u & 1) : 0;
     s_cnt[threadIdx.x] = 0;
     if constexpr (kBulk) {
@@ -275,14 +291,14 @@ __global__ void __launch_bounds__(kMsdThreads, 4) k_msd_scatter(Load ld, const M
           if constexpr (kBulk) {
             fence_proxy_async_smem();
             mbar_expect_tx(&s_bar[buf ^ 1], bytes);
-            bulk_g2s(&s_buf[buf ^ 1][0], ld.p + a + t0 + kMsdTile - mis, bytes, &s_bar[buf ^ 1]);
+            bulk_g2s(&s_buf[buf ^ 1][0], ld.p + a + t0 + kTile - mis, bytes, &s_bar[buf ^ 1]);
           }
         }
       }
     }
     __syncthreads();
     K k[kPer];
-    uint32_t rk2[kPer / 2];  // ranks in the tile (< 4096), two per word; 0xffff = no key
+    uint32_t rk2[kPer / 2];  // ranks in the tile (< kTile), two per word; 0xffff = no key
     bool bulk_tile = false;
     if constexpr (kBulk) {
       uint32_t mis, bytes;
