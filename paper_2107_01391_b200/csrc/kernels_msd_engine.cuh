@@ -464,7 +464,11 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   };
   uint32_t i = threadIdx.x;
   load(i, !scatter);
-  for (uint32_t z = threadIdx.x; z < words; z += blockDim.x) s_w[z] = 0;
+  if ((words & 3) == 0) {  // 16-byte stores (words is a power of two here)
+    for (uint32_t z = threadIdx.x; z < words / 4; z += blockDim.x) reinterpret_cast<uint4*>(s_w)[z] = make_uint4(0, 0, 0, 0);
+  } else {
+    for (uint32_t z = threadIdx.x; z < words; z += blockDim.x) s_w[z] = 0;
+  }
   __syncthreads();
   for (;;) {
 #pragma unroll
@@ -482,12 +486,23 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   // exclusive scan over cells: each thread owns a contiguous run of words
   const uint32_t per = (words + kLeafGridThreads - 1) / kLeafGridThreads;
   const uint32_t w0 = threadIdx.x * per;
+  // words >= threads: each thread owns whole words w0 .. w0+per-1 (per | 32,
+  // w0 a multiple of per), whose swizzle is one XOR with xr; no bounds
+  const bool whole = words >= kLeafGridThreads;
+  const uint32_t xr = (w0 >> 5) & 31u;
   uint32_t sum = 0;
-  for (uint32_t j = 0; j < per; ++j) {
-    const uint32_t w = w0 + j;
-    if (w < words) {
-      const uint32_t x = s_w[leaf_gw(w)];
+  if (whole) {
+    for (uint32_t j = 0; j < per; ++j) {
+      const uint32_t x = s_w[(w0 + j) ^ xr];
       sum += (x & 0xffffu) + (x >> 16);
+    }
+  } else {
+    for (uint32_t j = 0; j < per; ++j) {
+      const uint32_t w = w0 + j;
+      if (w < words) {
+        const uint32_t x = s_w[leaf_gw(w)];
+        sum += (x & 0xffffu) + (x >> 16);
+      }
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -504,10 +519,11 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   if (scatter) {
     for (uint32_t j = 0; j < per; ++j) {  // counts -> exclusive offsets (< 65536: no carry between halves)
       const uint32_t w = w0 + j;
-      if (w < words) {
-        const uint32_t x = s_w[leaf_gw(w)];
+      if (whole || w < words) {
+        const uint32_t pw = whole ? (w ^ xr) : leaf_gw(w);
+        const uint32_t x = s_w[pw];
         const uint32_t c0 = x & 0xffffu, c1 = x >> 16;
-        s_w[leaf_gw(w)] = run | ((run + c0) << 16);
+        s_w[pw] = run | ((run + c0) << 16);
         run += c0 + c1;
       }
     }
