@@ -291,6 +291,49 @@ def test_cfg2_kv_full_size_stability(rs):
     torch.cuda.empty_cache()
 
 
+def test_cfg3_full_size_properties(rs, oracle):
+    """2^28 float64 k/1000 (half Zipf) at BASELINE size: sorted, and the same
+    multiset of mantissas as round(x * 1000) (exact for these decimals)."""
+    import torch
+
+    n = 1 << 28
+    cdf = torch.from_numpy(oracle.zipf_cdf()).cuda()
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    rs._check(rs._lib.load().rs_gen_f64_cfg3(rs_seed(3), 0, n, rs._ptr(cdf), cdf.numel(), rs._ptr(x), rs._stream()))
+    out, rep = rs.sort_f64(x, 3, key_digits=6)
+    assert rep.written == n and (rep.spec.total_digits, rep.spec.integer_digits) == (6, 3)
+    want = torch.round(x * 1000.0).long()
+    del x
+    _sorted_and_same_multiset(want, out.view(torch.int64), 10**6)
+    del out, want
+    torch.cuda.empty_cache()
+
+
+def test_cfg4_full_size_properties(rs):
+    """2^26 eight-letter strings at BASELINE size through the MSD path: rows in
+    lexicographic order, and the same multiset by order-independent hashes."""
+    import torch
+
+    n = 1 << 26
+    recs = torch.empty((n, 8), dtype=torch.uint8, device="cuda")
+    rs._check(rs._lib.load().rs_gen_str_cfg4(rs_seed(4), 0, n, rs._ptr(recs), rs._stream()))
+    out, rep = rs.sort_fixed_str(recs, msd=True)
+    assert rep.written == n and rep.spec.radix == 27 and rep.spec.total_digits == 8
+
+    def as_key(r):  # big-endian: lexicographic byte order == integer order (ASCII < 128)
+        k = torch.zeros(r.shape[0], dtype=torch.int64, device=r.device)
+        for i in range(8):
+            k = (k << 8) | r[:, i].long()
+        return k
+
+    a, b = as_key(recs), as_key(out)
+    assert bool((b[1:] >= b[:-1]).all())
+    for mul in (0x9E3779B97F4A7C15 & 0x7FFFFFFFFFFFFFFF, 0x2545F4914F6CDD1D):
+        assert int(((a * mul) >> 13).sum()) == int(((b * mul) >> 13).sum())
+    del recs, out, a, b
+    torch.cuda.empty_cache()
+
+
 def rs_seed(cfg):
     from oracle import Oracle
 
