@@ -43,6 +43,20 @@ def cell_ranges(prefix: torch.Tensor, world: int) -> list[tuple[int, int]]:
     return [(bounds[i], bounds[i + 1]) for i in range(world)]
 
 
+def cell_bounds_device(prefix: torch.Tensor, world: int) -> torch.Tensor:
+    """cell_ranges on the prefix's own device: the world+1 range bounds as a
+    tensor (same cuts: first cell whose prefix reaches ceil(r*total/world),
+    plus one, clamped to be monotone and <= cells)."""
+    cells = prefix.numel()
+    total = prefix[-1]
+    r = torch.arange(1, world, device=prefix.device, dtype=torch.int64)
+    targets = (r * total + world - 1) // world
+    cuts = torch.searchsorted(prefix, targets, right=False) + 1
+    cuts = torch.cummax(cuts.clamp(min=0, max=cells), 0).values
+    zero = torch.zeros(1, dtype=torch.int64, device=prefix.device)
+    return torch.cat([zero, cuts, torch.full((1,), cells, dtype=torch.int64, device=prefix.device)])
+
+
 def bucket_splitters(hist: torch.Tensor, world: int) -> list[int]:
     """Part bounds over buckets (len world+1, bounds[0]=0, bounds[-1]=buckets)
     with about total/world keys per part, cut on bucket boundaries."""
@@ -111,9 +125,12 @@ def sharded_grid_sort(keys: torch.Tensor, cells: int, ops=None, group=None) -> t
     rank = dist.get_rank(group)
     counts = ops.count(keys, cells)
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)  # C1: the grid over NVLink
-    prefix = torch.cumsum(counts.to(torch.int64), 0)
-    lo, hi = cell_ranges(prefix.cpu(), world)[rank]
-    n_out = int(prefix[hi - 1] - (prefix[lo - 1] if lo > 0 else 0)) if hi > lo else 0
+    prefix = torch.cumsum(counts, 0, dtype=torch.int64)
+    # this rank's cell range and key count, cut on the device: one 24-byte copy back
+    bounds = cell_bounds_device(prefix, world)
+    lo_hi = bounds[rank:rank + 2]
+    ends = torch.where(lo_hi > 0, prefix[(lo_hi - 1).clamp(min=0)], torch.zeros_like(lo_hi))
+    lo, hi, n_out = (int(v) for v in torch.stack([lo_hi[0], lo_hi[1], ends[1] - ends[0]]).cpu())
     return ops.emit(counts, lo, hi, n_out)
 
 

@@ -86,6 +86,21 @@ def test_cell_ranges_balance_and_cover():
     assert abs(left - (28 - left)) <= 9  # never splits a cell; within one cell of balance
 
 
+def test_device_cell_bounds_match_host_ranges():
+    from paper_2107_01391_b200.dist import cell_bounds_device
+
+    g = torch.Generator().manual_seed(5)
+    for trial in range(40):
+        cells = int(torch.randint(1, 300, (1,), generator=g))
+        counts = torch.randint(0, 4, (cells,), generator=g) * (torch.rand(cells, generator=g) < 0.5)
+        if trial % 5 == 0:
+            counts[int(torch.randint(0, cells, (1,), generator=g))] += 500  # one hot cell
+        prefix = torch.cumsum(counts, 0, dtype=torch.int64)
+        for world in (1, 2, 3, 5, 8):
+            want = [lo for lo, _ in cell_ranges(prefix, world)] + [cells]
+            assert cell_bounds_device(prefix, world).tolist() == want
+
+
 def test_bucket_splitters_cover_all_buckets():
     hist = torch.tensor([0, 100, 3, 3, 3, 200, 0, 50])
     b = bucket_splitters(hist, 4)
