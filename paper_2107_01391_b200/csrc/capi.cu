@@ -326,6 +326,19 @@ void count_pass(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, 
     return;
   }
   TwoLevel t{};
+  if constexpr (map_first<Map>::value) {
+    if (plan_two_level<MapU32>(cells, n, t)) {  // map pass, then the uint32 partition
+      auto* mapped = ws.get<uint32_t>(kSlotMapped, n);
+      {
+        PassTimer pt_(RS_PASS_PARTITION, ws.stream);
+        k_map_cells<Map><<<stream_grid(n, kThreads * 8, 8), kThreads, 0, ws.stream>>>(in, n, map, aligned16(in),
+                                                                                        mapped, ws.stats);
+        RS_LAUNCH_CHECK();
+      }
+      two_level_count(ws, mapped, n, MapU32{}, t, counts);
+      return;
+    }
+  }
   if (plan_two_level<Map>(cells, n, t)) {
     two_level_count(ws, in, n, map, t, counts);
     return;

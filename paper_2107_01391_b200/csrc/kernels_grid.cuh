@@ -121,9 +121,25 @@ struct MapU64 {
 //    half-up result is decided by x*P versus m+1/2, exactly.
 // IEEE division of two exact doubles (m < 2^53, P <= 10^15) is correctly
 // rounded, so every "rounds to x" test is exact.
+// Is x == RN(c / d) (d > 0)?  Without dividing: with h = d * ulp(x) / 2
+// (exact) the exact residual c - x*d is below h iff c/d lies inside x's
+// rounding interval, and r = fma(-x, d, c) rounds it once, so r < h proves
+// it and r > h refutes it (rounding is monotone and h is representable).
+// r == h (a tie or a rounding onto h) and powers of two (narrower spacing
+// below x) stay undecided.  1 yes, 0 no, -1 undecided.
+__device__ __forceinline__ int quotient_is(double x, double c, double d) {
+  const unsigned long long xb = static_cast<unsigned long long>(__double_as_longlong(x));
+  const double ulp = __longlong_as_double(static_cast<long long>((xb & 0x7ff0000000000000ull) - (52ull << 52)));
+  const double h = d * ulp * 0.5;
+  const double r = fabs(fma(-x, d, c));
+  const bool pow2 = (xb & 0x000fffffffffffffull) == 0;
+  return (pow2 || r == h) ? -1 : (r < h ? 1 : 0);
+}
+
 struct MapF64 {
   using In = double;
   using Key = unsigned long long;
+  static constexpr bool kMapFirst = true;  // a separate streaming map pass, then the uint32 partition
   double P;      // 10^scale
   double P2;     // 2 * 10^scale
   double limit;  // 2^53 / 100
@@ -162,7 +178,87 @@ struct MapF64 {
     const bool up = fr > 0.5 || (fr == 0.5 && err > 0.0);
     return up ? m + 1 : m;
   }
+  // The same mapping without branches or division (the map pass has the ILP
+  // to interleave many keys): the candidate test is quotient_is; keys it
+  // cannot decide and keys outside the domain set `undecided` and go through
+  // operator() (mirrored by tests/test_f64_mapping.py::kernel_f64_fast).
+  __device__ __forceinline__ unsigned long long fast(double x, bool& undecided) const {
+    const double p = x * P;
+    const bool bad = !(x >= 0.0) || !(p < limit) || (x > 0.0 && x < tiny);
+    const double err = fma(x, P, -p);
+    double f = floor(p);
+    f = (p == f && err < 0.0) ? f - 1.0 : f;
+    const unsigned long long m = static_cast<unsigned long long>(bad ? 0.0 : f);
+    const double fr = p - f;
+    const bool near_int = fr < 0.02 || fr > 0.98;
+    const bool near_half = fr > 0.48 && fr < 0.52;
+    const unsigned long long c = fr < 0.5 ? m : m + 1;
+    const double cv = near_int ? static_cast<double>(c) : static_cast<double>(2 * m + 1);
+    const double dv = near_int ? P : P2;
+    const int q = x == 0.0 ? 1 : ((near_int || near_half) ? quotient_is(x, cv, dv) : 0);  // 0 maps to 0
+    undecided = bad || q < 0;
+    const bool up = fr > 0.5 || (fr == 0.5 && err > 0.0);
+    return q > 0 ? (near_int ? c : m + 1) : (up ? m + 1 : m);
+  }
 };
+
+template <class M, class = void>
+struct map_first : std::false_type {};
+template <class M>
+struct map_first<M, std::void_t<decltype(M::kMapFirst)>> : std::true_type {};
+
+// Heavy mappers (float64): every input mapped once into a uint32 cell by a
+// streaming pass at full occupancy (cells >= 2^32 clamp to 0xFFFFFFFF, which
+// still lies outside any grid the two-level split serves), so the tuned
+// uint32 partition runs on the cells; max key and flags as in the fused path.
+template <class Map>
+__global__ void __launch_bounds__(kThreads) k_map_cells(const typename Map::In* __restrict__ in, uint64_t n, Map map,
+                                                        bool aligned, uint32_t* __restrict__ out, DevStats* st) {
+  using In = typename Map::In;
+  unsigned long long mx = 0;
+  unsigned flags = 0;
+  auto cell = [&](In x) -> uint32_t {
+    unsigned long long k;
+    if constexpr (std::is_same<Map, MapF64>::value) {
+      bool und;
+      k = map.fast(x, und);
+      if (und) k = map(x, flags);  // rare: exact path (also classifies bad inputs)
+    } else {
+      k = map(x, flags);
+    }
+    mx = k > mx ? k : mx;
+    return k < 0xFFFFFFFFull ? static_cast<uint32_t>(k) : 0xFFFFFFFFu;
+  };
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if constexpr (sizeof(In) == 8) {
+    if (aligned) {  // two inputs per 16-byte load, four loads in flight, two cells per 8-byte store
+      const uint64_t pairs = n / 2;
+      const auto* src = reinterpret_cast<const ulonglong2*>(in);
+      auto* dst = reinterpret_cast<uint2*>(out);
+      uint64_t p = i;
+      for (; p + 3 * stride < pairs; p += 4 * stride) {
+        ulonglong2 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u] = __ldcs(src + p + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          dst[p + u * stride] = make_uint2(cell(*reinterpret_cast<const In*>(&w[u].x)),
+                                           cell(*reinterpret_cast<const In*>(&w[u].y)));
+      }
+      for (; p < pairs; p += stride) {
+        const ulonglong2 w = __ldcs(src + p);
+        dst[p] = make_uint2(cell(*reinterpret_cast<const In*>(&w.x)), cell(*reinterpret_cast<const In*>(&w.y)));
+      }
+      if ((n & 1) && i == 0) out[n - 1] = cell(in[n - 1]);
+      i = n;  // done
+    }
+  }
+  for (; i < n; i += stride) out[i] = cell(in[i]);
+  warp_max_to(mx, &st->max_key);
+  flags = warp_or(flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(&st->flags, flags);
+}
 
 // ----------------------------------------------------------- K0: max pass
 // The reference derives the geometry from the dataset max (sort.cpp:31-40);

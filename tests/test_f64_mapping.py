@@ -41,6 +41,86 @@ def kernel_f64(x: float, scale: int):
     return m + 1 if up else m
 
 
+def _fma(a: float, b: float, c: float) -> float:
+    """Exactly rounded a*b + c (IEEE fma)."""
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def quotient_is(x: float, c: float, d: float):
+    """Mirror of quotient_is (kernels_grid.cuh): is x == RN(c / d)?  1 yes,
+    0 no, -1 undecided (the kernel then takes the exact path)."""
+    xb = np.float64(x).view(np.uint64).item()
+    ulp = np.uint64((xb & 0x7FF0000000000000) - (52 << 52)).view(np.float64).item()
+    h = d * ulp * 0.5
+    r = abs(_fma(-x, d, c))
+    if (xb & ((1 << 52) - 1)) == 0 or r == h:
+        return -1
+    return 1 if r < h else 0
+
+
+def kernel_f64_fast(x: float, scale: int):
+    """Mirror of MapF64::fast; None = undecided (the kernel falls back to
+    MapF64::operator(), mirrored by kernel_f64)."""
+    P = float(10 ** scale)
+    p = x * P
+    if not (x >= 0.0) or not (p < LIMIT) or (x > 0.0 and x < 1.0000001 * 10.0 ** -(scale + 3)):
+        return None
+    err = _fma(x, P, -p)
+    f = float(math.floor(p))
+    if p == f and err < 0.0:
+        f -= 1.0
+    m = int(f)
+    fr = p - f
+    near_int = fr < 0.02 or fr > 0.98
+    near_half = 0.48 < fr < 0.52
+    c = m if fr < 0.5 else m + 1
+    cv, dv = (float(c), P) if near_int else (float(2 * m + 1), 2.0 * P)
+    q = 1 if x == 0.0 else (quotient_is(x, cv, dv) if (near_int or near_half) else 0)
+    if q == -1:
+        return None
+    if q == 1:
+        return c if near_int else m + 1
+    return m + 1 if (fr > 0.5 or (fr == 0.5 and err > 0.0)) else m
+
+
+def test_fast_path_matches_exact_path(oracle):
+    rng = np.random.default_rng(5)
+    undecided = decided = 0
+    for scale in (0, 1, 2, 3, 6, 9, 12, 15):
+        xs = [float(v) / 10.0 ** scale for v in rng.integers(0, 10 ** 7, 2000)]
+        xs += [(2 * float(v) + 1) / (2 * 10.0 ** scale) for v in rng.integers(0, 10 ** 7, 1000)]
+        xs += [float(np.nextafter((2 * float(v) + 1) / (2 * 10.0 ** scale), np.inf if v % 2 else 0.0))
+               for v in rng.integers(0, 10 ** 7, 500)]
+        xs += list(rng.random(1000) * 1e3) + [2.0 ** e for e in range(-40, 30)] + [0.0]
+        for x in xs:
+            if not in_domain(x, scale):
+                continue
+            got = kernel_f64_fast(x, scale)
+            if got is None:
+                undecided += 1
+            else:
+                decided += 1
+                assert got == kernel_f64(x, scale) == oracle.float_to_decimal(x, scale), (x, scale)
+    assert undecided < decided / 20
+
+
+def test_quotient_test_agrees_with_division():
+    """Whenever the division-free test decides, it agrees with IEEE division."""
+    rng = np.random.default_rng(7)
+    decided = 0
+    for _ in range(20000):
+        scale = int(rng.integers(0, 16))
+        d = float(10 ** scale) * (2.0 if rng.random() < 0.3 else 1.0)
+        c = float(int(rng.integers(0, 2 ** 40)))
+        q = c / d
+        for x in (q, float(np.nextafter(q, np.inf)), float(np.nextafter(q, 0.0))):
+            t = quotient_is(x, c, d)
+            if t != -1:
+                decided += 1
+                assert (t == 1) == (c / d == x), (x, c, d)
+    assert decided > 50000
+
+
 def in_domain(x: float, scale: int) -> bool:
     return x * 10.0 ** scale < LIMIT and (x == 0.0 or x >= 1.0000001 * 10.0 ** -(scale + 3))
 
