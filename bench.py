@@ -104,78 +104,84 @@ class ClockSampler:
 
 
 # -------------------------------------------------------- reference arm
-def reference_arm(args, rank: int):
-    """The reference's own CPU implementation (oracle/_ref: the unmodified
-    library compiled from /root/reference/proj/src) on the same cfg2 stream,
-    one bounded sample per step.  The reference is single-threaded, so it
-    uses one core (nproc is reported)."""
-    if rank != 0:
-        return
+def _reference_workers():
+    """Host threads for the reference arm and the sample each one sorts: the
+    reference library is single-threaded and reentrant, so every
+    thread runs its own sort_integers on its own copy of the cfg2 sample
+    (ctypes releases the GIL); <= 32 threads, 2^23 keys each above 16 threads
+    to bound host memory."""
+    threads = max(1, min(os.cpu_count() or 1, 32))
+    sample = CPU_SAMPLE if threads <= 16 else CPU_SAMPLE // 2
+    return threads, sample
+
+
+def _reference_step_fn(sample):
+    """One reference sort of `sample` cfg2 keys (the unmodified library in
+    oracle/_ref when built, else the oracle restatement)."""
     import numpy as np
 
     from oracle import Oracle, Reference
 
     o = Oracle()
     kind = "reference" if Reference.available() else "port"
-    impl = Reference() if kind == "reference" else o
-    keys = o.gen_u32(o.config_seed(2), 0, CPU_SAMPLE, KEY_BOUND)
-    wide = keys.astype(np.int64)
+    keys = o.gen_u32(o.config_seed(2), 0, sample, KEY_BOUND)
+    if kind == "reference":
+        r = Reference()
+        wide = keys.astype(np.int64)
+        return kind, lambda: r.sort_integers(wide)
+    return kind, lambda: o.sort_integers_u32(keys)
 
-    def step():
-        if kind == "reference":
-            impl.sort_integers(wide)
-        else:
-            impl.sort_integers_u32(keys)
 
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = (time.perf_counter() - t0) / args.steps
-    value = CPU_SAMPLE / dt / 1e9
+def _timed_parallel(fn, threads: int, steps: int) -> float:
+    """Seconds per step, a step = `threads` concurrent calls of fn."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            list(pool.map(lambda _: fn(), range(threads)))
+        return (time.perf_counter() - t0) / steps
+
+
+def reference_arm(args, rank: int):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    library compiled from /root/reference/proj/src) on the cfg2 stream, with
+    all the host threads it can use: one independent bounded sample per
+    thread per step (the library is single-threaded)."""
+    if rank != 0:
+        return
+    threads, sample = _reference_workers()
+    kind, fn = _reference_step_fn(sample)
+    _timed_parallel(fn, threads, max(args.warmup, 1))
+    dt = _timed_parallel(fn, threads, args.steps)
+    value = threads * sample / dt / 1e9
     line = {
         "impl": "reference", "metric": "sorted Gkeys/s", "value": value, "unit": "Gkeys/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": "cfg2: uint32 keys uniform in [0,10^6) (SplitMix64 seed mix(42,2)), key-only, "
-                               "sort_integers facade", "sample_keys": CPU_SAMPLE},
-        "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": 1, "kind": kind,
-                         "sample": f"sort_integers on the first {CPU_SAMPLE} cfg2 keys per step "
-                                   f"(single-threaded library; host nproc={os.cpu_count()})"},
+                               "sort_integers facade", "sample_keys_per_thread": sample, "threads": threads},
+        "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": threads, "kind": kind,
+                         "sample": f"sort_integers on the first {sample} cfg2 keys, one independent sort per "
+                                   f"host thread per step ({threads} threads; host nproc={os.cpu_count()})"},
         "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline_sample():
-    """cpu_baseline for our line: same as the reference arm, 1 warm-up + 2 trials."""
-    import numpy as np
-
-    from oracle import Oracle, Reference
-
-    o = Oracle()
-    kind = "reference" if Reference.available() else "port"
-    keys = o.gen_u32(o.config_seed(2), 0, CPU_SAMPLE, KEY_BOUND)
-    if kind == "reference":
-        r = Reference()
-        wide = keys.astype(np.int64)
-        fn = lambda: r.sort_integers(wide)  # noqa: E731
-    else:
-        fn = lambda: o.sort_integers_u32(keys)  # noqa: E731
-    fn()
-    times = []
-    for _ in range(2):
-        t0 = time.perf_counter()
-        fn()
-        times.append(time.perf_counter() - t0)
-    dt = min(times)
-    return {"value": CPU_SAMPLE / dt / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": kind,
-            "sample": f"reference sort_integers (facade) on {CPU_SAMPLE} cfg2 keys, best of 2 after 1 warm-up; "
-                      f"single-threaded library, host nproc={os.cpu_count()}"}
+    """cpu_baseline for our line: the reference arm's measurement (all host
+    threads, one independent sample each), 1 warm-up step + 2 timed steps."""
+    threads, sample = _reference_workers()
+    kind, fn = _reference_step_fn(sample)
+    _timed_parallel(fn, threads, 1)
+    dt = _timed_parallel(fn, threads, 2)
+    return {"value": threads * sample / dt / 1e9, "unit": "Gkeys/s", "cores": threads, "kind": kind,
+            "sample": f"reference sort_integers on {sample} cfg2 keys per host thread, {threads} threads "
+                      f"concurrently (single-threaded library, one sort per thread), 2 steps after 1 warm-up; "
+                      f"host nproc={os.cpu_count()}"}
 
 
-# ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
