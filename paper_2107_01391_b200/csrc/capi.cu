@@ -304,12 +304,13 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
   }
   RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
   const uint64_t max_groups = P / t.group_pages + t.B + 1;
-  if (t.S * sizeof(uint32_t) > 48 * 1024)
+  const size_t cnt_smem = (t.S + 1) * sizeof(uint32_t);  // + the dump bin of pad entries
+  if (cnt_smem > 48 * 1024)
     RS_CUDA(cudaFuncSetAttribute(k_page_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(t.S * sizeof(uint32_t))));
+                                 static_cast<int>(cnt_smem)));
   {
     PassTimer pt_(RS_PASS_COUNT, ws.stream);
-    k_page_count<<<static_cast<unsigned>(max_groups), kGatherThreads, t.S * sizeof(uint32_t), ws.stream>>>(
+    k_page_count<<<static_cast<unsigned>(max_groups), kGatherThreads, cnt_smem, ws.stream>>>(
         pages, page_fill, list, po_bm, work, total, t, counts);
     RS_LAUNCH_CHECK();
   }

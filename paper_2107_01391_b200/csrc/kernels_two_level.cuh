@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_page_count(const uint16_t* _
                                                                const uint32_t* __restrict__ work_start,
                                                                const unsigned long long* total, TwoLevel t,
                                                                uint32_t* __restrict__ counts) {
-  extern __shared__ uint32_t s_c[];  // [S]
+  extern __shared__ uint32_t s_c[];  // [S + 1]
   __shared__ uint32_t s_b, s_p0, s_p1;
   __shared__ uint32_t s_pg[kMaxGroupPages], s_fl[kMaxGroupPages];  // the group's pages and fills
   const uint32_t w = blockIdx.x;
@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_page_count(const uint16_t* _
     s_p0 = p0;
     s_p1 = p0 + t.group_pages < last ? p0 + t.group_pages : last;
   }
-  for (uint32_t i = threadIdx.x; i < t.S; i += blockDim.x) s_c[i] = 0;
+  for (uint32_t i = threadIdx.x; i <= t.S; i += blockDim.x) s_c[i] = 0;  // [S]: dump bin of pad entries
   __syncthreads();
   const uint32_t np = s_p1 - s_p0;  // <= kMaxGroupPages
   for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
@@ -687,11 +687,19 @@ __global__ void __launch_bounds__(kGatherThreads) k_page_count(const uint16_t* _
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint32_t ws[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+      if (lim[u] == 8) {  // a full slot (all but a bucket's last page): pad entries land in the dump bin S
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t e0 = ws[j] & 0xffffu, e1 = ws[j] >> 16;
-        if (2 * j < lim[u] && e0 != kPagePad) atomicAdd(&s_c[e0], 1u);
-        if (2 * j + 1 < lim[u] && e1 != kPagePad) atomicAdd(&s_c[e1], 1u);
+        for (int j = 0; j < 4; ++j) {
+          atomicAdd(&s_c[min(ws[j] & 0xffffu, t.S)], 1u);
+          atomicAdd(&s_c[min(ws[j] >> 16, t.S)], 1u);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t e0 = ws[j] & 0xffffu, e1 = ws[j] >> 16;
+          if (2 * j < lim[u]) atomicAdd(&s_c[min(e0, t.S)], 1u);
+          if (2 * j + 1 < lim[u]) atomicAdd(&s_c[min(e1, t.S)], 1u);
+        }
       }
     }
   }
