@@ -42,6 +42,7 @@ constexpr uint32_t kTlMaxInner = 16384;             // inner cells (smem hist <=
 constexpr uint32_t kPage = 1024;                    // inner digits per page (2 KB)
 constexpr uint16_t kPagePad = 0xffff;               // padding entry (inner digits are < 16384)
 constexpr int kGatherThreads = 256;
+constexpr int kTlRep = 4;                           // lane replicas of a bucket's rank counter (skewed tiles)
 constexpr uint32_t kMaxGroupPages = 256;            // pages per page-count work item (16 * S / kPage <= 256)
 
 struct TwoLevel {
@@ -370,7 +371,8 @@ template <class Map>
 __host__ __device__ constexpr size_t page_tma_smem() {
   return 2 * (size_t)kTlTile * sizeof(typename Map::In)  // s_in[2]; the consumed buffer stages the tile
          + 256 * 16                                      // s_run: this tile's run geometry per bucket
-         + 258 * 4 * 4;                                  // s_cnt, s_page, s_fill, s_np
+         + 258 * 4 * 4                                   // s_cnt, s_page, s_fill, s_np
+         + 258 * 4 * (size_t)kTlRep;                     // s_rep
 }
 template <class Map>
 constexpr int page_tma_min_blocks() { return sizeof(typename Map::In) == 4 ? 4 : 2; }
@@ -385,10 +387,17 @@ __global__ void __launch_bounds__(kTlThreads, page_tma_min_blocks<Map>())
   extern __shared__ __align__(128) unsigned char sm[];
   In* s_in = reinterpret_cast<In*>(sm);                         // [2][kTlTile]
   uint4* s_run = reinterpret_cast<uint4*>(s_in + 2 * kTlTile);       // [256]: start, plen, dst_a, dst_b
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_run + 256);        // [258]: buckets, total, dummy
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_run + 256);        // [258]: bucket totals -> starts
   uint32_t* s_page = s_cnt + 258;
   uint32_t* s_fill = s_page + 258;
   uint32_t* s_np = s_fill + 258;
+  // rank counters, replica-major [kTlRep][258].  A tile whose predecessor had
+  // a hot bucket (> 1/8 of the tile) spreads every bucket's atomics over
+  // kTlRep lane replicas (same-address atomics serialise: skewed keys, cfg3's
+  // Zipf half); otherwise all lanes use replica 0, the plain layout.
+  uint32_t* s_rep = s_np + 258;
+  const uint32_t lane_rep = threadIdx.x & (kTlRep - 1);
+  uint32_t rmask = 0;  // 0: one counter per bucket; kTlRep-1: replicas
   __shared__ uint32_t s_scan[kTlThreads / 32];
   __shared__ uint32_t s_next;
   __shared__ __align__(8) unsigned long long s_bar[2];
@@ -398,6 +407,7 @@ __global__ void __launch_bounds__(kTlThreads, page_tma_min_blocks<Map>())
   const uint32_t page0 = blockIdx.x * t.pages_per_cta;
   uint16_t* my_pages = pages + (uint64_t)page0 * kPage;
   const uint32_t full_tiles = static_cast<uint32_t>(n / kTlTile);
+  for (uint32_t i = threadIdx.x; i < 258 * kTlRep; i += kTlThreads) s_rep[i] = 0;
   if (threadIdx.x < 258) {
     s_cnt[threadIdx.x] = 0;
     s_page[threadIdx.x] = 0xffffffffu;
@@ -445,6 +455,8 @@ __global__ void __launch_bounds__(kTlThreads, page_tma_min_blocks<Map>())
       }
     }
     uint32_t pk[kTlPerThread], lo2[kTlPerThread / 2];
+    const uint32_t prev_mask = rmask;  // this tile's replica mask (rmask is updated for the next tile below)
+    uint32_t* const my_cnt = s_rep + (lane_rep & rmask) * 258;  // this lane's counters for this tile
     // bucket = floor(cell / S) as one 32-bit high product (magic < 2^32,
     // shift >= 32); keys outside the grid count in the dummy bin B+1 and
     // raise the overflow flag through the running max (checked at the end)
@@ -476,7 +488,7 @@ __global__ void __launch_bounds__(kTlThreads, page_tma_min_blocks<Map>())
         }
         const uint32_t bk = __umulhi(kk, magic32) >> shift32;
         const uint32_t b = ing ? bk : dummy;
-        pk[j] = (b << 16) | atomicAdd(&s_cnt[b], 1u);
+        pk[j] = (b << 16) | atomicAdd(&my_cnt[b], 1u);
         const uint32_t l = (kk - bk * t.S) & 0xffffu;
         if (j & 1) lo2[j >> 1] |= l << 16;
         else lo2[j >> 1] = l;
@@ -490,7 +502,14 @@ __global__ void __launch_bounds__(kTlThreads, page_tma_min_blocks<Map>())
     // run and every page split stays 16-byte aligned for the bulk stores.
     uint16_t* stage = reinterpret_cast<uint16_t*>(s_in + buf * kTlTile);  // the tile was consumed above
     const uint32_t b = threadIdx.x;
-    const uint32_t len = b < B ? s_cnt[b] : 0u;
+    // the bucket's length: its replica counts summed
+    uint32_t len = 0;
+    if (b < B) {
+      len = s_rep[b];
+      if (rmask)
+#pragma unroll
+        for (int r = 1; r < kTlRep; ++r) len += s_rep[r * 258 + b];
+    }
     const uint32_t plen = (len + 7) & ~7u;
     {
       uint32_t start;
@@ -537,14 +556,28 @@ __global__ void __launch_bounds__(kTlThreads, page_tma_min_blocks<Map>())
         s_run[b] = make_uint4(start, plen, pa * kPage + fa, pb * kPage);
         for (uint32_t r = len; r < plen; ++r) stage[start + r] = kPagePad;
       }
+      if (b < B) {  // replica counts become staging positions (exclusive, from the run start)
+        if (rmask) {
+          uint32_t run = start;
+#pragma unroll
+          for (int r = 0; r < kTlRep; ++r) {
+            const uint32_t v = s_rep[r * 258 + b];
+            s_rep[r * 258 + b] = run;
+            run += v;
+          }
+        } else {
+          s_rep[b] = start;
+        }
+      }
       __syncwarp();
       if (b < B) s_cnt[b] = start;
     }
-    __syncthreads();
+    // the next tile spreads its atomics if this one had a hot bucket
+    rmask = __syncthreads_or(b < B && len > kTlTile / 8) ? kTlRep - 1 : 0u;
     {  // branch-free: all 16 run starts are read up front (the dummy bin's counter is a valid read)
       uint32_t pos[kTlPerThread];
 #pragma unroll
-      for (int j = 0; j < kTlPerThread; ++j) pos[j] = s_cnt[pk[j] >> 16] + (pk[j] & 0xffffu);
+      for (int j = 0; j < kTlPerThread; ++j) pos[j] = my_cnt[pk[j] >> 16] + (pk[j] & 0xffffu);
 #pragma unroll
       for (int j = 0; j < kTlPerThread; ++j)
         if ((pk[j] >> 16) != dummy) stage[pos[j]] = static_cast<uint16_t>(lo2[j >> 1] >> ((j & 1) * 16));
@@ -553,7 +586,7 @@ __global__ void __launch_bounds__(kTlThreads, page_tma_min_blocks<Map>())
     __syncthreads();
     // every read of the counters is behind the barrier above: clear them for
     // the next tile (its atomics come after the barrier closing this tile)
-    for (uint32_t i = threadIdx.x; i < B + 2; i += kTlThreads) s_cnt[i] = 0;
+    for (uint32_t i = threadIdx.x; i < 258 * (prev_mask + 1); i += kTlThreads) s_rep[i] = 0;
     if (b < B && len) {  // the run, as one or two TMA bulk stores
       const uint4 r = s_run[b];  // start, plen, dst_a, dst_b
       const uint32_t thr = kPage - (r.z & (kPage - 1));
