@@ -555,12 +555,6 @@ struct StrTable {
   uint32_t radix;
 };
 
-struct MapStr {
-  using In = uint8_t;  // not used for vector loads
-  const uint8_t* recs;
-  uint32_t width, digits, radix;
-  const uint16_t* ord;  // device table
-};
 
 __global__ void __launch_bounds__(kThreads) k_str_keys(const uint8_t* __restrict__ recs, uint64_t n,
                                                        uint32_t width, uint32_t digits,

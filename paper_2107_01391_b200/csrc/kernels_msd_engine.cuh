@@ -17,10 +17,16 @@
 //   k_msd_classify each (segment, digit) run becomes a leaf or a segment
 //                  of the next level
 // Leaves (no key leaves its final position again):
-//   k_leaf_grid    dense leaves (remaining bits <= 16): the recombinant
-//                  step itself — a shared-memory count grid over the
-//                  remaining 2^bits cells, scan, run-length emit         R + W
-//   k_leaf_bitonic small sparse leaves (<= 2048 keys): shared bitonic sort R + W
+//   k_leaf_grid    dense leaves (remaining bits <= 16, occupancy >= 1/16):
+//                  the recombinant step itself — a shared-memory count grid
+//                  over the remaining 2^bits cells, counts -> offsets, a
+//                  counting-sort scatter through shared memory (run-length
+//                  emit for segments too large to stage)                 R + W
+//   k_leaf_radix   mid-size leaves (<= 4096 keys, <= 24 remaining bits):
+//                  stable 8-bit LSD passes in shared memory               R + W
+//   k_leaf_warp    tiny leaves (<= 32 keys): register bitonic network    R + W
+//   k_leaf_bitonic small leaves of the last digit (<= 2048 keys)         R + W
+//   k_leaf_copy    single keys / exhausted digits                        R + W
 #pragma once
 
 #include <cuda_runtime.h>
@@ -37,7 +43,6 @@ namespace rsb {
 
 constexpr int kMsdDigitBits = 8;
 constexpr int kMsdBins = 1 << kMsdDigitBits;
-constexpr int kMsdTile = 8192;          // largest scatter tile
 // keys per scatter tile: 32-bit keys 8192 (128-byte digit runs), 64-bit keys
 // 4096 (the 64-bit register tile already costs ~120 registers at 4096)
 template <class K>
@@ -66,7 +71,7 @@ struct LoadKeys {
   const K* p;
   unsigned long long n_total;  // readable elements at p (bulk copies never read past them)
   __device__ __forceinline__ K operator()(unsigned long long i) const { return __ldcs(p + i); }
-  // A tile of up to kMsdTile keys at a: 16-byte vectors when a is aligned
+  // A tile of up to kTile keys at a: 16-byte vectors when a is aligned
   // (thread t takes elements 4t..4t+3 of each 1024-element quarter), else
   // element j*256+t.  Order inside a tile is irrelevant to the partition.
   static constexpr int kTile = msd_tile<K>();
@@ -727,49 +732,9 @@ __global__ void __launch_bounds__(kLeafRadixThreads) k_leaf_radix(const K* __res
 }
 
 // ------------------------------------------------------------- report
-// Single-grid report for packed string keys: row = first
-// ordinal; span = last - first suffix (in base `radix`) within the row.
-__device__ __forceinline__ unsigned long long packed_to_radix(unsigned long long key, uint32_t width, uint32_t w,
-                                                              uint32_t radix) {
-  // key holds `width` 5-bit ordinals; the reference key uses the first w
-  unsigned long long v = 0;
-  for (uint32_t j = 0; j < w; ++j) v = v * radix + ((key >> (5 * (width - 1 - j))) & 31u);
-  return v;
-}
-
-__global__ void k_report_packed(const unsigned long long* __restrict__ sorted, uint64_t n, uint32_t width, uint32_t w,
-                                uint32_t radix, DevStats* st) {
-  unsigned long long span = 0;
-  const unsigned long long mod = d_pow(radix, w - 1);
-  for (uint32_t r = threadIdx.x; r < radix; r += blockDim.x) {
-    // keys with first ordinal r: [r << 5(width-1), (r+1) << 5(width-1))
-    const unsigned long long lo_key = (unsigned long long)r << (5 * (width - 1));
-    const unsigned long long hi_key = (unsigned long long)(r + 1) << (5 * (width - 1));
-    uint64_t a = 0, b = n;
-    while (a < b) {
-      const uint64_t mid = (a + b) >> 1;
-      if (sorted[mid] >= lo_key) b = mid;
-      else a = mid + 1;
-    }
-    uint64_t c = a, e = n;
-    while (c < e) {
-      const uint64_t mid = (c + e) >> 1;
-      if (sorted[mid] >= hi_key) e = mid;
-      else c = mid + 1;
-    }
-    if (a < c)
-      span += packed_to_radix(sorted[c - 1], width, w, radix) % mod -
-              packed_to_radix(sorted[a], width, w, radix) % mod + 1;
-  }
-  for (int o = 16; o > 0; o >>= 1) span += __shfl_xor_sync(0xffffffffu, span, o);
-  if (threadIdx.x == 0) {
-    st->cells_traversed = span;
-    st->report_digits = w;
-  }
-}
-
-// Same report read directly off sorted fixed-width records: row = ordinal of
-// the first byte, suffix = base-radix value of bytes 1..w-1 (pad = 0).
+// Single-grid report read directly off the sorted
+// fixed-width records: row = ordinal of the first byte, suffix = base-radix
+// value of bytes 1..w-1 (pad = 0).
 __device__ __forceinline__ uint32_t rec_ord(const uint8_t* r, uint32_t j, uint32_t width, const uint16_t* ord) {
   for (uint32_t q = 0; q < j; ++q)
     if (r[q] == 0) return 0;
