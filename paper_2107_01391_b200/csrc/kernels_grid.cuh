@@ -188,17 +188,18 @@ struct MapF64 {
     const double err = fma(x, P, -p);
     double f = floor(p);
     f = (p == f && err < 0.0) ? f - 1.0 : f;
-    const unsigned long long m = static_cast<unsigned long long>(bad ? 0.0 : f);
     const double fr = p - f;
     const bool near_int = fr < 0.02 || fr > 0.98;
     const bool near_half = fr > 0.48 && fr < 0.52;
-    const unsigned long long c = fr < 0.5 ? m : m + 1;
-    const double cv = near_int ? static_cast<double>(c) : static_cast<double>(2 * m + 1);
+    // candidates in double (exact: f < 2^53 / 100): nearest integer, or the half-integer 2f+1 over 2P
+    const double ci = fr < 0.5 ? f : f + 1.0;
+    const double cv = near_int ? ci : 2.0 * f + 1.0;
     const double dv = near_int ? P : P2;
     const int q = x == 0.0 ? 1 : ((near_int || near_half) ? quotient_is(x, cv, dv) : 0);  // 0 maps to 0
     undecided = bad || q < 0;
     const bool up = fr > 0.5 || (fr == 0.5 && err > 0.0);
-    return q > 0 ? (near_int ? c : m + 1) : (up ? m + 1 : m);
+    const double r = q > 0 ? (near_int ? ci : f + 1.0) : (up ? f + 1.0 : f);
+    return static_cast<unsigned long long>(bad ? 0.0 : r);  // one conversion
   }
 };
 
