@@ -194,6 +194,7 @@ unsigned long long device_max(Workspace& ws, const typename Map::In* in, uint64_
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
 
 // Exclusive scan of `count` uint32 values (decoupled look-back); the grand
 // total lands in *total (device).
@@ -966,7 +967,7 @@ rs_status rs_sort_u32(const uint32_t* keys, uint64_t n, uint32_t* out, uint64_t 
 rs_status rs_sort_i64(const int64_t* values, uint64_t n, int64_t* out, uint64_t out_capacity,
                       const rs_options* opt, rs_report* report, void* stream) {
   return guarded([&] {
-    OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned16(out)};
+    OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned32(out)};
     integer_sort(values, n, MapI64{}, o, reinterpret_cast<const uint64_t*>(out), out_capacity, opt,
                  report, static_cast<cudaStream_t>(stream), 19);
   });
@@ -987,7 +988,7 @@ rs_status rs_sort_keys(const uint64_t* keys, uint64_t n, rs_key_spec spec, uint6
     }
     if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
-    OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned16(out)};
+    OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned32(out)};
     grid_sort(ws, reinterpret_cast<const unsigned long long*>(keys), n, MapU64{}, cells, o, out,
               spec.radix, spec.total_digits, 0);
     if (ws.h_stats->overflow)
@@ -1021,7 +1022,7 @@ rs_status rs_sort_f64(const double* x, uint64_t n, uint32_t scale, uint64_t* out
     }
     make_key_spec(10, total, total - scale, budget);
     if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
-    OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned16(out)};
+    OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned32(out)};
     grid_sort(ws, x, n, map, pow10u(total), o, out, 10, 0, scale);
     check_flags(ws.h_stats->flags);
     if (ws.h_stats->overflow) {
@@ -1355,7 +1356,7 @@ rs_status rs_sort_decimal_strings(const char* chars, const uint64_t* offsets, ui
       k_dec_scale<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(mant, own, n, scale);
       RS_LAUNCH_CHECK();
     }
-    OutU64 o{reinterpret_cast<unsigned long long*>(keys_out), 0ull, aligned16(keys_out)};
+    OutU64 o{reinterpret_cast<unsigned long long*>(keys_out), 0ull, aligned32(keys_out)};
     grid_sort(ws, mant, n, MapU64{}, checked_pow(10, lambda + scale), o, keys_out, 10, lambda + scale, 0);
     if (report) *report = rs_report{n, ws.h_stats->cells_traversed, spec};
   });

@@ -599,24 +599,29 @@ struct OutU32 {
   }
 };
 
+// 256-bit streaming store of four 64-bit values (sm_100: STG.E.EF.ENL2.256);
+// p must be 32-byte aligned.
+__device__ __forceinline__ void st_cs_v4_b64(unsigned long long* p, unsigned long long a, unsigned long long b,
+                                             unsigned long long c, unsigned long long d) {
+  asm volatile("st.global.cs.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+
 struct OutU64 {
   static constexpr int kWordBytes = 8;
   unsigned long long* out;
   unsigned long long base;
-  bool aligned;
+  bool aligned;  // 32-byte aligned: positions 4k take one 256-bit store
   __device__ __forceinline__ void put1(uint64_t p, uint32_t c) const { out[p] = c + base; }
   __device__ __forceinline__ void put4_full(uint64_t p, const uint32_t (&c)[4]) const {
     if (aligned) {
-      __stcs(reinterpret_cast<ulonglong2*>(out + p), make_ulonglong2(c[0] + base, c[1] + base));
-      __stcs(reinterpret_cast<ulonglong2*>(out + p + 2), make_ulonglong2(c[2] + base, c[3] + base));
+      st_cs_v4_b64(out + p, c[0] + base, c[1] + base, c[2] + base, c[3] + base);
     } else {
       for (int e = 0; e < 4; ++e) out[p + e] = c[e] + base;
     }
   }
   __device__ __forceinline__ void put4(uint64_t p, const uint32_t (&c)[4], uint64_t end) const {
     if (aligned && p + 4 <= end) {
-      __stcs(reinterpret_cast<ulonglong2*>(out + p), make_ulonglong2(c[0] + base, c[1] + base));
-      __stcs(reinterpret_cast<ulonglong2*>(out + p + 2), make_ulonglong2(c[2] + base, c[3] + base));
+      st_cs_v4_b64(out + p, c[0] + base, c[1] + base, c[2] + base, c[3] + base);
     } else {
       for (int e = 0; e < 4; ++e)
         if (p + e < end) out[p + e] = c[e] + base;
