@@ -520,7 +520,16 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   if (lane == 31) s_scan[warp] = inc;
   __syncthreads();
   uint32_t run = inc - sum;
-  for (int w = 0; w < warp; ++w) run += s_scan[w];
+  {  // exclusive prefix of the 32 warp totals: one load and a warp scan, not a 31-step loop
+    const uint32_t t = s_scan[lane];
+    uint32_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    run += __shfl_sync(0xffffffffu, ti - t, warp);
+  }
   if (scatter) {
     for (uint32_t j = 0; j < per; ++j) {  // counts -> exclusive offsets (< 65536: no carry between halves)
       const uint32_t w = w0 + j;
