@@ -288,8 +288,9 @@ def main():
         "clocks": clk.summary(),
     }
 
-    if rank == 0 and not use_dist:
-        # per-pass device time with CUDA events on the library's stream
+    if rank == 0 or use_dist:
+        # per-pass device time with CUDA events on the library's stream (every
+        # rank runs the steps: the sharded step has collectives; rank 0 reports)
         lib.rs_profile_enable(1)
         lib.rs_profile_reset()
         for _ in range(args.steps):
@@ -326,7 +327,41 @@ def main():
                               "algorithmic_bytes": algo_bytes[dom], "peak_source": peak_src,
                               "step_frac": (8 * n) / (ms / 1e3) / 1e9 / peak}
 
-        if not args.no_kv:
+        if use_dist and not args.no_e2e:
+            # end to end at N GPUs through the multi-GPU API: each rank copies
+            # its pinned shard in, sorts (count, all-reduce, own cell range)
+            # and reads its slice of the global order back; max over ranks
+            h_in = torch.empty(n, dtype=torch.int32, pin_memory=True)
+            h_in.copy_(keys.cpu())
+            h_out = torch.empty(2 * n, dtype=torch.int32, pin_memory=True)  # a rank's slice: ~n (+ one cell)
+            dev = torch.empty_like(keys)
+            got = {}
+
+            def e2e_step_dist():
+                dev.copy_(h_in, non_blocking=True)
+                res = rsd.sharded_grid_sort(dev, KEY_BOUND)
+                m = min(res.numel(), h_out.numel())
+                h_out[:m].copy_(res[:m], non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                got["out"] = h_out[:m]
+                got["bytes"] = m * 4
+
+            e2e_step_dist()
+            reps = max(3, args.steps // 2)
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                e2e_step_dist()
+            torch.cuda.synchronize()
+            t = torch.tensor([(time.perf_counter() - t0) / reps], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+            result["e2e"] = {"value": n * world / dt / 1e9, "unit": "Gkeys/s", "h2d_bytes_per_step": 4 * n,
+                             "d2h_bytes_per_step": got["bytes"], "ms_per_step": dt * 1e3,
+                             "api": "dist.sharded_grid_sort (pinned shard in, own slice out)",
+                             "checked": bool((got["out"][1:] >= got["out"][:-1]).all())}
+        if not args.no_kv and not use_dist:
             vals = torch.empty_like(keys)
             rs._check(lib.rs_gen_iota_u32(0, n, rs._ptr(vals), stream()))
             ko, vo = torch.empty_like(keys), torch.empty_like(keys)
@@ -349,7 +384,7 @@ def main():
                             "workload": "cfg2 key/value: uint32 payload = original index, stable"}
             del vals, ko, vo
 
-        if not args.no_e2e:
+        if not args.no_e2e and not use_dist:
             h_in = torch.empty(n, dtype=torch.int32, pin_memory=True)
             h_out = torch.empty(n, dtype=torch.int32, pin_memory=True)
             h_in.copy_(keys.cpu())
@@ -367,7 +402,7 @@ def main():
             result["e2e"] = {"value": n / dt / 1e9, "unit": "Gkeys/s", "h2d_bytes_per_step": 4 * n,
                              "d2h_bytes_per_step": 4 * n, "ms_per_step": dt * 1e3, "api": "rs_sort_u32_host",
                              "checked": ok}
-        if not args.no_cpu:
+        if not args.no_cpu and rank == 0 and not use_dist:
             result["cpu_baseline"] = cpu_baseline_sample()
 
     if rank == 0:
