@@ -83,7 +83,7 @@ class GpuOps:
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
     def count(self, keys: torch.Tensor, cells: int) -> torch.Tensor:
-        counts = torch.zeros(cells, dtype=torch.int32, device=keys.device)
+        counts = torch.empty(cells, dtype=torch.int32, device=keys.device)  # rs_count_u32 overwrites it
         self._check(self._lib().rs_count_u32(ctypes.c_void_p(keys.data_ptr()), keys.numel(),
                                              ctypes.c_void_p(counts.data_ptr()), cells, None, self._stream()))
         return counts
