@@ -130,13 +130,16 @@ def sort_u32_kv(keys, vals, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits:
     return ko, vo, _report(rep)
 
 
-def sort_i64(values, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits: int = 0):
+def sort_i64(values, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits: int = 0, msd: bool = False):
+    """sort_integers for non-negative int64 values in a CUDA tensor.  With
+    ``msd=True`` a key space above ``max_cells`` is split by MSD bucket passes
+    over the values' bit width."""
     torch = _torch()
     values = _cuda_tensor(values, (torch.int64,), "values")
     out = torch.empty_like(values)
     rep = RsReport()
     _check(_lib.load().rs_sort_i64(_ptr(values), values.numel(), _ptr(out), out.numel(),
-                                   ctypes.byref(_opts(max_cells, key_digits)), ctypes.byref(rep), _stream()))
+                                   ctypes.byref(_opts(max_cells, key_digits, msd)), ctypes.byref(rep), _stream()))
     return out, _report(rep)
 
 

@@ -421,14 +421,15 @@ void grid_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, u
 
 uint64_t pow10u(uint32_t e) { return checked_pow(10, e); }
 
-void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t* out);
+void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t* out, uint32_t key_bits);
+void msd_i64_entry(Workspace& ws, const int64_t* in, uint64_t n, const uint64_t* out, uint32_t key_bits);
 
 // Shared driver for the decimal-integer paths (u32 and i64).
 template <class Map, class Out, class K>
 void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, const K* sorted,
                   uint64_t out_capacity, const rs_options* opt, rs_report* report,
                   cudaStream_t stream, uint32_t max_digits,
-                  void (*msd_u32)(Workspace&, const typename Map::In*, uint64_t, const K*) = nullptr) {
+                  void (*msd_u32)(Workspace&, const typename Map::In*, uint64_t, const K*, uint32_t) = nullptr) {
   ensure_device();
   const uint64_t budget = budget_of(opt);
   if (n > 0 && (!in || !sorted)) fail(RS_INVALID_ARGUMENT, "null device pointer");
@@ -441,17 +442,22 @@ void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, cons
   const uint32_t hint = opt ? opt->key_digits : 0;
   const bool hinted = hint >= 1 && hint <= max_digits && pow10u(hint) <= budget;
   uint32_t digits = hint;
-  // a declared width already above the budget goes to the MSD path without
-  // the max pass (the MSD sort does not need the geometry up front)
+  // a declared width already above the budget goes to the 32-bit MSD path
+  // without the max pass (the MSD sort does not need the geometry up front;
+  // int64 input keeps the pass, it rejects negative values)
   const bool msd_declared = msd_u32 && opt && opt->msd && hint >= 1 && hint <= max_digits &&
-                            pow10u(hint) > budget;
+                            pow10u(hint) > budget && sizeof(typename Map::In) == 4;
+  uint32_t key_bits = 8 * sizeof(typename Map::In);
   if (!hinted && !msd_declared) {
-    digits = digit_count(device_max(ws, in, n, map));
+    const unsigned long long mx = device_max(ws, in, n, map);
+    digits = digit_count(mx);
+    key_bits = 1;  // MSD digits cover the max's bit width only
+    while (key_bits < 64 && (mx >> key_bits)) ++key_bits;
   }
   if (msd_u32 && opt && opt->msd && pow10u(digits) > budget) {
     // wide keys: MSD bucket passes + per-bucket grids
     if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
-    msd_u32(ws, in, n, sorted);
+    msd_u32(ws, in, n, sorted, key_bits);
     const uint32_t d = static_cast<uint32_t>(ws.h_stats->report_digits);
     if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{10, d, d}};
     return;
@@ -829,12 +835,26 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
     shift = shift > kMsdDigitBits ? shift - kMsdDigitBits : 0;
   }
 }
-void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t* out) {
+void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t* out, uint32_t key_bits) {
   reset_stats(ws);
-  msd_sort(ws, LoadKeys<uint32_t>{in, n}, n, 32, EmitKey<uint32_t>{const_cast<uint32_t*>(out)});
+  msd_sort(ws, LoadKeys<uint32_t>{in, n}, n, key_bits, EmitKey<uint32_t>{const_cast<uint32_t*>(out)});
   {
     PassTimer pt_(RS_PASS_REPORT, ws.stream);
     k_report<uint32_t><<<1, report_threads(10), 0, ws.stream>>>(out, n, 10, 0, 0, 0, ws.stats);
+    RS_LAUNCH_CHECK();
+  }
+  pull_stats(ws);
+}
+
+// int64 input (non-negative, checked by the max pass): the same engine over
+// 64-bit keys, digits over the max's bit width
+void msd_i64_entry(Workspace& ws, const int64_t* in, uint64_t n, const uint64_t* out, uint32_t key_bits) {
+  reset_stats(ws);
+  msd_sort(ws, LoadKeys<uint64_t>{reinterpret_cast<const uint64_t*>(in), n}, n, key_bits,
+           EmitKey<uint64_t>{const_cast<uint64_t*>(out)});
+  {
+    PassTimer pt_(RS_PASS_REPORT, ws.stream);
+    k_report<uint64_t><<<1, report_threads(10), 0, ws.stream>>>(out, n, 10, 0, 0, 0, ws.stats);
     RS_LAUNCH_CHECK();
   }
   pull_stats(ws);
@@ -969,7 +989,7 @@ rs_status rs_sort_i64(const int64_t* values, uint64_t n, int64_t* out, uint64_t 
   return guarded([&] {
     OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned32(out)};
     integer_sort(values, n, MapI64{}, o, reinterpret_cast<const uint64_t*>(out), out_capacity, opt,
-                 report, static_cast<cudaStream_t>(stream), 19);
+                 report, static_cast<cudaStream_t>(stream), 19, &msd_i64_entry);
   });
 }
 

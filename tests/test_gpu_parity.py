@@ -359,6 +359,44 @@ def test_msd_u32_skew_and_duplicates(rs, oracle):
     assert np.array_equal(_np_u32(out), np.sort(keys))
 
 
+@pytest.mark.parametrize("n,bits", [(1 << 22, 63), (300_001, 40), (1 << 20, 33), (4097, 63), (1, 63)])
+def test_msd_i64_vs_oracle(rs, oracle, n, bits):
+    """int64 values past any grid budget: MSD digits over the max's bit width
+    (A17 for the integer facade); report as the reference would compute it
+    with an unlimited budget."""
+    import torch
+
+    rng = np.random.default_rng(bits * 7 + n)
+    vals = rng.integers(0, 1 << bits, n, dtype=np.int64)
+    if n > 100:
+        vals[rng.random(n) < 0.3] = vals[0]  # one heavy value
+    want = np.sort(vals)
+    out, rep = rs.sort_i64(torch.from_numpy(vals).cuda(), msd=True)
+    assert np.array_equal(out.cpu().numpy(), want)
+    d = len(str(int(want[-1])))
+    assert _rep(rep) == oracle.report_from_sorted(want.astype(np.uint64), 10, d)
+
+
+def test_msd_i64_rejects_negative(rs):
+    import torch
+
+    vals = torch.tensor([5, 10**15, -1, 3], dtype=torch.int64, device="cuda")
+    with pytest.raises(rs.Error) as e:
+        rs.sort_i64(vals, msd=True)
+    assert e.value.code == "negative_value"
+
+
+@pytest.mark.parametrize("bound", [1 << 21, 12_000_000, (1 << 27) + 5])
+def test_msd_u32_narrow_keys(rs, oracle, bound):
+    """Keys above the budget but well below 2^32: the MSD levels start at the
+    max's bit width (21, 24 and 28 bits here)."""
+    keys = oracle.gen_u32(oracle.config_seed(5), 1, 1 << 21, bound)
+    out, rep = rs.sort_u32(_t(keys.view(np.int32)), msd=True)
+    want = np.sort(keys)
+    assert np.array_equal(_np_u32(out), want)
+    assert _rep(rep) == oracle.report_from_sorted(want.astype(np.uint64), 10, len(str(int(want[-1]))))
+
+
 def test_msd_count_grid_leaf_modes(rs, oracle):
     """16-bit count-grid leaves on both sides of the shared-memory staging
     capacity (~50K keys: scatter below, run-length emit above), a segment at
