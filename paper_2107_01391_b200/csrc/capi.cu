@@ -531,7 +531,7 @@ void kv_sort(Workspace& ws, const uint32_t* keys, const uint32_t* vals, uint64_t
     {
       PassTimer pt_(RS_PASS_KV_HIST, ws.stream);
       RS_CUDA(cudaMemsetAsync(hist, 0, bg * sizeof(uint32_t), ws.stream));
-      k_kv_chunk_hist<<<p.G * kKvHistSplit, kKvThreads, 0, ws.stream>>>(sk, n, p, aligned16(sk), hist, ws.stats);
+      k_kv_chunk_hist<<<p.G * kKvHistSplit, kKvHistThreads, 0, ws.stream>>>(sk, n, p, aligned16(sk), hist, ws.stats);
       RS_LAUNCH_CHECK();
     }
     exscan_u32(ws, hist, bg, off, total);

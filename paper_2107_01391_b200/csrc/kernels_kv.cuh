@@ -35,6 +35,7 @@ namespace rsb {
 constexpr int kKvThreads = 256;
 constexpr int kKvItems = 16;                    // records per thread per tile
 constexpr int kKvTile = kKvThreads * kKvItems;  // 4096 records
+constexpr int kKvHistThreads = 256;             // histogram CTA: 4 x 1024-key quarters per tile
 constexpr int kKvBins = 100;                    // two decimal digits
 constexpr int kKvBits = 7;                      // 100 < 2^7
 constexpr int kKvMaxPasses = 5;                 // 10-digit uint32 keys
@@ -49,11 +50,14 @@ struct KvPass {
   uint32_t G;                     // CTAs
 };
 
+// 32-bit high products (magic < 2^32, shift >= 32, exact for every uint32;
+// capi.cu div_magic32); shift 0 = divisor 1, shift 64 = 64-bit fallback
 __device__ __forceinline__ uint32_t kv_digit(uint32_t key, const KvPass& p) {
-  const uint32_t q = p.shift_div == 64
-                         ? static_cast<uint32_t>(__umul64hi(static_cast<unsigned long long>(key), p.magic_div))
-                         : static_cast<uint32_t>((static_cast<unsigned long long>(key) * p.magic_div) >> p.shift_div);
-  return q - 100u * static_cast<uint32_t>((static_cast<unsigned long long>(q) * p.magic_1000) >> p.shift_1000);
+  uint32_t q;
+  if (p.shift_div == 64) q = static_cast<uint32_t>(__umul64hi(static_cast<unsigned long long>(key), p.magic_div));
+  else if (p.shift_div == 0) q = key;
+  else q = __umulhi(key, static_cast<uint32_t>(p.magic_div)) >> (p.shift_div - 32);
+  return q - 100u * (__umulhi(q, static_cast<uint32_t>(p.magic_1000)) >> (p.shift_1000 - 32));
 }
 
 // grid = G x kKvHistSplit: CTA (c, s) counts sub-range s of chunk c and adds
@@ -71,35 +75,34 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __
   const uint64_t cend = (uint64_t)c * p.chunk + p.chunk < n ? (uint64_t)c * p.chunk + p.chunk : n;
   const uint64_t c0 = (uint64_t)c * p.chunk + sub * span;
   const uint64_t c1 = sub + 1 == kKvHistSplit ? cend : (c0 + span < cend ? c0 + span : cend);
-  unsigned long long mx = 0;
-  for (uint64_t base = c0; base < c1; base += kKvTile) {
+  uint32_t mx = 0;
+  uint64_t base = c0;
+  if (aligned) {  // whole tiles: 4 vectors in flight per thread, no bounds checks
+    for (; base + kKvTile <= c1; base += kKvTile) {
+      uint4 w[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint64_t i0 = base + q * 1024 + threadIdx.x * 4;
-      uint32_t v[4];
-      if (aligned && i0 + 4 <= c1) {
-        const uint4 w = __ldcs(reinterpret_cast<const uint4*>(keys + i0));
-        v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
-      } else {
-        for (int e = 0; e < 4; ++e) v[e] = i0 + e < c1 ? keys[i0 + e] : 0u;
-      }
+      for (int q = 0; q < 4; ++q) w[q] = __ldcs(reinterpret_cast<const uint4*>(keys + base + q * 1024 + threadIdx.x * 4));
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (i0 + e < c1) {
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t v[4] = {w[q].x, w[q].y, w[q].z, w[q].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
           mx = v[e] > mx ? v[e] : mx;
           atomicAdd(&s_h[kv_digit(v[e], p)], 1u);
         }
       }
     }
   }
+  for (uint64_t i = base + threadIdx.x; i < c1; i += blockDim.x) {
+    const uint32_t v = keys[i];
+    mx = v > mx ? v : mx;
+    atomicAdd(&s_h[kv_digit(v, p)], 1u);
+  }
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < p.bins; b += blockDim.x)
     if (s_h[b]) atomicAdd(&hist[(uint64_t)b * p.G + c], s_h[b]);
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long w = __shfl_xor_sync(0xffffffffu, mx, o);
-    mx = w > mx ? w : mx;
-  }
-  if ((threadIdx.x & 31) == 0 && mx) atomicMax(&st->max_key, mx);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(&st->max_key, static_cast<unsigned long long>(mx));
 }
 
 // Shared layout: two input buffers of one tile (keys then values, 32 KB
@@ -154,13 +157,14 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
   for (uint64_t t0 = c0; t0 < c1; t0 += kKvTile, buf ^= 1) {
     const uint64_t nt = t0 + kKvTile;
     if (threadIdx.x == 0 && nt < c1 && full_tile(nt)) issue(nt, buf ^ 1);
+    const bool full = full_tile(t0);  // block-uniform
     uint32_t* in_k = s_in + buf * 2 * kKvTile;
     uint32_t* in_v = in_k + kKvTile;
     // striped order: record t0 + warp*512 + j*32 + lane (input order =
     // warp-major, then j, then lane)
     uint32_t k[kKvItems], v[kKvItems], rank[kKvItems];
     uint32_t d[kKvItems];
-    if (full_tile(t0)) {
+    if (full) {
       mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
       phase ^= 1u << buf;
 #pragma unroll
@@ -183,8 +187,8 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
     // stable warp ranks: peers = lanes with the same digit, from 7 ballots
 #pragma unroll
     for (int j = 0; j < kKvItems; ++j) {
-      const bool ok = d[j] != 0xffffu;
-      unsigned peers = __ballot_sync(0xffffffffu, ok);
+      const bool ok = full || d[j] != 0xffffu;
+      unsigned peers = full ? 0xffffffffu : __ballot_sync(0xffffffffu, ok);
 #pragma unroll
       for (int b = 0; b < kKvBits; ++b) {
         const bool bit = (d[j] >> b) & 1u;

@@ -7,6 +7,14 @@ and each rank then emits a contiguous range of cells holding about total/G
 keys (rs_emit_u32).  No key moves between GPUs: rank r's output is slice r
 of the globally sorted sequence.
 
+Stable key/value (cfg2 KV): the same all-reduced grid fixes the cell cuts;
+every rank sorts its shard stably (rs_sort_u32_kv), sends the records of
+cell range r to rank r (one all-to-all of keys and one of values) and sorts
+the concatenation of what it received — source ranks arrive in rank order,
+so equal keys keep their global input order (records of rank g' < g first,
+then the local order).  The reference's stable order (radix_sort_lsd_by,
+baselines.hpp:24-46) is unique, so the rank slices concatenate to it.
+
 Wide keys (cfg5): the leading-digit bucket histogram (rs_bucket_hist_u32) is
 all-reduced, G-1 splitters are cut on bucket boundaries, keys are range
 partitioned (rs_partition_u32) and exchanged with one all-to-all; every rank
@@ -111,6 +119,12 @@ class GpuOps:
                                                  parts, ctypes.c_void_p(out.data_ptr()), hc, self._stream()))
         return out, [int(c) for c in hc]
 
+    def sort_kv(self, keys: torch.Tensor, vals: torch.Tensor, cells: int) -> tuple[torch.Tensor, torch.Tensor]:
+        from . import DEFAULT_CELL_BUDGET, sort_u32_kv
+
+        k, v, _ = sort_u32_kv(keys, vals, max_cells=max(cells, DEFAULT_CELL_BUDGET))
+        return k, v
+
     def sort(self, keys: torch.Tensor, key_digits: int = 0) -> torch.Tensor:
         from . import sort_u32
 
@@ -132,6 +146,33 @@ def sharded_grid_sort(keys: torch.Tensor, cells: int, ops=None, group=None) -> t
     ends = torch.where(lo_hi > 0, prefix[(lo_hi - 1).clamp(min=0)], torch.zeros_like(lo_hi))
     lo, hi, n_out = (int(v) for v in torch.stack([lo_hi[0], lo_hi[1], ends[1] - ends[0]]).cpu())
     return ops.emit(counts, lo, hi, n_out)
+
+
+def sharded_kv_sort(keys: torch.Tensor, vals: torch.Tensor, cells: int, ops=None,
+                    group=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Stable key/value across ranks: local count -> all-reduce ->
+    cell cuts; local stable sort -> all-to-all by cell range -> stable sort of
+    the received runs (concatenated in source-rank order).  Rank g's shard must
+    be slice g of the global input; returns slice r of the global stable
+    order (cut on cell boundaries, as sharded_grid_sort)."""
+    ops = ops or GpuOps()
+    world = dist.get_world_size(group)
+    counts = ops.count(keys, cells)
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)  # C1
+    bounds = cell_bounds_device(torch.cumsum(counts, 0, dtype=torch.int64), world)
+    ks, vs = ops.sort_kv(keys, vals, cells)
+    # records of cell range r are the run [cut[r], cut[r+1]) of the sorted shard
+    cut = torch.searchsorted(ks.to(torch.int64), bounds)
+    send = cut[1:] - cut[:-1]
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    both = torch.stack([send, recv]).cpu()
+    send_counts, recv_counts = both[0].tolist(), both[1].tolist()
+    rk = torch.empty(sum(recv_counts), dtype=keys.dtype, device=keys.device)
+    rv = torch.empty(sum(recv_counts), dtype=vals.dtype, device=vals.device)
+    dist.all_to_all_single(rk, ks, output_split_sizes=recv_counts, input_split_sizes=send_counts, group=group)
+    dist.all_to_all_single(rv, vs, output_split_sizes=recv_counts, input_split_sizes=send_counts, group=group)
+    return ops.sort_kv(rk, rv, cells)
 
 
 def range_partition_sort(keys: torch.Tensor, divisor: int, buckets: int, ops=None, group=None,

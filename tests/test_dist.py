@@ -13,7 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2107_01391_b200.dist import bucket_splitters, cell_ranges, range_partition_sort, sharded_grid_sort
+from paper_2107_01391_b200.dist import (bucket_splitters, cell_ranges, range_partition_sort, sharded_grid_sort,
+                                        sharded_kv_sort)
 
 
 class NumpyOps:
@@ -38,6 +39,12 @@ class NumpyOps:
         order = np.argsort(part, kind="stable")
         return torch.from_numpy(keys.numpy()[order].copy()), np.bincount(part, minlength=len(bounds) - 1).tolist()
 
+    def sort_kv(self, keys, vals, cells):
+        k = keys.numpy().view(np.uint32)
+        assert k.size == 0 or int(k.max()) < cells
+        order = np.argsort(k, kind="stable")
+        return torch.from_numpy(keys.numpy()[order].copy()), torch.from_numpy(vals.numpy()[order].copy())
+
     def sort(self, keys, key_digits=0):
         return torch.from_numpy(np.sort(keys.numpy().view(np.uint32)).view(np.int32))
 
@@ -60,6 +67,9 @@ def _worker(rank, world, port, mode, shared):
         mine = keys[rank * n // world:(rank + 1) * n // world].clone()
         if mode == "grid":
             out = sharded_grid_sort(mine, shared["cells"], ops=NumpyOps())
+        elif mode == "kv":
+            vals = torch.arange(rank * n // world, (rank + 1) * n // world, dtype=torch.int32)
+            out = torch.stack(sharded_kv_sort(mine, vals, shared["cells"], ops=NumpyOps()))
         else:
             out = range_partition_sort(mine, shared["divisor"], shared["buckets"], ops=NumpyOps())
         torch.save(out, shared["dir"] + f"/out{rank}.pt")
@@ -124,3 +134,17 @@ def test_range_partition_sort_gloo(tmp_path):
     outs = _run("range", keys, tmp_path, divisor=10**7, buckets=430)
     got = np.concatenate([o.numpy().view(np.uint32) for o in outs])
     assert np.array_equal(got, np.sort(keys.numpy().view(np.uint32)))
+
+
+@pytest.mark.parametrize("bound", [1000, 10**5])
+def test_sharded_kv_sort_gloo_is_globally_stable(tmp_path, bound):
+    """Values are global input indices: the rank slices, concatenated, must be
+    the unique stable order (equal keys of rank 0's shard before rank 1's)."""
+    rng = np.random.default_rng(bound)
+    keys = rng.integers(0, bound, 150_001).astype(np.int32)
+    keys[rng.random(keys.size) < 0.2] = 7  # a hot cell spread over both shards
+    outs = _run("kv", torch.from_numpy(keys), tmp_path, cells=bound)
+    got = np.concatenate([o.numpy() for o in outs], axis=1)
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(got[0], keys[order])
+    assert np.array_equal(got[1], order.astype(np.int32))

@@ -478,16 +478,17 @@ def test_cfg5_full_size_properties(rs):
 
 # ------------------------------------- multi-GPU device phases (1-rank NCCL)
 def test_dist_paths_on_device_nccl(rs, oracle):
-    """The sharded-grid and range-partition orchestration of dist.py with the
-    real device phases (rs_count_u32 / rs_emit_u32 / rs_bucket_hist_u32 /
-    rs_partition_u32) over a one-rank NCCL group."""
+    """The sharded-grid, stable key/value and range-partition orchestration of
+    dist.py with the real device phases (rs_count_u32 / rs_emit_u32 /
+    rs_sort_u32_kv / rs_bucket_hist_u32 / rs_partition_u32) over a one-rank
+    NCCL group."""
     import os
     import socket
 
     import torch
     import torch.distributed as dist
 
-    from paper_2107_01391_b200.dist import range_partition_sort, sharded_grid_sort
+    from paper_2107_01391_b200.dist import range_partition_sort, sharded_grid_sort, sharded_kv_sort
 
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -502,6 +503,10 @@ def test_dist_paths_on_device_nccl(rs, oracle):
         wide = oracle.gen_u32(22, 0, 1 << 21, 0)
         out = range_partition_sort(_t(wide.view(np.int32)), 10**7, 430)
         assert np.array_equal(_np_u32(out), np.sort(wide))
+        vals = np.arange(keys.size, dtype=np.uint32)
+        ko, vo = sharded_kv_sort(_t(keys.view(np.int32)), _t(vals.view(np.int32)), 10**6)
+        wk, wv = oracle.radix_sort_lsd_kv(keys, vals)
+        assert np.array_equal(_np_u32(ko), wk) and np.array_equal(_np_u32(vo), wv)
     finally:
         dist.destroy_process_group()
 
