@@ -139,13 +139,25 @@ rs_status rs_sort_u32_kv(const uint32_t* keys, const uint32_t* vals, uint64_t n,
  * 135-158: shortest round-trip numeral rounded half-up), then KeySpec
  * {10, lambda+scale, lambda}, lambda = digits(max_mantissa / 10^scale)
  * (key_model.cpp:122-124).  Emits the sorted mantissas
- * (DecimalKeySortResult::keys, sort.hpp:19-23).  Exact (bit-identical to
- * the reference) on the domain x == 0 or 10^-(scale+3) < x with
- * x * 10^(scale+2) < 2^53, scale <= 15; any other finite value returns
- * RS_OUT_OF_RANGE (never a silent approximation). */
+ * (DecimalKeySortResult::keys, sort.hpp:19-23).  Bit-identical to the
+ * reference for every double (fast IEEE tests on the common domain, an exact
+ * shortest-numeral search elsewhere; kernels_f64.cuh).  Errors are the
+ * reference's for the first failing element in input order (non_finite,
+ * negative_value, cell_budget_exceeded); scale <= 40, and scale > 19 fails
+ * as the reference's 10^scale does.  The composition (per-element
+ * float_to_decimal, then the grid) is SURVEY 8c's cfg3 oracle. */
 rs_status rs_sort_f64(const double* x, uint64_t n, uint32_t scale,
                       uint64_t* mantissas_out, uint64_t out_capacity,
                       const rs_options* opt, rs_report* report, void* stream);
+
+/* float_to_decimal(x[i], scale).mantissa for every element (key_model.cpp:
+ * 135-158, DecimalValue::mantissa; the vectorised form of the reference's
+ * per-value call): shortest round-trip fixed numeral, rescaled to `scale`
+ * places (half up; an unchecked upscale wraps modulo 2^64 as in the
+ * reference).  The first failing element (input order) sets the status and
+ * the reference's message.  scale <= 40. */
+rs_status rs_float_to_decimal(const double* x, uint64_t n, uint32_t scale,
+                              uint64_t* mantissas_out, void* stream);
 
 /* sort_strings (sort.hpp:57-60, sort.cpp:61-77) over fixed-width records:
  * record i is chars[i*width .. i*width+width), its string ends at the first

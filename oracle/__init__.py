@@ -225,6 +225,7 @@ class Reference:
         L.ref_sort_keys_core.argtypes = [c_void_p, c_uint64, c_uint32, c_uint32, c_uint32, c_uint64, c_void_p,
                                          POINTER(RefReportC)]
         L.ref_float_to_decimal.argtypes = [c_double, c_uint32, POINTER(c_uint64)]
+        L.ref_float_to_decimal_many.argtypes = [c_void_p, c_uint64, c_uint32, c_void_p, c_void_p]
         L.ref_sort_f64.argtypes = [c_void_p, c_uint64, c_uint32, c_uint64, c_void_p, POINTER(RefReportC)]
         L.ref_sort_decimals.argtypes = [c_char_p, c_uint64, c_uint64, c_void_p, c_uint64, POINTER(RefReportC)]
         L.ref_sort_strings.argtypes = [c_void_p, c_uint64, c_uint32, c_char_p, c_uint64, c_void_p,
@@ -263,6 +264,19 @@ class Reference:
         m = c_uint64()
         st = self.L.ref_float_to_decimal(x, scale, ctypes.byref(m))
         return st, m.value
+
+    def float_to_decimal(self, x: float, scale: int) -> int:
+        m = c_uint64()
+        self._ok(self.L.ref_float_to_decimal(x, scale, ctypes.byref(m)))
+        return m.value
+
+    def float_to_decimal_many(self, x: np.ndarray, scale: int) -> tuple[np.ndarray, np.ndarray]:
+        """(mantissas, statuses) of float_to_decimal over every element."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        m = np.empty(x.size, dtype=np.uint64)
+        st = np.empty(x.size, dtype=np.int32)
+        self.L.ref_float_to_decimal_many(_p(x), x.size, scale, _p(m), _p(st))
+        return m, st
 
     def sort_f64(self, x: np.ndarray, scale: int, max_cells: int = 10**8):
         x = np.ascontiguousarray(x, dtype=np.float64)

@@ -97,6 +97,18 @@ int ref_float_to_decimal(double x, uint32_t scale, uint64_t* mantissa) {
   return guarded([&] { *mantissa = float_to_decimal(x, scale).mantissa; });
 }
 
+// float_to_decimal of every element: mantissa and status per element (the
+// per-element statuses let the GPU parity tests sample every exponent).
+int ref_float_to_decimal_many(const double* x, uint64_t n, uint32_t scale, uint64_t* mantissa,
+                              int32_t* status) {
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t m = 0;
+    status[i] = guarded([&] { m = float_to_decimal(x[i], scale).mantissa; });
+    mantissa[i] = m;
+  }
+  return 0;
+}
+
 // float_to_decimal per element, then the core with KeySpec{10, lambda+cd, lambda}
 // (key_model.cpp:122-124 for lambda).
 int ref_sort_f64(const double* x, uint64_t n, uint32_t scale, uint64_t max_cells,

@@ -157,6 +157,17 @@ def sort_f64(x, scale: int, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits:
     return out, _report(rep)
 
 
+def float_to_decimal_column(x, scale: int):
+    """float_to_decimal(x[i], scale).mantissa for a float64 CUDA tensor
+    (key_model.cpp:135-158, every double; errors as the reference's for the
+    first failing element).  Returns the uint64 mantissas in an int64 tensor."""
+    torch = _torch()
+    x = _cuda_tensor(x, (torch.float64,), "x")
+    out = torch.empty(x.numel(), dtype=torch.int64, device=x.device)
+    _check(_lib.load().rs_float_to_decimal(_ptr(x), x.numel(), int(scale), _ptr(out), _stream()))
+    return out
+
+
 def sort_fixed_str(records, *, alphabet: str = DEFAULT_ALPHABET, max_cells: int = DEFAULT_CELL_BUDGET,
                    msd: bool = False):
     """sort_strings over a uint8 CUDA tensor of shape (n, width) of NUL-padded
@@ -349,7 +360,7 @@ def sort_strings(values, alphabet: str = DEFAULT_ALPHABET, max_cells: int = DEFA
 __all__ = [
     "DEFAULT_CELL_BUDGET", "Error", "ExtractionReport", "KeySpec", "__version__",
     "sort_integers", "sort_decimals", "sort_decimal_keys", "sort_strings", "sort_decimal_column",
-    "format_decimal_column",
+    "format_decimal_column", "float_to_decimal_column",
     "sort_u32", "sort_u32_kv", "sort_i64", "sort_f64", "sort_fixed_str", "sort_keys",
     "recombinant_sort",
 ]

@@ -3,6 +3,7 @@
 // CUDA device every entry point returns RS_NO_DEVICE.
 #include <cuda_runtime.h>
 
+#include <charconv>
 #include <cmath>
 #include <cstdio>
 #include <algorithm>
@@ -174,14 +175,12 @@ void pull_stats(Workspace& ws) {
 void check_flags(unsigned flags) {
   if (flags & kFlagNonFinite) fail(RS_NON_FINITE, "value is not finite");
   if (flags & kFlagNegative) fail(RS_NEGATIVE_VALUE, "negative values are not supported");
-  if (flags & kFlagDomain)
-    fail(RS_OUT_OF_RANGE,
-         "value outside the exact float64 domain of rs_sort_f64 (x == 0 or 10^-(scale+3) < x, x*10^(scale+2) < 2^53)");
+  if (flags & kFlagBudget) fail(RS_CELL_BUDGET_EXCEEDED, "a value's numeral exceeds every cell budget");
 }
 
 // ---------------------------------------------------------------- passes
 template <class Map>
-unsigned long long device_max(Workspace& ws, const typename Map::In* in, uint64_t n, Map map) {
+unsigned long long device_max(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, bool check = true) {
   reset_stats(ws);
   {
     PassTimer pt_(RS_PASS_MAX, ws.stream);
@@ -189,8 +188,97 @@ unsigned long long device_max(Workspace& ws, const typename Map::In* in, uint64_
     RS_LAUNCH_CHECK();
   }
   pull_stats(ws);
-  check_flags(ws.h_stats->flags);
+  if (check) check_flags(ws.h_stats->flags);
   return ws.h_stats->max_key;
+}
+
+// ------------------------------------------------------ float64 mapping
+template <bool G>
+MapF64T<G> make_map_f64(uint32_t scale) {
+  // the fast tests need 10^(scale+2) * x < 2^53 (scale <= 15); above that
+  // every element leaves the fast domain (limit -1)
+  const bool fast = scale <= 15;
+  const double P = fast ? static_cast<double>(checked_pow(10, scale)) : 1.0;
+  return MapF64T<G>{P, 2.0 * P, fast ? 9007199254740992.0 / 100.0 : -1.0,
+                    fast ? 1.0000001 * std::pow(10.0, -static_cast<double>(scale + 3)) : 0.0, scale};
+}
+constexpr unsigned kF64Errors = kFlagNegative | kFlagNonFinite | kFlagBudget;
+
+// The first failing element in input order (the one the reference's
+// sequential float_to_decimal loop stops at).
+__global__ void k_f64_first_error(const double* __restrict__ x, uint64_t n, MapF64G map,
+                                  unsigned long long* first) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    unsigned fl = 0;
+    (void)map(x[i], fl);
+    if (fl) atomicMin(first, static_cast<unsigned long long>(i));
+  }
+}
+
+// The reference's error for x (key_model.cpp:135-158): non_finite, negative,
+// or cell_budget_exceeded from parse_decimal / checked_pow on x's shortest
+// fixed numeral.  Host-side formatting of the one failing element's message
+// (std::to_chars as the reference); the values themselves never come here.
+[[noreturn]] void fail_f64(double x, uint32_t scale) {
+  if (!std::isfinite(x)) fail(RS_NON_FINITE, "value is not finite");
+  if (x < 0.0) fail(RS_NEGATIVE_VALUE, "negative values are not supported");
+  if (std::signbit(x)) x = 0.0;
+  char buf[512];
+  const auto res = std::to_chars(buf, buf + sizeof buf, x, std::chars_format::fixed);
+  const std::string text(buf, res.ptr);
+  unsigned long long M = 0;
+  uint32_t F = 0;
+  bool frac = false;
+  for (const char ch : text) {
+    if (ch == '.') {
+      frac = true;
+      continue;
+    }
+    const unsigned d = static_cast<unsigned>(ch - '0');
+    if (M > (~0ull - d) / 10)
+      fail(RS_CELL_BUDGET_EXCEEDED, "numeral '" + text + "' has more digits than any cell budget admits");
+    M = M * 10 + d;
+    F += frac ? 1 : 0;
+  }
+  const uint32_t e = F <= scale ? scale - F : F - scale;
+  if (e <= 19) fail(RS_CUDA_ERROR, "float_to_decimal: device flagged " + text + " but it maps");
+  fail(RS_CELL_BUDGET_EXCEEDED, "key space 10^" + std::to_string(e) + " overflows 64 bits");
+}
+
+// After a pass whose flags hold no kFlagDomain: the first element error.
+void check_f64(Workspace& ws, const double* x, uint64_t n, uint32_t scale) {
+  if (!(ws.h_stats->flags & kF64Errors)) return;
+  const MapF64G map = make_map_f64<true>(scale);
+  auto* first = ws.get<unsigned long long>(kSlotScratch, 4);
+  RS_CUDA(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), ws.stream));
+  k_f64_first_error<<<stream_grid(n, kThreads * 8), kThreads, 0, ws.stream>>>(x, n, map, first);
+  RS_LAUNCH_CHECK();
+  unsigned long long i = 0;
+  RS_CUDA(cudaMemcpyAsync(&i, first, sizeof(i), cudaMemcpyDeviceToHost, ws.stream));
+  RS_CUDA(cudaStreamSynchronize(ws.stream));
+  if (i >= n) fail(RS_CUDA_ERROR, "float_to_decimal: flagged element not found");
+  double xi = 0.0;
+  RS_CUDA(cudaMemcpy(&xi, x + i, sizeof(double), cudaMemcpyDeviceToHost));
+  fail_f64(xi, scale);
+}
+
+// out[i] = float_to_decimal(x[i], scale).mantissa: the fast tests, the exact
+// search for the keys they cannot decide
+template <class Map>
+__global__ void __launch_bounds__(kThreads) k_f64_map_u64(const double* __restrict__ x, uint64_t n, Map map,
+                                                          unsigned long long* __restrict__ out, DevStats* st) {
+  unsigned flags = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double v = __ldcs(x + i);
+    bool und;
+    unsigned long long k = map.fast(v, und);
+    if (und) k = map(v, flags);
+    out[i] = k;
+  }
+  flags = warp_or(flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(&st->flags, flags);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -1017,41 +1105,90 @@ rs_status rs_sort_keys(const uint64_t* keys, uint64_t n, rs_key_spec spec, uint6
   });
 }
 
+// One float64 sort with mapper `map`; false when a value left the lean
+// mapper's fast domain (nothing is reported, the caller redoes the sort
+// with the general mapper).
+extern "C++" {
+template <class Map>
+bool sort_f64_with(Workspace& ws, const double* x, uint64_t n, uint32_t scale, Map map, uint64_t* out,
+                   uint64_t out_capacity, const rs_options* opt, uint64_t budget, rs_report* report) {
+  const uint64_t P = pow10u(scale);
+  const uint32_t hint = opt ? opt->key_digits : 0;
+  const bool hinted = hint > scale && hint <= 19 && pow10u(hint) <= budget;
+  uint32_t total = hint;
+  if (!hinted) {
+    const unsigned long long mx = device_max(ws, x, n, map, false);
+    if (ws.h_stats->flags & kFlagDomain) return false;
+    check_f64(ws, x, n, scale);
+    total = digit_count(mx / P) + scale;
+  }
+  make_key_spec(10, total, total - scale, budget);
+  if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
+  OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned32(out)};
+  grid_sort(ws, x, n, map, pow10u(total), o, out, 10, 0, scale);
+  if (ws.h_stats->flags & kFlagDomain) return false;
+  check_f64(ws, x, n, scale);
+  if (ws.h_stats->overflow) {
+    total = digit_count(ws.h_stats->max_key / P) + scale;
+    make_key_spec(10, total, total - scale, budget);
+    grid_sort(ws, x, n, map, pow10u(total), o, out, 10, 0, scale);
+  }
+  const uint32_t d = static_cast<uint32_t>(ws.h_stats->report_digits);
+  if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{10, d, d - scale}};
+  return true;
+}
+}  // extern "C++"
+
 rs_status rs_sort_f64(const double* x, uint64_t n, uint32_t scale, uint64_t* out,
                       uint64_t out_capacity, const rs_options* opt, rs_report* report,
                       void* stream) {
   return guarded([&] {
     ensure_device();
     const uint64_t budget = budget_of(opt);
-    if (scale > 15) fail(RS_OUT_OF_RANGE, "rs_sort_f64 supports scale <= 15");
+    if (scale > kF2dMaxScale) fail(RS_OUT_OF_RANGE, "float_to_decimal on the device supports scale <= 40");
     if (n > 0 && (!x || !out)) fail(RS_INVALID_ARGUMENT, "null device pointer");
-    const uint64_t P = pow10u(scale);
+    // lambda = digits(max / 10^scale) (key_model.cpp:122-124): 10^scale itself must fit
+    const std::string pow_msg = "key space 10^" + std::to_string(scale) + " overflows 64 bits";
     if (n == 0) {
+      if (scale > 19) fail(RS_CELL_BUDGET_EXCEEDED, pow_msg);
       if (report) *report = rs_report{0, 0, make_key_spec(10, 1, 1, budget)};
       return;
     }
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
-    MapF64 map{static_cast<double>(P), 2.0 * static_cast<double>(P), 9007199254740992.0 / 100.0,
-               1.0000001 * std::pow(10.0, -static_cast<double>(scale + 3))};
-    const uint32_t hint = opt ? opt->key_digits : 0;
-    const bool hinted = hint > scale && hint <= 19 && pow10u(hint) <= budget;
-    uint32_t total = hint;
-    if (!hinted) {
-      const unsigned long long mx = device_max(ws, x, n, map);
-      total = digit_count(mx / P) + scale;
+    if (scale > 19) {  // the element errors come first (in input order), then the geometry's
+      device_max(ws, x, n, make_map_f64<true>(scale), false);
+      check_f64(ws, x, n, scale);
+      fail(RS_CELL_BUDGET_EXCEEDED, pow_msg);
     }
-    make_key_spec(10, total, total - scale, budget);
-    if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
-    OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned32(out)};
-    grid_sort(ws, x, n, map, pow10u(total), o, out, 10, 0, scale);
-    check_flags(ws.h_stats->flags);
-    if (ws.h_stats->overflow) {
-      total = digit_count(ws.h_stats->max_key / P) + scale;
-      make_key_spec(10, total, total - scale, budget);
-      grid_sort(ws, x, n, map, pow10u(total), o, out, 10, 0, scale);
+    // the lean mapper first; a value outside its domain redoes the sort with the general one
+    if (scale > 15 || !sort_f64_with(ws, x, n, scale, make_map_f64<false>(scale), out, out_capacity, opt, budget,
+                                     report))
+      sort_f64_with(ws, x, n, scale, make_map_f64<true>(scale), out, out_capacity, opt, budget, report);
+  });
+}
+
+
+rs_status rs_float_to_decimal(const double* x, uint64_t n, uint32_t scale, uint64_t* out, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    if (scale > kF2dMaxScale) fail(RS_OUT_OF_RANGE, "float_to_decimal on the device supports scale <= 40");
+    if (n == 0) return;
+    if (!x || !out) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    auto run = [&](auto map) {
+      reset_stats(ws);
+      PassTimer pt_(RS_PASS_MAX, ws.stream);
+      k_f64_map_u64<<<stream_grid(n, kThreads * 8), kThreads, 0, ws.stream>>>(
+          x, n, map, reinterpret_cast<unsigned long long*>(out), ws.stats);
+      RS_LAUNCH_CHECK();
+    };
+    run(make_map_f64<false>(scale));  // lean; values outside its domain: again with the general mapper
+    pull_stats(ws);
+    if (ws.h_stats->flags & kFlagDomain) {
+      run(make_map_f64<true>(scale));
+      pull_stats(ws);
     }
-    const uint32_t d = static_cast<uint32_t>(ws.h_stats->report_digits);
-    if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{10, d, d - scale}};
+    check_f64(ws, x, n, scale);
   });
 }
 

@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "kernels_f64.cuh"
 #include "rs_internal.cuh"
 
 namespace rsb {
@@ -136,7 +137,12 @@ __device__ __forceinline__ int quotient_is(double x, double c, double d) {
   return (pow2 || r == h) ? -1 : (r < h ? 1 : 0);
 }
 
-struct MapF64 {
+// kGeneral = false: the lean mapper of the hot kernels — a value outside
+// the fast domain raises kFlagDomain and the host redoes the sort with
+// kGeneral = true, whose operator() takes the exact general search for
+// those values (a call the hot kernels' register budget never pays for).
+template <bool kGeneral>
+struct MapF64T {
   using In = double;
   using Key = unsigned long long;
   static constexpr bool kMapFirst = true;  // a separate streaming map pass, then the uint32 partition
@@ -144,6 +150,7 @@ struct MapF64 {
   double P2;     // 2 * 10^scale
   double limit;  // 2^53 / 100
   double tiny;   // just above 10^-(scale+3)
+  uint32_t scale;
   __device__ __forceinline__ unsigned long long operator()(double x, unsigned& flags) const {
     if (!isfinite(x)) {
       flags |= kFlagNonFinite;
@@ -154,12 +161,19 @@ struct MapF64 {
       return 0;
     }
     const double p = x * P;
-    // Below 10^-(scale+3) the reference either returns 0 or raises
-    // cell_budget_exceeded when the shortest numeral has >= scale+20
-    // fractional digits (key_model.cpp:154); that band is outside the domain.
+    // Outside the fast domain (tiny values, whose shortest numeral may have
+    // >= scale+20 fractional digits, and x * 10^(scale+2) >= 2^53): the
+    // exact general search (kernels_f64.cuh)
     if (!(p < limit) || (x > 0.0 && x < tiny)) {
-      flags |= kFlagDomain;
-      return 0;
+      if constexpr (kGeneral) {
+        uint32_t code;
+        const unsigned long long k = f2d_general(x, scale, code);
+        if (code != kF2dOk) flags |= kFlagBudget;
+        return k;
+      } else {
+        flags |= kFlagDomain;
+        return 0;
+      }
     }
     const double err = fma(x, P, -p);  // x*P == p + err exactly
     double f = floor(p);
@@ -202,6 +216,12 @@ struct MapF64 {
     return static_cast<unsigned long long>(bad ? 0.0 : r);  // one conversion
   }
 };
+using MapF64 = MapF64T<false>;
+using MapF64G = MapF64T<true>;
+template <class M>
+struct is_f64_map : std::false_type {};
+template <bool G>
+struct is_f64_map<MapF64T<G>> : std::true_type {};
 
 template <class M, class = void>
 struct map_first : std::false_type {};
@@ -220,7 +240,7 @@ __global__ void __launch_bounds__(kThreads) k_map_cells(const typename Map::In* 
   unsigned flags = 0;
   auto cell = [&](In x) -> uint32_t {
     unsigned long long k;
-    if constexpr (std::is_same<Map, MapF64>::value) {
+    if constexpr (is_f64_map<Map>::value) {
       bool und;
       k = map.fast(x, und);
       if (und) k = map(x, flags);  // rare: exact path (also classifies bad inputs)

@@ -96,14 +96,15 @@ struct DevStats {
   unsigned long long n_occupied; // occupied cells (written by the last scan tile)
   unsigned long long total;      // keys counted (written by the last scan tile)
   unsigned int overflow;         // a key fell outside the grid
-  unsigned int flags;            // bit0 negative, bit1 non-finite, bit2 out-of-domain
+  unsigned int flags;            // kFlag* bits
   unsigned int tile_counter;     // dynamic tile ids for the look-back scan
   unsigned int long_spans;        // hot cells spanning >= 3 emit tiles (k_scan_cells -> k_fill_spans)
   unsigned long long cells_traversed;  // report (per-row spans)
   unsigned long long report_digits;    // total_digits found by the report kernel
 };
 
-enum : unsigned { kFlagNegative = 1u, kFlagNonFinite = 2u, kFlagDomain = 4u };
+// kFlagBudget: float_to_decimal raised cell_budget_exceeded (mantissa or 10^e overflow)
+enum : unsigned { kFlagNegative = 1u, kFlagNonFinite = 2u, kFlagDomain = 4u, kFlagBudget = 8u };
 
 // Per-(device, stream) scratch cache.  Buffers only grow; each stream owns
 // its own so concurrent calls on different streams never share scratch.
