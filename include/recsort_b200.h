@@ -163,8 +163,14 @@ rs_status rs_float_to_decimal(const double* x, uint64_t n, uint32_t scale,
  * record i is chars[i*width .. i*width+width), its string ends at the first
  * NUL byte or at width.  h_alphabet is a host NUL-terminated symbol list
  * (Alphabet, key_model.hpp:93-121); NULL = "abcdefghijklmnopqrstuvwxyz".
- * Output records are the sorted originals, NUL-padded.  width <= 12 and
- * radix^width < 2^63. */
+ * Output records are the sorted originals, NUL-padded.  Checks in the
+ * reference's order: KeySpec{radix, w, w} for the longest string w
+ * (make_key_spec: cell budget, radix^w overflow), then the first symbol
+ * outside the alphabet.  With rs_options.msd a key space above the budget is
+ * sorted by MSD passes over keys packed b bits per ordinal (b = bit length
+ * of the alphabet size: 5 for a-z, 6 for <= 63 symbols, 8 for <= 255) when
+ * width * b <= 64 (12 a-z characters, 16 of a 15-symbol alphabet, 8 of any
+ * byte alphabet); wider records keep the reference's budget error. */
 rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width,
                             const char* h_alphabet, uint8_t* out,
                             uint64_t out_capacity, const rs_options* opt,

@@ -300,7 +300,8 @@ class Reference:
         n, width = recs.shape
         out = np.empty_like(recs)
         rep = RefReportC()
-        self._ok(self.L.ref_sort_strings(_p(recs), n, width, alphabet.encode(), max_cells, _p(out),
+        alpha = alphabet if isinstance(alphabet, bytes) else alphabet.encode()
+        self._ok(self.L.ref_sort_strings(_p(recs), n, width, alpha, max_cells, _p(out),
                                          ctypes.byref(rep)))
         return out, rep.as_tuple()
 

@@ -179,7 +179,8 @@ def sort_fixed_str(records, *, alphabet: str = DEFAULT_ALPHABET, max_cells: int 
     n, width = records.shape
     out = torch.empty_like(records)
     rep = RsReport()
-    _check(_lib.load().rs_sort_fixed_str(_ptr(records), n, width, alphabet.encode(), _ptr(out), n,
+    alpha = alphabet if isinstance(alphabet, bytes) else alphabet.encode()  # bytes: any byte alphabet
+    _check(_lib.load().rs_sort_fixed_str(_ptr(records), n, width, alpha, _ptr(out), n,
                                          ctypes.byref(_opts(max_cells, 0, msd)), ctypes.byref(rep), _stream()))
     return out, _report(rep)
 
@@ -343,10 +344,7 @@ def sort_strings(values, alphabet: str = DEFAULT_ALPHABET, max_cells: int = DEFA
     if len(set(alphabet)) != len(alphabet):
         raise Error("invalid_argument", "duplicate symbol in alphabet")
     enc = [v.encode() for v in values]
-    width = max([len(e) for e in enc] + [1])
-    if width > 12:
-        w_cells = (len(alphabet) + 1) ** width
-        raise Error("cell_budget_exceeded", f"key space needs {w_cells} cells, budget is {max_cells}")
+    width = max([len(e) for e in enc] + [1])  # key_model.cpp:228-230; the spec check is the library's
     buf = bytearray(len(enc) * width)
     for i, e in enumerate(enc):
         buf[i * width:i * width + len(e)] = e

@@ -698,13 +698,15 @@ __global__ void __launch_bounds__(kThreads) k_str_keys(const uint8_t* __restrict
 
 
 // Width (longest string) and symbol validation for the MSD path, optionally
-// writing each record's packed key (5 bits per ordinal, first symbol most
-// significant, pad 0 — the MSD key order); 8-byte records read as two
+// writing each record's packed key (obits bits per ordinal, first symbol
+// most significant, pad 0 — the MSD key order); 8-byte records read as two
 // 16-byte loads per thread per round.
+template <int kBits>  // bits per packed ordinal; 0 = the runtime obits
 __global__ void __launch_bounds__(kThreads) k_str_scan(const uint8_t* __restrict__ recs, uint64_t n, uint32_t width,
                                                        bool w8, const uint16_t* __restrict__ ord_g, DevStats* st,
                                                        unsigned long long* __restrict__ packed, int lin,
-                                                       uint32_t alen) {
+                                                       uint32_t alen, uint32_t obits_rt) {
+  const uint32_t obits = kBits ? kBits : obits_rt;
   __shared__ uint16_t ord[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) ord[i] = ord_g[i];
   __syncthreads();
@@ -724,7 +726,7 @@ __global__ void __launch_bounds__(kThreads) k_str_scan(const uint8_t* __restrict
       const uint32_t o = ended ? 0u : (lin >= 0 ? (lo - 1u < alen ? lo : 0u) : ord[c]);
       len += ended ? 0u : 1u;
       bad |= !ended && o == 0;
-      k = (k << 5) | o;
+      k = (k << obits) | o;
     }
     mxlen = len > mxlen ? len : mxlen;
     return k;
@@ -768,7 +770,7 @@ __global__ void __launch_bounds__(kThreads) k_str_scan(const uint8_t* __restrict
             bad |= o == 0;
           }
         }
-        k = (k << 5) | o;
+        k = (k << obits) | o;
       }
       mxlen = len > mxlen ? len : mxlen;
       if (packed) packed[i] = k;
@@ -780,6 +782,22 @@ __global__ void __launch_bounds__(kThreads) k_str_scan(const uint8_t* __restrict
     mxlen = w > mxlen ? w : mxlen;
   }
   if ((threadIdx.x & 31) == 0 && mxlen) atomicMax(&st->max_key, mxlen);
+}
+
+// The first symbol outside the alphabet in (record, position) order — the
+// one Alphabet::ordinal raises for in strings_to_keys (key_model.cpp:
+// 208-214, 233-241).
+__global__ void k_str_first_bad(const uint8_t* __restrict__ recs, uint64_t n, uint32_t width,
+                                const uint16_t* __restrict__ ord, unsigned long long* first) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint8_t* r = recs + i * width;
+    for (uint32_t j = 0; j < width && r[j] != 0; ++j)
+      if (__ldg(ord + r[j]) == 0) {
+        atomicMin(first, i * width + j);
+        break;
+      }
+  }
 }
 
 // Emit writer for strings: key -> record bytes (key_to_string,
@@ -950,18 +968,20 @@ void msd_i64_entry(Workspace& ws, const int64_t* in, uint64_t n, const uint64_t*
 
 void msd_sort_str(Workspace& ws, const uint8_t* chars, uint64_t n, uint32_t width, uint32_t w, uint32_t radix,
                   const uint16_t* d_ord, const uint8_t* d_sym, uint8_t* out, int lin,
-                  const unsigned long long* packed) {
+                  const unsigned long long* packed, uint32_t obits) {
   reset_stats(ws);
   EmitStr em{out, width, d_sym};
   em.lin = lin;
+  em.obits = obits;
   em.w8 = width == 8 && (reinterpret_cast<uintptr_t>(out) & 7) == 0;
   if (packed) {  // keys packed by k_str_scan
-    msd_sort(ws, LoadKeys<unsigned long long>{packed, n}, n, 5 * width, em);
+    msd_sort(ws, LoadKeys<unsigned long long>{packed, n}, n, obits * width, em);
   } else {
     LoadStr ld{chars, width, d_ord};
     ld.w8 = width == 8 && (reinterpret_cast<uintptr_t>(chars) & 7) == 0;
     ld.lin = lin;
-    msd_sort(ws, ld, n, 5 * width, em);
+    ld.obits = obits;
+    msd_sort(ws, ld, n, obits * width, em);
   }
   {
     PassTimer pt_(RS_PASS_REPORT, ws.stream);
@@ -1228,12 +1248,11 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
   return guarded([&] {
     ensure_device();
     const uint64_t budget = budget_of(opt);
-    if (width == 0 || width > 12) fail(RS_INVALID_ARGUMENT, "record width must be in [1, 12]");
+    if (width == 0) fail(RS_INVALID_ARGUMENT, "record width must be at least 1");
     StrTable t{};
     const char* alpha = h_alphabet ? h_alphabet : "abcdefghijklmnopqrstuvwxyz";
     const size_t alen = strlen(alpha);
-    if (alen == 0) fail(RS_INVALID_ARGUMENT, "alphabet is empty");
-    if (alen > 254) fail(RS_INVALID_ARGUMENT, "alphabet too large");
+    if (alen == 0) fail(RS_INVALID_ARGUMENT, "alphabet is empty");  // Alphabet(), key_model.cpp:190-201
     for (size_t i = 0; i < alen; ++i) {
       const auto c = static_cast<unsigned char>(alpha[i]);
       if (t.ord[c] != 0) fail(RS_INVALID_ARGUMENT, std::string("duplicate symbol '") + alpha[i] + "' in alphabet");
@@ -1258,25 +1277,41 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
     if (static_cast<unsigned char>(alpha[0]) == 0) lin = -1;
     // width of the data = longest string (key_model.cpp:228-230), symbols checked;
     // with msd the same pass packs the keys the MSD levels read
-    const bool want_msd = opt && opt->msd && width <= 12;
+    uint32_t obits = 1;  // bits of the largest ordinal
+    while ((alen >> obits) != 0) ++obits;
+    const bool want_msd = opt && opt->msd && width * obits <= 64;
     unsigned long long* packed = want_msd ? ws.get<unsigned long long>(kSlotMisc2, n) : nullptr;
     reset_stats(ws);
     {
       PassTimer pt_(RS_PASS_OTHER, ws.stream);
       const bool w8 = width == 8 && (reinterpret_cast<uintptr_t>(chars) & 15) == 0;
-      k_str_scan<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w8, d_ord, ws.stats,
-                                                                              packed, lin, static_cast<uint32_t>(alen));
+      auto scan = obits == 5 ? k_str_scan<5> : k_str_scan<0>;
+      scan<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w8, d_ord, ws.stats, packed,
+                                                                        lin, static_cast<uint32_t>(alen), obits);
       RS_LAUNCH_CHECK();
     }
     pull_stats(ws);
-    if (ws.h_stats->flags & 8u) fail(RS_SYMBOL_OUT_OF_ALPHABET, "a symbol is not in the alphabet");
+    auto check_symbols = [&] {  // after the key spec, as strings_to_keys orders them
+      if (!(ws.h_stats->flags & 8u)) return;
+      auto* first = ws.get<unsigned long long>(kSlotScratch, 4);
+      RS_CUDA(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), ws.stream));
+      k_str_first_bad<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, d_ord, first);
+      RS_LAUNCH_CHECK();
+      unsigned long long at = 0;
+      RS_CUDA(cudaMemcpyAsync(&at, first, sizeof(at), cudaMemcpyDeviceToHost, ws.stream));
+      RS_CUDA(cudaStreamSynchronize(ws.stream));
+      uint8_t c = 0;
+      if (at < n * width) RS_CUDA(cudaMemcpy(&c, chars + at, 1, cudaMemcpyDeviceToHost));
+      fail(RS_SYMBOL_OUT_OF_ALPHABET, std::string("symbol '") + static_cast<char>(c) + "' is not in the alphabet");
+    };
     const uint32_t w = ws.h_stats->max_key ? static_cast<uint32_t>(ws.h_stats->max_key) : 1u;
     const uint64_t total_cells = [&] {
       try { return checked_pow(t.radix, w); } catch (const Failure&) { return ~uint64_t{0}; }
     }();
-    const bool msd = opt && opt->msd;
+    const bool msd = want_msd;  // MSD needs the packed key to fit 64 bits; else the reference's budget error
     if (!msd || total_cells <= budget) {
       const rs_key_spec spec = make_key_spec(t.radix, w, w, budget);
+      check_symbols();
       if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
       auto* keys = ws.get<unsigned long long>(kSlotMapped, n);
       {  // base-radix keys at the data width
@@ -1290,9 +1325,9 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
       if (report) *report = rs_report{n, ws.h_stats->cells_traversed, spec};
       return;
     }
+    check_symbols();
     if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
-    if (t.radix > 32) fail(RS_INVALID_ARGUMENT, "the MSD string path packs 5-bit ordinals: at most 31 symbols");
-    msd_sort_str(ws, chars, n, width, w, t.radix, d_ord, d_sym, out, lin, packed);
+    msd_sort_str(ws, chars, n, width, w, t.radix, d_ord, d_sym, out, lin, packed, obits);
     if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{t.radix, w, w}};
   });
 }

@@ -159,7 +159,6 @@ StringSortResult sort_strings(std::span<const std::string> values, const Alphabe
                               std::uint64_t max_cells) {
   std::size_t width = 1;
   for (const std::string& v : values) width = std::max(width, v.size());
-  if (width > 12) throw Error(errc::cell_budget_exceeded, "key space overflows the cell budget");
   const std::size_t n = values.size();
   std::vector<std::uint8_t> recs(n * width, 0);
   for (std::size_t i = 0; i < n; ++i) std::memcpy(recs.data() + i * width, values[i].data(), values[i].size());

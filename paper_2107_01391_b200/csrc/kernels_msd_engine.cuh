@@ -3,7 +3,7 @@
 // key_model.cpp:72-76).
 //
 // Keys are 32- or 64-bit integers whose order is the sort order (uint32
-// keys; fixed-width strings packed 5 bits per symbol ordinal, which keeps
+// keys; fixed-width strings packed obits bits per symbol ordinal, which keeps
 // lexicographic order because every ordinal < 32).  Each level splits every
 // open segment by its next 8-bit digit — a 256-cell sub-grid of the
 // Cartesian space:
@@ -98,8 +98,9 @@ struct LoadKeys {
   bool vec_ = false;
 };
 
-// Fixed-width records -> packed key (5 bits per ordinal, pad ordinal 0,
-// first symbol most significant).  bad |= symbol outside the alphabet.
+// Fixed-width records -> packed key (obits bits per ordinal — the bit
+// length of the largest ordinal, 5 for a-z — pad ordinal 0, first symbol
+// most significant; width * obits <= 64).
 struct LoadStr {
   using Key = unsigned long long;
   const uint8_t* recs;
@@ -116,6 +117,7 @@ struct LoadStr {
   __device__ __forceinline__ bool valid(int j, uint32_t tl) const { return (uint32_t)(j * kMsdThreads + threadIdx.x) < tl; }
   bool w8 = false;       // 8-byte records at an 8-byte aligned base: one 64-bit load each
   int lin = -1;          // contiguous alphabet: ordinal = byte - lin (symbols validated by k_str_scan)
+  uint32_t obits = 5;
   __device__ __forceinline__ uint32_t ord_of(uint32_t c) const {
     return lin >= 0 ? c - static_cast<uint32_t>(lin) : __ldg(ord + c);
   }
@@ -129,7 +131,7 @@ struct LoadStr {
         const uint32_t c = static_cast<uint32_t>(w >> (8 * j)) & 0xffu;
         ended |= c == 0;
         const uint32_t o = ended ? 0u : ord_of(c);
-        k = (k << 5) | o;
+        k = (k << obits) | o;
       }
       return k;
     }
@@ -143,7 +145,7 @@ struct LoadStr {
         if (c == 0) ended = true;
         else o = ord_of(c);
       }
-      k = (k << 5) | o;
+      k = (k << obits) | o;
     }
     return k;
   }
@@ -164,21 +166,24 @@ struct EmitStr {
   const uint8_t* sym;  // device: ordinal -> byte, sym[0] = 0
   int lin = -1;        // contiguous alphabet: byte = ordinal + lin (no table lookups)
   bool w8 = false;     // 8-byte records at an 8-byte aligned base: one 64-bit store each
+  uint32_t obits = 5;  // bits per packed ordinal
   __device__ __forceinline__ uint32_t byte_of(uint32_t o) const {
     return lin >= 0 ? (o ? o + static_cast<uint32_t>(lin) : 0u) : sym[o];
   }
   __device__ __forceinline__ void operator()(unsigned long long pos, unsigned long long key) const {
+    const uint32_t mask = (1u << obits) - 1u;
     if (w8) {
       unsigned long long w = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) w |= static_cast<unsigned long long>(byte_of((key >> (5 * (7 - j))) & 31u)) << (8 * j);
+      for (int j = 0; j < 8; ++j)
+        w |= static_cast<unsigned long long>(byte_of(static_cast<uint32_t>(key >> (obits * (7 - j))) & mask)) << (8 * j);
       reinterpret_cast<unsigned long long*>(out)[pos] = w;
       return;
     }
     uint8_t* r = out + pos * width;
     for (int j = (int)width - 1; j >= 0; --j) {
-      r[j] = static_cast<uint8_t>(byte_of(key & 31u));
-      key >>= 5;
+      r[j] = static_cast<uint8_t>(byte_of(static_cast<uint32_t>(key) & mask));
+      key >>= obits;
     }
   }
 };
