@@ -16,6 +16,7 @@
 #include "recsort/extraction.hpp"
 #include "recsort/hashing.hpp"
 #include "recsort/key_model.hpp"
+#include "recsort/bench.hpp"
 #include "recsort/sort.hpp"
 #include "recsort/splitmix64.hpp"
 
@@ -61,6 +62,12 @@ std::vector<std::string> records(const uint8_t* chars, uint64_t n, uint32_t widt
 }
 
 }  // namespace
+
+int copy_out(const std::string& s, char* out, uint64_t cap) {
+  if (s.size() + 1 > cap) fail(errc::buffer_too_small, "shim buffer");
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return 0;
+}
 
 extern "C" {
 
@@ -207,6 +214,53 @@ int ref_radix_sort_lsd(const uint64_t* values, uint64_t n, uint64_t* out) {
   return guarded([&] {
     std::vector<uint64_t> r = baselines::radix_sort_lsd(std::span<const uint64_t>(values, n));
     std::memcpy(out, r.data(), n * sizeof(uint64_t));
+  });
+}
+
+// bench::generate (bench.cpp:75-89): the values, NUL-separated.
+int ref_generate(uint64_t n, double lo, double hi, uint32_t cd, uint64_t seed, char* out, uint64_t cap) {
+  return guarded([&] {
+    bench::DatasetSpec ds;
+    ds.n_elements = n;
+    ds.range_lo = lo;
+    ds.range_hi = hi;
+    ds.cd = cd;
+    ds.seed = seed;
+    std::string flat;
+    for (const std::string& v : bench::generate(ds)) {
+      flat += v;
+      flat += '\0';
+    }
+    if (flat.size() > cap) fail(errc::buffer_too_small, "shim buffer");
+    std::memcpy(out, flat.data(), flat.size());
+  });
+}
+
+// bench::describe (bench.cpp:101-122) as "total,integer,cells,count_dims,h_min,h_max".
+int ref_describe(double lo, double hi, uint32_t cd, char* out, uint64_t cap) {
+  return guarded([&] {
+    const bench::KeyShape s = bench::describe(bench::CaseSpec{lo, hi, cd});
+    copy_out(std::to_string(s.total_digits) + "," + std::to_string(s.integer_digits) + "," +
+                 std::to_string(s.cell_count) + "," + s.count_dims + "," + s.h_min_dims + "," + s.h_max_dims,
+             out, cap);
+  });
+}
+
+// bench::emit_csv (bench.cpp:312-334) of one record; case_label as well.
+int ref_emit_csv_one(const char* alg, uint64_t n, double lo, double hi, uint32_t cd, uint32_t trial,
+                     double seconds, int has_cost, uint64_t cost, char* out, uint64_t cap) {
+  return guarded([&] {
+    bench::BenchRecord r;
+    r.algorithm = alg;
+    r.dataset.n_elements = n;
+    r.dataset.range_lo = lo;
+    r.dataset.range_hi = hi;
+    r.dataset.cd = cd;
+    r.trial = trial;
+    r.elapsed_seconds = seconds;
+    if (has_cost) r.extraction_cost = cost;
+    const std::vector<bench::BenchRecord> one{r};
+    copy_out(bench::emit_csv(one) + "|" + bench::case_label(bench::CaseSpec{lo, hi, cd}), out, cap);
   });
 }
 
