@@ -22,6 +22,8 @@ def main():
     ap.add_argument("csv")
     ap.add_argument("--traffic", default="")
     ap.add_argument("--step-kernels", type=int, default=9, help="launches per bench step")
+    ap.add_argument("--aggregate", type=int, default=0,
+                    help="per-kernel totals over the whole list divided by this many iterations")
     args = ap.parse_args()
     rows = list(csv.reader(open(args.csv)))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
@@ -33,6 +35,24 @@ def main():
             continue
         v = float(r[iv].replace(",", "")) * UNIT.get(r[iu], 1.0)
         per.setdefault(int(r[iid]), {"name": r[ik]})[r[im]] = v
+    if args.aggregate:
+        agg = collections.OrderedDict()
+        for d in per.values():
+            name = d["name"].split("(")[0].replace("void ", "").replace("rsb::", "")
+            a = agg.setdefault(name, [0, 0.0, 0.0, 0.0])
+            a[0] += 1
+            a[1] += d.get("gpu__time_duration.sum", 0.0)
+            a[2] += d.get("dram__bytes_read.sum", 0.0)
+            a[3] += d.get("dram__bytes_write.sum", 0.0)
+        total = sum(a[1] for a in agg.values())
+        print("| kernel | launches/iter | us/iter | share | DRAM read MB/iter | DRAM write MB/iter |")
+        print("|---|---|---|---|---|---|")
+        k = args.aggregate
+        for name, a in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+            print(f"| {name} | {a[0] / k:g} | {a[1] / k / 1e3:.1f} | {100 * a[1] / total:.1f}% | "
+                  f"{a[2] / k / 1e6:.1f} | {a[3] / k / 1e6:.1f} |")
+        print(f"\ntotal {total / k / 1e3:.1f} us per iteration under ncu (serialised, cold caches)")
+        return
     last = list(per)[-args.step_kernels:]
     total = sum(per[i]["gpu__time_duration.sum"] for i in last)
     print("| kernel | us | share | DRAM read MB | DRAM write MB |")

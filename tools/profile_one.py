@@ -1,7 +1,7 @@
 """One cfg2 key-only sort and one cfg2 key/value sort (2^28 keys), for ncu
 captures of individual kernels:
 
-    python tools/profile_one.py [--kv] [--f64] [--cfg4] [--cfg5]
+    python tools/profile_one.py [--kv] [--f64] [--cfg4] [--cfg5] [--no-cfg2]
     ncu --set full -k regex:k_outer_scatter -c 1 -o prof python tools/profile_one.py
 """
 import ctypes
@@ -23,8 +23,10 @@ def main():
     o = Oracle()
     keys = torch.empty(n, dtype=torch.int32, device="cuda")
     rs._check(lib.rs_gen_u32(o.config_seed(2), 0, n, 10**6, rs._ptr(keys), rs._stream()))
-    for _ in range(2):
-        out, rep = rs.sort_u32(keys, key_digits=6)
+    rep = None
+    if "--no-cfg2" not in sys.argv:  # other configs only (their launch lists)
+        for _ in range(2):
+            out, rep = rs.sort_u32(keys, key_digits=6)
     torch.cuda.synchronize()
     if "--kv" in sys.argv:
         vals = torch.empty_like(keys)
@@ -45,7 +47,8 @@ def main():
             rs.sort_fixed_str(r4, msd=True)
         del r4
     if "--cfg5" in sys.argv:
-        del keys, out
+        del keys
+        out = None
         torch.cuda.empty_cache()
         n5 = 1 << 31
         k5 = torch.empty(n5, dtype=torch.int32, device="cuda")
