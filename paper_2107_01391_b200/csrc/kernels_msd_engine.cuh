@@ -23,7 +23,11 @@
 //                  counting-sort scatter through shared memory (run-length
 //                  emit for segments too large to stage)                 R + W
 //   k_leaf_radix   mid-size leaves (<= 4096 keys, <= 24 remaining bits):
-//                  stable 8-bit LSD passes in shared memory               R + W
+//                  split by the top 11 remaining bits in shared memory,
+//                  each key ranked by counting the smaller keys of its
+//                  bucket and written straight to its place; skewed leaves:
+//                  8-bit LSD passes (the first by returning atomics, then
+//                  stable ballot ranks)                                  R + W
 //   k_leaf_warp    tiny leaves (<= 32 keys): register bitonic network    R + W
 //   k_leaf_bitonic small leaves of the last digit (<= 2048 keys)         R + W
 //   k_leaf_copy    single keys / exhausted digits                        R + W
@@ -51,7 +55,9 @@ constexpr uint32_t kMsdChunk = 65536;   // keys per (segment, chunk) work item
 constexpr uint32_t kLeafSmall = 2048;   // shared bitonic leaf capacity
 constexpr uint32_t kLeafWarp = 32;      // warp (register) bitonic leaf capacity
 constexpr uint32_t kLeafRadixMax = 4096;  // shared-memory LSD leaf: <= 4096 keys, <= 24 remaining bits
-constexpr int kLeafRadixThreads = 256;
+constexpr int kLeafRadixThreads = 256;     // one thread per top digit in the fast path
+constexpr uint32_t kLeafRankMax = 32;       // largest bucket the fast path ranks by counting
+static_assert(kLeafRadixThreads == 256, "the radix leaf's fast path keeps one top digit per thread");
 constexpr int kLeafGridBits = 16;       // count-grid leaf: <= 2^16 cells (u16 pairs, 128 KB)
 constexpr int kLeafGridThreads = 1024;  // one 128 KB CTA per SM: 32 warps to hide latency
 
@@ -674,12 +680,86 @@ __global__ void __launch_bounds__(kLeafRadixThreads) k_leaf_radix(const K* __res
   const unsigned lt = (1u << lane) - 1;
   for (uint32_t i = threadIdx.x; i < 2 * 256 * kW; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
-  // load, counting the first digit per (warp range, digit)
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const K key = src[g.start + i];
-    in[i] = key;
-    atomicAdd(&s_cnt[(i / per) * 256 + (static_cast<uint32_t>(key) & 255u)], 1u);
+  // Fast path: split by the top (up to) 11 remaining bits into 2048 buckets
+  // (returning atomics — an MSD split needs no stability), then every key
+  // finds its final place by counting the smaller keys of its bucket (1-2
+  // keys on average) and leaves straight from there.  A bucket above
+  // kLeafRankMax keys (skewed data, duplicates) sends the leaf down the LSD
+  // passes below.
+  constexpr int kFastBits = 11, kFastBins = 1 << kFastBits, kBinsPer = kFastBins / kLeafRadixThreads;
+  const uint32_t top = rem_bits > kFastBits ? rem_bits - kFastBits : 0;
+  const uint32_t dmask = (rem_bits < kFastBits ? (1u << rem_bits) : kFastBins) - 1u;
+  uint32_t* hs = s_cnt;                 // [2048] bucket counts -> scatter cursors
+  uint32_t* hstart = s_cnt + kFastBins; // [2048] bucket starts (the tables hold 2 * 256 * 8 words)
+  static_assert(2 * 256 * kW >= 2 * kFastBins, "count tables too small for the fast split");
+  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 8 * kLeafRadixThreads) {  // 8 loads in flight per thread
+    K k[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t i = i0 + u * kLeafRadixThreads;
+      k[u] = i < n ? __ldcs(src + g.start + i) : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t i = i0 + u * kLeafRadixThreads;
+      if (i < n) {
+        in[i] = k[u];
+        atomicAdd(&hs[static_cast<uint32_t>(k[u] >> top) & dmask], 1u);
+      }
+    }
   }
+  __syncthreads();
+  uint32_t bc[kBinsPer], bsum = 0, bmax = 0;  // this thread's buckets: kBinsPer consecutive ones
+#pragma unroll
+  for (int q = 0; q < kBinsPer; ++q) {
+    bc[q] = hs[threadIdx.x * kBinsPer + q];
+    bsum += bc[q];
+    bmax = bc[q] > bmax ? bc[q] : bmax;
+  }
+  if (!__syncthreads_or(bmax > kLeafRankMax)) {
+    uint32_t inc = bsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_part[warp] = inc;
+    __syncthreads();
+    uint32_t run = inc - bsum;
+    for (int w = 0; w < warp; ++w) run += s_part[w];
+#pragma unroll
+    for (int q = 0; q < kBinsPer; ++q) {
+      hs[threadIdx.x * kBinsPer + q] = run;
+      hstart[threadIdx.x * kBinsPer + q] = run;
+      run += bc[q];
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const K key = in[i];
+      out[atomicAdd(&hs[static_cast<uint32_t>(key >> top) & dmask], 1u)] = key;
+    }
+    __syncthreads();
+    // hs[d] is now the end of bucket d
+    for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) {
+      const K x = out[p];
+      const uint32_t d = static_cast<uint32_t>(x >> top) & dmask;
+      const uint32_t s = hstart[d], e = hs[d];
+      uint32_t r = s;
+      for (uint32_t q = s; q < e; ++q) {
+        const K y = out[q];
+        r += (y < x || (y == x && q < p)) ? 1u : 0u;
+      }
+      emit(g.start + r, x);
+    }
+    return;
+  }
+  // LSD passes: count the first digit per (warp range, digit)
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kBinsPer; ++q) hs[threadIdx.x * kBinsPer + q] = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+    atomicAdd(&s_cnt[(i / per) * 256 + (static_cast<uint32_t>(in[i]) & 255u)], 1u);
   __syncthreads();
   int cur = 0;
   for (uint32_t sh = 0; sh < rem_bits; sh += 8, cur ^= 1) {
@@ -720,16 +800,21 @@ __global__ void __launch_bounds__(kLeafRadixThreads) k_leaf_radix(const K* __res
       const bool v = i < w1;
       const K key = v ? in[i] : K(0);
       const uint32_t d = static_cast<uint32_t>(key >> sh) & 255u;
-      unsigned pm = __ballot_sync(0xffffffffu, v);  // same-digit lanes: 8 ballots
+      uint32_t pos;
+      if (sh == 0) {  // the first LSD pass may order equal digits freely: one returning atomic
+        pos = v ? atomicAdd(&cnt[warp * 256 + d], 1u) : 0u;
+      } else {        // later passes keep the previous order: same-digit lanes from 8 ballots
+        unsigned pm = __ballot_sync(0xffffffffu, v);
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const unsigned x = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        pm &= ((d >> b) & 1u) ? x : ~x;
+        for (int b = 0; b < 8; ++b) {
+          const unsigned x = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+          pm &= ((d >> b) & 1u) ? x : ~x;
+        }
+        pos = v ? cnt[warp * 256 + d] + __popc(pm & lt) : 0u;
+        __syncwarp();
+        if (v && (pm & lt) == 0) cnt[warp * 256 + d] += __popc(pm);
+        __syncwarp();
       }
-      const uint32_t pos = v ? cnt[warp * 256 + d] + __popc(pm & lt) : 0u;
-      __syncwarp();
-      if (v && (pm & lt) == 0) cnt[warp * 256 + d] += __popc(pm);
-      __syncwarp();
       if (v) {
         out[pos] = key;
         if (more) atomicAdd(&nxt[(pos / per) * 256 + (static_cast<uint32_t>(key >> (sh + 8)) & 255u)], 1u);

@@ -397,6 +397,27 @@ def test_msd_u32_narrow_keys(rs, oracle, bound):
     assert _rep(rep) == oracle.report_from_sorted(want.astype(np.uint64), 10, len(str(int(want[-1]))))
 
 
+def test_msd_radix_leaf_fast_and_skewed(rs, oracle):
+    """Leaves of ~3000 keys with 24 remaining bits: uniform ones take the
+    split + insertion fast path, skewed ones (a handful of low values, so a
+    sub-bucket holds hundreds of keys) the LSD passes; both with duplicates."""
+    rng = np.random.default_rng(77)
+    n = 256 * 3000
+    hi = rng.integers(0, 256, n, dtype=np.uint64)
+    low = rng.integers(0, 1 << 24, n, dtype=np.uint64)
+    skew = (hi % 3) == 0
+    low[skew] = rng.choice(np.array([5, 6, 1 << 20, (1 << 24) - 1], dtype=np.uint64), int(skew.sum()))
+    low[::97] = low[::89][: low[::97].size]  # duplicates inside uniform leaves
+    keys = ((hi << np.uint64(24)) | low).astype(np.uint32)
+    out, _ = rs.sort_u32(_t(keys.view(np.int32)), msd=True)
+    assert np.array_equal(_np_u32(out), np.sort(keys))
+    wide = (keys.astype(np.uint64) << np.uint64(16)) | np.uint64(3)  # the same leaves as 64-bit keys
+    import torch
+
+    got, _ = rs.sort_i64(torch.from_numpy(wide.view(np.int64)).cuda(), msd=True)
+    assert np.array_equal(got.cpu().numpy().view(np.uint64), np.sort(wide))
+
+
 def test_msd_count_grid_leaf_modes(rs, oracle):
     """16-bit count-grid leaves on both sides of the shared-memory staging
     capacity (~50K keys: scatter below, run-length emit above), a segment at
