@@ -242,7 +242,7 @@ class Reference:
     def _ok(self, st: int) -> None:
         if st != 0:
             err = OracleError(st)
-            err.message = self.L.ref_last_error().decode()
+            err.message = self.L.ref_last_error().decode(errors="replace")
             raise err
 
     def sort_integers(self, values: np.ndarray, max_cells: int = 10**8):

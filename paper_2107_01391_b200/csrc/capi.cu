@@ -713,7 +713,30 @@ __global__ void __launch_bounds__(kThreads) k_str_scan(const uint8_t* __restrict
   unsigned bad = 0;
   unsigned long long mxlen = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  // 5-bit ordinals of a contiguous alphabet, SWAR on the record's two 32-bit
+  // halves: first NUL from the zero-byte mask, per-byte ordinal and range
+  // check with the byte-SIMD intrinsics, fields merged pairwise (first
+  // character most significant).  Same results as the byte loop below.
+  const uint32_t lin4 = 0x01010101u * static_cast<uint32_t>(lin + 1), alen4 = 0x01010101u * alen;
+  auto pack20 = [](uint32_t o) {  // bytes o0..o3 (o0 first) -> o0<<15 | o1<<10 | o2<<5 | o3
+    const uint32_t a = __byte_perm(o, 0, 0x0123);  // o3 | o2<<8 | o1<<16 | o0<<24
+    const uint32_t p = (a & 0x00FF00FFu) | ((a & 0xFF00FF00u) >> 3);
+    return (p & 0xFFFFu) | ((p >> 16) << 10);
+  };
+  auto scan8_lin5 = [&](unsigned long long w) {
+    const unsigned long long z = (w - 0x0101010101010101ull) & ~w & 0x8080808080808080ull;
+    const uint32_t len = z ? static_cast<uint32_t>(__ffsll(static_cast<long long>(z)) - 1) >> 3 : 8u;
+    const unsigned long long vm = len == 8 ? ~0ull : ((1ull << (8 * len)) - 1ull);
+    const uint32_t lo = static_cast<uint32_t>(w), hi = static_cast<uint32_t>(w >> 32);
+    const uint32_t vlo = static_cast<uint32_t>(vm), vhi = static_cast<uint32_t>(vm >> 32);
+    const uint32_t dlo = __vsub4(lo, lin4), dhi = __vsub4(hi, lin4);  // ordinal - 1 per byte
+    bad |= ((__vcmpgeu4(dlo, alen4) & vlo) | (__vcmpgeu4(dhi, alen4) & vhi)) != 0u;
+    const uint32_t olo = __vadd4(dlo, 0x01010101u) & vlo, ohi = __vadd4(dhi, 0x01010101u) & vhi;
+    mxlen = len > mxlen ? len : mxlen;
+    return (static_cast<unsigned long long>(pack20(olo)) << 20) | pack20(ohi);
+  };
   auto scan8 = [&](unsigned long long w) {
+    if (kBits == 5 && lin >= 0) return scan8_lin5(w);
     uint32_t len = 0;
     bool ended = false;
     unsigned long long k = 0;

@@ -130,3 +130,30 @@ def test_msd_too_wide_keeps_reference_error(rs, ref):
     with pytest.raises(rs.Error) as got:
         rs.sort_fixed_str(_t(recs), msd=True)
     assert str(got.value) == want.value.message
+
+
+@pytest.mark.parametrize("bad_byte", [ord("`"), ord("{"), ord("A"), 0xFF, 1])
+def test_w8_contiguous_alphabet_symbol_check(rs, ref, bad_byte):
+    """8-byte records over a-z take the SWAR scan: a byte just below or above
+    the alphabet, anywhere before the first NUL, is reported like the
+    reference (after the key spec); bytes after a NUL are ignored."""
+    from oracle import OracleError
+
+    recs = _records(11, 5000, 8, "abcdefghijklmnopqrstuvwxyz", short_every=2)
+    ok = recs.copy()
+    ok[7, 3] = 0
+    ok[7, 4:] = 0
+    order, _ = _ordinal_order(ok, "abcdefghijklmnopqrstuvwxyz")
+    ok[7, 5] = bad_byte  # after the NUL: not part of the string (the output record is NUL-padded)
+    got, _ = rs.sort_fixed_str(_t(ok), msd=True)
+    want = ok[order].copy()
+    want[want[:, 3] == 0, 4:] = 0
+    assert np.array_equal(got.cpu().numpy(), want)
+    recs[4000, 0] = ord("a")
+    recs[4000, 1] = bad_byte
+    recs[4000, 2:] = ord("b")
+    with pytest.raises(OracleError) as w:  # fails at the symbol, before any count space exists
+        ref.sort_strings(recs, "abcdefghijklmnopqrstuvwxyz", 10**12)
+    with pytest.raises(rs.Error) as g:
+        rs.sort_fixed_str(_t(recs), msd=True)
+    assert str(g.value) == w.value.message
