@@ -493,6 +493,35 @@ void grid_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, u
   if (cells > 0xFFFFFFFFull)
     fail(RS_CELL_BUDGET_EXCEEDED, "a single grid holds at most 2^32-1 cells");
   reset_stats(ws);
+  if constexpr (Out::kWordBytes > 0) {
+    if (n > 0 && n <= kSmallMax && cells <= kSmemCellsMax) {  // one cooperative launch
+      auto* g = ws.get<uint32_t>(kSlotCounts, cells + 1);
+      RS_CUDA(cudaMemsetAsync(g, 0, (cells + 1) * sizeof(uint32_t), ws.stream));
+      auto* kern = k_small_sort<Map, Out>;
+      const size_t smem = (cells + 1) * sizeof(uint32_t);
+      static int per_sm = [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>((kSmemCellsMax + 1) * sizeof(uint32_t)));
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kSmallThreads, (kSmemCellsMax + 1) * sizeof(uint32_t));
+        return b < 1 ? 1 : b;
+      }();
+      const uint64_t want = (n + 4 * kSmallThreads - 1) / (4 * kSmallThreads);
+      // at most one CTA per SM: the flush into the global grid is cells x CTAs atomics
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(want, (uint64_t)sm_count()));
+      uint32_t cells32 = static_cast<uint32_t>(cells);
+      DevStats* stp = ws.stats;
+      void* args[] = {const_cast<typename Map::In**>(&in), &n, &map, &cells32, &out, &g, &stp, &radix, &total_digits,
+                      &frac_digits};
+      {
+        PassTimer pt_(RS_PASS_COUNT, ws.stream);
+        RS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kSmallThreads), args, smem,
+                                            ws.stream));
+      }
+      pull_stats(ws);
+      return;
+    }
+  }
   auto* counts = ws.get<uint32_t>(kSlotCounts, cells);
   count_pass(ws, in, n, map, cells, counts);
   scan_pass(ws, counts, cells, n);

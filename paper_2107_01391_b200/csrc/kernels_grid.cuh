@@ -863,4 +863,161 @@ __global__ void k_report(const K* __restrict__ sorted, uint64_t n, uint32_t radi
   }
 }
 
+// ------------------------------------------------- small inputs, one launch
+// Grids of at most kSmemCellsMax cells and inputs of at most kSmallMax keys
+// (cfg1: 2^20 keys, 10^3 cells) are launch-bound on the multi-pass path.
+// Here count, scan, emit and report are ONE cooperative launch (every CTA
+// resident): each CTA counts a slice into a shared grid and flushes it into
+// the global grid, a grid-wide barrier, then every CTA scans the global grid
+// in shared memory and writes its share of output positions (each thread
+// four consecutive positions: one binary search, then a walk), and CTA 0
+// computes the report (per-row spans, as k_report).  A key outside the grid
+// or a flagged input skips the emit (the host redoes or raises).
+constexpr uint64_t kSmallMax = 1ull << 22;
+constexpr int kSmallThreads = 1024;
+
+template <class Map, class Out>
+__global__ void __launch_bounds__(kSmallThreads) k_small_sort(const typename Map::In* __restrict__ in, uint64_t n,
+                                                              Map map, uint32_t cells, Out out,
+                                                              uint32_t* gcount,  // [cells + 1] zeroed; [cells] = barrier
+                                                              DevStats* st, uint32_t radix, uint32_t total_digits,
+                                                              uint32_t frac_digits) {
+  extern __shared__ uint32_t s_c[];  // [cells + 1]: counts, then exclusive offsets (s_c[cells] = n)
+  __shared__ uint32_t s_scan[kSmallThreads / 32];
+  __shared__ unsigned long long s_span[kSmallThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t c = threadIdx.x; c <= cells; c += blockDim.x) s_c[c] = 0;
+  __syncthreads();
+  unsigned long long mx = 0;
+  unsigned flags = 0;
+  bool ovf = false;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  auto count = [&](typename Map::In x) {
+    const unsigned long long k = map(x, flags);
+    mx = k > mx ? k : mx;
+    if (k < cells) atomicAdd(&s_c[k], 1u);
+    else ovf = true;
+  };
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  using In = typename Map::In;
+  if constexpr (sizeof(In) == 4 && !is_f64_map<Map>::value) {  // 16-byte vectors, all of a thread's loads in flight
+    if ((reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+      const uint64_t nv = n / 4;
+      const auto* v4 = reinterpret_cast<const uint4*>(in);
+      for (uint64_t p = i; p < nv; p += 2 * stride) {
+        const uint4 a = __ldcs(v4 + p);
+        const bool two = p + stride < nv;
+        const uint4 b = two ? __ldcs(v4 + p + stride) : make_uint4(0, 0, 0, 0);
+        count(static_cast<In>(a.x)); count(static_cast<In>(a.y)); count(static_cast<In>(a.z)); count(static_cast<In>(a.w));
+        if (two) {
+          count(static_cast<In>(b.x)); count(static_cast<In>(b.y)); count(static_cast<In>(b.z)); count(static_cast<In>(b.w));
+        }
+      }
+      i = nv * 4 + i;
+    }
+  }
+  for (; i < n; i += stride) count(__ldcs(in + i));
+  __syncthreads();
+  for (uint32_t c = threadIdx.x; c < cells; c += blockDim.x)
+    if (s_c[c]) atomicAdd(&gcount[c], s_c[c]);
+  warp_max_to(mx, &st->max_key);
+  flags = warp_or(flags | (ovf ? 0x80000000u : 0u));
+  if (lane == 0 && flags) {
+    if (flags & 0x7fffffffu) atomicOr(&st->flags, flags & 0x7fffffffu);
+    if (flags & 0x80000000u) atomicOr(&st->overflow, 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // grid-wide barrier (cooperative launch: all CTAs are resident)
+    __threadfence();
+    atomicAdd(&gcount[cells], 1u);
+    while (*reinterpret_cast<volatile uint32_t*>(&gcount[cells]) < gridDim.x) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+  if (*reinterpret_cast<volatile unsigned*>(&st->overflow) || *reinterpret_cast<volatile unsigned*>(&st->flags))
+    return;
+  // exclusive offsets of the global grid, in every CTA
+  const uint32_t per = (cells + blockDim.x - 1) / blockDim.x, c0 = threadIdx.x * per;
+  uint32_t sum = 0;
+  for (uint32_t j = 0; j < per; ++j)
+    if (c0 + j < cells) {
+      const uint32_t v = __ldcg(gcount + c0 + j);
+      s_c[c0 + j] = v;
+      sum += v;
+    }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_scan[warp] = inc;
+  __syncthreads();
+  uint32_t run = inc - sum;
+  {
+    const uint32_t t = s_scan[lane];
+    uint32_t ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    run += __shfl_sync(0xffffffffu, ti - t, warp);
+  }
+  for (uint32_t j = 0; j < per; ++j)
+    if (c0 + j < cells) {
+      const uint32_t v = s_c[c0 + j];
+      s_c[c0 + j] = run;
+      run += v;
+    }
+  if (threadIdx.x == blockDim.x - 1) s_c[cells] = run;
+  __syncthreads();
+  // emit: this CTA's share of positions, four per thread
+  const uint64_t share = ((n + gridDim.x - 1) / gridDim.x + 3) & ~3ull;
+  const uint64_t p0 = (uint64_t)blockIdx.x * share, p1 = p0 + share < n ? p0 + share : n;
+  for (uint64_t p = p0 + 4ull * threadIdx.x; p < p1; p += 4ull * blockDim.x) {
+    uint32_t lo = 0, hi = cells;  // the last cell whose offset is <= p (it is occupied)
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_c[mid] <= p) lo = mid;
+      else hi = mid;
+    }
+    uint32_t cv[4];
+    uint32_t cell = lo;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      while (cell + 1 < cells && s_c[cell + 1] <= p + e) ++cell;
+      cv[e] = cell;
+    }
+    out.put4(p, cv, p1);
+  }
+  if (blockIdx.x != 0) return;
+  // report (k_report's definition): per occupied leading-digit row, max - min + 1
+  const unsigned long long top = *reinterpret_cast<volatile unsigned long long*>(&st->max_key);
+  const uint32_t digits = total_digits ? total_digits : d_digit_count(top / d_pow(10, frac_digits)) + frac_digits;
+  const unsigned long long mod = d_pow(radix, digits - 1);
+  unsigned long long span = 0;
+  for (uint32_t r = warp; r < radix && (unsigned long long)r * mod < cells; r += blockDim.x / 32) {
+    const uint32_t a = static_cast<uint32_t>(r * mod);
+    const uint32_t b = (unsigned long long)(r + 1) * mod < cells ? static_cast<uint32_t>((r + 1) * mod) : cells;
+    uint32_t first = 0xffffffffu, last = 0;
+    for (uint32_t c = a + lane; c < b; c += 32)
+      if (s_c[c + 1] > s_c[c]) {
+        first = c < first ? c : first;
+        last = c;
+      }
+    first = __reduce_min_sync(0xffffffffu, first);
+    last = __reduce_max_sync(0xffffffffu, last);
+    if (first != 0xffffffffu) span += last - first + 1;
+  }
+  if (lane == 0) s_span[warp] = span;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long total = 0;
+    for (int w = 0; w < kSmallThreads / 32; ++w) total += s_span[w];
+    st->cells_traversed = total;
+    st->report_digits = digits;
+  }
+}
+
 }  // namespace rsb
