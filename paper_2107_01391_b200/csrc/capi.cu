@@ -484,6 +484,34 @@ void emit_pass(Workspace& ws, uint64_t n, Out out) {
   }
 }
 
+// The one-launch path for small inputs (k_small_sort); with auto_cells the
+// grid comes from the max inside the launch.  Stats pulled on return;
+// h_stats->overflow == 2: the grid did not qualify (max known).
+template <class Map, class Out>
+void small_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, uint32_t cells, Out out,
+                uint32_t radix, uint32_t total_digits, uint32_t frac_digits, bool auto_cells, uint64_t budget) {
+  reset_stats(ws);
+  auto* g = ws.get<uint32_t>(kSlotCounts, kSmemCellsMax + 2);
+  RS_CUDA(cudaMemsetAsync(g, 0, (kSmemCellsMax + 2) * sizeof(uint32_t), ws.stream));
+  auto* kern = k_small_sort<Map, Out>;
+  const size_t smem = (kSmemCellsMax + 1) * sizeof(uint32_t);
+  static const bool attr = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem)), true);
+  (void)attr;
+  // at most one CTA per SM: the flush into the global grid is cells x CTAs atomics
+  const uint64_t want = (n + 4 * kSmallThreads - 1) / (4 * kSmallThreads);
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(want, (uint64_t)sm_count()));
+  DevStats* stp = ws.stats;
+  void* args[] = {const_cast<typename Map::In**>(&in), &n, &map, &cells, &out, &g, &stp, &radix, &total_digits,
+                  &frac_digits, &auto_cells, &budget};
+  {
+    PassTimer pt_(RS_PASS_COUNT, ws.stream);
+    RS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kSmallThreads), args, smem,
+                                        ws.stream));
+  }
+  pull_stats(ws);
+}
+
 // One full single-grid sort: count -> scan -> emit -> report.  Leaves the
 // stats (max, overflow, flags, report) in ws.h_stats after one sync.
 template <class Map, class Out, class K>
@@ -495,30 +523,7 @@ void grid_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, u
   reset_stats(ws);
   if constexpr (Out::kWordBytes > 0) {
     if (n > 0 && n <= kSmallMax && cells <= kSmemCellsMax) {  // one cooperative launch
-      auto* g = ws.get<uint32_t>(kSlotCounts, cells + 1);
-      RS_CUDA(cudaMemsetAsync(g, 0, (cells + 1) * sizeof(uint32_t), ws.stream));
-      auto* kern = k_small_sort<Map, Out>;
-      const size_t smem = (cells + 1) * sizeof(uint32_t);
-      static int per_sm = [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>((kSmemCellsMax + 1) * sizeof(uint32_t)));
-        int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kSmallThreads, (kSmemCellsMax + 1) * sizeof(uint32_t));
-        return b < 1 ? 1 : b;
-      }();
-      const uint64_t want = (n + 4 * kSmallThreads - 1) / (4 * kSmallThreads);
-      // at most one CTA per SM: the flush into the global grid is cells x CTAs atomics
-      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(want, (uint64_t)sm_count()));
-      uint32_t cells32 = static_cast<uint32_t>(cells);
-      DevStats* stp = ws.stats;
-      void* args[] = {const_cast<typename Map::In**>(&in), &n, &map, &cells32, &out, &g, &stp, &radix, &total_digits,
-                      &frac_digits};
-      {
-        PassTimer pt_(RS_PASS_COUNT, ws.stream);
-        RS_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kSmallThreads), args, smem,
-                                            ws.stream));
-      }
-      pull_stats(ws);
+      small_sort(ws, in, n, map, static_cast<uint32_t>(cells), out, radix, total_digits, frac_digits, false, 0);
       return;
     }
   }
@@ -566,7 +571,21 @@ void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, cons
                             pow10u(hint) > budget && sizeof(typename Map::In) == 4;
   uint32_t key_bits = 8 * sizeof(typename Map::In);
   if (!hinted && !msd_declared) {
-    const unsigned long long mx = device_max(ws, in, n, map);
+    unsigned long long mx;
+    if (Out::kWordBytes > 0 && n <= kSmallMax && out_capacity >= n) {
+      // small input: max, grid, count, scan, emit and report in one launch when
+      // the grid fits shared memory and the budget
+      small_sort(ws, in, n, map, 0u, out, 10u, 0u, 0u, true, budget);
+      check_flags(ws.h_stats->flags);
+      if (ws.h_stats->overflow != 2) {
+        const uint32_t d = static_cast<uint32_t>(ws.h_stats->report_digits);
+        if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{10, d, d}};
+        return;
+      }
+      mx = ws.h_stats->max_key;
+    } else {
+      mx = device_max(ws, in, n, map);
+    }
     digits = digit_count(mx);
     key_bits = 1;  // MSD digits cover the max's bit width only
     while (key_bits < 64 && (mx >> key_bits)) ++key_bits;

@@ -876,16 +876,55 @@ __global__ void k_report(const K* __restrict__ sorted, uint64_t n, uint32_t radi
 constexpr uint64_t kSmallMax = 1ull << 22;
 constexpr int kSmallThreads = 1024;
 
+// With auto_cells (decimal integers without a declared width) the grid is
+// derived in the same launch: a max phase, a first barrier, cells =
+// 10^digits(max); a grid above the shared limit or the budget stops the
+// launch (st->overflow = 2) and the host takes the multi-pass path with the
+// max it now knows.
+__device__ __forceinline__ void grid_barrier(uint32_t* ctr) {  // all CTAs resident (cooperative launch)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (*reinterpret_cast<volatile uint32_t*>(ctr) < gridDim.x) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 template <class Map, class Out>
 __global__ void __launch_bounds__(kSmallThreads) k_small_sort(const typename Map::In* __restrict__ in, uint64_t n,
                                                               Map map, uint32_t cells, Out out,
-                                                              uint32_t* gcount,  // [cells + 1] zeroed; [cells] = barrier
+                                                              uint32_t* gcount,  // [kSmemCellsMax + 2] zeroed
                                                               DevStats* st, uint32_t radix, uint32_t total_digits,
-                                                              uint32_t frac_digits) {
+                                                              uint32_t frac_digits, bool auto_cells, uint64_t budget) {
   extern __shared__ uint32_t s_c[];  // [cells + 1]: counts, then exclusive offsets (s_c[cells] = n)
   __shared__ uint32_t s_scan[kSmallThreads / 32];
   __shared__ unsigned long long s_span[kSmallThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* bar = gcount + kSmemCellsMax;  // two barrier counters
+  if (auto_cells) {
+    unsigned long long m = 0;
+    unsigned fl = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      const unsigned long long k = map(__ldcs(in + i), fl);
+      m = k > m ? k : m;
+    }
+    warp_max_to(m, &st->max_key);
+    fl = warp_or(fl);
+    if (lane == 0 && fl) atomicOr(&st->flags, fl);
+    grid_barrier(bar + 1);
+    if (*reinterpret_cast<volatile unsigned*>(&st->flags)) return;  // the host raises
+    const unsigned long long mxk = *reinterpret_cast<volatile unsigned long long*>(&st->max_key);
+    const uint32_t d = d_digit_count(mxk);
+    const unsigned long long need = d_pow(10, d);
+    if (need > kSmemCellsMax || need > budget) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) st->overflow = 2;  // multi-pass path (or the budget error)
+      return;
+    }
+    cells = static_cast<uint32_t>(need);
+  }
   for (uint32_t c = threadIdx.x; c <= cells; c += blockDim.x) s_c[c] = 0;
   __syncthreads();
   unsigned long long mx = 0;
@@ -926,14 +965,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_sort(const typename Map
     if (flags & 0x7fffffffu) atomicOr(&st->flags, flags & 0x7fffffffu);
     if (flags & 0x80000000u) atomicOr(&st->overflow, 1u);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // grid-wide barrier (cooperative launch: all CTAs are resident)
-    __threadfence();
-    atomicAdd(&gcount[cells], 1u);
-    while (*reinterpret_cast<volatile uint32_t*>(&gcount[cells]) < gridDim.x) __nanosleep(64);
-    __threadfence();
-  }
-  __syncthreads();
+  grid_barrier(bar);
   if (*reinterpret_cast<volatile unsigned*>(&st->overflow) || *reinterpret_cast<volatile unsigned*>(&st->flags))
     return;
   // exclusive offsets of the global grid, in every CTA
