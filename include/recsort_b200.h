@@ -238,6 +238,20 @@ rs_status rs_partition_u32(const uint32_t* keys, uint64_t n, uint64_t divisor,
                            const uint32_t* h_bounds, uint32_t parts,
                            uint32_t* out, uint64_t* h_counts, void* stream);
 
+/* The two passes of rs_partition_u32 apart, for the multi-GPU exchange of
+ * SURVEY 8e (wide keys): per-part counts of this rank's keys, then the
+ * scatter with part p written at h_dst[p] + h_offsets[p] + rank-in-part —
+ * h_dst[p] a device address (a peer GPU's receive buffer mapped over NVLink,
+ * e.g. torch symmetric memory), so the partition kernel itself performs the
+ * all-to-all.  h_dst / h_offsets: `parts` host values. */
+rs_status rs_part_counts_u32(const uint32_t* keys, uint64_t n, uint64_t divisor,
+                             const uint32_t* h_bounds, uint32_t parts,
+                             uint64_t* h_counts, void* stream);
+rs_status rs_partition_u32_to(const uint32_t* keys, uint64_t n, uint64_t divisor,
+                              const uint32_t* h_bounds, uint32_t parts,
+                              const uint64_t* h_dst, const uint64_t* h_offsets,
+                              void* stream);
+
 /* ---- synthetic config inputs (bench/test utility, not part of the sort) --
  * Counter-addressed SplitMix64 (splitmix64.hpp:14-19): element i
  * of Splitmix64(seed).  Bit-identical to the host generators in oracle/. */

@@ -1427,49 +1427,103 @@ rs_status rs_bucket_hist_u32(const uint32_t* keys, uint64_t n, uint64_t divisor,
   });
 }
 
+// Per-part counts and the scatter of rs_partition_u32, shared with the
+// multi-GPU exchange (rs_part_counts_u32 / rs_partition_u32_to).
+extern "C++" {
+struct PartSetup {
+  unsigned long long magic;
+  uint32_t* d_bounds;
+  unsigned long long* counts;
+  unsigned long long* cursors;
+  uint32_t** d_dst;
+};
+
+PartSetup part_setup(Workspace& ws, uint64_t divisor, const uint32_t* h_bounds, uint32_t parts) {
+  if (parts == 0 || parts > 1024) fail(RS_INVALID_ARGUMENT, "parts must be in [1, 1024]");
+  if (divisor == 0) fail(RS_INVALID_ARGUMENT, "divisor must be positive");
+  for (uint32_t p = 0; p < parts; ++p)
+    if (h_bounds[p] > h_bounds[p + 1]) fail(RS_INVALID_RANGE, "part bounds must be non-decreasing");
+  auto* scratch = ws.get<unsigned long long>(kSlotHist, 2048 + 1024 + 1025);
+  PartSetup s;
+  s.counts = scratch;
+  s.cursors = scratch + 1024;
+  s.d_dst = reinterpret_cast<uint32_t**>(scratch + 2048);
+  s.d_bounds = reinterpret_cast<uint32_t*>(scratch + 3072);
+  s.magic = divisor == 1 ? 0ull : magic_div(divisor);
+  RS_CUDA(cudaMemcpyAsync(s.d_bounds, h_bounds, (parts + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, ws.stream));
+  return s;
+}
+
+std::vector<unsigned long long> part_counts(Workspace& ws, const uint32_t* keys, uint64_t n, const PartSetup& s,
+                                            uint32_t parts) {
+  std::vector<unsigned long long> hc(parts, 0);
+  RS_CUDA(cudaMemsetAsync(s.counts, 0, parts * sizeof(unsigned long long), ws.stream));
+  if (n > 0) {
+    PassTimer pt_(RS_PASS_MSD_HIST, ws.stream);
+    k_part_count<<<stream_grid(n, kMsdThreads * 16, 8), kMsdThreads, 0, ws.stream>>>(keys, n, s.magic, s.d_bounds,
+                                                                                     parts, s.counts);
+    RS_LAUNCH_CHECK();
+  }
+  RS_CUDA(cudaMemcpyAsync(hc.data(), s.counts, parts * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ws.stream));
+  RS_CUDA(cudaStreamSynchronize(ws.stream));
+  return hc;
+}
+
+void part_scatter(Workspace& ws, const uint32_t* keys, uint64_t n, const PartSetup& s, uint32_t parts,
+                  const uint64_t* h_dst, const unsigned long long* h_cursor0) {
+  RS_CUDA(cudaMemcpyAsync(s.cursors, h_cursor0, parts * sizeof(unsigned long long), cudaMemcpyHostToDevice, ws.stream));
+  RS_CUDA(cudaMemcpyAsync(s.d_dst, h_dst, parts * sizeof(uint64_t), cudaMemcpyHostToDevice, ws.stream));
+  if (n > 0) {
+    PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
+    k_part_scatter<<<stream_grid(n, kPartChunk, 4), kMsdThreads, 0, ws.stream>>>(keys, n, s.magic, s.d_bounds, parts,
+                                                                                 s.cursors, s.d_dst);
+    RS_LAUNCH_CHECK();
+  }
+  RS_CUDA(cudaStreamSynchronize(ws.stream));  // the host arrays above are stack memory
+}
+}  // extern "C++"
+
 rs_status rs_partition_u32(const uint32_t* keys, uint64_t n, uint64_t divisor, const uint32_t* h_bounds,
                            uint32_t parts, uint32_t* out, uint64_t* h_counts, void* stream) {
   return guarded([&] {
     ensure_device();
-    if (parts == 0 || parts > 1024) fail(RS_INVALID_ARGUMENT, "parts must be in [1, 1024]");
-    if (divisor == 0) fail(RS_INVALID_ARGUMENT, "divisor must be positive");
-    for (uint32_t p = 0; p < parts; ++p)
-      if (h_bounds[p] > h_bounds[p + 1]) fail(RS_INVALID_RANGE, "part bounds must be non-decreasing");
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
-    auto* scratch = ws.get<unsigned long long>(kSlotHist, 2048 + 1025);
-    unsigned long long* counts = scratch;
-    unsigned long long* cursors = scratch + 1024;
-    auto* d_bounds = reinterpret_cast<uint32_t*>(scratch + 2048);
-    RS_CUDA(cudaMemcpyAsync(d_bounds, h_bounds, (parts + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, ws.stream));
-    RS_CUDA(cudaMemsetAsync(counts, 0, parts * sizeof(unsigned long long), ws.stream));
-    const unsigned long long magic = divisor == 1 ? 0ull : magic_div(divisor);
-    std::vector<unsigned long long> hc(parts, 0);
-    if (n > 0) {
-      {
-        PassTimer pt_(RS_PASS_MSD_HIST, ws.stream);
-        k_part_count<<<stream_grid(n, kMsdThreads * 16, 8), kMsdThreads, 0, ws.stream>>>(keys, n, magic, d_bounds,
-                                                                                         parts, counts);
-        RS_LAUNCH_CHECK();
-      }
-      RS_CUDA(cudaMemcpyAsync(hc.data(), counts, parts * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ws.stream));
-      RS_CUDA(cudaStreamSynchronize(ws.stream));
-      std::vector<unsigned long long> starts(parts, 0);
-      unsigned long long run = 0;
-      for (uint32_t p = 0; p < parts; ++p) {
-        starts[p] = run;
-        run += hc[p];
-      }
-      RS_CUDA(cudaMemcpyAsync(cursors, starts.data(), parts * sizeof(unsigned long long), cudaMemcpyHostToDevice, ws.stream));
-      {
-        PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
-        k_part_scatter<<<stream_grid(n, kPartChunk, 4), kMsdThreads, 0, ws.stream>>>(keys, n, magic, d_bounds, parts,
-                                                                                     cursors, out);
-        RS_LAUNCH_CHECK();
-      }
-      RS_CUDA(cudaStreamSynchronize(ws.stream));
+    const PartSetup s = part_setup(ws, divisor, h_bounds, parts);
+    const std::vector<unsigned long long> hc = part_counts(ws, keys, n, s, parts);
+    std::vector<unsigned long long> starts(parts, 0);
+    std::vector<uint64_t> dst(parts, reinterpret_cast<uint64_t>(out));
+    unsigned long long run = 0;
+    for (uint32_t p = 0; p < parts; ++p) {
+      starts[p] = run;
+      run += hc[p];
     }
+    if (n > 0) part_scatter(ws, keys, n, s, parts, dst.data(), starts.data());
     if (h_counts)
       for (uint32_t p = 0; p < parts; ++p) h_counts[p] = hc[p];
+  });
+}
+
+rs_status rs_part_counts_u32(const uint32_t* keys, uint64_t n, uint64_t divisor, const uint32_t* h_bounds,
+                             uint32_t parts, uint64_t* h_counts, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    if (!h_counts) fail(RS_INVALID_ARGUMENT, "null counts");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    const PartSetup s = part_setup(ws, divisor, h_bounds, parts);
+    const std::vector<unsigned long long> hc = part_counts(ws, keys, n, s, parts);
+    for (uint32_t p = 0; p < parts; ++p) h_counts[p] = hc[p];
+  });
+}
+
+rs_status rs_partition_u32_to(const uint32_t* keys, uint64_t n, uint64_t divisor, const uint32_t* h_bounds,
+                              uint32_t parts, const uint64_t* h_dst, const uint64_t* h_offsets, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    if (!h_dst || !h_offsets) fail(RS_INVALID_ARGUMENT, "null destination arrays");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    const PartSetup s = part_setup(ws, divisor, h_bounds, parts);
+    std::vector<unsigned long long> cur(h_offsets, h_offsets + parts);
+    part_scatter(ws, keys, n, s, parts, h_dst, cur.data());
   });
 }
 

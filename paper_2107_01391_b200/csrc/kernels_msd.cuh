@@ -81,17 +81,22 @@ __global__ void __launch_bounds__(kMsdThreads) k_part_count(const uint32_t* __re
 
 // Scatter into part-contiguous order (pass 2).  Each CTA takes a chunk of
 // keys, ranks them per part in shared memory and reserves its run in every
-// part with one global atomic per (CTA chunk, part).
+// part with one global atomic per (CTA chunk, part).  Part p is written at
+// dst[p] + cursor: one buffer for a local partition, or — the multi-GPU
+// exchange — each part straight into its destination rank's receive buffer
+// through NVLink peer pointers (no separate all-to-all).
 constexpr int kPartChunk = 4096;
 __global__ void __launch_bounds__(kMsdThreads) k_part_scatter(const uint32_t* __restrict__ keys, uint64_t n,
                                                               unsigned long long magic,
                                                               const uint32_t* __restrict__ bounds, uint32_t parts,
                                                               unsigned long long* __restrict__ cursors,
-                                                              uint32_t* __restrict__ out) {
+                                                              uint32_t* const* __restrict__ dst) {
   __shared__ uint32_t s_bounds[1025];
   __shared__ uint32_t s_c[1024];
   __shared__ unsigned long long s_base[1024];
+  __shared__ uint32_t* s_dst[1024];
   for (uint32_t i = threadIdx.x; i <= parts; i += blockDim.x) s_bounds[i] = bounds[i];
+  for (uint32_t i = threadIdx.x; i < parts; i += blockDim.x) s_dst[i] = dst[i];
   for (uint64_t c0 = (uint64_t)blockIdx.x * kPartChunk; c0 < n; c0 += (uint64_t)gridDim.x * kPartChunk) {
     for (uint32_t i = threadIdx.x; i < parts; i += blockDim.x) s_c[i] = 0;
     __syncthreads();
@@ -113,7 +118,7 @@ __global__ void __launch_bounds__(kMsdThreads) k_part_scatter(const uint32_t* __
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kPartChunk / kMsdThreads; ++j)
-      if (p[j] != 0xffffffffu) out[s_base[p[j]] + r[j]] = k[j];
+      if (p[j] != 0xffffffffu) s_dst[p[j]][s_base[p[j]] + r[j]] = k[j];
     __syncthreads();
   }
 }

@@ -16,9 +16,16 @@ then the local order).  The reference's stable order (radix_sort_lsd_by,
 baselines.hpp:24-46) is unique, so the rank slices concatenate to it.
 
 Wide keys (cfg5): the leading-digit bucket histogram (rs_bucket_hist_u32) is
-all-reduced, G-1 splitters are cut on bucket boundaries, keys are range
-partitioned (rs_partition_u32) and exchanged with one all-to-all; every rank
-then sorts what it received.
+all-reduced, G-1 splitters are cut on bucket boundaries and every rank sorts
+the key range it owns.  The exchange is fused into the partition kernel:
+per-destination counts are all-gathered (a G x G table, G^2 integers), each
+rank's write offset in every destination follows from it, and the scatter
+(rs_partition_u32_to) stores each part straight into its destination rank's
+receive buffer through NVLink peer pointers (torch symmetric memory) — no
+separate all-to-all pass over the keys.  A device-side barrier of the
+symmetric buffer orders the writes before the local sorts.  The NCCL
+all-to-all path (rs_partition_u32 + all_to_all_single) remains for process
+groups without peer memory.
 
 The device phases are injected (``ops``) so the collective and splitter logic
 can be exercised on CPU with the gloo backend in tests; the product path
@@ -27,7 +34,6 @@ always uses ``GpuOps`` (the CUDA library) and there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
@@ -72,9 +78,12 @@ def bucket_splitters(hist: torch.Tensor, world: int) -> list[int]:
     return [lo for lo, _ in cell_ranges(prefix, world)] + [hist.numel()]
 
 
-@dataclass
 class GpuOps:
     """Device phases through the C-ABI (include/recsort_b200.h)."""
+
+    def __init__(self):
+        self._symm = None  # (local tensor, symmetric-memory handle) of the receive buffer
+        self._symm_cap = 0
 
     def _lib(self):
         from . import _lib
@@ -124,6 +133,45 @@ class GpuOps:
 
         k, v, _ = sort_u32_kv(keys, vals, max_cells=max(cells, DEFAULT_CELL_BUDGET))
         return k, v
+
+    def part_counts(self, keys: torch.Tensor, divisor: int, bounds: list[int]) -> list[int]:
+        parts = len(bounds) - 1
+        hb = (ctypes.c_uint32 * (parts + 1))(*bounds)
+        hc = (ctypes.c_uint64 * parts)()
+        self._check(self._lib().rs_part_counts_u32(ctypes.c_void_p(keys.data_ptr()), keys.numel(), divisor, hb, parts,
+                                                   hc, self._stream()))
+        return [int(x) for x in hc]
+
+    def partition_to(self, keys: torch.Tensor, divisor: int, bounds: list[int], dsts: list[int],
+                     offsets: list[int]) -> None:
+        """Part p of `keys` written at device address dsts[p] + 4 * offsets[p]."""
+        parts = len(bounds) - 1
+        hb = (ctypes.c_uint32 * (parts + 1))(*bounds)
+        hd = (ctypes.c_uint64 * parts)(*dsts)
+        ho = (ctypes.c_uint64 * parts)(*offsets)
+        self._check(self._lib().rs_partition_u32_to(ctypes.c_void_p(keys.data_ptr()), keys.numel(), divisor, hb,
+                                                    parts, hd, ho, self._stream()))
+
+    def peer_buffer(self, cap: int, group=None) -> tuple[torch.Tensor, list[int]]:
+        """This rank's receive buffer (>= cap int32) and every rank's address of
+        it (symmetric memory over NVLink); grown identically on every rank."""
+        import torch.distributed._symmetric_memory as symm
+
+        if self._symm is None or self._symm_cap < cap:
+            size = max(cap, 2 * self._symm_cap, 1 << 20)
+            t = symm.empty(size, dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
+            h = symm.rendezvous(t, group or dist.group.WORLD)
+            self._symm, self._symm_cap = (t, h), size
+        t, h = self._symm
+        return t, [int(p) for p in h.buffer_ptrs]
+
+    def exchange_barrier(self, group=None) -> None:
+        """Device-side barrier over the receive buffer: every rank's writes
+        before it are visible to every rank after it (stream-ordered)."""
+        self._symm[1].barrier()
+
+    def peer_exchange_ok(self, group=None) -> bool:
+        return dist.get_backend(group) == "nccl"
 
     def sort(self, keys: torch.Tensor, key_digits: int = 0) -> torch.Tensor:
         from . import sort_u32
@@ -175,15 +223,42 @@ def sharded_kv_sort(keys: torch.Tensor, vals: torch.Tensor, cells: int, ops=None
     return ops.sort_kv(rk, rv, cells)
 
 
+_GPU_OPS = None
+
+
+def _gpu_ops() -> "GpuOps":
+    global _GPU_OPS
+    if _GPU_OPS is None:  # one receive buffer per process, reused across calls
+        _GPU_OPS = GpuOps()
+    return _GPU_OPS
+
+
 def range_partition_sort(keys: torch.Tensor, divisor: int, buckets: int, ops=None, group=None,
-                         key_digits: int = 0) -> torch.Tensor:
-    """Wide keys: MSD histogram -> all-reduce -> splitters -> partition ->
-    all-to-all -> local sort.  Returns this rank's slice of the global order."""
-    ops = ops or GpuOps()
+                         key_digits: int = 0, exchange: str = "auto") -> torch.Tensor:
+    """Wide keys: MSD histogram -> all-reduce -> splitters -> partition fused
+    with the exchange (peer stores) -> local sort.  Returns this rank's slice
+    of the global order.  exchange: "p2p" (partition kernel writes into the
+    peers' receive buffers), "nccl" (partition + all_to_all_single), "auto"."""
+    ops = ops or _gpu_ops()
     world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
     hist = ops.bucket_hist(keys, divisor, buckets)
     dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)  # C2
     bounds = bucket_splitters(hist.cpu(), world)
+    if exchange == "auto":
+        exchange = "p2p" if getattr(ops, "peer_exchange_ok", lambda g: False)(group) else "nccl"
+    if exchange == "p2p":
+        send = torch.tensor(ops.part_counts(keys, divisor, bounds), dtype=torch.int64, device=keys.device)
+        table = torch.empty(world * world, dtype=torch.int64, device=keys.device)
+        dist.all_gather_into_tensor(table, send, group=group)  # C[g][r]: keys rank g sends to rank r
+        table = table.view(world, world).cpu()
+        offsets = table[:rank].sum(0).tolist()  # where this rank's part r starts in rank r's buffer
+        n_recv = int(table[:, rank].sum())
+        buf, dsts = ops.peer_buffer(int(table.sum(0).max()), group)
+        ops.exchange_barrier(group)  # every rank is done with the buffer's previous contents
+        ops.partition_to(keys, divisor, bounds, dsts, offsets)
+        ops.exchange_barrier(group)  # every part has landed
+        return ops.sort(buf[:n_recv], key_digits)
     parted, send_counts = ops.partition(keys, divisor, bounds)
     send = torch.tensor(send_counts, dtype=torch.int64, device=keys.device)
     recv = torch.empty_like(send)

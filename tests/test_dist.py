@@ -45,6 +45,32 @@ class NumpyOps:
         order = np.argsort(k, kind="stable")
         return torch.from_numpy(keys.numpy()[order].copy()), torch.from_numpy(vals.numpy()[order].copy())
 
+    # the fused exchange: "peer memory" = tensors shared by the test's processes
+    def __init__(self, bufs=None, rank=0):
+        self.bufs, self.rank = bufs, rank
+
+    def part_counts(self, keys, divisor, bounds):
+        k = keys.numpy().view(np.uint32).astype(np.int64)
+        part = np.searchsorted(np.asarray(bounds[1:-1]), k // divisor, side="right")
+        return np.bincount(part, minlength=len(bounds) - 1).tolist()
+
+    def partition_to(self, keys, divisor, bounds, dsts, offsets):
+        k = keys.numpy().view(np.uint32).astype(np.int64)
+        part = np.searchsorted(np.asarray(bounds[1:-1]), k // divisor, side="right")
+        for r, off in enumerate(offsets):
+            mine = keys.numpy()[part == r]
+            dsts[r][off:off + mine.size] = torch.from_numpy(mine.copy())
+
+    def peer_buffer(self, cap, group=None):
+        assert cap <= self.bufs[self.rank].numel()
+        return self.bufs[self.rank], self.bufs
+
+    def exchange_barrier(self, group=None):
+        dist.barrier(group)
+
+    def peer_exchange_ok(self, group=None):
+        return self.bufs is not None
+
     def sort(self, keys, key_digits=0):
         return torch.from_numpy(np.sort(keys.numpy().view(np.uint32)).view(np.int32))
 
@@ -70,8 +96,11 @@ def _worker(rank, world, port, mode, shared):
         elif mode == "kv":
             vals = torch.arange(rank * n // world, (rank + 1) * n // world, dtype=torch.int32)
             out = torch.stack(sharded_kv_sort(mine, vals, shared["cells"], ops=NumpyOps()))
+        elif mode == "p2p":
+            out = range_partition_sort(mine, shared["divisor"], shared["buckets"],
+                                       ops=NumpyOps(shared["bufs"], rank), exchange="p2p")
         else:
-            out = range_partition_sort(mine, shared["divisor"], shared["buckets"], ops=NumpyOps())
+            out = range_partition_sort(mine, shared["divisor"], shared["buckets"], ops=NumpyOps(), exchange="nccl")
         torch.save(out, shared["dir"] + f"/out{rank}.pt")
     finally:
         dist.destroy_process_group()
@@ -148,3 +177,19 @@ def test_sharded_kv_sort_gloo_is_globally_stable(tmp_path, bound):
     order = np.argsort(keys, kind="stable")
     assert np.array_equal(got[0], keys[order])
     assert np.array_equal(got[1], order.astype(np.int32))
+
+
+def test_range_partition_fused_exchange_gloo(tmp_path):
+    """The fused exchange's bookkeeping (per-destination counts all-gathered,
+    write offsets per source rank, parts stored straight into the peers'
+    buffers, barrier, local sort) with two processes writing into each
+    other's shared buffers; twice in a row, so the reused buffers are
+    overwritten in order."""
+    rng = np.random.default_rng(9)
+    keys = torch.from_numpy(rng.integers(0, 2**32, 100_003, dtype=np.uint64).astype(np.uint32).view(np.int32))
+    keys[:30_000] = keys[0]  # a hot bucket on rank 0's side
+    bufs = [torch.zeros(keys.numel(), dtype=torch.int32).share_memory_() for _ in range(2)]
+    for _ in range(2):
+        outs = _run("p2p", keys, tmp_path, divisor=10**7, buckets=430, bufs=bufs)
+        got = np.concatenate([o.numpy().view(np.uint32) for o in outs])
+        assert np.array_equal(got, np.sort(keys.numpy().view(np.uint32)))

@@ -522,8 +522,9 @@ def test_dist_paths_on_device_nccl(rs, oracle):
         out = sharded_grid_sort(_t(keys.view(np.int32)), 10**6)
         assert np.array_equal(_np_u32(out), np.sort(keys))
         wide = oracle.gen_u32(22, 0, 1 << 21, 0)
-        out = range_partition_sort(_t(wide.view(np.int32)), 10**7, 430)
-        assert np.array_equal(_np_u32(out), np.sort(wide))
+        for exchange in ("p2p", "p2p", "nccl"):  # the fused peer-store exchange (twice: buffer reuse), then NCCL
+            out = range_partition_sort(_t(wide.view(np.int32)), 10**7, 430, exchange=exchange)
+            assert np.array_equal(_np_u32(out), np.sort(wide)), exchange
         vals = np.arange(keys.size, dtype=np.uint32)
         ko, vo = sharded_kv_sort(_t(keys.view(np.int32)), _t(vals.view(np.int32)), 10**6)
         wk, wv = oracle.radix_sort_lsd_kv(keys, vals)
