@@ -216,6 +216,19 @@ rs_status rs_sort_u32_kv_host(const uint32_t* h_keys, const uint32_t* h_vals,
                               rs_report* report, void* stream);
 
 /* ---- phase API (multi-GPU orchestration) -------------------- */
+/* Multi-GPU stable key/value placement ("within a cell, rank =
+ * sum of earlier ranks' counts + local rank"): keys/vals hold this rank's
+ * records in stable local order; record i with key k is written at
+ * h_dst_keys[o] / h_dst_vals[o] + cell_off[k] + i, o = cell_owner[k] — device
+ * addresses of the owners' output slices (peer buffers over NVLink), so the
+ * placement is the exchange and the slices come out in the reference's
+ * unique stable order (radix_sort_lsd_by, baselines.hpp:24-46).  cell_off
+ * (int64) and cell_owner (uint8) are device arrays of `cells` entries. */
+rs_status rs_kv_place_u32(const uint32_t* keys, const uint32_t* vals, uint64_t n,
+                          const int64_t* cell_off, const uint8_t* cell_owner, uint64_t cells,
+                          const uint64_t* h_dst_keys, const uint64_t* h_dst_vals,
+                          uint32_t ranks, void* stream);
+
 /* Count uint32 keys into a caller-owned grid of `cells` uint32 counters
  * (overwritten; the same counting pass as rs_sort_u32).  Keys >= cells are
  * not counted; h_max, if not NULL, receives the maximum key (host pointer;

@@ -1568,6 +1568,30 @@ rs_status rs_sort_u32_kv_host(const uint32_t* h_keys, const uint32_t* h_vals, ui
 }
 
 // ------------------------------------------------------------- phase API
+rs_status rs_kv_place_u32(const uint32_t* keys, const uint32_t* vals, uint64_t n, const int64_t* cell_off,
+                          const uint8_t* cell_owner, uint64_t cells, const uint64_t* h_dst_keys,
+                          const uint64_t* h_dst_vals, uint32_t ranks, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    if (ranks == 0 || ranks > 64) fail(RS_INVALID_ARGUMENT, "ranks must be in [1, 64]");
+    if (n > 0 && (!keys || !vals || !cell_off || !cell_owner)) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    if (!h_dst_keys || !h_dst_vals) fail(RS_INVALID_ARGUMENT, "null destination arrays");
+    (void)cells;
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    auto* d = ws.get<unsigned long long>(kSlotMisc, 128);
+    RS_CUDA(cudaMemcpyAsync(d, h_dst_keys, ranks * sizeof(uint64_t), cudaMemcpyHostToDevice, ws.stream));
+    RS_CUDA(cudaMemcpyAsync(d + 64, h_dst_vals, ranks * sizeof(uint64_t), cudaMemcpyHostToDevice, ws.stream));
+    if (n > 0) {
+      PassTimer pt_(RS_PASS_KV_SCATTER, ws.stream);
+      k_kv_place<<<stream_grid(n, 256 * 8, 8), 256, 0, ws.stream>>>(
+          keys, vals, n, reinterpret_cast<const long long*>(cell_off), cell_owner, reinterpret_cast<uint32_t* const*>(d),
+          reinterpret_cast<uint32_t* const*>(d + 64), ranks);
+      RS_LAUNCH_CHECK();
+    }
+    RS_CUDA(cudaStreamSynchronize(ws.stream));  // the host pointer arrays are the caller's
+  });
+}
+
 rs_status rs_count_u32(const uint32_t* keys, uint64_t n, uint32_t* counts, uint64_t cells,
                        uint32_t* h_max, void* stream) {
   return guarded([&] {

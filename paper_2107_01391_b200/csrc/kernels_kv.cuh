@@ -264,4 +264,34 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
   }
 }
 
+// Multi-GPU stable key/value placement: records already in
+// this rank's stable local order (record i, key k) go to their final global
+// position P = cell_off[k] + i in the output slice of the rank owning cell k
+// (cell_off folds in the global cell start, the earlier ranks' counts of k
+// and this rank's local start of k, minus the owner's slice start).  The
+// destination is a peer GPU's buffer mapped over NVLink, so the placement
+// kernel is the all-to-all; records of one cell land as one contiguous run.
+__global__ void __launch_bounds__(256) k_kv_place(const uint32_t* __restrict__ keys,
+                                                  const uint32_t* __restrict__ vals, uint64_t n,
+                                                  const long long* __restrict__ cell_off,
+                                                  const uint8_t* __restrict__ cell_owner,
+                                                  uint32_t* const* __restrict__ dst_k,
+                                                  uint32_t* const* __restrict__ dst_v, uint32_t ranks) {
+  __shared__ uint32_t* s_k[64];
+  __shared__ uint32_t* s_v[64];
+  for (uint32_t r = threadIdx.x; r < ranks; r += blockDim.x) {
+    s_k[r] = dst_k[r];
+    s_v[r] = dst_v[r];
+  }
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t k = __ldcs(keys + i);
+    const uint32_t r = __ldg(cell_owner + k);
+    const uint64_t off = static_cast<uint64_t>(__ldg(cell_off + k) + static_cast<long long>(i));
+    s_k[r][off] = k;
+    s_v[r][off] = __ldcs(vals + i);
+  }
+}
+
 }  // namespace rsb

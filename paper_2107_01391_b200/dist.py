@@ -7,13 +7,17 @@ and each rank then emits a contiguous range of cells holding about total/G
 keys (rs_emit_u32).  No key moves between GPUs: rank r's output is slice r
 of the globally sorted sequence.
 
-Stable key/value (cfg2 KV): the same all-reduced grid fixes the cell cuts;
-every rank sorts its shard stably (rs_sort_u32_kv), sends the records of
-cell range r to rank r (one all-to-all of keys and one of values) and sorts
-the concatenation of what it received — source ranks arrive in rank order,
-so equal keys keep their global input order (records of rank g' < g first,
-then the local order).  The reference's stable order (radix_sort_lsd_by,
-baselines.hpp:24-46) is unique, so the rank slices concatenate to it.
+Stable key/value (cfg2 KV): the per-rank grids are all-gathered (a G x cells
+table), which fixes the cell cuts and, for every record, its final global
+position: global start of its cell + the earlier ranks' counts of that cell
++ its rank among this rank's equal keys.  Every rank sorts its
+shard stably (rs_sort_u32_kv) and a placement kernel (rs_kv_place_u32)
+writes each record straight to that position in the owning rank's output
+slice through NVLink peer pointers — the exchange and the merge in one pass,
+no receive-side sort.  The reference's stable order (radix_sort_lsd_by,
+baselines.hpp:24-46) is unique, so the rank slices concatenate to it.  The
+NCCL variant (all-to-all by cell range, then a stable sort of the received
+runs) remains for groups without peer memory.
 
 Wide keys (cfg5): the leading-digit bucket histogram (rs_bucket_hist_u32) is
 all-reduced, G-1 splitters are cut on bucket boundaries and every rank sorts
@@ -82,8 +86,7 @@ class GpuOps:
     """Device phases through the C-ABI (include/recsort_b200.h)."""
 
     def __init__(self):
-        self._symm = None  # (local tensor, symmetric-memory handle) of the receive buffer
-        self._symm_cap = 0
+        self._symm = {}  # name -> (local tensor, symmetric-memory handle, capacity)
 
     def _lib(self):
         from . import _lib
@@ -152,23 +155,33 @@ class GpuOps:
         self._check(self._lib().rs_partition_u32_to(ctypes.c_void_p(keys.data_ptr()), keys.numel(), divisor, hb,
                                                     parts, hd, ho, self._stream()))
 
-    def peer_buffer(self, cap: int, group=None) -> tuple[torch.Tensor, list[int]]:
-        """This rank's receive buffer (>= cap int32) and every rank's address of
-        it (symmetric memory over NVLink); grown identically on every rank."""
+    def peer_buffer(self, cap: int, group=None, name: str = "keys") -> tuple[torch.Tensor, list[int]]:
+        """This rank's receive buffer `name` (>= cap int32) and every rank's
+        address of it (symmetric memory over NVLink); grown identically on
+        every rank (cap is a global quantity)."""
         import torch.distributed._symmetric_memory as symm
 
-        if self._symm is None or self._symm_cap < cap:
-            size = max(cap, 2 * self._symm_cap, 1 << 20)
+        t, h, have = self._symm.get(name, (None, None, 0))
+        if have < cap:
+            size = max(cap, 2 * have, 1 << 20)
             t = symm.empty(size, dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
             h = symm.rendezvous(t, group or dist.group.WORLD)
-            self._symm, self._symm_cap = (t, h), size
-        t, h = self._symm
+            self._symm[name] = (t, h, size)
         return t, [int(p) for p in h.buffer_ptrs]
 
     def exchange_barrier(self, group=None) -> None:
-        """Device-side barrier over the receive buffer: every rank's writes
+        """Device-side barrier over the symmetric buffers: every rank's writes
         before it are visible to every rank after it (stream-ordered)."""
-        self._symm[1].barrier()
+        next(iter(self._symm.values()))[1].barrier()
+
+    def kv_place(self, ks, vs, cell_off, owner, dst_k: list[int], dst_v: list[int]) -> None:
+        ranks = len(dst_k)
+        hk = (ctypes.c_uint64 * ranks)(*dst_k)
+        hv = (ctypes.c_uint64 * ranks)(*dst_v)
+        self._check(self._lib().rs_kv_place_u32(ctypes.c_void_p(ks.data_ptr()), ctypes.c_void_p(vs.data_ptr()),
+                                                ks.numel(), ctypes.c_void_p(cell_off.data_ptr()),
+                                                ctypes.c_void_p(owner.data_ptr()), cell_off.numel(), hk, hv, ranks,
+                                                self._stream()))
 
     def peer_exchange_ok(self, group=None) -> bool:
         return dist.get_backend(group) == "nccl"
@@ -196,16 +209,56 @@ def sharded_grid_sort(keys: torch.Tensor, cells: int, ops=None, group=None) -> t
     return ops.emit(counts, lo, hi, n_out)
 
 
+def kv_placement(grids: torch.Tensor, rank: int, world: int):
+    """From the all-gathered grids C[g][k]: every cell's owner rank, this
+    rank's per-cell placement offset (final global position of its record i
+    with key k = offset[k] + i, relative to the owner's slice) and every
+    rank's slice size.  Cuts as sharded_grid_sort (cell_bounds_device)."""
+    C = grids.view(world, -1).to(torch.int64)
+    cells = C.shape[1]
+    total = C.sum(0)
+    prefix = torch.cumsum(total, 0)
+    gstart = prefix - total
+    bounds = cell_bounds_device(prefix, world)
+    cell_idx = torch.arange(cells, device=grids.device, dtype=torch.int64)
+    owner = torch.searchsorted(bounds[1:-1].contiguous(), cell_idx, right=True)
+    zero = torch.zeros(1, dtype=torch.int64, device=grids.device)
+    ends = torch.cat([zero, prefix])[bounds]  # position where each rank's slice starts (world + 1 entries)
+    before = C[:rank].sum(0)
+    mine = C[rank]
+    local_start = torch.cumsum(mine, 0) - mine
+    offset = gstart + before - local_start - ends[owner]
+    return offset, owner.to(torch.uint8), (ends[1:] - ends[:-1])
+
+
 def sharded_kv_sort(keys: torch.Tensor, vals: torch.Tensor, cells: int, ops=None,
-                    group=None) -> tuple[torch.Tensor, torch.Tensor]:
-    """Stable key/value across ranks: local count -> all-reduce ->
-    cell cuts; local stable sort -> all-to-all by cell range -> stable sort of
-    the received runs (concatenated in source-rank order).  Rank g's shard must
-    be slice g of the global input; returns slice r of the global stable
-    order (cut on cell boundaries, as sharded_grid_sort)."""
-    ops = ops or GpuOps()
+                    group=None, exchange: str = "auto") -> tuple[torch.Tensor, torch.Tensor]:
+    """Stable key/value across ranks.  p2p: local count ->
+    all-gather of the grids -> per-record final positions -> local stable
+    sort -> placement straight into the owners' slices over NVLink.  nccl:
+    local count -> all-reduce -> cell cuts; local stable sort -> all-to-all by
+    cell range -> stable sort of the received runs.  Rank g's shard must be
+    slice g of the global input; returns slice r of the global stable order
+    (cut on cell boundaries, as sharded_grid_sort)."""
+    ops = ops or _gpu_ops()
     world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
     counts = ops.count(keys, cells)
+    if exchange == "auto":
+        exchange = "p2p" if getattr(ops, "peer_exchange_ok", lambda g: False)(group) else "nccl"
+    if exchange == "p2p":
+        grids = torch.empty(world * cells, dtype=counts.dtype, device=counts.device)
+        dist.all_gather_into_tensor(grids, counts, group=group)  # C4: the per-rank grids
+        offset, owner, sizes = kv_placement(grids, rank, world)
+        ks, vs = ops.sort_kv(keys, vals, cells)
+        sizes = sizes.tolist()
+        bk, dk = ops.peer_buffer(int(max(sizes)), group, "kv_keys")
+        bv, dv = ops.peer_buffer(int(max(sizes)), group, "kv_vals")
+        ops.exchange_barrier(group)  # every rank is done with the buffers' previous contents
+        ops.kv_place(ks, vs, offset, owner, dk, dv)
+        ops.exchange_barrier(group)  # every record has landed
+        n = int(sizes[rank])
+        return bk[:n].clone(), bv[:n].clone()
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)  # C1
     bounds = cell_bounds_device(torch.cumsum(counts, 0, dtype=torch.int64), world)
     ks, vs = ops.sort_kv(keys, vals, cells)

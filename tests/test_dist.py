@@ -61,9 +61,19 @@ class NumpyOps:
             mine = keys.numpy()[part == r]
             dsts[r][off:off + mine.size] = torch.from_numpy(mine.copy())
 
-    def peer_buffer(self, cap, group=None):
-        assert cap <= self.bufs[self.rank].numel()
-        return self.bufs[self.rank], self.bufs
+    def peer_buffer(self, cap, group=None, name="keys"):
+        bufs = self.bufs[name] if isinstance(self.bufs, dict) else self.bufs
+        assert cap <= bufs[self.rank].numel()
+        return bufs[self.rank], bufs
+
+    def kv_place(self, ks, vs, cell_off, owner, dst_k, dst_v):
+        k = ks.numpy().view(np.uint32).astype(np.int64)
+        pos = cell_off.numpy()[k] + np.arange(k.size)
+        own = owner.numpy()[k]
+        for r in range(len(dst_k)):
+            sel = own == r
+            dst_k[r][torch.from_numpy(pos[sel])] = torch.from_numpy(ks.numpy()[sel].copy())
+            dst_v[r][torch.from_numpy(pos[sel])] = torch.from_numpy(vs.numpy()[sel].copy())
 
     def exchange_barrier(self, group=None):
         dist.barrier(group)
@@ -93,9 +103,13 @@ def _worker(rank, world, port, mode, shared):
         mine = keys[rank * n // world:(rank + 1) * n // world].clone()
         if mode == "grid":
             out = sharded_grid_sort(mine, shared["cells"], ops=NumpyOps())
-        elif mode == "kv":
+        elif mode in ("kv", "kvp2p"):
             vals = torch.arange(rank * n // world, (rank + 1) * n // world, dtype=torch.int32)
-            out = torch.stack(sharded_kv_sort(mine, vals, shared["cells"], ops=NumpyOps()))
+            if mode == "kv":
+                out = torch.stack(sharded_kv_sort(mine, vals, shared["cells"], ops=NumpyOps(), exchange="nccl"))
+            else:
+                out = torch.stack(sharded_kv_sort(mine, vals, shared["cells"], ops=NumpyOps(shared["bufs"], rank),
+                                                  exchange="p2p"))
         elif mode == "p2p":
             out = range_partition_sort(mine, shared["divisor"], shared["buckets"],
                                        ops=NumpyOps(shared["bufs"], rank), exchange="p2p")
@@ -193,3 +207,38 @@ def test_range_partition_fused_exchange_gloo(tmp_path):
         outs = _run("p2p", keys, tmp_path, divisor=10**7, buckets=430, bufs=bufs)
         got = np.concatenate([o.numpy().view(np.uint32) for o in outs])
         assert np.array_equal(got, np.sort(keys.numpy().view(np.uint32)))
+
+
+@pytest.mark.parametrize("bound", [1000, 10**5])
+def test_sharded_kv_fused_placement_gloo(tmp_path, bound):
+    """The fused key/value placement (all-gathered grids -> every record's
+    final position -> stores into the owners' shared buffers): the rank
+    slices concatenate to the unique stable order, hot cell included."""
+    rng = np.random.default_rng(bound + 1)
+    keys = rng.integers(0, bound, 150_001).astype(np.int32)
+    keys[rng.random(keys.size) < 0.2] = 7
+    bufs = {name: [torch.zeros(keys.size, dtype=torch.int32).share_memory_() for _ in range(2)]
+            for name in ("kv_keys", "kv_vals")}
+    outs = _run("kvp2p", torch.from_numpy(keys), tmp_path, cells=bound, bufs=bufs)
+    got = np.concatenate([o.numpy() for o in outs], axis=1)
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(got[0], keys[order])
+    assert np.array_equal(got[1], order.astype(np.int32))
+
+
+def test_kv_placement_tables():
+    """kv_placement on a hand-checked 2-rank, 4-cell case."""
+    from paper_2107_01391_b200.dist import kv_placement
+
+    grids = torch.tensor([2, 0, 1, 3,   # rank 0's counts per cell
+                          1, 2, 0, 1])  # rank 1's
+    off0, owner, sizes = kv_placement(grids, 0, 2)
+    off1, _, _ = kv_placement(grids, 1, 2)
+    # totals [3, 2, 1, 4] -> starts [0, 3, 5, 6]; cuts at ceil(10/2) = 5 -> rank 0 owns cells 0-1
+    assert owner.tolist() == [0, 0, 1, 1] and sizes.tolist() == [5, 5]
+    # rank 0's sorted records: cell 0 (i = 0, 1), cell 2 (i = 2), cell 3 (i = 3, 4, 5)
+    #   -> slice 0 positions 0, 1; slice 1 positions 0 (global 5) and 1, 2, 3 (global 6-8)
+    assert [int(off0[k]) + i for k, i in [(0, 0), (0, 1), (2, 2), (3, 3), (3, 5)]] == [0, 1, 0, 1, 3]
+    # rank 1's: cell 0 (i = 0) after rank 0's two -> 2; cell 1 (i = 1, 2) -> 3, 4; cell 3 (i = 3)
+    #   after rank 0's three -> global 9 -> slice 1 position 4
+    assert [int(off1[k]) + i for k, i in [(0, 0), (1, 1), (1, 2), (3, 3)]] == [2, 3, 4, 4]

@@ -526,9 +526,10 @@ def test_dist_paths_on_device_nccl(rs, oracle):
             out = range_partition_sort(_t(wide.view(np.int32)), 10**7, 430, exchange=exchange)
             assert np.array_equal(_np_u32(out), np.sort(wide)), exchange
         vals = np.arange(keys.size, dtype=np.uint32)
-        ko, vo = sharded_kv_sort(_t(keys.view(np.int32)), _t(vals.view(np.int32)), 10**6)
         wk, wv = oracle.radix_sort_lsd_kv(keys, vals)
-        assert np.array_equal(_np_u32(ko), wk) and np.array_equal(_np_u32(vo), wv)
+        for exchange in ("p2p", "p2p", "nccl"):  # fused placement over peer memory (twice), then NCCL
+            ko, vo = sharded_kv_sort(_t(keys.view(np.int32)), _t(vals.view(np.int32)), 10**6, exchange=exchange)
+            assert np.array_equal(_np_u32(ko), wk) and np.array_equal(_np_u32(vo), wv), exchange
     finally:
         dist.destroy_process_group()
 
