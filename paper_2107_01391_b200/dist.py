@@ -184,7 +184,17 @@ class GpuOps:
                                                 self._stream()))
 
     def peer_exchange_ok(self, group=None) -> bool:
-        return dist.get_backend(group) == "nccl"
+        """NCCL groups whose symmetric-memory rendezvous works (tried once;
+        a failure falls back to the NCCL exchanges)."""
+        if dist.get_backend(group) != "nccl":
+            return False
+        if getattr(self, "_p2p_ok", None) is None:
+            try:
+                self.peer_buffer(1, group, "probe")
+                self._p2p_ok = True
+            except Exception:  # noqa: BLE001 — no peer memory here: the NCCL path
+                self._p2p_ok = False
+        return self._p2p_ok
 
     def sort(self, keys: torch.Tensor, key_digits: int = 0) -> torch.Tensor:
         from . import sort_u32
