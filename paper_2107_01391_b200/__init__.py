@@ -233,28 +233,6 @@ def sort_integers(values, max_cells: int = DEFAULT_CELL_BUDGET):
     return out.cpu().tolist(), rep
 
 
-def _parse_decimal(text: str) -> tuple[int, int]:
-    """parse_decimal grammar (key_model.cpp:80-105): digits, optional '.',
-    digits; no sign or exponent."""
-    if not text:
-        raise Error("parse_error", "empty numeral")
-    if text[0] == "-":
-        raise Error("negative_value", f"negative values are not supported: '{text}'")
-    ip, dot, fp = text.partition(".")
-    if dot and "." in fp:
-        raise Error("parse_error", f"multiple decimal points in '{text}'")
-    if dot and not fp:
-        raise Error("parse_error", f"no digits after decimal point in '{text}'")
-    if not ip and not fp:
-        raise Error("parse_error", f"no digits in '{text}'")
-    if not all("0" <= c <= "9" for c in ip + fp):
-        raise Error("parse_error", f"invalid character in numeral '{text}'")
-    mantissa = int(ip + fp) if ip + fp else 0
-    if mantissa > 0xFFFFFFFFFFFFFFFF:
-        raise Error("cell_budget_exceeded", f"numeral '{text}' has more digits than any cell budget admits")
-    return mantissa, len(fp)
-
-
 def _format_scaled(mantissa: int, scale: int) -> str:
     """format_scaled_decimal (key_model.cpp:170-180)."""
     p = 10 ** scale
@@ -263,9 +241,6 @@ def _format_scaled(mantissa: int, scale: int) -> str:
         out += "." + str(mantissa % p).rjust(scale, "0")
     return out
 
-
-def _digit_count(v: int) -> int:
-    return len(str(v)) if v > 0 else 1
 
 
 def _string_column(values):

@@ -73,23 +73,11 @@ def test_python_mirror_raises_without_gpu():
     assert isinstance(e.value, ValueError)  # bindings.cpp:20
 
 
-def test_host_text_ingest_matches_reference_grammar():
-    # parse_decimal grammar (test_key_model.cpp:58-78) as the host ingest
-    # of sort_decimals applies it before the GPU passes.
+def test_format_scaled_helper():
+    # format_scaled_decimal (key_model.cpp:170-180), the host rendering the
+    # decimal facade's tests compare with
     import paper_2107_01391_b200 as rs
 
-    assert rs._parse_decimal("5") == (5, 0)
-    assert rs._parse_decimal(".5") == (5, 1)
-    assert rs._parse_decimal("007.5") == (75, 1)
-    assert rs._parse_decimal("2.10") == (210, 2)
-    for bad in ["", ".", "5.", "1.2.3", "+1", "1e5", " 1", "abc"]:
-        with pytest.raises(rs.Error) as e:
-            rs._parse_decimal(bad)
-        assert e.value.code == "parse_error"
-    for neg in ["-3", "-0.0"]:
-        with pytest.raises(rs.Error) as e:
-            rs._parse_decimal(neg)
-        assert e.value.code == "negative_value"
     assert rs._format_scaled(45, 1) == "4.5"
     assert rs._format_scaled(3, 1) == "0.3"
     assert rs._format_scaled(105, 2) == "1.05"
