@@ -126,6 +126,20 @@ rs_status rs_sort_i64(const int64_t* values, uint64_t n, int64_t* out,
                       uint64_t out_capacity, const rs_options* opt,
                       rs_report* report, void* stream);
 
+/* sort_integers over keys spread across several GPUs of one process
+ * ("rs_sort_u32_multi"): shard g = h_keys[g][0 .. h_n[g]) on
+ * device h_devices[g].  One max over all shards fixes KeySpec{10, d, d}
+ * (sort.cpp:31-40, budget-checked before any grid); every GPU counts its
+ * shard, the first GPU gathers and sums the grids over NVLink, cuts the
+ * cells into ngpus contiguous ranges of ~total/ngpus keys, and GPU g emits
+ * range g into h_out[g] (h_written[g] keys): the concatenation of the
+ * outputs in device order is the sorted whole.  The report is the
+ * single-grid one.  Fewer than 2^32 keys in total; synchronous. */
+rs_status rs_sort_u32_multi(uint32_t ngpus, const int* h_devices, const uint32_t* const* h_keys,
+                            const uint64_t* h_n, uint32_t* const* h_out,
+                            const uint64_t* h_out_capacity, uint64_t* h_written,
+                            const rs_options* opt, rs_report* report);
+
 /* Stable key/value sort of uint32 keys with uint32 payloads.  The reference
  * library has no record API; its stable order is rsort's originals_by_key
  * (rsort.cpp:133-145) == baselines::radix_sort_lsd_by (baselines.hpp:24-46):

@@ -116,6 +116,29 @@ def sort_u32(keys, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits: int = 0,
     return out, _report(rep)
 
 
+def sort_u32_multi(shards, *, max_cells: int = DEFAULT_CELL_BUDGET):
+    """sort_integers over uint32 keys spread across CUDA tensors on one or
+    more devices (rs_sort_u32_multi): returns (outputs, report), output g on
+    shard g's device holding slice g of the sorted whole (contiguous cell
+    ranges of about total/len(shards) keys)."""
+    torch = _torch()
+    shards = [_cuda_tensor(s, (torch.int32, torch.uint32), "shard") for s in shards]
+    g = len(shards)
+    total = sum(s.numel() for s in shards)
+    outs = [torch.empty(max(total, 1), dtype=s.dtype, device=s.device) for s in shards]
+    devs = (ctypes.c_int * g)(*[s.device.index for s in shards])
+    keys = (ctypes.c_void_p * g)(*[s.data_ptr() for s in shards])
+    ns = (ctypes.c_uint64 * g)(*[s.numel() for s in shards])
+    outp = (ctypes.c_void_p * g)(*[o.data_ptr() for o in outs])
+    caps = (ctypes.c_uint64 * g)(*[o.numel() for o in outs])
+    written = (ctypes.c_uint64 * g)()
+    rep = RsReport()
+    torch.cuda.synchronize()
+    _check(_lib.load().rs_sort_u32_multi(g, devs, keys, ns, outp, caps, written, ctypes.byref(_opts(max_cells)),
+                                         ctypes.byref(rep)))
+    return [o[: int(w)] for o, w in zip(outs, written)], _report(rep)
+
+
 def sort_u32_kv(keys, vals, *, max_cells: int = DEFAULT_CELL_BUDGET, key_digits: int = 0):
     """Stable key/value sort (uint32 keys, uint32 payloads)."""
     torch = _torch()
@@ -334,6 +357,6 @@ __all__ = [
     "DEFAULT_CELL_BUDGET", "Error", "ExtractionReport", "KeySpec", "__version__",
     "sort_integers", "sort_decimals", "sort_decimal_keys", "sort_strings", "sort_decimal_column",
     "format_decimal_column", "float_to_decimal_column",
-    "sort_u32", "sort_u32_kv", "sort_i64", "sort_f64", "sort_fixed_str", "sort_keys",
+    "sort_u32", "sort_u32_multi", "sort_u32_kv", "sort_i64", "sort_f64", "sort_fixed_str", "sort_keys",
     "recombinant_sort",
 ]

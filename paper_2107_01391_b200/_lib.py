@@ -64,6 +64,8 @@ SIGNATURES = {
     "rs_sort_u32": (c_int, [c_void_p, c_uint64, c_void_p, c_uint64, POINTER(RsOptions), POINTER(RsReport), c_void_p]),
     "rs_sort_i64": (c_int, [c_void_p, c_uint64, c_void_p, c_uint64, POINTER(RsOptions), POINTER(RsReport), c_void_p]),
     "rs_sort_u32_kv": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p, c_uint64, POINTER(RsOptions), POINTER(RsReport), c_void_p]),
+    "rs_sort_u32_multi": (c_int, [c_uint32, POINTER(c_int), POINTER(c_void_p), POINTER(c_uint64), POINTER(c_void_p),
+                                  POINTER(c_uint64), POINTER(c_uint64), POINTER(RsOptions), POINTER(RsReport)]),
     "rs_sort_f64": (c_int, [c_void_p, c_uint64, c_uint32, c_void_p, c_uint64, POINTER(RsOptions), POINTER(RsReport), c_void_p]),
     "rs_float_to_decimal": (c_int, [c_void_p, c_uint64, c_uint32, c_void_p, c_void_p]),
     "rs_sort_fixed_str": (c_int, [c_void_p, c_uint64, c_uint32, c_char_p, c_void_p, c_uint64, POINTER(RsOptions), POINTER(RsReport), c_void_p]),

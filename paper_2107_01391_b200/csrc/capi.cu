@@ -1062,6 +1062,35 @@ void msd_sort_str(Workspace& ws, const uint8_t* chars, uint64_t n, uint32_t widt
   pull_stats(ws);
 }
 
+// ---------------------------------------------- single-process multi-GPU
+// rs_sort_u32_multi: the per-GPU grids summed on the first device...
+__global__ void k_grid_add(uint32_t* __restrict__ acc, const uint32_t* __restrict__ other, uint32_t parts,
+                           uint64_t cells) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += stride) {
+    uint32_t s = acc[c];
+    for (uint32_t p = 0; p < parts; ++p) s += other[(uint64_t)p * cells + c];
+    acc[c] = s;
+  }
+}
+
+// ...and cut into `parts` contiguous cell ranges of about total/parts keys:
+// cut r (1 <= r < parts) = 1 + the cell where the inclusive prefix first
+// reaches ceil(r * total / parts) (dist.cell_bounds_device's rule).
+__global__ void k_grid_cuts(const uint32_t* __restrict__ excl, const uint32_t* __restrict__ cnt, uint64_t cells,
+                            const unsigned long long* __restrict__ total, uint32_t parts,
+                            unsigned long long* __restrict__ cuts) {
+  const unsigned long long tot = *total;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += stride) {
+    const unsigned long long lo = excl[c], hi = lo + cnt[c];
+    for (uint32_t r = 1; r < parts; ++r) {
+      const unsigned long long t = (r * tot + parts - 1) / parts;
+      if (lo < t && t <= hi) cuts[r - 1] = c + 1;
+    }
+  }
+}
+
 }  // namespace rsb
 
 using namespace rsb;
@@ -1283,6 +1312,124 @@ rs_status rs_float_to_decimal(const double* x, uint64_t n, uint32_t scale, uint6
   });
 }
 
+
+rs_status rs_sort_u32_multi(uint32_t ngpus, const int* h_devices, const uint32_t* const* h_keys,
+                            const uint64_t* h_n, uint32_t* const* h_out, const uint64_t* h_out_capacity,
+                            uint64_t* h_written, const rs_options* opt, rs_report* report) {
+  return guarded([&] {
+    if (ngpus == 0 || ngpus > 64 || !h_devices || !h_keys || !h_n || !h_out || !h_out_capacity || !h_written)
+      fail(RS_INVALID_ARGUMENT, "bad multi-GPU arguments");
+    int prev = 0;
+    RS_CUDA(cudaGetDevice(&prev));
+    struct Restore {
+      int d;
+      ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
+    const uint64_t budget = budget_of(opt);
+    uint64_t n_total = 0;
+    unsigned long long mx = 0;
+    for (uint32_t g = 0; g < ngpus; ++g) {  // the max (sort.cpp:31-38) over every shard
+      RS_CUDA(cudaSetDevice(h_devices[g]));
+      ensure_device();
+      n_total += h_n[g];
+      if (h_n[g] > 0) {
+        if (!h_keys[g] || !h_out[g]) fail(RS_INVALID_ARGUMENT, "null device pointer");
+        Workspace& ws = workspace_for(nullptr);
+        const unsigned long long m = device_max(ws, h_keys[g], h_n[g], MapU32{});
+        mx = m > mx ? m : mx;
+      }
+    }
+    if (n_total >= 0xFFFFFFFFull) fail(RS_INVALID_ARGUMENT, "rs_sort_u32_multi sorts fewer than 2^32 keys");
+    if (n_total == 0) {
+      for (uint32_t g = 0; g < ngpus; ++g) h_written[g] = 0;
+      if (report) *report = rs_report{0, 0, make_key_spec(10, 1, 1, budget)};
+      return;
+    }
+    const uint32_t digits = digit_count(mx);
+    const rs_key_spec spec = make_key_spec(10, digits, digits, budget);
+    const uint64_t cells = pow10u(digits);
+    // every GPU counts its shard into its own grid (allocated per shard: a
+    // device may hold several shards)
+    struct Grids {
+      std::vector<uint32_t*> p;
+      std::vector<int> dev;
+      ~Grids() {
+        for (size_t i = 0; i < p.size(); ++i)
+          if (p[i]) {
+            cudaSetDevice(dev[i]);
+            cudaFree(p[i]);
+          }
+      }
+    } gr;
+    gr.p.assign(ngpus, nullptr);
+    gr.dev.assign(h_devices, h_devices + ngpus);
+    std::vector<uint32_t*>& grids = gr.p;
+    for (uint32_t g = 0; g < ngpus; ++g) {
+      RS_CUDA(cudaSetDevice(h_devices[g]));
+      RS_CUDA(cudaMalloc(&grids[g], cells * sizeof(uint32_t)));
+      Workspace& ws = workspace_for(nullptr);
+      reset_stats(ws);
+      count_pass(ws, h_keys[g], h_n[g], MapU32{}, cells, grids[g]);
+    }
+    for (uint32_t g = 0; g < ngpus; ++g) {
+      RS_CUDA(cudaSetDevice(h_devices[g]));
+      RS_CUDA(cudaDeviceSynchronize());
+    }
+    // the first GPU gathers the other grids over NVLink and sums them
+    RS_CUDA(cudaSetDevice(h_devices[0]));
+    Workspace& w0 = workspace_for(nullptr);
+    if (ngpus > 1) {
+      auto* gather = w0.get<uint32_t>(kSlotExtra1, (ngpus - 1) * cells);
+      for (uint32_t g = 1; g < ngpus; ++g)
+        RS_CUDA(cudaMemcpyPeerAsync(gather + (g - 1) * cells, h_devices[0], grids[g], h_devices[g],
+                                    cells * sizeof(uint32_t), w0.stream));
+      k_grid_add<<<stream_grid(cells, kThreads * 4), kThreads, 0, w0.stream>>>(grids[0], gather, ngpus - 1, cells);
+      RS_LAUNCH_CHECK();
+    }
+    // cell cuts from the global prefix
+    auto* excl = w0.get<uint32_t>(kSlotTmpKeys, cells);
+    auto* tot = w0.get<unsigned long long>(kSlotScratch, 4 + 64);
+    auto* cuts = tot + 4;
+    exscan_u32(w0, grids[0], cells, excl, tot);
+    std::vector<unsigned long long> hcuts(ngpus > 1 ? ngpus - 1 : 1, cells);
+    if (ngpus > 1) {
+      RS_CUDA(cudaMemcpyAsync(cuts, hcuts.data(), (ngpus - 1) * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                              w0.stream));
+      k_grid_cuts<<<stream_grid(cells, kThreads * 4), kThreads, 0, w0.stream>>>(excl, grids[0], cells, tot, ngpus,
+                                                                              cuts);
+      RS_LAUNCH_CHECK();
+      RS_CUDA(cudaMemcpyAsync(hcuts.data(), cuts, (ngpus - 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                              w0.stream));
+    }
+    RS_CUDA(cudaStreamSynchronize(w0.stream));
+    std::vector<uint64_t> bounds(ngpus + 1, 0);
+    bounds[ngpus] = cells;
+    for (uint32_t r = 1; r < ngpus; ++r) bounds[r] = std::max<uint64_t>(bounds[r - 1], std::min<uint64_t>(hcuts[r - 1], cells));
+    // the global grid to every GPU, each emits its own cell range
+    for (uint32_t g = 1; g < ngpus; ++g)
+      RS_CUDA(cudaMemcpyPeer(grids[g], h_devices[g], grids[0], h_devices[0], cells * sizeof(uint32_t)));
+    for (uint32_t g = 0; g < ngpus; ++g) {
+      RS_CUDA(cudaSetDevice(h_devices[g]));
+      uint64_t wr = 0;
+      const rs_status st = rs_emit_u32(grids[g], cells, bounds[g], bounds[g + 1], 0, h_out[g], h_out_capacity[g], &wr,
+                                       nullptr);
+      if (st != RS_OK) fail(st, rs_last_error());
+      h_written[g] = wr;
+    }
+    // the report from the global grid (first GPU)
+    RS_CUDA(cudaSetDevice(h_devices[0]));
+    reset_stats(w0);
+    scan_pass(w0, grids[0], cells, n_total);
+    {
+      PassTimer pt_(RS_PASS_REPORT, w0.stream);
+      k_report<uint32_t><<<1, report_threads(10), 0, w0.stream>>>(static_cast<const uint32_t*>(w0.buf[kSlotOccCell]),
+                                                                  0, 10, digits, 0, 0, w0.stats, true);
+      RS_LAUNCH_CHECK();
+    }
+    pull_stats(w0);
+    if (report) *report = rs_report{n_total, w0.h_stats->cells_traversed, spec};
+  });
+}
 
 rs_status rs_sort_u32_kv(const uint32_t* keys, const uint32_t* vals, uint64_t n, uint32_t* keys_out,
                          uint32_t* vals_out, uint64_t out_capacity, const rs_options* opt,

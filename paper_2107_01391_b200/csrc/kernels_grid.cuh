@@ -493,7 +493,8 @@ __global__ void __launch_bounds__(kThreads) k_scan_cells(const uint32_t* __restr
   const uint32_t tile = s_tile;
   const unsigned long long c0 = (unsigned long long)tile * kScanTile + threadIdx.x * kScanPerThread;
   uint32_t c[kScanPerThread];
-  if (c0 + kScanPerThread <= cells) {
+  // 16-byte loads need a 16-byte aligned grid (rs_emit_u32 scans sub-ranges from any cell)
+  if (c0 + kScanPerThread <= cells && (reinterpret_cast<uintptr_t>(counts) & 15) == 0) {
     const uint4* p = reinterpret_cast<const uint4*>(counts + c0);
 #pragma unroll
     for (int q = 0; q < kScanPerThread / 4; ++q) {

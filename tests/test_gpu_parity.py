@@ -534,6 +534,25 @@ def test_dist_paths_on_device_nccl(rs, oracle):
         dist.destroy_process_group()
 
 
+def test_emit_phase_any_cell_range(rs, oracle):
+    """rs_emit_u32 over cell ranges starting anywhere (the per-rank ranges of
+    the multi-GPU paths): unaligned sub-grids take the scalar scan."""
+    import torch
+
+    lib = rs._lib.load()
+    keys = oracle.gen_u32(31, 0, 1 << 20, 10**5)
+    d = _t(keys.view(np.int32))
+    counts = torch.empty(10**5, dtype=torch.int32, device="cuda")
+    rs._check(lib.rs_count_u32(rs._ptr(d), d.numel(), rs._ptr(counts), 10**5, None, rs._stream()))
+    for lo, hi in [(0, 10**5), (1, 77_777), (3, 5), (12_345, 10**5), (99_999, 10**5), (50_001, 50_001)]:
+        out = torch.empty(keys.size, dtype=torch.int32, device="cuda")
+        w = ctypes.c_uint64()
+        rs._check(lib.rs_emit_u32(rs._ptr(counts), 10**5, lo, hi, 0, rs._ptr(out), out.numel(), ctypes.byref(w),
+                                  rs._stream()))
+        want = np.sort(keys[(keys >= lo) & (keys < hi)])
+        assert np.array_equal(_np_u32(out[: w.value]), want), (lo, hi)
+
+
 def test_partition_phase_api(rs, oracle):
     import torch
 
@@ -556,3 +575,21 @@ def test_partition_phase_api(rs, oracle):
         seg = got[start:start + hc[p]]
         assert np.array_equal(np.sort(seg), np.sort(keys[part == p]))
         start += hc[p]
+
+
+@pytest.mark.parametrize("parts", [1, 3])
+def test_sort_u32_multi_shards(rs, oracle, parts):
+    """rs_sort_u32_multi with `parts` shards (on the one device here): the
+    outputs concatenate to the sorted whole, the report is the single-grid
+    one, and the slices are balanced cell ranges."""
+    keys = oracle.gen_u32(77, 0, 3_000_001, 10**6)
+    keys[:200_000] = 123_456  # a hot cell
+    cuts = np.linspace(0, keys.size, parts + 1).astype(np.int64)
+    shards = [_t(keys[a:b].view(np.int32)) for a, b in zip(cuts[:-1], cuts[1:])]
+    outs, rep = rs.sort_u32_multi(shards)
+    got = np.concatenate([_np_u32(o) for o in outs])
+    want, wrep = oracle.sort_integers_u32(keys)
+    assert np.array_equal(got, want)
+    assert (rep.written, rep.cells_traversed) == wrep[:2]
+    if parts > 1:
+        assert all(_np_u32(a)[-1] < _np_u32(b)[0] for a, b in zip(outs, outs[1:]) if a.numel() and b.numel())
