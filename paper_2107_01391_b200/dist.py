@@ -164,8 +164,14 @@ class GpuOps:
         t, h, have = self._symm.get(name, (None, None, 0))
         if have < cap:
             size = max(cap, 2 * have, 1 << 20)
+            grp = group or dist.group.WORLD
+            try:  # older releases need the group registered first; newer ones do it themselves
+                if not symm.is_symm_mem_enabled_for_group(grp.group_name):
+                    symm.enable_symm_mem_for_group(grp.group_name)
+            except Exception:  # noqa: BLE001
+                pass
             t = symm.empty(size, dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
-            h = symm.rendezvous(t, group or dist.group.WORLD)
+            h = symm.rendezvous(t, grp)
             self._symm[name] = (t, h, size)
         return t, [int(p) for p in h.buffer_ptrs]
 

@@ -593,3 +593,50 @@ def test_sort_u32_multi_shards(rs, oracle, parts):
     assert (rep.written, rep.cells_traversed) == wrep[:2]
     if parts > 1:
         assert all(_np_u32(a)[-1] < _np_u32(b)[0] for a, b in zip(outs, outs[1:]) if a.numel() and b.numel())
+
+
+def test_two_rank_exchanges_emulated_on_one_gpu(rs, oracle):
+    """The multi-GPU device phases with two "ranks" whose shards and receive
+    buffers all live on this GPU (no collective needed): kv_placement tables
+    + rs_kv_place_u32 into two buffers, and rs_part_counts_u32 +
+    rs_partition_u32_to into two buffers — the exact writes two GPUs would
+    make over NVLink; the rank slices must concatenate to the reference's
+    stable order / the sorted keys."""
+    import torch
+
+    from paper_2107_01391_b200.dist import GpuOps, bucket_splitters, kv_placement
+
+    ops = GpuOps()
+    keys = oracle.gen_u32(41, 0, 2_000_003, 10**6)
+    keys[::7] = 424_242  # a hot cell straddling both shards
+    vals = np.arange(keys.size, dtype=np.uint32)
+    half = keys.size // 2 + 5
+    sk = [_t(keys[:half].view(np.int32)), _t(keys[half:].view(np.int32))]
+    sv = [_t(vals[:half].view(np.int32)), _t(vals[half:].view(np.int32))]
+    grids = torch.cat([ops.count(k, 10**6) for k in sk])
+    bufk = [torch.zeros(keys.size, dtype=torch.int32, device="cuda") for _ in range(2)]
+    bufv = [torch.zeros(keys.size, dtype=torch.int32, device="cuda") for _ in range(2)]
+    sizes = None
+    for r in range(2):
+        off, owner, sizes = kv_placement(grids, r, 2)
+        ks, vs = ops.sort_kv(sk[r], sv[r], 10**6)
+        ops.kv_place(ks, vs, off, owner, [b.data_ptr() for b in bufk], [b.data_ptr() for b in bufv])
+    torch.cuda.synchronize()
+    n0, n1 = (int(s) for s in sizes.tolist())
+    got_k = np.concatenate([_np_u32(bufk[0][:n0]), _np_u32(bufk[1][:n1])])
+    got_v = np.concatenate([_np_u32(bufv[0][:n0]), _np_u32(bufv[1][:n1])])
+    wk, wv = oracle.radix_sort_lsd_kv(keys, vals)
+    assert n0 > 0 and n1 > 0
+    assert np.array_equal(got_k, wk) and np.array_equal(got_v, wv)
+    # wide keys: counts -> the 2 x 2 table -> offsets -> parts stored into both buffers
+    wide = oracle.gen_u32(43, 0, 1_000_001, 0)
+    sw = [_t(wide[:400_000].view(np.int32)), _t(wide[400_000:].view(np.int32))]
+    hist = sum(ops.bucket_hist(k, 10**7, 430) for k in sw)
+    bounds = bucket_splitters(hist.cpu(), 2)
+    table = np.array([ops.part_counts(k, 10**7, bounds) for k in sw])  # [src][dst]
+    recv = [torch.zeros(wide.size, dtype=torch.int32, device="cuda") for _ in range(2)]
+    for g in range(2):
+        ops.partition_to(sw[g], 10**7, bounds, [b.data_ptr() for b in recv], table[:g].sum(0).tolist())
+    torch.cuda.synchronize()
+    parts = [np.sort(_np_u32(recv[r][: int(table[:, r].sum())])) for r in range(2)]
+    assert np.array_equal(np.concatenate(parts), np.sort(wide))
