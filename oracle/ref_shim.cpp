@@ -264,6 +264,27 @@ int ref_emit_csv_one(const char* alg, uint64_t n, double lo, double hi, uint32_t
   });
 }
 
+// bench::parse_csv + bench::fit_scaling (bench.cpp:228-297, 365-393) of a
+// one-group CSV; the worst-case constant table entry for d.
+int ref_fit_scaling_csv(const char* csv, double* slope, double* intercept, double* r2) {
+  return guarded([&] {
+    const std::vector<bench::BenchRecord> recs = bench::parse_csv(csv);
+    const bench::ScalingReport rep = bench::fit_scaling(recs);
+    *slope = rep.slope;
+    *intercept = rep.intercept;
+    *r2 = rep.r_squared;
+  });
+}
+
+int ref_worst_case_constant(uint32_t d, uint64_t* num, uint64_t* den, int* below) {
+  return guarded([&] {
+    const bench::WorstCaseConstant w = bench::worst_case_constant(d);
+    *num = w.numerator;
+    *den = w.denominator;
+    *below = w.below_squared_bound() ? 1 : 0;
+  });
+}
+
 uint64_t ref_splitmix64_next(uint64_t* state) {
   Splitmix64 g(*state);
   const uint64_t v = g.next();
