@@ -65,3 +65,18 @@ def _t(a):
     import torch
 
     return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).to("cuda")
+
+
+@pytest.mark.parametrize("n", [(1 << 22) - 1, 1 << 22, (1 << 22) + 1])
+@pytest.mark.parametrize("bound", [7, 10**4, 10**4 + 1])
+def test_small_path_switch(rs, oracle, n, bound):
+    """Around the one-launch small path's limits (2^22 keys; grids up to 10^4
+    cells — 10^4 + 1 needs 5 digits, the multi-pass path): same keys and
+    report either way, with and without a declared width."""
+    rng = np.random.default_rng(n + bound)
+    keys = rng.integers(0, bound, n, dtype=np.uint64).astype(np.uint32)
+    want, wrep = oracle.sort_integers_u32(keys, max_cells=10**9)
+    for hint in (0, len(str(bound - 1))):
+        out, rep = rs.sort_u32(_t(keys), key_digits=hint, max_cells=10**9)
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want), hint
+        assert (rep.written, rep.cells_traversed) == wrep[:2], hint
