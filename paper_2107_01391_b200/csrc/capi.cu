@@ -1879,7 +1879,7 @@ rs_status rs_format_decimals(const uint64_t* keys, uint64_t n, uint32_t scale, c
     if (n) {
       if (!out_chars) fail(RS_INVALID_ARGUMENT, "null device pointer");
       PassTimer pt_(RS_PASS_OTHER, ws.stream);
-      k_dec_format<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(
+      k_dec_format_staged<<<stream_grid(n, kDecFmtKeys * 4, 8), kDecFmtKeys, 0, ws.stream>>>(
           reinterpret_cast<const unsigned long long*>(keys), n, scale, off, out_chars);
       RS_LAUNCH_CHECK();
       RS_CUDA(cudaStreamSynchronize(ws.stream));

@@ -181,6 +181,56 @@ __global__ void __launch_bounds__(kThreads) k_dec_format(const unsigned long lon
   }
 }
 
+// The same rendering, staged: a CTA formats 256 consecutive keys into shared
+// memory (their output bytes are one contiguous range of the column) and
+// writes the range out with 16-byte stores — the per-byte global stores of
+// k_dec_format become one vector store per 16 bytes.  The staging keeps the
+// range's alignment (its start sits at `lead` = start mod 16).
+constexpr int kDecFmtKeys = 256;
+constexpr int kDecFmtMaxBytes = 41;  // 20 integer digits + '.' + 19 fractional digits (+1 slack)
+__global__ void __launch_bounds__(kDecFmtKeys) k_dec_format_staged(const unsigned long long* __restrict__ keys,
+                                                                   uint64_t n, uint32_t scale,
+                                                                   const unsigned long long* __restrict__ offsets,
+                                                                   char* __restrict__ out) {
+  __shared__ __align__(16) char s_buf[kDecFmtKeys * kDecFmtMaxBytes + 32];
+  for (uint64_t i0 = (uint64_t)blockIdx.x * kDecFmtKeys; i0 < n; i0 += (uint64_t)gridDim.x * kDecFmtKeys) {
+    const uint64_t i1 = i0 + kDecFmtKeys < n ? i0 + kDecFmtKeys : n;
+    const unsigned long long gbase = offsets[i0], gend = offsets[i1];
+    const uint32_t lead = static_cast<uint32_t>(gbase & 15u);
+    const uint64_t i = i0 + threadIdx.x;
+    if (i < i1) {
+      unsigned long long v = keys[i];
+      char* end = s_buf + lead + (offsets[i + 1] - gbase);
+      uint32_t j = 0;
+      auto emit = [&](uint32_t dg) {
+        if (scale != 0 && j == scale) *--end = '.';
+        *--end = static_cast<char>('0' + dg);
+        ++j;
+      };
+      while (v >> 32) {
+        emit(static_cast<uint32_t>(v % 10));
+        v /= 10;
+      }
+      uint32_t x = static_cast<uint32_t>(v);
+      do {
+        emit(x % 10);
+        x /= 10;
+      } while (x != 0 || j <= scale);
+    }
+    __syncthreads();
+    const unsigned long long a16 = (gbase + 15) & ~15ull, e16 = gend & ~15ull;
+    if (a16 >= e16) {  // short range: bytes
+      for (unsigned long long p = gbase + threadIdx.x; p < gend; p += blockDim.x) out[p] = s_buf[lead + (p - gbase)];
+    } else {
+      for (unsigned long long p = gbase + threadIdx.x; p < a16; p += blockDim.x) out[p] = s_buf[lead + (p - gbase)];
+      for (unsigned long long p = a16 + 16ull * threadIdx.x; p < e16; p += 16ull * blockDim.x)
+        *reinterpret_cast<uint4*>(out + p) = *reinterpret_cast<const uint4*>(s_buf + lead + (p - gbase));
+      for (unsigned long long p = e16 + threadIdx.x; p < gend; p += blockDim.x) out[p] = s_buf[lead + (p - gbase)];
+    }
+    __syncthreads();
+  }
+}
+
 // Offsets of the rendered column: exclusive scan of the rendered lengths of
 // format_scaled_decimal(key, scale) — the integer part key / 10^scale has
 // max(1, digits(key) - scale) digits, so no division — computed while the
