@@ -12,7 +12,8 @@
 //                 sequential loop stops at) by an atomicMin of (index, code)
 //   k_dec_scale   key = mantissa * 10^(dataset scale - own scale)
 //   k_dec_offsets rendered length per key, scanned into the output offsets
-//   k_dec_format  digits written right to left into the output column
+//   k_dec_format_staged  digits right to left into shared memory, the CTA's
+//                 contiguous output range written with 16-byte stores
 #pragma once
 
 #include <cuda_runtime.h>
@@ -152,36 +153,8 @@ __device__ __forceinline__ uint32_t dec_digits(unsigned long long v) {
   return d;
 }
 
-// to_string(mantissa / p) [ '.' zero-padded(mantissa % p, scale) ]: digits
-// written right to left from the end of the numeral's slot, the point
-// before the (scale+1)-th digit; 32-bit arithmetic once the value fits.
-__global__ void __launch_bounds__(kThreads) k_dec_format(const unsigned long long* __restrict__ keys, uint64_t n,
-                                                         uint32_t scale,
-                                                         const unsigned long long* __restrict__ offsets,
-                                                         char* __restrict__ out) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    unsigned long long v = keys[i];
-    char* end = out + offsets[i + 1];
-    uint32_t j = 0;  // digits written
-    auto emit = [&](uint32_t dg) {
-      if (scale != 0 && j == scale) *--end = '.';
-      *--end = static_cast<char>('0' + dg);
-      ++j;
-    };
-    while (v >> 32) {
-      emit(static_cast<uint32_t>(v % 10));
-      v /= 10;
-    }
-    uint32_t x = static_cast<uint32_t>(v);
-    do {  // at least scale + 1 digits: a leading 0 before the point
-      emit(x % 10);
-      x /= 10;
-    } while (x != 0 || j <= scale);
-  }
-}
-
-// The same rendering, staged: a CTA formats 256 consecutive keys into shared
+// to_string(mantissa / p) [ '.' zero-padded(mantissa % p, scale) ] (format_scaled_decimal,
+// key_model.cpp:170-180), staged: a CTA formats 256 consecutive keys into shared
 // memory (their output bytes are one contiguous range of the column) and
 // writes the range out with 16-byte stores — the per-byte global stores of
 // k_dec_format become one vector store per 16 bytes.  The staging keeps the
