@@ -148,9 +148,9 @@ __global__ void __launch_bounds__(kThreads) k_dec_scale(unsigned long long* __re
 }
 
 __device__ __forceinline__ uint32_t dec_digits(unsigned long long v) {
-  uint32_t d = 1;
-  while (d < 20 && v >= c_pow10[d]) ++d;
-  return d;
+  if (v == 0) return 1;
+  const uint32_t t = (static_cast<uint32_t>(64 - __clzll(static_cast<long long>(v))) * 1233u) >> 12;  // ~log10(2^bits)
+  return t + (v >= c_pow10[t] ? 1u : 0u);
 }
 
 // to_string(mantissa / p) [ '.' zero-padded(mantissa % p, scale) ] (format_scaled_decimal,
