@@ -640,3 +640,20 @@ def test_two_rank_exchanges_emulated_on_one_gpu(rs, oracle):
     torch.cuda.synchronize()
     parts = [np.sort(_np_u32(recv[r][: int(table[:, r].sum())])) for r in range(2)]
     assert np.array_equal(np.concatenate(parts), np.sort(wide))
+
+
+def test_more_than_2_pow_32_keys(rs, oracle):
+    """2^32 + 4096 keys in one call (64-bit positions throughout): sorted,
+    every key written, the report of a fully occupied 10^6-cell grid."""
+    import torch
+
+    lib = rs._lib.load()
+    n = (1 << 32) + 4096
+    k = torch.empty(n, dtype=torch.int32, device="cuda")
+    rs._check(lib.rs_gen_u32(oracle.config_seed(2), 0, n, 10**6, rs._ptr(k), rs._stream()))
+    out, rep = rs.sort_u32(k, key_digits=6)
+    assert rep.written == n and rep.cells_traversed == 10**6
+    assert bool((out[1:] >= out[:-1]).all())
+    assert int(out[0]) == 0 and int(out[-1]) == 10**6 - 1
+    del k, out
+    torch.cuda.empty_cache()
