@@ -333,7 +333,7 @@ def main():
             # and reads its slice of the global order back; max over ranks
             h_in = torch.empty(n, dtype=torch.int32, pin_memory=True)
             h_in.copy_(keys.cpu())
-            h_out = torch.empty(2 * n, dtype=torch.int32, pin_memory=True)  # a rank's slice: ~n (+ one cell)
+            h_out = torch.empty(n + n // 4, dtype=torch.int32, pin_memory=True)  # a rank's slice: ~n (+ one cell)
             dev = torch.empty_like(keys)
             got = {}
 
@@ -363,7 +363,7 @@ def main():
             # k+1's H2D overlaps step k's D2H on each GPU's own PCIe link
             streams = [torch.cuda.Stream(), torch.cuda.Stream()]
             devs = [torch.empty_like(keys) for _ in range(2)]
-            h_outs = [torch.empty(2 * n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+            h_outs = [torch.empty(n + n // 4, dtype=torch.int32, pin_memory=True) for _ in range(2)]
             sizes = [0, 0]
 
             def pipe_step_dist(k):
