@@ -657,3 +657,27 @@ def test_more_than_2_pow_32_keys(rs, oracle):
     assert int(out[0]) == 0 and int(out[-1]) == 10**6 - 1
     del k, out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_sort_keys_any_radix_vs_reference(rs, ref, seed):
+    """sort_keys (extraction.cpp:34-45) for radices 2..36 and widths whose
+    grids span the shared, two-level and global count paths: keys and the
+    report against the reference library's build_count_space + extract."""
+    import torch
+
+    rng = np.random.default_rng(700 + seed)
+    radix = int(rng.integers(2, 37))
+    d = 1
+    while radix ** (d + 1) <= 3 * 10**6 and rng.random() < 0.85:
+        d += 1
+    ip = int(rng.integers(0, d + 1))
+    cells = radix ** d
+    n = int(rng.choice([1, 999, 100_000, 1_000_003]))
+    keys = rng.integers(0, cells, n, dtype=np.uint64)
+    if seed % 3 == 0:
+        keys[: n // 2] = keys[0]  # a hot cell
+    want, wrep = ref.sort_keys_core(keys, (radix, d, ip), max_cells=10**8)
+    out, rep = rs.sort_keys(torch.from_numpy(keys.view(np.int64)).cuda(), rs.KeySpec(radix, d, ip), max_cells=10**8)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (radix, d)
+    assert _rep(rep) == wrep, (radix, d)
