@@ -9,15 +9,25 @@ than L2 (126 MB), so no flush is needed between steps.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-For N>1 (torchrun, one rank per GPU, NCCL): weak scaling, 2^28 keys per rank,
-sorted by the small-grid sharding of SURVEY 8e (local count, all-reduce of
-the 10^6-cell grid, each rank emits its own contiguous cell range).
+--gpus N > 1 without torchrun re-launches this script under
+torch.distributed.run (one rank per GPU, NCCL), after checking that N GPUs are
+visible.  For N>1: weak scaling, 2^28 cfg2 keys per rank sorted by the
+small-grid sharding of SURVEY 8e (local count, all-reduce of the 10^6-cell
+grid, each rank emits its own contiguous cell range); the `configs` object
+adds the sharded stable key/value sort and cfg5 (2^31 keys in total,
+range-partitioned by leading digits and exchanged over NVLink peer stores).
 
-Extra keys on the JSON line: roofline (dominant kernel, live CUDA-event
-timing), passes (per-pass bytes / time / fraction of measured HBM peak), kv
-(the stable key/value variant of cfg2), e2e (through the C-ABI host-buffer
-entry point, H2D + sort + D2H each step), cpu_baseline (the reference library
-compiled from its sources, timed on this host), clocks, gpu_launches.
+Every BASELINE config is also timed on the line (`configs`): cfg1, cfg2
+key/value, cfg3, cfg4, cfg5 (one GPU: MSD), and the facade semantics of
+sort_integers without a declared width (uint32 and int64 inputs).  Each entry
+carries its SURVEY 8(d) algorithmic bytes per key and the fraction of the
+measured HBM peak they reach, plus per-pass device times from CUDA events the
+library records on its own stream.
+
+Other keys on the line: roofline (dominant kernel, live CUDA-event timing,
+§8(d) bytes), passes, e2e (host buffers, H2D + sort + D2H every step),
+cpu_baseline (the reference library compiled from its sources, timed on this
+host), clocks, gpu_launches.
 """
 from __future__ import annotations
 
@@ -38,6 +48,11 @@ N_KEYS = 1 << 28          # cfg2 keys per GPU
 KEY_BOUND = 10 ** 6       # cfg2 key domain
 KEY_DIGITS = 6            # declared decimal width of the domain (rs_options.key_digits)
 CPU_SAMPLE = 1 << 24      # bounded reference sample (~1.5 s per sort on one core)
+CFG5_KEYS = 1 << 31       # cfg5 keys in total (sharded across the ranks)
+
+# algorithmic bytes per key of the minimal pass structure
+ALGO_BPK = {"cfg1": 8, "cfg2": 8, "cfg2_kv": 20, "cfg3": 16, "cfg4": 40, "cfg5": 20, "cfg5_dist": 28,
+            "facade_u32": 8, "facade_i64": 16}
 
 
 def measured_peak():
@@ -101,6 +116,36 @@ class ClockSampler:
         os.unlink(self.path)
         return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": max(maxes) if maxes else None,
                 "samples": len(sms), "reasons": sorted(reasons)}
+
+
+# -------------------------------------------------------------- launcher
+def launch_cmd(argv: list[str], gpus: int, port: int) -> list[str]:
+    """The torchrun command that re-runs this script with one rank per GPU."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def maybe_relaunch(args, argv: list[str]) -> int | None:
+    """--gpus N > 1 outside torchrun: check N GPUs are visible, then run the
+    N ranks under torch.distributed.run and return its exit code.  Under
+    torchrun (WORLD_SIZE set) the world must equal --gpus.  None: carry on
+    in this process."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+            return 2
+        return None
+    if args.gpus <= 1 or args.impl == "reference":
+        return None  # the reference arm runs on rank 0 only
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}", file=sys.stderr)
+        return 2
+    port = int(os.environ.get("MASTER_PORT", "29517"))
+    return subprocess.call(launch_cmd(argv, args.gpus, port))
 
 
 # -------------------------------------------------------- reference arm
@@ -182,6 +227,334 @@ def cpu_baseline_sample():
                       f"host nproc={os.cpu_count()}"}
 
 
+# ------------------------------------------------------------ measurement
+class Bench:
+    """Timing helpers shared by every config: CUDA events on the current
+    stream (the library launches on it), max over ranks."""
+
+    def __init__(self, args, rank: int, world: int, use_dist: bool):
+        import torch
+
+        import paper_2107_01391_b200 as rs
+
+        self.torch, self.rs = torch, rs
+        self.lib = rs._lib.load()
+        self.args, self.rank, self.world, self.use_dist = args, rank, world, use_dist
+        self.peak, self.peak_src = measured_peak()
+
+    def max_over_ranks(self, v: float) -> float:
+        if not self.use_dist:
+            return v
+        import torch.distributed as dist
+
+        t = self.torch.tensor([v], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier(self):
+        if self.use_dist:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    def time_steps(self, fn, steps: int, warmup: int) -> tuple[float, int]:
+        """ms per step (max over ranks) and this library's launches per step."""
+        torch = self.torch
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        self.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = self.lib.rs_launch_count()
+        a.record()
+        for _ in range(steps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        launches = (self.lib.rs_launch_count() - l0) // steps
+        return self.max_over_ranks(a.elapsed_time(b) / steps), int(launches)
+
+    def pass_profile(self, fn, steps: int) -> dict:
+        """Per-pass device ms per step from the library's own CUDA events."""
+        rs, lib = self.rs, self.lib
+        lib.rs_profile_enable(1)
+        lib.rs_profile_reset()
+        for _ in range(steps):
+            fn()
+        self.torch.cuda.synchronize()
+        ms_arr = (ctypes.c_double * rs._lib.RS_NUM_PASSES)()
+        ln_arr = (ctypes.c_uint64 * rs._lib.RS_NUM_PASSES)()
+        lib.rs_profile_read(ms_arr, ln_arr)
+        lib.rs_profile_enable(0)
+        return {lib.rs_pass_name(i).decode(): {"ms": ms_arr[i] / steps, "launches_per_step": int(ln_arr[i]) // steps}
+                for i in range(rs._lib.RS_NUM_PASSES) if ln_arr[i]}
+
+    def entry(self, name: str, keys_total: int, ms: float, launches: int, passes: dict, workload: str,
+              extra: dict | None = None) -> dict:
+        bpk = ALGO_BPK[name]
+        gbs = bpk * keys_total / (ms / 1e3) / 1e9 / max(self.world, 1)  # per GPU
+        return {"value": keys_total / (ms / 1e3) / 1e9, "unit": "Gkeys/s", "ms_per_step": ms, "keys": keys_total,
+                "algorithmic_bytes_per_key": bpk, "hbm_gbs_per_gpu": gbs, "frac": gbs / self.peak,
+                "gpu_launches": launches, "passes_ms": {k: round(v["ms"], 4) for k, v in passes.items()},
+                "workload": workload, **(extra or {})}
+
+
+def gen_u32(b: Bench, cfg: int, first: int, n: int, bound: int):
+    t = b.torch.empty(n, dtype=b.torch.int32, device="cuda")
+    from oracle import Oracle  # seed derivation only (bench.cpp:149 pattern)
+
+    b.rs._check(b.lib.rs_gen_u32(Oracle().config_seed(cfg), first, n, bound, b.rs._ptr(t), b.rs._stream()))
+    return t
+
+
+def single_gpu_configs(b: Bench) -> dict:
+    """cfg1, cfg2 key/value, cfg3, cfg4, cfg5 (MSD on one GPU) and the facade
+    semantics (no declared width), each with its own timed region."""
+    torch, rs, lib = b.torch, b.rs, b.lib
+    from oracle import Oracle
+
+    o = Oracle()
+    steps, warm = b.args.steps, max(b.args.warmup, 3)
+    res = {}
+
+    def run(name, fn, n, workload, extra=None, steps_=None):
+        try:
+            ms, launches = b.time_steps(fn, steps_ or steps, warm)
+            passes = b.pass_profile(fn, min(steps_ or steps, 5))
+            res[name] = b.entry(name, n, ms, launches, passes, workload, extra)
+        except Exception as e:  # noqa: BLE001 — one config failing must not take the line down
+            res[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+
+    # cfg1: 2^20 keys in [0, 1000): the one-launch small path (launch-bound, H4)
+    n = 1 << 20
+    k = gen_u32(b, 1, 0, n, 1000)
+    out = torch.empty_like(k)
+    run("cfg1", lambda: rs.sort_u32(k, out=out), n, "cfg1: 2^20 uint32 uniform in [0,1000), 10x10x10 grid")
+    del k, out
+
+    # cfg2 key/value: payload = original index, stable
+    n = N_KEYS
+    k = gen_u32(b, 2, 0, n, KEY_BOUND)
+    v = torch.empty_like(k)
+    rs._check(lib.rs_gen_iota_u32(0, n, rs._ptr(v), rs._stream()))
+    ko, vo = torch.empty_like(k), torch.empty_like(k)
+    opts, rep = rs._opts(rs.DEFAULT_CELL_BUDGET, KEY_DIGITS), rs.RsReport()
+
+    def kv():
+        rs._check(lib.rs_sort_u32_kv(rs._ptr(k), rs._ptr(v), n, rs._ptr(ko), rs._ptr(vo), n, ctypes.byref(opts),
+                                     ctypes.byref(rep), rs._stream()))
+    run("cfg2_kv", kv, n, "cfg2 key/value: 2^28 uint32 keys in [0,10^6), uint32 payload = original index, stable")
+    del v, ko, vo
+
+    # facade semantics (sort.cpp:29-59): no declared width, the grid from the max
+    out = torch.empty_like(k)
+    run("facade_u32", lambda: rs.sort_u32(k, out=out), n,
+        "cfg2 keys through rs_sort_u32 without key_digits (the grid derived from the data, as sort_integers)")
+    del out
+    k64 = k.to(torch.int64)
+    del k
+    out64 = torch.empty_like(k64)
+    opts0 = rs._opts(rs.DEFAULT_CELL_BUDGET)
+
+    def i64():
+        rs._check(lib.rs_sort_i64(rs._ptr(k64), n, rs._ptr(out64), n, ctypes.byref(opts0), ctypes.byref(rep),
+                                  rs._stream()))
+    run("facade_i64", i64, n, "cfg2 keys as int64 through rs_sort_i64 without key_digits (sort_integers: "
+                              "span<const int64_t>, sort.cpp:29-59)")
+    del k64, out64
+    torch.cuda.empty_cache()
+
+    # cfg3: float64 k/1000, half Zipf(1.2)
+    cdf = torch.from_numpy(o.zipf_cdf()).cuda()
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    rs._check(lib.rs_gen_f64_cfg3(o.config_seed(3), 0, n, rs._ptr(cdf), cdf.numel(), rs._ptr(x), rs._stream()))
+    mo = torch.empty(n, dtype=torch.int64, device="cuda")
+    opts3 = rs._opts(rs.DEFAULT_CELL_BUDGET, 6)
+
+    def f64():
+        rs._check(lib.rs_sort_f64(rs._ptr(x), n, 3, rs._ptr(mo), n, ctypes.byref(opts3), ctypes.byref(rep),
+                                  rs._stream()))
+    run("cfg3", f64, n, "cfg3: 2^28 float64 x = k/1000, k uniform in [0,10^6) (even i) or Zipf(1.2) rank-1 (odd i); "
+                        "output uint64 mantissas at scale 3")
+    del x, mo, cdf
+    torch.cuda.empty_cache()
+
+    # cfg4: 2^26 eight-letter strings, MSD
+    n4 = 1 << 26
+    recs = torch.empty((n4, 8), dtype=torch.uint8, device="cuda")
+    rs._check(lib.rs_gen_str_cfg4(o.config_seed(4), 0, n4, rs._ptr(recs), rs._stream()))
+    so = torch.empty_like(recs)
+    opts4 = rs._opts(rs.DEFAULT_CELL_BUDGET, 0, True)
+
+    def strs():
+        rs._check(lib.rs_sort_fixed_str(rs._ptr(recs), n4, 8, b"abcdefghijklmnopqrstuvwxyz", rs._ptr(so), n4,
+                                        ctypes.byref(opts4), ctypes.byref(rep), rs._stream()))
+    run("cfg4", strs, n4, "cfg4: 2^26 fixed 8-byte strings, chars uniform in 'a'..'z', MSD levels + leaf grids")
+    del recs, so
+    torch.cuda.empty_cache()
+
+    # cfg5 on one GPU: 2^31 full-range keys, MSD
+    k5 = gen_u32(b, 5, 0, CFG5_KEYS, 0)
+    o5 = torch.empty_like(k5)
+    opts5 = rs._opts(rs.DEFAULT_CELL_BUDGET, 10, True)
+
+    def wide():
+        rs._check(lib.rs_sort_u32(rs._ptr(k5), CFG5_KEYS, rs._ptr(o5), CFG5_KEYS, ctypes.byref(opts5),
+                                  ctypes.byref(rep), rs._stream()))
+    run("cfg5", wide, CFG5_KEYS, "cfg5 on one GPU: 2^31 uint32 uniform over the full 32-bit range (10 digits), "
+                                 "MSD bucket passes + per-bucket grids", steps_=min(steps, 5))
+    del k5, o5
+    torch.cuda.empty_cache()
+    return res
+
+
+def dist_configs(b: Bench) -> dict:
+    """N ranks: the stable key/value sort across ranks and cfg5 (2^31 keys in
+    total, range-partitioned and exchanged over NVLink peer stores)."""
+    torch, rs, lib = b.torch, b.rs, b.lib
+    from paper_2107_01391_b200 import dist as rsd
+
+    steps, warm = b.args.steps, max(b.args.warmup, 3)
+    res = {}
+    n = N_KEYS
+    k = gen_u32(b, 2, b.rank * n, n, KEY_BOUND)
+    v = torch.empty_like(k)
+    rs._check(lib.rs_gen_iota_u32(b.rank * n, n, rs._ptr(v), rs._stream()))
+    try:
+        ms, launches = b.time_steps(lambda: rsd.sharded_kv_sort(k, v, KEY_BOUND), steps, warm)
+        passes = b.pass_profile(lambda: rsd.sharded_kv_sort(k, v, KEY_BOUND), min(steps, 5))
+        res["cfg2_kv"] = b.entry("cfg2_kv", n * b.world, ms, launches, passes,
+                                 "cfg2 key/value sharded: local stable sort, all-gathered grids, placement into the "
+                                 "owners' slices over NVLink (dist.sharded_kv_sort)")
+    except Exception as e:  # noqa: BLE001
+        res["cfg2_kv"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    del k, v
+    torch.cuda.empty_cache()
+    per = CFG5_KEYS // b.world
+    k5 = gen_u32(b, 5, b.rank * per, per, 0)
+    try:
+        fn = lambda: rsd.range_partition_sort(k5, 10**7, 430, key_digits=10)  # noqa: E731
+        ms, launches = b.time_steps(fn, min(steps, 5), warm)
+        passes = b.pass_profile(fn, min(steps, 3))
+        res["cfg5_dist"] = b.entry("cfg5_dist", per * b.world, ms, launches, passes,
+                                   f"cfg5: 2^31 uint32 full-range keys in total, {per} per rank; leading-digit "
+                                   "histogram all-reduced, splitters on 430 buckets of key/10^7, partition fused with "
+                                   "the NVLink exchange (peer stores), local MSD sort (dist.range_partition_sort)")
+    except Exception as e:  # noqa: BLE001
+        res["cfg5_dist"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    del k5
+    torch.cuda.empty_cache()
+    return res
+
+
+def e2e_single(b: Bench, keys, out, opts) -> dict:
+    """End to end through the public C-ABI with host buffers: each step copies
+    its 1 GiB of keys in from pinned memory, sorts them and copies the 1 GiB
+    result back.  Consecutive steps alternate between two CUDA streams so
+    step k+1's H2D overlaps step k's D2H (PCIe is full duplex); the one-call
+    synchronous rs_sort_u32_host is reported beside it."""
+    torch, rs, lib = b.torch, b.rs, b.lib
+    n = keys.numel()
+    rep = rs.RsReport()
+    h_in = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    h_out = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    h_in.copy_(keys.cpu())
+    want = out.cpu()
+
+    def e2e_step():
+        rs._check(lib.rs_sort_u32_host(rs._ptr(h_in), n, rs._ptr(h_out), ctypes.byref(opts), ctypes.byref(rep),
+                                       rs._stream()))
+
+    e2e_step()
+    reps = max(3, b.args.steps // 2)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        e2e_step()
+    dt_sync = (time.perf_counter() - t0) / reps
+    ok = bool(torch.equal(h_out, want))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    d_in = [torch.empty_like(keys) for _ in range(2)]
+    d_out = [torch.empty_like(keys) for _ in range(2)]
+    h_outs = [torch.empty(n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+    reps2 = [rs.RsReport(), rs.RsReport()]
+
+    def pipe_step(k):
+        s, i = streams[k & 1], k & 1
+        with torch.cuda.stream(s):
+            d_in[i].copy_(h_in, non_blocking=True)
+            rs._check(lib.rs_sort_u32(rs._ptr(d_in[i]), n, rs._ptr(d_out[i]), n, ctypes.byref(opts),
+                                      ctypes.byref(reps2[i]), ctypes.c_void_p(s.cuda_stream)))
+            h_outs[i].copy_(d_out[i], non_blocking=True)
+
+    for k in range(2):
+        pipe_step(k)
+    torch.cuda.synchronize()
+    steps2 = max(4, b.args.steps)
+    t0 = time.perf_counter()
+    for k in range(steps2):
+        pipe_step(k)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps2
+    ok = ok and all(bool(torch.equal(h, want)) for h in h_outs)
+    return {"value": n / dt / 1e9, "unit": "Gkeys/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
+            "ms_per_step": dt * 1e3,
+            "api": "rs_sort_u32 on two CUDA streams (pinned host buffers; H2D of step k+1 overlaps D2H of step k)",
+            "sync_api": {"value": n / dt_sync / 1e9, "ms_per_step": dt_sync * 1e3,
+                         "api": "rs_sort_u32_host (one call per step: H2D, sort, D2H)"},
+            "checked": ok, "checked_how": "every output element of every e2e step against the device sort"}
+
+
+def e2e_dist(b: Bench, keys) -> dict:
+    """End to end at N GPUs through dist.sharded_grid_sort: each rank copies
+    its pinned shard in, sorts (count, all-reduce, own cell range) and reads
+    its slice of the global order back; max over ranks."""
+    torch = b.torch
+    import torch.distributed as dist
+
+    from paper_2107_01391_b200 import dist as rsd
+
+    n = keys.numel()
+    h_in = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    h_in.copy_(keys.cpu())
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    devs = [torch.empty_like(keys) for _ in range(2)]
+    h_outs = [None, None]
+    sizes = [0, 0]
+
+    def pipe_step(k):
+        i = k & 1
+        with torch.cuda.stream(streams[i]):
+            devs[i].copy_(h_in, non_blocking=True)
+            res = rsd.sharded_grid_sort(devs[i], KEY_BOUND)
+            if h_outs[i] is None or h_outs[i].numel() < res.numel():  # sized from the slice, never truncated
+                streams[i].synchronize()
+                h_outs[i] = torch.empty(res.numel() + res.numel() // 8 + 1, dtype=torch.int32, pin_memory=True)
+            h_outs[i][:res.numel()].copy_(res, non_blocking=True)
+            res.record_stream(streams[i])
+            sizes[i] = res.numel()
+
+    for k in range(2):
+        pipe_step(k)
+    torch.cuda.synchronize()
+    dist.barrier()
+    steps2 = max(4, b.args.steps)
+    t0 = time.perf_counter()
+    d2h = 0
+    for k in range(steps2):
+        pipe_step(k)
+        d2h += sizes[k & 1] * 4
+    torch.cuda.synchronize()
+    dt = b.max_over_ranks((time.perf_counter() - t0) / steps2)
+    checked = all(bool((h[1:sizes[i]] >= h[:sizes[i] - 1]).all()) for i, h in enumerate(h_outs))
+    total = torch.tensor([sizes[0]], dtype=torch.int64, device="cuda")
+    dist.all_reduce(total)
+    checked = checked and int(total) == n * b.world
+    return {"value": n * b.world / dt / 1e9, "unit": "Gkeys/s", "h2d_bytes_per_step": 4 * n,
+            "d2h_bytes_per_step": d2h // steps2, "ms_per_step": dt * 1e3,
+            "api": "dist.sharded_grid_sort on two CUDA streams (pinned shard in, own slice out)",
+            "checked": checked, "checked_how": "each rank's slice sorted; slices sum to the global key count"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -190,13 +563,17 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-kv", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="headline only (cfg2 key-only)")
     ap.add_argument("--dist", action="store_true",
-                    help="use the multi-GPU sharded-grid path even at N=1 (one-rank NCCL group)")
+                    help="use the multi-GPU paths even at N=1 (one-rank NCCL group)")
     ap.add_argument("--no-clock-window", action="store_true",
                     help="skip the untimed steps around the timed region (for ncu launch lists)")
-    args = ap.parse_args()
+    argv = sys.argv[1:]
+    args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    rc = maybe_relaunch(args, argv)
+    if rc is not None:
+        sys.exit(rc)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -217,15 +594,10 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
-    lib = rs._lib.load()
-    stream = rs._stream
-
-    from oracle import Oracle  # seed derivation only (bench.cpp:149 pattern)
-
-    seed = Oracle().config_seed(2)
+    b = Bench(args, rank, world, use_dist)
+    lib = b.lib
     n = N_KEYS
-    keys = torch.empty(n, dtype=torch.int32, device="cuda")
-    rs._check(lib.rs_gen_u32(seed, rank * n, n, KEY_BOUND, rs._ptr(keys), stream()))
+    keys = gen_u32(b, 2, rank * n, n, KEY_BOUND)
     out = torch.empty_like(keys)
     opts = rs._opts(rs.DEFAULT_CELL_BUDGET, KEY_DIGITS)
     rep = rs.RsReport()
@@ -233,7 +605,7 @@ def main():
     def step():
         if not use_dist:
             rs._check(lib.rs_sort_u32(rs._ptr(keys), n, rs._ptr(out), n, ctypes.byref(opts), ctypes.byref(rep),
-                                      stream()))
+                                      rs._stream()))
         else:
             rsd.sharded_grid_sort(keys, KEY_BOUND)
 
@@ -253,8 +625,7 @@ def main():
         while time.perf_counter() < t_end:
             step()
         torch.cuda.synchronize()
-        if use_dist:
-            dist.barrier()
+        b.barrier()
         launches0 = lib.rs_launch_count()
         ev0.record()
         for _ in range(args.steps):
@@ -266,15 +637,10 @@ def main():
         while time.perf_counter() < t_end:
             step()
         torch.cuda.synchronize()
-    if use_dist:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if use_dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    b.barrier()
+    ms = b.max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     value = n * world / (ms / 1e3) / 1e9
-    peak, peak_src = measured_peak()
+    peak, peak_src = b.peak, b.peak_src
 
     result = {
         "metric": "sorted Gkeys/s", "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
@@ -288,205 +654,41 @@ def main():
         "clocks": clk.summary(),
     }
 
-    if rank == 0 or use_dist:
-        # per-pass device time with CUDA events on the library's stream (every
-        # rank runs the steps: the sharded step has collectives; rank 0 reports)
-        lib.rs_profile_enable(1)
-        lib.rs_profile_reset()
-        for _ in range(args.steps):
-            step()
-        torch.cuda.synchronize()
-        ms_arr = (ctypes.c_double * rs._lib.RS_NUM_PASSES)()
-        ln_arr = (ctypes.c_uint64 * rs._lib.RS_NUM_PASSES)()
-        lib.rs_profile_read(ms_arr, ln_arr)
-        lib.rs_profile_enable(0)
-        # algorithmic bytes per pass of the two-level plan (csrc/kernels_two_level.cuh):
-        # partition R4 + W2 (keys in, uint16 inner digits out to pages), page
-        # count R2, emit W4; the scans touch only the grid (10^6 cells) and the
-        # [100][G] per-CTA page counts.  (msd_* entries: the MSD engine.)
-        algo_bytes = {"msd_hist": 4 * n, "msd_scatter": 8 * n, "partition": 6 * n, "count": 2 * n, "emit": 4 * n,
-                      "scan": KEY_BOUND * 4 + KEY_BOUND * 12, "report": 0}
-        passes = {}
-        for i in range(rs._lib.RS_NUM_PASSES):
-            if ln_arr[i] == 0:
-                continue
-            name = lib.rs_pass_name(i).decode()
-            per_step_ms = ms_arr[i] / args.steps
-            b = algo_bytes.get(name)
-            passes[name] = {"ms": per_step_ms, "launches_per_step": ln_arr[i] // args.steps,
-                            "bytes": b, "gbs": (b / (per_step_ms / 1e3) / 1e9) if b else None,
-                            "frac": (b / (per_step_ms / 1e3) / 1e9 / peak) if b else None}
-        result["passes"] = passes
-        dom = max((p for p in passes if algo_bytes.get(p)), key=lambda p: passes[p]["ms"])
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tpath):
-            traffic = json.load(open(tpath)).get(dom)
-        result["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": passes[dom]["gbs"], "peak": peak,
-                              "unit": "GB/s", "frac": passes[dom]["frac"], "traffic": traffic,
-                              "algorithmic_bytes": algo_bytes[dom], "peak_source": peak_src,
-                              "step_frac": (8 * n) / (ms / 1e3) / 1e9 / peak}
+    # per-pass device time with CUDA events on the library's stream (every
+    # rank runs the steps: the sharded step has collectives; rank 0 reports)
+    passes = b.pass_profile(step, args.steps)
+    # SURVEY 8(d) bytes per pass of cfg2 key-only: the count pass reads every
+    # key once (R4: its first kernel, the partition, does the reading), the
+    # emit writes every key once (W4); the page count, scans and report move
+    # only this design's own scratch (design bytes, not algorithmic).
+    algo = {"partition": 4 * n, "emit": 4 * n, "count": 0, "scan": 0, "report": 0,
+            "msd_hist": 4 * n, "msd_scatter": 8 * n}
+    design = {"partition": 6 * n, "count": 2 * n, "emit": 4 * n, "scan": KEY_BOUND * 16}
+    for name, p in passes.items():
+        a = algo.get(name)
+        p["bytes"] = a
+        p["design_bytes"] = design.get(name)
+        p["gbs"] = a / (p["ms"] / 1e3) / 1e9 if a else None
+        p["frac"] = p["gbs"] / peak if a else None
+    result["passes"] = passes
+    dom = max((p for p in passes if algo.get(p)), key=lambda p: passes[p]["ms"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    result["roofline"] = {"bound": "hbm", "kernel": dom, "achieved": passes[dom]["gbs"], "peak": peak,
+                          "unit": "GB/s", "frac": passes[dom]["frac"], "traffic": traffic,
+                          "traffic_source": "profiles/traffic.json (ncu --set full dram__bytes_read+write of this "
+                                            "kernel, one launch)",
+                          "algorithmic_bytes": algo.get(dom), "design_bytes": design.get(dom),
+                          "peak_source": peak_src, "step_frac": (8 * n) / (ms / 1e3) / 1e9 / peak}
 
-        if use_dist and not args.no_e2e:
-            # end to end at N GPUs through the multi-GPU API: each rank copies
-            # its pinned shard in, sorts (count, all-reduce, own cell range)
-            # and reads its slice of the global order back; max over ranks
-            h_in = torch.empty(n, dtype=torch.int32, pin_memory=True)
-            h_in.copy_(keys.cpu())
-            h_out = torch.empty(n + n // 4, dtype=torch.int32, pin_memory=True)  # a rank's slice: ~n (+ one cell)
-            dev = torch.empty_like(keys)
-            got = {}
-
-            def e2e_step_dist():
-                dev.copy_(h_in, non_blocking=True)
-                res = rsd.sharded_grid_sort(dev, KEY_BOUND)
-                m = min(res.numel(), h_out.numel())
-                h_out[:m].copy_(res[:m], non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-                got["out"] = h_out[:m]
-                got["bytes"] = m * 4
-
-            e2e_step_dist()
-            reps = max(3, args.steps // 2)
-            dist.barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            for _ in range(reps):
-                e2e_step_dist()
-            torch.cuda.synchronize()
-            t = torch.tensor([(time.perf_counter() - t0) / reps], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
-            checked = bool((got["out"][1:] >= got["out"][:-1]).all())
-            # streaming, as at N=1: consecutive steps alternate between two
-            # streams (collectives in the same order on every rank), so step
-            # k+1's H2D overlaps step k's D2H on each GPU's own PCIe link
-            streams = [torch.cuda.Stream(), torch.cuda.Stream()]
-            devs = [torch.empty_like(keys) for _ in range(2)]
-            h_outs = [torch.empty(n + n // 4, dtype=torch.int32, pin_memory=True) for _ in range(2)]
-            sizes = [0, 0]
-
-            def pipe_step_dist(k):
-                b = k & 1
-                with torch.cuda.stream(streams[b]):
-                    devs[b].copy_(h_in, non_blocking=True)
-                    res = rsd.sharded_grid_sort(devs[b], KEY_BOUND)
-                    m = min(res.numel(), h_outs[b].numel())
-                    h_outs[b][:m].copy_(res[:m], non_blocking=True)
-                    res.record_stream(streams[b])
-                    sizes[b] = m
-
-            for k in range(2):
-                pipe_step_dist(k)
-            torch.cuda.synchronize()
-            dist.barrier()
-            steps2 = max(4, args.steps)
-            t0 = time.perf_counter()
-            for k in range(steps2):
-                pipe_step_dist(k)
-            torch.cuda.synchronize()
-            t = torch.tensor([(time.perf_counter() - t0) / steps2], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dtp = float(t.item())
-            checked = checked and all(bool((h[1:sizes[i]] >= h[:sizes[i] - 1]).all()) for i, h in enumerate(h_outs))
-            result["e2e"] = {"value": n * world / dtp / 1e9, "unit": "Gkeys/s", "h2d_bytes_per_step": 4 * n,
-                             "d2h_bytes_per_step": got["bytes"], "ms_per_step": dtp * 1e3,
-                             "api": "dist.sharded_grid_sort on two CUDA streams (pinned shard in, own slice out; "
-                                    "H2D of step k+1 overlaps D2H of step k)",
-                             "sync_api": {"value": n * world / dt / 1e9, "ms_per_step": dt * 1e3,
-                                          "api": "dist.sharded_grid_sort, copies not overlapped"},
-                             "checked": checked}
-        if not args.no_kv:
-            try:
-                vals = torch.empty_like(keys)
-                rs._check(lib.rs_gen_iota_u32(rank * n, n, rs._ptr(vals), stream()))  # payload = global index
-                ko, vo = torch.empty_like(keys), torch.empty_like(keys)
-
-                def kv_step():
-                    if use_dist:  # local stable sort, then placement into the owners' slices (dist.sharded_kv_sort)
-                        rsd.sharded_kv_sort(keys, vals, KEY_BOUND)
-                        return
-                    rs._check(lib.rs_sort_u32_kv(rs._ptr(keys), rs._ptr(vals), n, rs._ptr(ko), rs._ptr(vo), n,
-                                                 ctypes.byref(opts), ctypes.byref(rep), stream()))
-
-                for _ in range(3):
-                    kv_step()
-                torch.cuda.synchronize()
-                if use_dist:
-                    dist.barrier()
-                ev0.record()
-                for _ in range(args.steps):
-                    kv_step()
-                ev1.record()
-                torch.cuda.synchronize()
-                kms = ev0.elapsed_time(ev1) / args.steps
-                if use_dist:
-                    t = torch.tensor([kms], device="cuda")
-                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                    kms = float(t.item())
-                result["kv"] = {"value": n * world / (kms / 1e3) / 1e9, "unit": "Gkeys/s", "ms_per_step": kms,
-                                "algorithmic_bytes": 20 * n, "step_frac": 20 * n / (kms / 1e3) / 1e9 / peak,
-                                "workload": "cfg2 key/value: uint32 payload = original index, stable" +
-                                            (" (dist.sharded_kv_sort)" if use_dist else "")}
-                del vals, ko, vo
-            except Exception as e:  # noqa: BLE001 — the headline line must still print
-                result["kv"] = {"error": f"{type(e).__name__}: {e}"[:300]}
-
-        if not args.no_e2e and not use_dist:
-            h_in = torch.empty(n, dtype=torch.int32, pin_memory=True)
-            h_out = torch.empty(n, dtype=torch.int32, pin_memory=True)
-            h_in.copy_(keys.cpu())
-
-            def e2e_step():
-                rs._check(lib.rs_sort_u32_host(rs._ptr(h_in), n, rs._ptr(h_out), ctypes.byref(opts),
-                                               ctypes.byref(rep), stream()))
-
-            e2e_step()
-            reps = max(3, args.steps // 2)
-            t0 = time.perf_counter()
-            for _ in range(reps):
-                e2e_step()
-            dt_sync = (time.perf_counter() - t0) / reps
-            ok = bool(torch.equal(h_out[:1000], out[:1000].cpu()))
-            # Streaming: consecutive steps alternate between two CUDA streams, so
-            # step k+1's host->device copy overlaps step k's device->host copy
-            # (PCIe is full duplex).  Every step still copies its whole input in
-            # from pinned memory, sorts it (rs_sort_u32 on that stream) and copies
-            # its whole sorted output back.
-            streams = [torch.cuda.Stream(), torch.cuda.Stream()]
-            d_in = [torch.empty_like(keys) for _ in range(2)]
-            d_out = [torch.empty_like(keys) for _ in range(2)]
-            h_outs = [torch.empty(n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
-            reps2 = [rs.RsReport(), rs.RsReport()]
-
-            def pipe_step(k):
-                s, b = streams[k & 1], k & 1
-                with torch.cuda.stream(s):
-                    d_in[b].copy_(h_in, non_blocking=True)
-                    rs._check(lib.rs_sort_u32(rs._ptr(d_in[b]), n, rs._ptr(d_out[b]), n, ctypes.byref(opts),
-                                              ctypes.byref(reps2[b]), ctypes.c_void_p(s.cuda_stream)))
-                    h_outs[b].copy_(d_out[b], non_blocking=True)
-
-            for k in range(2):
-                pipe_step(k)
-            torch.cuda.synchronize()
-            steps2 = max(4, args.steps)
-            t0 = time.perf_counter()
-            for k in range(steps2):
-                pipe_step(k)
-            torch.cuda.synchronize()
-            dt = (time.perf_counter() - t0) / steps2
-            ok = ok and all(bool(torch.equal(h[:1000], out[:1000].cpu())) and
-                            bool(torch.equal(h[-1000:], out[-1000:].cpu())) for h in h_outs)
-            result["e2e"] = {"value": n / dt / 1e9, "unit": "Gkeys/s", "h2d_bytes_per_step": 4 * n,
-                             "d2h_bytes_per_step": 4 * n, "ms_per_step": dt * 1e3,
-                             "api": "rs_sort_u32 on two CUDA streams (pinned host buffers; H2D of step k+1 "
-                                    "overlaps D2H of step k)",
-                             "sync_api": {"value": n / dt_sync / 1e9, "ms_per_step": dt_sync * 1e3,
-                                          "api": "rs_sort_u32_host (one call per step, copies not overlapped)"},
-                             "checked": ok}
-        if not args.no_cpu and rank == 0 and not use_dist:
-            result["cpu_baseline"] = cpu_baseline_sample()
+    if not args.no_configs:
+        result["configs"] = dist_configs(b) if use_dist else single_gpu_configs(b)
+    if not args.no_e2e:
+        result["e2e"] = e2e_dist(b, keys) if use_dist else e2e_single(b, keys, out, opts)
+    if not args.no_cpu and rank == 0 and not use_dist:
+        result["cpu_baseline"] = cpu_baseline_sample()
 
     if rank == 0:
         print(json.dumps(result), flush=True)

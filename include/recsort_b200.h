@@ -220,8 +220,14 @@ rs_status rs_format_decimals(const uint64_t* keys, uint64_t n, uint32_t scale, c
                              uint64_t* h_chars_needed, void* stream);
 
 /* ---- host-buffer entry points (H2D / sort / D2H inside one call) -------- */
-/* Same semantics as rs_sort_u32 / rs_sort_u32_kv on HOST buffers; the copies
- * are chunked and overlapped with the counting and emit passes. */
+/* Same semantics as rs_sort_u32 / rs_sort_u32_kv on HOST buffers: one
+ * host->device copy of the input, the device sort, one device->host copy of
+ * the output, all on `stream`, returning after the stream synchronises.  The
+ * device staging buffers belong to the call (no pass of the sort reuses
+ * them).  A sort cannot emit before it has counted every key, so within one
+ * call the copies do not overlap; callers sorting a stream of batches overlap
+ * consecutive calls on two streams (H2D of batch k+1 beside D2H of batch k,
+ * PCIe being full duplex), as bench.py's e2e figure does. */
 rs_status rs_sort_u32_host(const uint32_t* h_keys, uint64_t n, uint32_t* h_out,
                            const rs_options* opt, rs_report* report, void* stream);
 rs_status rs_sort_u32_kv_host(const uint32_t* h_keys, const uint32_t* h_vals,

@@ -451,7 +451,8 @@ void count_pass(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, 
 
 // Occupancy + look-back scan + tile starts; returns nothing, results live in
 // ws slots kSlotOccCell/kSlotOccEnd/kSlotTileFirst and stats->n_occupied.
-void scan_pass(Workspace& ws, const uint32_t* counts, uint64_t cells, uint64_t n) {
+template <class C>
+void scan_pass(Workspace& ws, const C* counts, uint64_t cells, uint64_t n) {
   const uint32_t tiles = static_cast<uint32_t>((cells + kScanTile - 1) / kScanTile);
   auto* desc = ws.get<unsigned long long>(kSlotTileDesc, 2ull * tiles);
   auto* occ_cell = ws.get<uint32_t>(kSlotOccCell, cells);
@@ -512,6 +513,15 @@ void small_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, 
   pull_stats(ws);
 }
 
+// Keys counted per uint32 grid pass: below 2^32, so no counter can wrap.
+constexpr uint64_t kCountChunk = 0xFFFFFFFFull;
+
+__global__ void k_grid_acc64(unsigned long long* __restrict__ wide, const uint32_t* __restrict__ counts,
+                             uint64_t cells) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += stride) wide[c] += counts[c];
+}
+
 // One full single-grid sort: count -> scan -> emit -> report.  Leaves the
 // stats (max, overflow, flags, report) in ws.h_stats after one sync.
 template <class Map, class Out, class K>
@@ -528,8 +538,25 @@ void grid_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, u
     }
   }
   auto* counts = ws.get<uint32_t>(kSlotCounts, cells);
-  count_pass(ws, in, n, map, cells, counts);
-  scan_pass(ws, counts, cells, n);
+  if (n <= kCountChunk) {
+    count_pass(ws, in, n, map, cells, counts);
+    scan_pass(ws, counts, cells, n);
+  } else {
+    // 2^32 keys or more: one cell may hold more than a uint32 counter can
+    // (the reference's CountSpace counts in uint64, hashing.hpp:86).  Chunks
+    // of kCountChunk keys are counted into the uint32 grid (no chunk can wrap
+    // a counter) and accumulated into a uint64 grid, which the scan reads.
+    auto* wide = ws.get<unsigned long long>(kSlotCounts64, cells);
+    RS_CUDA(cudaMemsetAsync(wide, 0, cells * sizeof(unsigned long long), ws.stream));
+    for (uint64_t off = 0; off < n; off += kCountChunk) {
+      const uint64_t len = std::min<uint64_t>(kCountChunk, n - off);
+      count_pass(ws, in + off, len, map, cells, counts);
+      PassTimer pt_(RS_PASS_COUNT, ws.stream);
+      k_grid_acc64<<<stream_grid(cells, kThreads * 4), kThreads, 0, ws.stream>>>(wide, counts, cells);
+      RS_LAUNCH_CHECK();
+    }
+    scan_pass(ws, static_cast<const unsigned long long*>(wide), cells, n);
+  }
   emit_pass(ws, n, out);
   (void)sorted;
   {
@@ -880,7 +907,7 @@ struct OutStr {
   const uint8_t* sym;  // device: ordinal -> byte, sym[0] = 0
   unsigned long long base;
   __device__ __forceinline__ void put_key(uint64_t p, unsigned long long key) const {
-    uint8_t buf[16];
+    uint8_t buf[32];  // a single grid has < 2^32 cells and radix >= 2, so digits <= 31
     for (int j = (int)digits - 1; j >= 0; --j) {
       const unsigned long long q = key / radix;
       buf[j] = sym[key - q * radix];
@@ -1680,8 +1707,9 @@ rs_status rs_sort_u32_host(const uint32_t* h_keys, uint64_t n, uint32_t* h_out, 
   return guarded([&] {
     ensure_device();
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
-    uint32_t* d_in = ws.get<uint32_t>(kSlotTmpKeys2, n ? n : 1);
-    uint32_t* d_out = ws.get<uint32_t>(kSlotTmpVals2, n ? n : 1);
+    // staging slots of their own: no internal pass of the sort reuses them
+    uint32_t* d_in = ws.get<uint32_t>(kSlotHostIn, n ? n : 1);
+    uint32_t* d_out = ws.get<uint32_t>(kSlotHostOut, n ? n : 1);
     if (n) RS_CUDA(cudaMemcpyAsync(d_in, h_keys, n * 4, cudaMemcpyHostToDevice, ws.stream));
     const rs_status st = rs_sort_u32(d_in, n, d_out, n, opt, report, stream);
     if (st != RS_OK) throw Failure{st, g_last_error};
@@ -1696,9 +1724,9 @@ rs_status rs_sort_u32_kv_host(const uint32_t* h_keys, const uint32_t* h_vals, ui
     ensure_device();
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
     const uint64_t m = n ? n : 1;
-    uint32_t* d_k = ws.get<uint32_t>(kSlotTmpKeys2, 2 * m);
+    uint32_t* d_k = ws.get<uint32_t>(kSlotHostIn, 2 * m);
     uint32_t* d_v = d_k + m;
-    uint32_t* d_ko = ws.get<uint32_t>(kSlotTmpVals2, 2 * m);
+    uint32_t* d_ko = ws.get<uint32_t>(kSlotHostOut, 2 * m);
     uint32_t* d_vo = d_ko + m;
     if (n) {
       RS_CUDA(cudaMemcpyAsync(d_k, h_keys, n * 4, cudaMemcpyHostToDevice, ws.stream));
@@ -1723,19 +1751,24 @@ rs_status rs_kv_place_u32(const uint32_t* keys, const uint32_t* vals, uint64_t n
     if (ranks == 0 || ranks > 64) fail(RS_INVALID_ARGUMENT, "ranks must be in [1, 64]");
     if (n > 0 && (!keys || !vals || !cell_off || !cell_owner)) fail(RS_INVALID_ARGUMENT, "null device pointer");
     if (!h_dst_keys || !h_dst_vals) fail(RS_INVALID_ARGUMENT, "null destination arrays");
-    (void)cells;
+    if (cells == 0 || cells > 0xFFFFFFFFull) fail(RS_INVALID_ARGUMENT, "cells out of range");
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
-    auto* d = ws.get<unsigned long long>(kSlotMisc, 128);
+    auto* d = ws.get<unsigned long long>(kSlotMisc, 129);
+    auto* bad = reinterpret_cast<unsigned*>(d + 128);
+    RS_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned), ws.stream));
     RS_CUDA(cudaMemcpyAsync(d, h_dst_keys, ranks * sizeof(uint64_t), cudaMemcpyHostToDevice, ws.stream));
     RS_CUDA(cudaMemcpyAsync(d + 64, h_dst_vals, ranks * sizeof(uint64_t), cudaMemcpyHostToDevice, ws.stream));
     if (n > 0) {
       PassTimer pt_(RS_PASS_KV_SCATTER, ws.stream);
       k_kv_place<<<stream_grid(n, 256 * 8, 8), 256, 0, ws.stream>>>(
           keys, vals, n, reinterpret_cast<const long long*>(cell_off), cell_owner, reinterpret_cast<uint32_t* const*>(d),
-          reinterpret_cast<uint32_t* const*>(d + 64), ranks);
+          reinterpret_cast<uint32_t* const*>(d + 64), ranks, cells, bad);
       RS_LAUNCH_CHECK();
     }
+    unsigned h_bad = 0;
+    RS_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof(h_bad), cudaMemcpyDeviceToHost, ws.stream));
     RS_CUDA(cudaStreamSynchronize(ws.stream));  // the host pointer arrays are the caller's
+    if (h_bad) fail(RS_OUT_OF_RANGE, "a key lies outside the placement grid or its owner is not a rank");
   });
 }
 
@@ -1744,13 +1777,16 @@ rs_status rs_count_u32(const uint32_t* keys, uint64_t n, uint32_t* counts, uint6
   return guarded([&] {
     ensure_device();
     if (cells == 0 || cells > 0xFFFFFFFFull) fail(RS_INVALID_ARGUMENT, "cells out of range");
+    // uint32 counters: fewer than 2^32 keys per call, so no cell can wrap
+    if (n > kCountChunk) fail(RS_INVALID_ARGUMENT, "rs_count_u32 counts fewer than 2^32 keys per call");
+    if (n > 0 && (!keys || !counts)) fail(RS_INVALID_ARGUMENT, "null device pointer");
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
     reset_stats(ws);
     count_pass(ws, keys, n, MapU32{}, cells, counts);  // same counting pass as rs_sort_u32
-    if (h_max) {
-      pull_stats(ws);
-      *h_max = static_cast<uint32_t>(ws.h_stats->max_key);
-    }
+    pull_stats(ws);
+    if (h_max) *h_max = static_cast<uint32_t>(ws.h_stats->max_key);
+    // a key outside the grid would silently drop out of the counts
+    if (ws.h_stats->overflow) fail(RS_OUT_OF_RANGE, "a key lies outside the grid of " + std::to_string(cells) + " cells");
   });
 }
 

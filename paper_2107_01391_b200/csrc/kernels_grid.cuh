@@ -476,7 +476,8 @@ __device__ __forceinline__ unsigned long long warp_lookback(volatile unsigned lo
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_scan_cells(const uint32_t* __restrict__ counts,
+template <class C>
+__global__ void __launch_bounds__(kThreads) k_scan_cells(const C* __restrict__ counts,
                                                          unsigned long long cells,
                                                          uint32_t* __restrict__ occ_cell,
                                                          unsigned long long* __restrict__ occ_end,
@@ -492,9 +493,10 @@ __global__ void __launch_bounds__(kThreads) k_scan_cells(const uint32_t* __restr
   __syncthreads();
   const uint32_t tile = s_tile;
   const unsigned long long c0 = (unsigned long long)tile * kScanTile + threadIdx.x * kScanPerThread;
-  uint32_t c[kScanPerThread];
-  // 16-byte loads need a 16-byte aligned grid (rs_emit_u32 scans sub-ranges from any cell)
-  if (c0 + kScanPerThread <= cells && (reinterpret_cast<uintptr_t>(counts) & 15) == 0) {
+  C c[kScanPerThread];
+  // 16-byte loads need a 16-byte aligned grid (rs_emit_u32 scans sub-ranges from any cell);
+  // 64-bit counts (inputs of 2^32 keys or more) are read one by one
+  if (sizeof(C) == 4 && c0 + kScanPerThread <= cells && (reinterpret_cast<uintptr_t>(counts) & 15) == 0) {
     const uint4* p = reinterpret_cast<const uint4*>(counts + c0);
 #pragma unroll
     for (int q = 0; q < kScanPerThread / 4; ++q) {
@@ -503,7 +505,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_cells(const uint32_t* __restr
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < kScanPerThread; ++k) c[k] = (c0 + k < cells) ? counts[c0 + k] : 0u;
+    for (int k = 0; k < kScanPerThread; ++k) c[k] = (c0 + k < cells) ? counts[c0 + k] : C{0};
   }
   uint32_t occ = 0;
   unsigned long long sum = 0;

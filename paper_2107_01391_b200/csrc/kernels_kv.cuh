@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(256) k_kv_place(const uint32_t* __restrict__ k
                                                   const long long* __restrict__ cell_off,
                                                   const uint8_t* __restrict__ cell_owner,
                                                   uint32_t* const* __restrict__ dst_k,
-                                                  uint32_t* const* __restrict__ dst_v, uint32_t ranks) {
+                                                  uint32_t* const* __restrict__ dst_v, uint32_t ranks,
+                                                  uint64_t cells, unsigned* __restrict__ bad) {
   __shared__ uint32_t* s_k[64];
   __shared__ uint32_t* s_v[64];
   for (uint32_t r = threadIdx.x; r < ranks; r += blockDim.x) {
@@ -287,7 +288,15 @@ __global__ void __launch_bounds__(256) k_kv_place(const uint32_t* __restrict__ k
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t k = __ldcs(keys + i);
+    if (k >= cells) {  // outside the grid the placement tables cover: flagged, never stored
+      *bad = 1u;
+      continue;
+    }
     const uint32_t r = __ldg(cell_owner + k);
+    if (r >= ranks) {
+      *bad = 1u;
+      continue;
+    }
     const uint64_t off = static_cast<uint64_t>(__ldg(cell_off + k) + static_cast<long long>(i));
     s_k[r][off] = k;
     s_v[r][off] = __ldcs(vals + i);

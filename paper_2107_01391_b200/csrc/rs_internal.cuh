@@ -111,7 +111,7 @@ enum : unsigned { kFlagNegative = 1u, kFlagNonFinite = 2u, kFlagDomain = 4u, kFl
 struct Workspace {
   int device = -1;
   cudaStream_t stream = nullptr;
-  static constexpr int kSlots = 22;
+  static constexpr int kSlots = 25;
   void* buf[kSlots] = {};
   size_t cap[kSlots] = {};
   DevStats* stats = nullptr;   // device
@@ -167,6 +167,9 @@ enum Slot : int {
   kSlotExtra1 = 19,     // MSD radix-leaf list
   kSlotSpans = 20,      // long emit-tile spans of hot cells
   kSlotMisc2 = 21,      // packed string keys (MSD)
+  kSlotCounts64 = 22,   // 64-bit grid of inputs with 2^32 keys or more
+  kSlotHostIn = 23,     // device staging of the host-buffer entry points (no internal pass uses it)
+  kSlotHostOut = 24,
 };
 
 }  // namespace rsb

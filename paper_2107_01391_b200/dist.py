@@ -214,6 +214,10 @@ def sharded_grid_sort(keys: torch.Tensor, cells: int, ops=None, group=None) -> t
     ops = ops or GpuOps()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    # the grid travels as 32-bit counters: below 2^32 keys in all, no cell can
+    # wrap (bounded here from the local shard, no extra collective)
+    if keys.numel() * world >= 1 << 32:
+        raise ValueError("sharded_grid_sort: fewer than 2^32 keys in total (world x shard) per call")
     counts = ops.count(keys, cells)
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)  # C1: the grid over NVLink
     prefix = torch.cumsum(counts, 0, dtype=torch.int64)

@@ -1,0 +1,137 @@
+"""GPU edge cases of the C-ABI beyond the sort kernels themselves: the
+host-buffer entry points (their device staging must not alias any buffer a
+sort pass uses), decoding of wide string keys, and the multi-GPU phase API's
+checks on keys outside the grid."""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _host_sort(rs, keys: np.ndarray, stream=None, **opt):
+    lib = rs._lib.load()
+    out = np.zeros_like(keys)
+    rep = rs.RsReport()
+    st = lib.rs_sort_u32_host(keys.ctypes.data_as(ctypes.c_void_p), keys.size, out.ctypes.data_as(ctypes.c_void_p),
+                              ctypes.byref(rs._opts(opt.get("max_cells", rs.DEFAULT_CELL_BUDGET),
+                                                    opt.get("key_digits", 0), opt.get("msd", False))),
+                              ctypes.byref(rep), stream if stream is not None else rs._stream())
+    rs._check(st)
+    return out, rep
+
+
+@pytest.mark.parametrize("n", [1, 7, 5000, 300_000, 3_000_001])
+def test_host_entry_fresh_stream(rs, oracle, n):
+    """rs_sort_u32_host on a stream that has never run a sort (a fresh
+    workspace: every internal slot is allocated inside the call)."""
+    import torch
+
+    keys = oracle.gen_u32(900 + n, 0, n, 10**6)
+    s = torch.cuda.Stream()
+    out, rep = _host_sort(rs, keys, ctypes.c_void_p(s.cuda_stream))
+    want, wrep = oracle.sort_integers_u32(keys)
+    assert np.array_equal(out, want)
+    assert (rep.written, rep.cells_traversed) == wrep[:2]
+
+
+def test_host_entry_msd(rs, oracle):
+    """msd=1 on host buffers: the MSD levels' segment lists are larger than
+    the keys and must not land in the staging buffers."""
+    import torch
+
+    n = 2_000_003
+    keys = oracle.gen_u32(77, 0, n, 0)
+    s = torch.cuda.Stream()
+    out, rep = _host_sort(rs, keys, ctypes.c_void_p(s.cuda_stream), msd=True)
+    assert np.array_equal(out, np.sort(keys))
+    assert rep.written == n and rep.spec.total_digits == 10
+    out2, _ = _host_sort(rs, keys, ctypes.c_void_p(s.cuda_stream), msd=True)  # reused workspace
+    assert np.array_equal(out2, out)
+
+
+def test_host_entry_too_small_hint(rs, oracle):
+    """A declared width below the data's redoes the sort with the derived
+    width, reading the input a second time: the input must be intact."""
+    n = 1_500_000
+    keys = oracle.gen_u32(78, 0, n, 10**7)
+    out, rep = _host_sort(rs, keys, key_digits=5)
+    want, wrep = oracle.sort_integers_u32(keys)
+    assert np.array_equal(out, want)
+    assert (rep.written, rep.cells_traversed) == wrep[:2]
+    assert rep.spec.total_digits == 7
+
+
+def test_host_kv_entry(rs, oracle):
+    lib = rs._lib.load()
+    n = 1_000_003
+    keys = oracle.gen_u32(79, 0, n, 10**6)
+    vals = np.arange(n, dtype=np.uint32)
+    ko, vo = np.zeros_like(keys), np.zeros_like(vals)
+    rep = rs.RsReport()
+    rs._check(lib.rs_sort_u32_kv_host(keys.ctypes.data_as(ctypes.c_void_p), vals.ctypes.data_as(ctypes.c_void_p), n,
+                                      ko.ctypes.data_as(ctypes.c_void_p), vo.ctypes.data_as(ctypes.c_void_p),
+                                      ctypes.byref(rs._opts(rs.DEFAULT_CELL_BUDGET)), ctypes.byref(rep), rs._stream()))
+    wk, wv = oracle.radix_sort_lsd_kv(keys, vals)
+    assert np.array_equal(ko, wk) and np.array_equal(vo, wv)
+
+
+@pytest.mark.parametrize("alphabet,width,budget", [("a", 20, 10**8), ("ab", 18, 10**9), ("z", 26, 10**8)])
+def test_wide_string_keys_decode(rs, oracle, alphabet, width, budget):
+    """Keys of more than 16 symbols (a 1- or 2-symbol alphabet: radix 2 or 3
+    admits widths up to 26 / 18 within the budget) decoded back to records."""
+    import torch
+
+    n = 20_000
+    rng = np.random.default_rng(width)
+    sym = np.frombuffer(alphabet.encode(), dtype=np.uint8)
+    recs = sym[rng.integers(0, len(sym), (n, width))]
+    lens = rng.integers(0, width + 1, n)
+    for i, l in enumerate(lens):
+        recs[i, l:] = 0
+    want, wrep = oracle.sort_fixed_strings(np.ascontiguousarray(recs), alphabet)
+    out, rep = rs.sort_fixed_str(torch.from_numpy(np.ascontiguousarray(recs)).cuda(), alphabet=alphabet,
+                                 max_cells=budget)
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert (rep.written, rep.cells_traversed) == wrep[:2]
+
+
+def test_count_phase_rejects_keys_outside_the_grid(rs):
+    """rs_count_u32 (the multi-GPU count phase) fails on a key >= cells
+    instead of silently dropping it from the grid."""
+    import torch
+
+    lib = rs._lib.load()
+    k = torch.arange(1000, dtype=torch.int32, device="cuda")
+    counts = torch.empty(1000, dtype=torch.int32, device="cuda")
+    rs._check(lib.rs_count_u32(rs._ptr(k), 1000, rs._ptr(counts), 1000, None, rs._stream()))
+    assert bool((counts == 1).all())
+    k[500] = 1000
+    st = lib.rs_count_u32(rs._ptr(k), 1000, rs._ptr(counts), 1000, None, rs._stream())
+    assert lib.rs_status_name(st).decode() == "out_of_range"
+
+
+def test_kv_place_rejects_keys_outside_the_grid(rs):
+    """rs_kv_place_u32 never stores a record whose key lies outside the
+    placement tables (it would index past them and write into a peer's
+    memory); the call fails instead."""
+    import torch
+
+    lib = rs._lib.load()
+    n, cells = 1000, 100
+    k = torch.arange(n, dtype=torch.int32, device="cuda") % cells
+    v = torch.arange(n, dtype=torch.int32, device="cuda")
+    off = torch.zeros(cells, dtype=torch.int64, device="cuda")
+    owner = torch.zeros(cells, dtype=torch.uint8, device="cuda")
+    dk = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+    dv = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+    hk = (ctypes.c_uint64 * 1)(dk.data_ptr())
+    hv = (ctypes.c_uint64 * 1)(dv.data_ptr())
+    k[7] = cells + 5
+    st = lib.rs_kv_place_u32(rs._ptr(k), rs._ptr(v), n, rs._ptr(off), rs._ptr(owner), cells, hk, hv, 1, rs._stream())
+    assert lib.rs_status_name(st).decode() == "out_of_range"
+    owner[3] = 9  # an owner that is not a rank
+    k[7] = 3
+    st = lib.rs_kv_place_u32(rs._ptr(k), rs._ptr(v), n, rs._ptr(off), rs._ptr(owner), cells, hk, hv, 1, rs._stream())
+    assert lib.rs_status_name(st).decode() == "out_of_range"
