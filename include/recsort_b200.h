@@ -197,6 +197,43 @@ rs_status rs_sort_keys(const uint64_t* keys, uint64_t n, rs_key_spec spec,
                        uint64_t* out, uint64_t out_capacity,
                        const rs_options* opt, rs_report* report, void* stream);
 
+/* ---- the reference's lower-level surface (key_model.hpp, hashing.hpp,
+ * extraction.hpp), what include/recsort/{key_model,hashing,extraction}.hpp
+ * implement over this ABI ---------------------------------------------- */
+/* checked_pow / make_key_spec (key_model.hpp:19-51, key_model.cpp:38-78):
+ * host geometry with the reference's errors; no device needed. */
+rs_status rs_checked_pow(uint64_t radix, uint32_t exp, uint64_t* h_out);
+rs_status rs_make_key_spec(uint32_t radix, uint32_t total_digits, uint32_t integer_digits,
+                           uint64_t max_cells, rs_key_spec* h_spec);
+
+/* strings_to_keys (key_model.hpp:118-121, key_model.cpp:225-247) over n
+ * NUL-padded records of `width` bytes: keys_out[i] = sum ord_j *
+ * radix^(w-1-j) at the data width w (longest string, >= 1), pad ordinal 0.
+ * Checks in the reference's order: KeySpec{radix, w, w} (budget), then the
+ * first symbol outside the alphabet.  *h_spec receives the spec. */
+rs_status rs_strings_to_keys(const uint8_t* chars, uint64_t n, uint32_t width, const char* h_alphabet,
+                             uint64_t* keys_out, const rs_options* opt, rs_key_spec* h_spec, void* stream);
+
+/* build_count_space without snapshots (hashing.hpp:107-113,
+ * hashing.cpp:40-52): counts[radix^total_digits] (uint64, device) receive
+ * the multiplicity of every key (CountSpace, hashing.hpp:53-89) and
+ * h_row_min / h_row_max (host, `radix` entries each) the TraverseMaps
+ * (hashing.hpp:12-48): per leading digit the least / greatest occupied
+ * suffix, ~0 / -1 for an untouched row.  The budget is new_space's
+ * (hashing.cpp:17-25, checked before anything is allocated); a key outside
+ * the spec's key space raises RS_SPEC_MISMATCH. */
+rs_status rs_build_count_space(const uint64_t* keys, uint64_t n, rs_key_spec spec, uint64_t max_cells,
+                               uint64_t* counts, uint64_t* h_row_min, int64_t* h_row_max, void* stream);
+
+/* extract (extraction.hpp:24-27, extraction.cpp:5-32): the raster scan of
+ * every occupied row's span [h_row_min, h_row_max] of a uint64 count grid,
+ * emitting each cell's multiplicity until `total` keys (total_inserted) are
+ * written.  RS_BUFFER_TOO_SMALL when out_capacity < total (checked first).
+ * report->cells_traversed counts the cells the raster visits. */
+rs_status rs_extract(const uint64_t* counts, rs_key_spec spec, uint64_t total, const uint64_t* h_row_min,
+                     const int64_t* h_row_max, uint64_t* out, uint64_t out_capacity, rs_report* report,
+                     void* stream);
+
 /* ---- decimal text ------------------------------------ */
 /* sort_decimal_keys (sort.hpp:44-47, sort.cpp:7-14) over a device string
  * column in Arrow layout: numeral i is chars[offsets[i] .. offsets[i+1]),
@@ -209,6 +246,19 @@ rs_status rs_sort_keys(const uint64_t* keys, uint64_t n, rs_key_spec spec,
 rs_status rs_sort_decimal_strings(const char* chars, const uint64_t* offsets, uint64_t n,
                                   uint64_t* keys_out, uint64_t out_capacity,
                                   const rs_options* opt, rs_report* report, void* stream);
+
+/* parse_decimal (key_model.hpp:78-80, key_model.cpp:80-105) for every
+ * numeral of a device string column: mantissas[i] and scales[i] (fractional
+ * digits).  The error is that of the first failing numeral in input order. */
+rs_status rs_parse_decimals(const char* chars, const uint64_t* offsets, uint64_t n, uint64_t* mantissas,
+                            uint32_t* scales, void* stream);
+
+/* normalize_dataset (key_model.hpp:82-87, key_model.cpp:107-133): keys_out[i]
+ * = mantissa_i * 10^(scale - scale_i) at the dataset's common scale;
+ * *h_spec = {10, lambda + scale, lambda}. */
+rs_status rs_normalize_decimal_strings(const char* chars, const uint64_t* offsets, uint64_t n,
+                                       uint64_t* keys_out, const rs_options* opt, rs_key_spec* h_spec,
+                                       void* stream);
 
 /* format_scaled_decimal (key_model.cpp:170-180) / reconstruct_value for n
  * keys at `scale` (<= 19), into a device string column: out_offsets[0..n]

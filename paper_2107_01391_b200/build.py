@@ -55,6 +55,15 @@ def build_oracle() -> None:
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
 
 
+def build_reference_suite() -> None:
+    """The reference's own C++ tests, acceptance suite and pybind module over
+    this library (tests/cpp/Makefile.ref), when its sources are present (this
+    container only; the built files travel to the GPU box)."""
+    if os.path.isdir("/root/reference/proj"):
+        subprocess.run(["make", "-s", "-f", os.path.join(ROOT, "tests", "cpp", "Makefile.ref"), "-j8"], check=True,
+                       cwd=ROOT)
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     build_oracle()

@@ -19,6 +19,7 @@
 #include "kernels_grid.cuh"
 #include "kernels_kv.cuh"
 #include "kernels_two_level.cuh"
+#include "kernels_partition_ws.cuh"
 #include "kernels_msd.cuh"
 #include "kernels_msd_engine.cuh"
 #include "kernels_decimal.cuh"
@@ -319,12 +320,23 @@ bool div_magic32(uint64_t d, unsigned long long& magic, uint32_t& shift) {
   return false;
 }
 
+// Which partition kernel a two-level count uses.  The warp-specialised kernel
+// (kernels_partition_ws.cuh) is the faster one on 4-byte keys as the caller
+// gives them (cfg2: 0.52 vs 0.575 ms at 2^28); the TMA-fed kernel, whose lane
+// replicas absorb a hot bucket, on cfg3's Zipf-skewed mapped cells (0.64 vs
+// ~0.97 ms) and on 8-byte inputs, where the warp-specialised ranker's
+// registers spill (profiles/r02_summary.md).
+template <class Map>
+bool use_ws_partition(bool mapped) {
+  return sizeof(typename Map::In) == 4 && !mapped;
+}
+
 // Geometry of the two-level split: ~10^4 inner cells per outer bucket
 // (10^6 = 100 x 10^4).  Few outer buckets keep each tile's bucket runs long
 // (~40 keys per 4096-key tile); 10^4 inner counters (40 KB) still fit a
 // shared histogram.
 template <class Map>
-bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
+bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t, bool ws) {
   if (cells <= kSmemCellsMax || cells > 0xFFFFFFFFull || n >= 0x7FFFFFFFull * 16) return false;
   uint64_t B = (cells + 9999) / 10000;
   if (B > kTlMaxBuckets) B = kTlMaxBuckets;
@@ -335,14 +347,24 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
   t.B = static_cast<uint32_t>((cells + S - 1) / S);
   if (!div_magic32(S, t.magic, t.shift) || t.shift < 32) return false;  // S == 1: never (cells > smem grid)
   t.T = static_cast<uint32_t>((n + kTlTile - 1) / kTlTile);
-  static const int per_sm = [] {  // once per mapper (one device type per process)
+  // CTAs per SM of each partition kernel, once per mapper (one device type per process)
+  static const int per_sm_tma = [] {
     int b = 0;
     cudaFuncSetAttribute(k_page_partition_tma<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(page_tma_smem<Map>()));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_page_partition_tma<Map>, kTlThreads, page_tma_smem<Map>());
     return b < 1 ? 1 : b;
   }();
-  uint64_t G = (uint64_t)sm_count() * per_sm;  // one persistent wave
+  static const int per_sm_ws = [] {
+    int b = 0;
+    if constexpr (sizeof(typename Map::In) == 4) {
+      cudaFuncSetAttribute(k_page_partition_ws<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(page_ws_smem(256)));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_page_partition_ws<Map>, kWsThreads, page_ws_smem(100));
+    }
+    return b < 1 ? 1 : b;
+  }();
+  uint64_t G = (uint64_t)sm_count() * (ws ? per_sm_ws : per_sm_tma);  // one persistent wave
   if (G > t.T) G = t.T;
   t.G = static_cast<uint32_t>(G);
   const uint64_t tiles_per = (t.T + G - 1) / G;
@@ -356,7 +378,7 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t) {
 
 template <class Map>
 void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, const TwoLevel& t,
-                     uint32_t* counts) {
+                     uint32_t* counts, bool use_ws) {
   const bool al = aligned16(in);
   const uint64_t P = (uint64_t)t.G * t.pages_per_cta;
   const uint64_t bg = (uint64_t)t.B * t.G;
@@ -372,9 +394,20 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
   if (smem > 48 * 1024)
     RS_CUDA(cudaFuncSetAttribute(k_page_partition<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
+  // zeroed before the partition: keys whose staging range is full are counted straight into it
+  RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
   {
     PassTimer pt_(RS_PASS_PARTITION, ws.stream);
-    if (al && t.B <= 256) {  // TMA-fed tiles, bulk-stored pages
+    bool launched = false;
+    if constexpr (sizeof(typename Map::In) == 4) {
+      if (al && t.B <= 256 && use_ws) {  // warp-specialised: rankers + page-store warps
+        k_page_partition_ws<Map><<<t.G, kWsThreads, page_ws_smem(t.B), ws.stream>>>(
+            in, n, map, t, pages, page_bucket, page_fill, pc_bm, counts, ws.stats);
+        launched = true;
+      }
+    }
+    if (launched) {
+    } else if (al && t.B <= 256) {  // TMA-fed tiles, bulk-stored pages
       k_page_partition_tma<Map><<<t.G, kTlThreads, page_tma_smem<Map>(), ws.stream>>>(
           in, n, map, t, pages, page_bucket, page_fill, pc_bm, ws.stats);
     } else {
@@ -391,7 +424,6 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
     k_page_work<<<1, kTlMaxBuckets, 0, ws.stream>>>(po_bm, total, t, work);
     RS_LAUNCH_CHECK();
   }
-  RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
   const uint64_t max_groups = P / t.group_pages + t.B + 1;
   const size_t cnt_smem = (t.S + 1) * sizeof(uint32_t);  // + the dump bin of pad entries
   if (cnt_smem > 48 * 1024)
@@ -417,7 +449,7 @@ void count_pass(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, 
   }
   TwoLevel t{};
   if constexpr (map_first<Map>::value) {
-    if (plan_two_level<MapU32>(cells, n, t)) {  // map pass, then the uint32 partition
+    if (plan_two_level<MapU32>(cells, n, t, use_ws_partition<MapU32>(true))) {  // map pass, then the uint32 partition
       auto* mapped = ws.get<uint32_t>(kSlotMapped, n);
       {
         PassTimer pt_(RS_PASS_PARTITION, ws.stream);
@@ -425,12 +457,12 @@ void count_pass(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, 
                                                                                         mapped, ws.stats);
         RS_LAUNCH_CHECK();
       }
-      two_level_count(ws, mapped, n, MapU32{}, t, counts);
+      two_level_count(ws, mapped, n, MapU32{}, t, counts, use_ws_partition<MapU32>(true));
       return;
     }
   }
-  if (plan_two_level<Map>(cells, n, t)) {
-    two_level_count(ws, in, n, map, t, counts);
+  if (plan_two_level<Map>(cells, n, t, use_ws_partition<Map>(false))) {
+    two_level_count(ws, in, n, map, t, counts, use_ws_partition<Map>(false));
     return;
   }
   RS_CUDA(cudaMemsetAsync(counts, 0, cells * sizeof(uint32_t), ws.stream));
@@ -1487,6 +1519,87 @@ rs_status rs_sort_u32_kv(const uint32_t* keys, const uint32_t* vals, uint64_t n,
   });
 }
 
+extern "C++" {
+// Alphabet (key_model.cpp:190-223) as a device table in ws kSlotAlphabet, the
+// data's width (longest record, key_model.cpp:228-230) and symbol check by
+// one scan; `packed` (optional) receives the MSD-packed keys.
+struct StrSetup {
+  StrTable t;
+  size_t alen;
+  int lin;            // contiguous alphabet: ordinal = byte - lin
+  uint32_t obits;     // bits of the largest ordinal
+  const uint16_t* d_ord;
+  const uint8_t* d_sym;
+  uint32_t w;         // width of the data (>= 1)
+  bool bad;           // a symbol outside the alphabet
+};
+
+StrSetup str_setup(Workspace& ws, const uint8_t* chars, uint64_t n, uint32_t width, const char* h_alphabet,
+                   unsigned long long* packed) {
+  StrSetup r{};
+  const char* alpha = h_alphabet ? h_alphabet : "abcdefghijklmnopqrstuvwxyz";
+  r.alen = strlen(alpha);
+  if (r.alen == 0) fail(RS_INVALID_ARGUMENT, "alphabet is empty");  // Alphabet(), key_model.cpp:190-201
+  for (size_t i = 0; i < r.alen; ++i) {
+    const auto c = static_cast<unsigned char>(alpha[i]);
+    if (r.t.ord[c] != 0) fail(RS_INVALID_ARGUMENT, std::string("duplicate symbol '") + alpha[i] + "' in alphabet");
+    r.t.ord[c] = static_cast<uint16_t>(i + 1);
+    r.t.sym[i + 1] = c;
+  }
+  r.t.radix = static_cast<uint32_t>(r.alen) + 1;
+  r.lin = static_cast<int>(static_cast<unsigned char>(alpha[0])) - 1;
+  for (size_t i = 1; i < r.alen; ++i)
+    if (static_cast<unsigned char>(alpha[i]) != static_cast<unsigned char>(alpha[0]) + i) r.lin = -1;
+  if (static_cast<unsigned char>(alpha[0]) == 0) r.lin = -1;
+  r.obits = 1;
+  while ((r.alen >> r.obits) != 0) ++r.obits;
+  auto* tab = ws.get<uint8_t>(kSlotAlphabet, sizeof(StrTable));
+  RS_CUDA(cudaMemcpyAsync(tab, &r.t, sizeof(StrTable), cudaMemcpyHostToDevice, ws.stream));
+  r.d_ord = reinterpret_cast<const uint16_t*>(tab);
+  r.d_sym = tab + offsetof(StrTable, sym);
+  r.w = 1;
+  if (n == 0) return r;
+  reset_stats(ws);
+  {
+    PassTimer pt_(RS_PASS_OTHER, ws.stream);
+    const bool w8 = width == 8 && (reinterpret_cast<uintptr_t>(chars) & 15) == 0;
+    auto scan = r.obits == 5 ? k_str_scan<5> : k_str_scan<0>;
+    scan<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w8, r.d_ord, ws.stats, packed,
+                                                                      r.lin, static_cast<uint32_t>(r.alen), r.obits);
+    RS_LAUNCH_CHECK();
+  }
+  pull_stats(ws);
+  r.bad = (ws.h_stats->flags & 8u) != 0;
+  r.w = ws.h_stats->max_key ? static_cast<uint32_t>(ws.h_stats->max_key) : 1u;
+  return r;
+}
+
+// The first symbol outside the alphabet in (record, position) order, raised
+// as Alphabet::ordinal does (key_model.cpp:208-214, 233-241).
+[[noreturn]] void fail_first_symbol(Workspace& ws, const uint8_t* chars, uint64_t n, uint32_t width,
+                                    const uint16_t* d_ord) {
+  auto* first = ws.get<unsigned long long>(kSlotScratch, 4);
+  RS_CUDA(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), ws.stream));
+  k_str_first_bad<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, d_ord, first);
+  RS_LAUNCH_CHECK();
+  unsigned long long at = 0;
+  RS_CUDA(cudaMemcpyAsync(&at, first, sizeof(at), cudaMemcpyDeviceToHost, ws.stream));
+  RS_CUDA(cudaStreamSynchronize(ws.stream));
+  uint8_t c = 0;
+  if (at < n * width) RS_CUDA(cudaMemcpy(&c, chars + at, 1, cudaMemcpyDeviceToHost));
+  fail(RS_SYMBOL_OUT_OF_ALPHABET, std::string("symbol '") + static_cast<char>(c) + "' is not in the alphabet");
+}
+
+// strings_to_keys' keys at width w into `keys` (base-radix, pad ordinal 0)
+void str_keys(Workspace& ws, const uint8_t* chars, uint64_t n, uint32_t width, const StrSetup& su,
+              unsigned long long* keys) {
+  PassTimer pt_(RS_PASS_OTHER, ws.stream);
+  k_str_keys<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, su.w, su.t.radix, su.d_ord,
+                                                                            keys, ws.stats);
+  RS_LAUNCH_CHECK();
+}
+}  // extern "C++"
+
 rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, const char* h_alphabet,
                             uint8_t* out, uint64_t out_capacity, const rs_options* opt,
                             rs_report* report, void* stream) {
@@ -1494,89 +1607,251 @@ rs_status rs_sort_fixed_str(const uint8_t* chars, uint64_t n, uint32_t width, co
     ensure_device();
     const uint64_t budget = budget_of(opt);
     if (width == 0) fail(RS_INVALID_ARGUMENT, "record width must be at least 1");
-    StrTable t{};
-    const char* alpha = h_alphabet ? h_alphabet : "abcdefghijklmnopqrstuvwxyz";
-    const size_t alen = strlen(alpha);
-    if (alen == 0) fail(RS_INVALID_ARGUMENT, "alphabet is empty");  // Alphabet(), key_model.cpp:190-201
-    for (size_t i = 0; i < alen; ++i) {
-      const auto c = static_cast<unsigned char>(alpha[i]);
-      if (t.ord[c] != 0) fail(RS_INVALID_ARGUMENT, std::string("duplicate symbol '") + alpha[i] + "' in alphabet");
-      t.ord[c] = static_cast<uint16_t>(i + 1);
-      t.sym[i + 1] = c;
-    }
-    t.radix = static_cast<uint32_t>(alen) + 1;
-    if (n == 0) {
-      if (report) *report = rs_report{0, 0, make_key_spec(t.radix, 1, 1, budget)};
-      return;
-    }
-    if (!chars || !out) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    if (n > 0 && (!chars || !out)) fail(RS_INVALID_ARGUMENT, "null device pointer");
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
-    auto* tab = ws.get<uint8_t>(kSlotAlphabet, sizeof(StrTable));
-    RS_CUDA(cudaMemcpyAsync(tab, &t, sizeof(StrTable), cudaMemcpyHostToDevice, ws.stream));
-    const auto* d_ord = reinterpret_cast<const uint16_t*>(tab);
-    const auto* d_sym = tab + offsetof(StrTable, sym);
-    // contiguous alphabet (e.g. 'a'..'z'): ordinal <-> byte is arithmetic
-    int lin = static_cast<int>(static_cast<unsigned char>(alpha[0])) - 1;
-    for (size_t i = 1; i < alen; ++i)
-      if (static_cast<unsigned char>(alpha[i]) != static_cast<unsigned char>(alpha[0]) + i) lin = -1;
-    if (static_cast<unsigned char>(alpha[0]) == 0) lin = -1;
     // width of the data = longest string (key_model.cpp:228-230), symbols checked;
     // with msd the same pass packs the keys the MSD levels read
-    uint32_t obits = 1;  // bits of the largest ordinal
+    size_t alen = h_alphabet ? strlen(h_alphabet) : 26;
+    uint32_t obits = 1;
     while ((alen >> obits) != 0) ++obits;
     const bool want_msd = opt && opt->msd && width * obits <= 64;
-    unsigned long long* packed = want_msd ? ws.get<unsigned long long>(kSlotMisc2, n) : nullptr;
-    reset_stats(ws);
-    {
-      PassTimer pt_(RS_PASS_OTHER, ws.stream);
-      const bool w8 = width == 8 && (reinterpret_cast<uintptr_t>(chars) & 15) == 0;
-      auto scan = obits == 5 ? k_str_scan<5> : k_str_scan<0>;
-      scan<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w8, d_ord, ws.stats, packed,
-                                                                        lin, static_cast<uint32_t>(alen), obits);
-      RS_LAUNCH_CHECK();
+    unsigned long long* packed = want_msd && n ? ws.get<unsigned long long>(kSlotMisc2, n) : nullptr;
+    const StrSetup su = str_setup(ws, chars, n, width, h_alphabet, packed);
+    if (n == 0) {
+      if (report) *report = rs_report{0, 0, make_key_spec(su.t.radix, 1, 1, budget)};
+      return;
     }
-    pull_stats(ws);
-    auto check_symbols = [&] {  // after the key spec, as strings_to_keys orders them
-      if (!(ws.h_stats->flags & 8u)) return;
-      auto* first = ws.get<unsigned long long>(kSlotScratch, 4);
-      RS_CUDA(cudaMemsetAsync(first, 0xff, sizeof(unsigned long long), ws.stream));
-      k_str_first_bad<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, d_ord, first);
-      RS_LAUNCH_CHECK();
-      unsigned long long at = 0;
-      RS_CUDA(cudaMemcpyAsync(&at, first, sizeof(at), cudaMemcpyDeviceToHost, ws.stream));
-      RS_CUDA(cudaStreamSynchronize(ws.stream));
-      uint8_t c = 0;
-      if (at < n * width) RS_CUDA(cudaMemcpy(&c, chars + at, 1, cudaMemcpyDeviceToHost));
-      fail(RS_SYMBOL_OUT_OF_ALPHABET, std::string("symbol '") + static_cast<char>(c) + "' is not in the alphabet");
-    };
-    const uint32_t w = ws.h_stats->max_key ? static_cast<uint32_t>(ws.h_stats->max_key) : 1u;
+    const uint32_t w = su.w;
     const uint64_t total_cells = [&] {
-      try { return checked_pow(t.radix, w); } catch (const Failure&) { return ~uint64_t{0}; }
+      try { return checked_pow(su.t.radix, w); } catch (const Failure&) { return ~uint64_t{0}; }
     }();
     const bool msd = want_msd;  // MSD needs the packed key to fit 64 bits; else the reference's budget error
     if (!msd || total_cells <= budget) {
-      const rs_key_spec spec = make_key_spec(t.radix, w, w, budget);
-      check_symbols();
+      const rs_key_spec spec = make_key_spec(su.t.radix, w, w, budget);
+      if (su.bad) fail_first_symbol(ws, chars, n, width, su.d_ord);  // after the key spec, as strings_to_keys orders them
       if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
       auto* keys = ws.get<unsigned long long>(kSlotMapped, n);
-      {  // base-radix keys at the data width
-        PassTimer pt_(RS_PASS_OTHER, ws.stream);
-        k_str_keys<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, n, width, w, t.radix,
-                                                                                  d_ord, keys, ws.stats);
-        RS_LAUNCH_CHECK();
-      }
-      OutStr o{out, width, w, t.radix, d_sym, 0ull};
-      grid_sort(ws, keys, n, MapU64{}, total_cells, o, keys, t.radix, w, 0);
+      str_keys(ws, chars, n, width, su, keys);
+      OutStr o{out, width, w, su.t.radix, su.d_sym, 0ull};
+      grid_sort(ws, keys, n, MapU64{}, total_cells, o, keys, su.t.radix, w, 0);
       if (report) *report = rs_report{n, ws.h_stats->cells_traversed, spec};
       return;
     }
-    check_symbols();
+    if (su.bad) fail_first_symbol(ws, chars, n, width, su.d_ord);
     if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
-    msd_sort_str(ws, chars, n, width, w, t.radix, d_ord, d_sym, out, lin, packed, obits);
-    if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{t.radix, w, w}};
+    msd_sort_str(ws, chars, n, width, w, su.t.radix, su.d_ord, su.d_sym, out, su.lin, packed, su.obits);
+    if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{su.t.radix, w, w}};
   });
 }
 
+rs_status rs_strings_to_keys(const uint8_t* chars, uint64_t n, uint32_t width, const char* h_alphabet,
+                             uint64_t* keys_out, const rs_options* opt, rs_key_spec* h_spec, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    const uint64_t budget = budget_of(opt);
+    if (width == 0) fail(RS_INVALID_ARGUMENT, "record width must be at least 1");
+    if (n > 0 && (!chars || !keys_out)) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    const StrSetup su = str_setup(ws, chars, n, width, h_alphabet, nullptr);
+    const rs_key_spec spec = make_key_spec(su.t.radix, su.w, su.w, budget);  // budget before symbols
+    if (n > 0) {
+      if (su.bad) fail_first_symbol(ws, chars, n, width, su.d_ord);
+      str_keys(ws, chars, n, width, su, reinterpret_cast<unsigned long long*>(keys_out));
+      RS_CUDA(cudaStreamSynchronize(ws.stream));
+    }
+    if (h_spec) *h_spec = spec;
+  });
+}
+
+extern "C++" {
+// TraverseMaps (hashing.hpp:12-48) of a count grid: per leading-digit row the
+// least and greatest occupied suffix (row_min ~0 / row_max -1 while a row is
+// untouched).  A warp's cells mostly share a row: its lanes reduce first.
+__global__ void k_row_bounds(const unsigned long long* __restrict__ counts, uint64_t cells, unsigned long long mod,
+                             unsigned long long* __restrict__ row_min, long long* __restrict__ row_max) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t base0 = (uint64_t)blockIdx.x * blockDim.x;
+  for (uint64_t b = base0; b < cells; b += stride) {  // warp-uniform trip count
+    const uint64_t c = b + threadIdx.x;
+    const bool occ = c < cells && counts[c] != 0;
+    const unsigned long long row = occ ? c / mod : ~0ull;
+    const unsigned long long suf = occ ? c - row * mod : 0ull;
+    const unsigned long long r0 = __shfl_sync(0xffffffffu, row, 0);
+    const bool same = __all_sync(0xffffffffu, !occ || row == r0);
+    if (same && r0 != ~0ull) {
+      unsigned long long mn = occ ? suf : ~0ull, mx = occ ? suf : 0ull;
+      bool any = occ;
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o), d = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = d > mx ? d : mx;
+      }
+      any = __any_sync(0xffffffffu, any);
+      if ((threadIdx.x & 31) == 0 && any) {
+        atomicMin(&row_min[r0], mn);
+        atomicMax(&row_max[r0], static_cast<long long>(mx));
+      }
+    } else if (occ) {
+      atomicMin(&row_min[row], suf);
+      atomicMax(&row_max[row], static_cast<long long>(suf));
+    }
+  }
+}
+
+// extract's traversal set (extraction.cpp:16-30): cells inside their row's
+// [min, max] span of an occupied row keep their count, the rest read as 0.
+__global__ void k_mask_counts(const unsigned long long* __restrict__ counts, uint64_t cells, unsigned long long mod,
+                              const unsigned long long* __restrict__ row_min, const long long* __restrict__ row_max,
+                              unsigned long long* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += stride) {
+    const unsigned long long row = c / mod, suf = c - row * mod;
+    const long long hi = row_max[row];
+    out[c] = (hi >= 0 && suf >= row_min[row] && suf <= static_cast<unsigned long long>(hi)) ? counts[c] : 0ull;
+  }
+}
+
+// The occupied cell holding output position pos (the cell whose emission
+// completes `pos + 1` keys).
+__global__ void k_cell_at(const uint32_t* __restrict__ occ_cell, const unsigned long long* __restrict__ occ_end,
+                          const DevStats* st, unsigned long long pos, unsigned long long* out) {
+  unsigned long long lo = 0, hi = st->n_occupied;
+  while (lo < hi) {
+    const unsigned long long mid = (lo + hi) >> 1;
+    if (occ_end[mid] > pos) hi = mid;
+    else lo = mid + 1;
+  }
+  *out = lo < st->n_occupied ? occ_cell[lo] : ~0ull;
+}
+
+// counts (uint64 grid) += the keys' cells, chunk by chunk through the uint32
+// counting pass (fewer than 2^32 keys per chunk: no counter wraps)
+template <class Map>
+void count_into_u64(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, uint64_t cells,
+                    unsigned long long* wide) {
+  auto* counts = ws.get<uint32_t>(kSlotCounts, cells);
+  for (uint64_t off = 0; off < n; off += kCountChunk) {
+    const uint64_t len = std::min<uint64_t>(kCountChunk, n - off);
+    count_pass(ws, in + off, len, map, cells, counts);
+    PassTimer pt_(RS_PASS_COUNT, ws.stream);
+    k_grid_acc64<<<stream_grid(cells, kThreads * 4), kThreads, 0, ws.stream>>>(wide, counts, cells);
+    RS_LAUNCH_CHECK();
+  }
+}
+}  // extern "C++"
+
+rs_status rs_build_count_space(const uint64_t* keys, uint64_t n, rs_key_spec spec, uint64_t max_cells,
+                               uint64_t* counts, uint64_t* h_row_min, int64_t* h_row_max, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    make_key_spec(spec.radix, spec.total_digits, spec.integer_digits, ~uint64_t{0});  // the geometry itself
+    const uint64_t cells = checked_pow(spec.radix, spec.total_digits);
+    if (cells > max_cells)  // new_space (hashing.cpp:17-25): the budget before any allocation
+      fail(RS_CELL_BUDGET_EXCEEDED,
+           "count space needs " + std::to_string(cells) + " cells, budget is " + std::to_string(max_cells));
+    if (cells > 0xFFFFFFFFull) fail(RS_CELL_BUDGET_EXCEEDED, "a single grid holds at most 2^32-1 cells");
+    if (!counts || (n > 0 && !keys)) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    reset_stats(ws);
+    auto* wide = reinterpret_cast<unsigned long long*>(counts);
+    RS_CUDA(cudaMemsetAsync(wide, 0, cells * sizeof(uint64_t), ws.stream));
+    if (n > 0) count_into_u64(ws, reinterpret_cast<const unsigned long long*>(keys), n, MapU64{}, cells, wide);
+    const unsigned long long mod = checked_pow(spec.radix, spec.total_digits - 1);
+    auto* rows = ws.get<unsigned long long>(kSlotHist, 2ull * spec.radix);
+    auto* rmax = reinterpret_cast<long long*>(rows + spec.radix);
+    RS_CUDA(cudaMemsetAsync(rows, 0xff, 2ull * spec.radix * sizeof(uint64_t), ws.stream));  // min ~0, max -1
+    {
+      PassTimer pt_(RS_PASS_SCAN, ws.stream);
+      k_row_bounds<<<stream_grid(cells, kThreads * 4), kThreads, 0, ws.stream>>>(wide, cells, mod, rows, rmax);
+      RS_LAUNCH_CHECK();
+    }
+    if (h_row_min) RS_CUDA(cudaMemcpyAsync(h_row_min, rows, spec.radix * sizeof(uint64_t), cudaMemcpyDeviceToHost, ws.stream));
+    if (h_row_max) RS_CUDA(cudaMemcpyAsync(h_row_max, rmax, spec.radix * sizeof(int64_t), cudaMemcpyDeviceToHost, ws.stream));
+    pull_stats(ws);
+    if (ws.h_stats->overflow) fail(RS_SPEC_MISMATCH, "a key is outside its spec's key space");
+  });
+}
+
+rs_status rs_extract(const uint64_t* counts, rs_key_spec spec, uint64_t total, const uint64_t* h_row_min,
+                     const int64_t* h_row_max, uint64_t* out, uint64_t out_capacity, rs_report* report,
+                     void* stream) {
+  return guarded([&] {
+    ensure_device();
+    make_key_spec(spec.radix, spec.total_digits, spec.integer_digits, ~uint64_t{0});
+    const uint64_t cells = checked_pow(spec.radix, spec.total_digits);
+    if (cells > 0xFFFFFFFFull) fail(RS_CELL_BUDGET_EXCEEDED, "a single grid holds at most 2^32-1 cells");
+    if (out_capacity < total)  // extraction.cpp:8-12
+      fail(RS_BUFFER_TOO_SMALL, "output buffer holds " + std::to_string(out_capacity) + " keys, need " +
+                                    std::to_string(total));
+    if (!counts || !h_row_min || !h_row_max || (total > 0 && !out)) fail(RS_INVALID_ARGUMENT, "null pointer");
+    const unsigned long long mod = checked_pow(spec.radix, spec.total_digits - 1);
+    // cells_traversed: every occupied row's span, unless the output fills up
+    // inside one (then up to the cell that completes it)
+    unsigned long long spans = 0;
+    for (uint32_t r = 0; r < spec.radix; ++r)
+      if (h_row_max[r] >= 0) spans += static_cast<unsigned long long>(h_row_max[r]) - h_row_min[r] + 1;
+    if (total == 0) {
+      if (report) *report = rs_report{0, 0, spec};
+      return;
+    }
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    reset_stats(ws);
+    auto* rows = ws.get<unsigned long long>(kSlotHist, 2ull * spec.radix + 1);
+    auto* rmax = reinterpret_cast<long long*>(rows + spec.radix);
+    RS_CUDA(cudaMemcpyAsync(rows, h_row_min, spec.radix * sizeof(uint64_t), cudaMemcpyHostToDevice, ws.stream));
+    RS_CUDA(cudaMemcpyAsync(rmax, h_row_max, spec.radix * sizeof(int64_t), cudaMemcpyHostToDevice, ws.stream));
+    auto* masked = ws.get<unsigned long long>(kSlotCounts64, cells);
+    k_mask_counts<<<stream_grid(cells, kThreads * 4), kThreads, 0, ws.stream>>>(
+        reinterpret_cast<const unsigned long long*>(counts), cells, mod, rows, rmax, masked);
+    RS_LAUNCH_CHECK();
+    scan_pass(ws, static_cast<const unsigned long long*>(masked), cells, total);
+    pull_stats(ws);  // (also orders the host arrays above)
+    const unsigned long long sum = ws.h_stats->total;
+    const uint64_t written = std::min<uint64_t>(total, sum);
+    unsigned long long traversed = spans;
+    if (sum > total) {
+      // more keys in the spans than were inserted: the raster stops at the
+      // cell that completes `total` (extraction.cpp:27); tile starts for that length
+      const uint32_t etiles = static_cast<uint32_t>((total + kEmitTile - 1) / kEmitTile);
+      k_tile_first<<<(etiles + 1 + 255) / 256, 256, 0, ws.stream>>>(
+          static_cast<unsigned long long*>(ws.buf[kSlotOccEnd]), ws.stats, total, etiles,
+          static_cast<uint32_t*>(ws.buf[kSlotTileFirst]));
+      auto* at = ws.get<unsigned long long>(kSlotScratch, 4);
+      k_cell_at<<<1, 1, 0, ws.stream>>>(static_cast<uint32_t*>(ws.buf[kSlotOccCell]),
+                                        static_cast<unsigned long long*>(ws.buf[kSlotOccEnd]), ws.stats, total - 1, at);
+      RS_LAUNCH_CHECK();
+      unsigned long long stop = 0;
+      RS_CUDA(cudaMemcpyAsync(&stop, at, sizeof(stop), cudaMemcpyDeviceToHost, ws.stream));
+      RS_CUDA(cudaStreamSynchronize(ws.stream));
+      const unsigned long long srow = stop / mod, ssuf = stop - srow * mod;
+      traversed = 0;
+      for (uint32_t r = 0; r < srow; ++r)
+        if (h_row_max[r] >= 0) traversed += static_cast<unsigned long long>(h_row_max[r]) - h_row_min[r] + 1;
+      traversed += ssuf - h_row_min[srow] + 1;
+    }
+    if (written > 0) {
+      OutU64 o{reinterpret_cast<unsigned long long*>(out), 0ull, aligned32(out)};
+      emit_pass(ws, written, o);
+    }
+    RS_CUDA(cudaStreamSynchronize(ws.stream));
+    if (report) *report = rs_report{written, traversed, spec};
+  });
+}
+
+rs_status rs_checked_pow(uint64_t radix, uint32_t exp, uint64_t* h_out) {
+  return guarded([&] {
+    const uint64_t v = checked_pow(radix, exp);
+    if (h_out) *h_out = v;
+  });
+}
+
+rs_status rs_make_key_spec(uint32_t radix, uint32_t total_digits, uint32_t integer_digits, uint64_t max_cells,
+                           rs_key_spec* h_spec) {
+  return guarded([&] {
+    const rs_key_spec s = make_key_spec(radix, total_digits, integer_digits, max_cells);
+    if (h_spec) *h_spec = s;
+  });
+}
 
 rs_status rs_bucket_hist_u32(const uint32_t* keys, uint64_t n, uint64_t divisor, uint64_t* hist,
                              uint32_t buckets, void* stream) {
@@ -1834,6 +2109,57 @@ rs_status rs_emit_u32(const uint32_t* counts, uint64_t cells, uint64_t cell_lo, 
 }
 
 
+extern "C++" {
+// parse_decimal over a device string column into ws mant (kSlotMapped) /
+// own scales (kSlotTmpKeys); the first failing numeral in input order raises
+// the reference's error.  Returns the dataset's max scale / max integer part.
+DecStats decimal_parse(Workspace& ws, const char* chars, const uint64_t* offsets, uint64_t n,
+                       uint32_t* scale_u32 = nullptr) {
+  auto* mant = ws.get<unsigned long long>(kSlotMapped, n);
+  auto* own = ws.get<uint8_t>(kSlotTmpKeys, n);
+  auto* ds = reinterpret_cast<DecStats*>(ws.get<uint8_t>(kSlotAlphabet, sizeof(StrTable)));
+  const auto* off = reinterpret_cast<const unsigned long long*>(offsets);
+  RS_CUDA(cudaMemsetAsync(ds, 0, sizeof(DecStats), ws.stream));
+  RS_CUDA(cudaMemsetAsync(&ds->first_error, 0xff, sizeof(unsigned long long), ws.stream));
+  {
+    PassTimer pt_(RS_PASS_OTHER, ws.stream);
+    k_dec_parse<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, off, n, mant, own, ds, scale_u32);
+    RS_LAUNCH_CHECK();
+  }
+  DecStats h{};
+  RS_CUDA(cudaMemcpyAsync(&h, ds, sizeof(h), cudaMemcpyDeviceToHost, ws.stream));
+  RS_CUDA(cudaStreamSynchronize(ws.stream));
+  if (h.first_error != ~0ull) {  // the numeral the reference's loop stops at
+    const uint64_t i = h.first_error >> 8;
+    unsigned long long be[2];
+    RS_CUDA(cudaMemcpy(be, off + i, sizeof(be), cudaMemcpyDeviceToHost));
+    std::string text(be[1] - be[0], '\0');
+    if (!text.empty()) RS_CUDA(cudaMemcpy(text.data(), chars + be[0], text.size(), cudaMemcpyDeviceToHost));
+    const size_t dot = text.find('.');
+    fail_numeral(static_cast<uint32_t>(h.first_error & 0xff), text,
+                 dot == std::string::npos ? 0u : static_cast<uint32_t>(text.size() - dot - 1));
+  }
+  return h;
+}
+
+// normalize_dataset (key_model.cpp:107-133): lambda from the largest integer
+// part, the dataset scale from the longest fraction; keys (in ws kSlotMapped)
+// = mantissa * 10^(scale - own scale).
+rs_key_spec decimal_normalize(Workspace& ws, const char* chars, const uint64_t* offsets, uint64_t n,
+                              uint64_t budget) {
+  const DecStats h = decimal_parse(ws, chars, offsets, n);
+  const uint32_t scale = h.max_scale;
+  const uint32_t lambda = digit_count(h.max_integer);
+  const rs_key_spec spec = make_key_spec(10, lambda + scale, lambda, budget);
+  PassTimer pt_(RS_PASS_OTHER, ws.stream);
+  k_dec_scale<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(
+      static_cast<unsigned long long*>(ws.buf[kSlotMapped]), static_cast<const uint8_t*>(ws.buf[kSlotTmpKeys]), n,
+      scale);
+  RS_LAUNCH_CHECK();
+  return spec;
+}
+}  // extern "C++"
+
 rs_status rs_sort_decimal_strings(const char* chars, const uint64_t* offsets, uint64_t n, uint64_t* keys_out,
                                   uint64_t out_capacity, const rs_options* opt, rs_report* report, void* stream) {
   return guarded([&] {
@@ -1845,44 +2171,45 @@ rs_status rs_sort_decimal_strings(const char* chars, const uint64_t* offsets, ui
     }
     if (!offsets || !keys_out || !chars) fail(RS_INVALID_ARGUMENT, "null device pointer");
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
-    auto* mant = ws.get<unsigned long long>(kSlotMapped, n);
-    auto* own = ws.get<uint8_t>(kSlotTmpKeys, n);
-    auto* ds = reinterpret_cast<DecStats*>(ws.get<uint8_t>(kSlotAlphabet, sizeof(StrTable)));
-    const auto* off = reinterpret_cast<const unsigned long long*>(offsets);
-    RS_CUDA(cudaMemsetAsync(ds, 0, sizeof(DecStats), ws.stream));
-    RS_CUDA(cudaMemsetAsync(&ds->first_error, 0xff, sizeof(unsigned long long), ws.stream));
-    {
-      PassTimer pt_(RS_PASS_OTHER, ws.stream);
-      k_dec_parse<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(chars, off, n, mant, own, ds);
-      RS_LAUNCH_CHECK();
-    }
-    DecStats h{};
-    RS_CUDA(cudaMemcpyAsync(&h, ds, sizeof(h), cudaMemcpyDeviceToHost, ws.stream));
-    RS_CUDA(cudaStreamSynchronize(ws.stream));
-    if (h.first_error != ~0ull) {  // the numeral the reference's loop stops at
-      const uint64_t i = h.first_error >> 8;
-      unsigned long long be[2];
-      RS_CUDA(cudaMemcpy(be, off + i, sizeof(be), cudaMemcpyDeviceToHost));
-      std::string text(be[1] - be[0], '\0');
-      if (!text.empty()) RS_CUDA(cudaMemcpy(text.data(), chars + be[0], text.size(), cudaMemcpyDeviceToHost));
-      const size_t dot = text.find('.');
-      fail_numeral(static_cast<uint32_t>(h.first_error & 0xff), text,
-                   dot == std::string::npos ? 0u : static_cast<uint32_t>(text.size() - dot - 1));
-    }
-    // normalize_dataset (key_model.cpp:107-133): lambda from the largest
-    // integer part, the dataset scale from the longest fraction
-    const uint32_t scale = h.max_scale;
-    const uint32_t lambda = digit_count(h.max_integer);
-    const rs_key_spec spec = make_key_spec(10, lambda + scale, lambda, budget);
+    const rs_key_spec spec = decimal_normalize(ws, chars, offsets, n, budget);
     if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
-    {
-      PassTimer pt_(RS_PASS_OTHER, ws.stream);
-      k_dec_scale<<<stream_grid(n, kThreads * 4, 8), kThreads, 0, ws.stream>>>(mant, own, n, scale);
-      RS_LAUNCH_CHECK();
-    }
+    auto* mant = static_cast<const unsigned long long*>(ws.buf[kSlotMapped]);
     OutU64 o{reinterpret_cast<unsigned long long*>(keys_out), 0ull, aligned32(keys_out)};
-    grid_sort(ws, mant, n, MapU64{}, checked_pow(10, lambda + scale), o, keys_out, 10, lambda + scale, 0);
+    grid_sort(ws, mant, n, MapU64{}, checked_pow(10, spec.total_digits), o, keys_out, 10, spec.total_digits, 0);
     if (report) *report = rs_report{n, ws.h_stats->cells_traversed, spec};
+  });
+}
+
+rs_status rs_normalize_decimal_strings(const char* chars, const uint64_t* offsets, uint64_t n, uint64_t* keys_out,
+                                       const rs_options* opt, rs_key_spec* h_spec, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    const uint64_t budget = budget_of(opt);
+    if (n == 0) {
+      if (h_spec) *h_spec = make_key_spec(10, 1, 1, budget);
+      return;
+    }
+    if (!offsets || !keys_out || !chars) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    const rs_key_spec spec = decimal_normalize(ws, chars, offsets, n, budget);
+    RS_CUDA(cudaMemcpyAsync(keys_out, ws.buf[kSlotMapped], n * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                            ws.stream));
+    RS_CUDA(cudaStreamSynchronize(ws.stream));
+    if (h_spec) *h_spec = spec;
+  });
+}
+
+rs_status rs_parse_decimals(const char* chars, const uint64_t* offsets, uint64_t n, uint64_t* mantissas,
+                            uint32_t* scales, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    if (n == 0) return;
+    if (!offsets || !chars || !mantissas || !scales) fail(RS_INVALID_ARGUMENT, "null device pointer");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    decimal_parse(ws, chars, offsets, n, scales);
+    RS_CUDA(cudaMemcpyAsync(mantissas, ws.buf[kSlotMapped], n * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                            ws.stream));
+    RS_CUDA(cudaStreamSynchronize(ws.stream));
   });
 }
 

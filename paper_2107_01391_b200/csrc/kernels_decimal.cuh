@@ -54,7 +54,10 @@ struct DecStats {
 __global__ void __launch_bounds__(kThreads) k_dec_parse(const char* __restrict__ chars,
                                                         const unsigned long long* __restrict__ offsets, uint64_t n,
                                                         unsigned long long* __restrict__ mant,
-                                                        uint8_t* __restrict__ scale_out, DecStats* ds) {
+                                                        uint8_t* __restrict__ scale_out, DecStats* ds,
+                                                        uint32_t* __restrict__ scale_u32 = nullptr) {
+  // scale_u32 != nullptr: parse_decimal alone (rs_parse_decimals) — own scales
+  // as uint32, and no integer_part check (normalize_dataset's, 10^scale)
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const auto* bytes = reinterpret_cast<const unsigned char*>(chars);
   unsigned long long mx_int = 0;
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(kThreads) k_dec_parse(const char* __restrict__
       else if (ilen == 0 && flen == 0) code = kDecNoDigits;
       else if (bad) code = kDecBadChar;
       else if (overflow) code = kDecTooLong;
-      else if (flen > 19) code = kDecScaleOverflow;
+      else if (flen > 19 && !scale_u32) code = kDecScaleOverflow;
       frac = flen;
     }
     if (code != kDecOk) {
@@ -123,7 +126,8 @@ __global__ void __launch_bounds__(kThreads) k_dec_parse(const char* __restrict__
       frac = 0;
     }
     mant[i] = m;
-    scale_out[i] = static_cast<uint8_t>(frac);
+    if (scale_u32) scale_u32[i] = frac;
+    else scale_out[i] = static_cast<uint8_t>(frac);
     mx_int = ip > mx_int ? ip : mx_int;
     mx_scale = frac > mx_scale ? frac : mx_scale;
   }
