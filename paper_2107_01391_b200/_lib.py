@@ -84,6 +84,17 @@ SIGNATURES = {
                                    c_void_p]),
     "rs_partition_u32_to": (c_int, [c_void_p, c_uint64, c_uint64, POINTER(c_uint32), c_uint32, POINTER(c_uint64),
                                     POINTER(c_uint64), c_void_p]),
+    "rs_checked_pow": (c_int, [c_uint64, c_uint32, POINTER(c_uint64)]),
+    "rs_make_key_spec": (c_int, [c_uint32, c_uint32, c_uint32, c_uint64, POINTER(RsKeySpec)]),
+    "rs_strings_to_keys": (c_int, [c_void_p, c_uint64, c_uint32, c_char_p, c_void_p, POINTER(RsOptions),
+                                   POINTER(RsKeySpec), c_void_p]),
+    "rs_build_count_space": (c_int, [c_void_p, c_uint64, RsKeySpec, c_uint64, c_void_p, POINTER(c_uint64),
+                                     POINTER(ctypes.c_int64), c_void_p]),
+    "rs_extract": (c_int, [c_void_p, RsKeySpec, c_uint64, POINTER(c_uint64), POINTER(ctypes.c_int64), c_void_p,
+                           c_uint64, POINTER(RsReport), c_void_p]),
+    "rs_parse_decimals": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p, c_void_p]),
+    "rs_normalize_decimal_strings": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, POINTER(RsOptions),
+                                             POINTER(RsKeySpec), c_void_p]),
     "rs_gen_u32": (c_int, [c_uint64, c_uint64, c_uint64, c_uint64, c_void_p, c_void_p]),
     "rs_gen_iota_u32": (c_int, [c_uint64, c_uint64, c_void_p, c_void_p]),
     "rs_gen_f64_cfg3": (c_int, [c_uint64, c_uint64, c_uint64, c_void_p, c_uint32, c_void_p, c_void_p]),
