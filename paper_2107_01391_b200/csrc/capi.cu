@@ -605,6 +605,8 @@ uint64_t pow10u(uint32_t e) { return checked_pow(10, e); }
 void msd_u32_entry(Workspace& ws, const uint32_t* in, uint64_t n, const uint32_t* out, uint32_t key_bits);
 void msd_i64_entry(Workspace& ws, const int64_t* in, uint64_t n, const uint64_t* out, uint32_t key_bits);
 
+constexpr uint32_t kMaxSamples = 65536;  // strided sample that plans an undeclared width
+
 // Shared driver for the decimal-integer paths (u32 and i64).
 template <class Map, class Out, class K>
 void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, const K* sorted,
@@ -629,9 +631,27 @@ void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, cons
   const bool msd_declared = msd_u32 && opt && opt->msd && hint >= 1 && hint <= max_digits &&
                             pow10u(hint) > budget && sizeof(typename Map::In) == 4;
   uint32_t key_bits = 8 * sizeof(typename Map::In);
+  bool speculative = false;  // digits from a sample: the grid sort confirms or redoes
   if (!hinted && !msd_declared) {
     unsigned long long mx;
-    if (Out::kWordBytes > 0 && n <= kSmallMax && out_capacity >= n) {
+    if (n > kSmallMax && out_capacity >= n) {
+      // plan the grid from the max of a strided sample instead of a full
+      // max pass (0.18 ms at 2^28 keys); the counting pass folds in the true
+      // max and flags keys outside the planned grid
+      reset_stats(ws);
+      {
+        PassTimer pt_(RS_PASS_MAX, ws.stream);
+        k_max_sample<Map><<<64, kThreads, 0, ws.stream>>>(in, n, kMaxSamples, map, ws.stats);
+        RS_LAUNCH_CHECK();
+      }
+      pull_stats(ws);
+      check_flags(ws.h_stats->flags);
+      const uint32_t d = digit_count(ws.h_stats->max_key);
+      speculative = pow10u(d) <= budget;  // else: the full max pass decides (budget vs. MSD, error order)
+    }
+    if (speculative) {
+      digits = digit_count(ws.h_stats->max_key);
+    } else if (Out::kWordBytes > 0 && n <= kSmallMax && out_capacity >= n) {
       // small input: max, grid, count, scan, emit and report in one launch when
       // the grid fits shared memory and the budget
       small_sort(ws, in, n, map, 0u, out, 10u, 0u, 0u, true, budget);
@@ -642,12 +662,16 @@ void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, cons
         return;
       }
       mx = ws.h_stats->max_key;
+      digits = digit_count(mx);
     } else {
       mx = device_max(ws, in, n, map);
+      digits = digit_count(mx);
     }
-    digits = digit_count(mx);
-    key_bits = 1;  // MSD digits cover the max's bit width only
-    while (key_bits < 64 && (mx >> key_bits)) ++key_bits;
+    if (!speculative) {
+      mx = ws.h_stats->max_key;
+      key_bits = 1;  // MSD digits cover the max's bit width only
+      while (key_bits < 64 && (mx >> key_bits)) ++key_bits;
+    }
   }
   if (msd_u32 && opt && opt->msd && pow10u(digits) > budget) {
     // wide keys: MSD bucket passes + per-bucket grids
@@ -663,8 +687,18 @@ void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, cons
                                   " keys, need " + std::to_string(n));
   grid_sort(ws, in, n, map, pow10u(digits), out, sorted, 10, 0, 0);
   check_flags(ws.h_stats->flags);
-  if (ws.h_stats->overflow) {  // declared width too small: redo with the derived one
-    digits = digit_count(ws.h_stats->max_key);
+  if (ws.h_stats->overflow) {  // declared (or sampled) width too small: redo with the derived one
+    const unsigned long long mx = ws.h_stats->max_key;
+    digits = digit_count(mx);
+    if (msd_u32 && opt && opt->msd && pow10u(digits) > budget) {
+      key_bits = 1;
+      while (key_bits < 64 && (mx >> key_bits)) ++key_bits;
+      if (out_capacity < n) fail(RS_BUFFER_TOO_SMALL, "output buffer too small");
+      msd_u32(ws, in, n, sorted, key_bits);
+      const uint32_t d = static_cast<uint32_t>(ws.h_stats->report_digits);
+      if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{10, d, d}};
+      return;
+    }
     make_key_spec(10, digits, digits, budget);
     grid_sort(ws, in, n, map, pow10u(digits), out, sorted, 10, 0, 0);
   }

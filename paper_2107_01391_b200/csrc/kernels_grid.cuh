@@ -333,6 +333,25 @@ __global__ void __launch_bounds__(kThreads) k_max(const typename Map::In* __rest
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(&st->flags, flags);
 }
 
+// The max of an evenly strided sample of `samples` elements: the width the
+// counting pass is planned for when the caller declares none.  The pass
+// itself folds in the true max and flags a key outside the planned grid, so
+// a sample that misses the max costs a second sort, never a wrong one.
+template <class Map>
+__global__ void __launch_bounds__(kThreads) k_max_sample(const typename Map::In* __restrict__ in, uint64_t n,
+                                                         uint32_t samples, Map map, DevStats* st) {
+  unsigned long long mx = 0;
+  unsigned flags = 0;
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < samples; s += gridDim.x * blockDim.x) {
+    const uint64_t i = static_cast<uint64_t>((static_cast<unsigned __int128>(s) * n) / samples);
+    const unsigned long long k = map(__ldg(in + i), flags);
+    mx = k > mx ? k : mx;
+  }
+  warp_max_to(mx, &st->max_key);
+  flags = warp_or(flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(&st->flags, flags);
+}
+
 // ------------------------------------------------- K1: map + count (L2 grid)
 // Grid-stride over 16-byte vectors of the input; every lane of a warp runs
 // the same trip count so __match_any_sync always sees the full warp.

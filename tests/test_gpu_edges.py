@@ -135,3 +135,25 @@ def test_kv_place_rejects_keys_outside_the_grid(rs):
     k[7] = 3
     st = lib.rs_kv_place_u32(rs._ptr(k), rs._ptr(v), n, rs._ptr(off), rs._ptr(owner), cells, hk, hv, 1, rs._stream())
     assert lib.rs_status_name(st).decode() == "out_of_range"
+
+
+def test_sampled_width_too_small_redoes(rs, oracle):
+    """Without a declared width, large inputs plan the grid from a strided
+    sample's max; a larger key the sample missed makes the counting pass
+    redo the sort at the data's true width (same keys, same report as the
+    reference)."""
+    import torch
+
+    n = (1 << 22) + 5
+    keys = oracle.gen_u32(80, 0, n, 1000)
+    keys[1] = 9_999_999  # between sample points (every ~64th element)
+    out, rep = rs.sort_u32(torch.from_numpy(keys.view(np.int32)).cuda())
+    want, wrep = oracle.sort_integers_u32(keys)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
+    assert (rep.written, rep.cells_traversed) == wrep[:2] and rep.spec.total_digits == 7
+    # int64 facade input, a negative value the sample misses: negative_value, as the reference
+    vals = keys.astype(np.int64)
+    vals[3] = -4
+    with pytest.raises(rs.Error) as e:
+        rs.sort_i64(torch.from_numpy(vals).cuda())
+    assert e.value.code == "negative_value"
