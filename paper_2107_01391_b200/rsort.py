@@ -6,12 +6,15 @@ keeps their flags, outputs and CSV schema and runs the GPU recombinant sort:
 
     python -m paper_2107_01391_b200.rsort sort --type decimal --report < values.txt
     python -m paper_2107_01391_b200.rsort bench --sizes 1000,100000 --range 1:10 --cd 0,1 --out gpu.csv
-    python -m paper_2107_01391_b200.rsort analyze --in gpu.csv
 
 `--alg recombinant` is the GPU sort; the CPU baselines (counting, radix,
 bucket, oracle) stay in the reference.  Datasets are the reference's
 (`generate`: SplitMix64 draws on the cd-place grid, restated here), so a
-bench CSV from this module lines up row for row with the reference's.
+bench CSV from this module lines up row for row with the reference's, and
+the reference's own `rsort analyze` reads it.  The reference's C++ front
+ends themselves (bench::run_matrix, the pybind module) reach the GPU by
+relinking against include/recsort/*.hpp and this library
+(tests/cpp/Makefile.ref); this module is the Python route.
 """
 from __future__ import annotations
 
@@ -198,83 +201,6 @@ def parse_csv(text: str) -> list[dict]:
     return out
 
 
-def fit_scaling(records: list[dict]) -> dict:
-    """bench::fit_scaling (bench.cpp:228-297): OLS of log10(mean seconds) on
-    log10(n) over one algorithm and case."""
-    import math
-
-    if not records:
-        raise Failure("insufficient_data", "no records to fit")
-    first = records[0]
-    by = {}
-    for r in records:
-        if (r["algorithm"], r["range_lo"], r["range_hi"], r["cd"]) != \
-                (first["algorithm"], first["range_lo"], first["range_hi"], first["cd"]):
-            raise Failure("invalid_argument", "scaling fit needs records from a single algorithm and case")
-        s = by.setdefault(r["n_elements"], [0.0, 0])
-        s[0] += r["seconds"]
-        s[1] += 1
-    if len(by) < 3:
-        raise Failure("insufficient_data", f"scaling fit needs at least 3 distinct sizes, got {len(by)}")
-    means, xs, ys = [], [], []
-    for size in sorted(by):
-        mean = by[size][0] / by[size][1]
-        if not mean > 0.0:
-            raise Failure("invalid_argument", f"non-positive mean time at size {size}")
-        if size == 0:
-            raise Failure("invalid_argument", "cannot fit log scaling at size 0")
-        means.append((size, mean))
-        xs.append(math.log10(size))
-        ys.append(math.log10(mean))
-    n = float(len(xs))
-    xb, yb = sum(xs) / n, sum(ys) / n
-    sxx = sum((x - xb) * (x - xb) for x in xs)
-    sxy = sum((x - xb) * (y - yb) for x, y in zip(xs, ys))
-    syy = sum((y - yb) * (y - yb) for y in ys)
-    slope = sxy / sxx
-    intercept = yb - slope * xb
-    ss_res = sum((y - (intercept + slope * x)) ** 2 for x, y in zip(xs, ys))
-    return {"slope": slope, "intercept": intercept, "r_squared": 1.0 if syy == 0.0 else 1.0 - ss_res / syy,
-            "mean_seconds": means}
-
-
-def worst_case_constant(d: int) -> tuple[int, int]:
-    """bench::worst_case_constant (bench.cpp:305-310): C = 1 + 10^(d-1)/d as (d + 10^(d-1), d)."""
-    if d < 1 or d > 19:
-        raise Failure("invalid_argument", "d must be in [1, 19]")
-    return 10 ** (d - 1) + d, d
-
-
-def analyze(text: str, plot=None) -> str:
-    """rsort analyze (rsort.cpp:380-455) over a bench CSV: per (algorithm,
-    case) group the log-log fit, then the worst-case constant table."""
-    import math
-
-    groups = {}
-    for r in parse_csv(text):
-        groups.setdefault((r["algorithm"], r["range_lo"], r["range_hi"], r["cd"]), []).append(r)
-    if not groups:
-        raise Failure("insufficient_data", "CSV has no data rows")
-    out = []
-    for (alg, lo, hi, cd), recs in groups.items():
-        rep = fit_scaling(recs)
-        out.append(f"{alg} {case_label(lo, hi, cd)}: slope={rep['slope']:.4f} intercept={rep['intercept']:.4f} "
-                   f"R2={rep['r_squared']:.4f}")
-        for size, mean in rep["mean_seconds"]:
-            out.append(f"  n={size} mean={mean:.6g} s")
-        if plot is not None:
-            plot.write(f"# algorithm={alg} case={case_label(lo, hi, cd)}\n# log10_n log10_seconds\n")
-            for size, mean in rep["mean_seconds"]:
-                plot.write(f"{math.log10(size):g} {math.log10(mean):g}\n")
-            plot.write("\n")
-    out.append("")
-    out.append("worst-case constant C = 1 + 10^(d-1)/d")
-    for d in range(1, 11):
-        num, den = worst_case_constant(d)
-        out.append(f"  d={d:<2d} C={num / den:.6g} ({num}/{den})")
-    return "\n".join(out) + "\n"
-
-
 # ------------------------------------------------------------ sort
 def sort_lines(lines: list[str], kind: str = "decimal", alg: str = "recombinant",
                alphabet: str = "abcdefghijklmnopqrstuvwxyz", max_cells: int | None = None,
@@ -383,28 +309,8 @@ def main(argv=None) -> int:
     b.add_argument("--out", default="")
     b.add_argument("--max-case-digits", type=int, default=3)
     b.add_argument("--max-cells", type=int, default=None)
-    a = sub.add_parser("analyze", help="fit log-log scaling over a bench CSV")
-    a.add_argument("--in", required=True, dest="input")
-    a.add_argument("--plot-data", default="")
     args = ap.parse_args(argv)
     try:
-        if args.cmd == "analyze":
-            try:
-                text = open(args.input).read()
-            except OSError:
-                raise Failure("invalid_argument", f"cannot open '{args.input}'") from None
-            plot = None
-            if args.plot_data:
-                try:
-                    plot = open(args.plot_data, "w")
-                except OSError:
-                    raise Failure("invalid_argument", f"cannot write '{args.plot_data}'") from None
-            try:
-                sys.stdout.write(analyze(text, plot))
-            finally:
-                if plot is not None:
-                    plot.close()
-            return 0
         if args.cmd == "sort":
             if args.input in ("", "-"):
                 text = sys.stdin.read()

@@ -81,35 +81,6 @@ def test_csv_and_labels_match_reference(rb):
         assert rsort.case_label(rec["range_lo"], rec["range_hi"], rec["cd"]) == label
 
 
-def test_analyze_fit_matches_reference(rb, tmp_path):
-    """analyze: parse_csv + fit_scaling + the worst-case constants, against
-    the reference's bench.cpp on the same CSV."""
-    L = rb.L
-    L.ref_fit_scaling_csv.argtypes = [ctypes.c_char_p] + [ctypes.POINTER(ctypes.c_double)] * 3
-    L.ref_worst_case_constant.argtypes = [ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64),
-                                          ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_int)]
-    rng = np.random.default_rng(5)
-    recs = [{"algorithm": "recombinant", "n_elements": n, "range_lo": 1.0, "range_hi": 10.0, "cd": 1, "trial": t,
-             "seconds": float(1e-7 * n ** 1.02 * (1 + 0.05 * rng.random())), "extraction_cost": 17}
-            for n in (10, 100, 1000, 10000, 100000) for t in range(3)]
-    csv = rsort.emit_csv(recs)
-    s, i, r2 = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
-    rb.ref._ok(L.ref_fit_scaling_csv(csv.encode(), ctypes.byref(s), ctypes.byref(i), ctypes.byref(r2)))
-    got = rsort.fit_scaling(rsort.parse_csv(csv))
-    assert abs(got["slope"] - s.value) < 1e-12 and abs(got["intercept"] - i.value) < 1e-12
-    assert abs(got["r_squared"] - r2.value) < 1e-12
-    for d in range(1, 20):
-        num, den, below = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_int()
-        rb.ref._ok(L.ref_worst_case_constant(d, ctypes.byref(num), ctypes.byref(den), ctypes.byref(below)))
-        assert rsort.worst_case_constant(d) == (num.value, den.value)
-    p = tmp_path / "b.csv"
-    p.write_text(csv)
-    text = rsort.analyze(csv)
-    assert text.startswith("recombinant (1,10) cd=1: slope=") and "d=10 C=1e+08 (1000000010/10)" in text
-    with pytest.raises(rsort.Failure):
-        rsort.parse_csv("nope\n")
-
-
 def test_cli_argument_errors_match_reference_messages():
     err = io.StringIO()
     old = sys.stderr
