@@ -118,6 +118,21 @@ class ClockSampler:
                 "samples": len(sms), "reasons": sorted(reasons)}
 
 
+class stdout_to_stderr:
+    """File descriptor 1 points at stderr inside the block (C libraries'
+    prints included)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 # -------------------------------------------------------------- launcher
 def launch_cmd(argv: list[str], gpus: int, port: int) -> list[str]:
     """The torchrun command that re-runs this script with one rank per GPU."""
@@ -593,7 +608,11 @@ def main():
     if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
+        # NCCL's init lines (the rank count among them) go to the log on
+        # stderr, so stdout carries only the JSON line
+        with stdout_to_stderr():
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
+            dist.barrier()
     b = Bench(args, rank, world, use_dist)
     lib = b.lib
     n = N_KEYS
