@@ -157,3 +157,33 @@ def test_sampled_width_too_small_redoes(rs, oracle):
     with pytest.raises(rs.Error) as e:
         rs.sort_i64(torch.from_numpy(vals).cuda())
     assert e.value.code == "negative_value"
+
+
+@pytest.mark.parametrize("pattern", ["switch", "sparse", "outside"])
+def test_partition_ranges_under_shifting_buckets(rs, oracle, pattern):
+    """The warp-specialised partition sizes each bucket's staging range from
+    its count two tiles earlier; keys that find their range full are counted
+    straight into the grid.  Inputs whose bucket mix changes from tile to
+    tile (4096-key tiles): whole tiles of one bucket after uniform tiles
+    ("switch"), buckets that appear only every few tiles ("sparse"), and
+    keys outside a declared width mixed in (the dummy range, then the redo)."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    tiles = 2048
+    keys = oracle.gen_u32(81, 0, tiles * 4096, 10**6).reshape(tiles, 4096)
+    if pattern == "switch":
+        for t in range(0, tiles, 5):
+            keys[t] = 10**4 * (t % 100) + rng.integers(0, 10**4, 4096)  # one bucket per tile
+    elif pattern == "sparse":
+        for t in range(tiles):
+            if t % 7 == 3:
+                keys[t, :3000] = 990_000 + rng.integers(0, 10**4, 3000)  # bucket 99, 3000 keys, every 7th tile
+    else:
+        keys[::3, ::97] = 10**6 + rng.integers(0, 10**5, keys[::3, ::97].shape)
+    keys = keys.reshape(-1).astype(np.uint32)
+    digits = 6
+    out, rep = rs.sort_u32(torch.from_numpy(keys.view(np.int32)).cuda(), key_digits=digits)
+    want, wrep = oracle.sort_integers_u32(keys)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
+    assert (rep.written, rep.cells_traversed) == wrep[:2]
