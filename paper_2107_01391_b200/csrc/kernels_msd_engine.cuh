@@ -506,8 +506,18 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
   // w0 a multiple of per), whose swizzle is one XOR with xr; no bounds
   const bool whole = words >= kLeafGridThreads;
   const uint32_t xr = (w0 >> 5) & 31u;
+  // 2^16 cells (cfg5's leaves): the thread's 32 words stay in registers
+  // between the sum and the offsets pass (one shared read per word, not two)
+  const bool fast32 = whole && per == 32;
+  uint32_t xs[32];
   uint32_t sum = 0;
-  if (whole) {
+  if (fast32) {
+#pragma unroll
+    for (uint32_t j = 0; j < 32; ++j) {
+      xs[j] = s_w[(w0 + j) ^ xr];
+      sum += (xs[j] & 0xffffu) + (xs[j] >> 16);
+    }
+  } else if (whole) {
     for (uint32_t j = 0; j < per; ++j) {
       const uint32_t x = s_w[(w0 + j) ^ xr];
       sum += (x & 0xffffu) + (x >> 16);
@@ -542,7 +552,15 @@ __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restr
     run += __shfl_sync(0xffffffffu, ti - t, warp);
   }
   if (scatter) {
-    for (uint32_t j = 0; j < per; ++j) {  // counts -> exclusive offsets (< 65536: no carry between halves)
+    if (fast32) {
+#pragma unroll
+      for (uint32_t j = 0; j < 32; ++j) {  // counts -> exclusive offsets (< 65536: no carry between halves)
+        const uint32_t c0 = xs[j] & 0xffffu, c1 = xs[j] >> 16;
+        s_w[(w0 + j) ^ xr] = run | ((run + c0) << 16);
+        run += c0 + c1;
+      }
+    }
+    for (uint32_t j = 0; j < (fast32 ? 0u : per); ++j) {  // counts -> exclusive offsets (< 65536: no carry between halves)
       const uint32_t w = w0 + j;
       if (whole || w < words) {
         const uint32_t pw = whole ? (w ^ xr) : leaf_gw(w);
