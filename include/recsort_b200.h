@@ -311,6 +311,17 @@ rs_status rs_count_u32(const uint32_t* keys, uint64_t n, uint32_t* counts,
 rs_status rs_emit_u32(const uint32_t* counts, uint64_t cells, uint64_t cell_lo,
                       uint64_t cell_hi, uint32_t key_base, uint32_t* out,
                       uint64_t out_capacity, uint64_t* h_written, void* stream);
+
+/* The small-grid sharding's emit in one call: over the global
+ * (all-reduced) grid, the cells are cut into `parts` contiguous ranges of
+ * about total/parts keys, on cell boundaries (cut r, 1 <= r < parts, = 1 + the
+ * cell whose inclusive prefix first reaches ceil(r * total / parts);
+ * dist.cell_ranges), and range `part` is emitted into out (its keys in
+ * order; *h_written, host, receives how many).  h_cells (host, optional)
+ * receives the range [lo, hi). */
+rs_status rs_emit_part_u32(const uint32_t* counts, uint64_t cells, uint32_t part, uint32_t parts,
+                           uint32_t* out, uint64_t out_capacity, uint64_t* h_written,
+                           uint64_t* h_cells, void* stream);
 /* Histogram of key / divisor into `buckets` uint64 counters (MSD splitters). */
 rs_status rs_bucket_hist_u32(const uint32_t* keys, uint64_t n, uint64_t divisor,
                              uint64_t* hist, uint32_t buckets, void* stream);

@@ -76,6 +76,8 @@ SIGNATURES = {
     "rs_sort_u32_kv_host": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p, POINTER(RsOptions), POINTER(RsReport), c_void_p]),
     "rs_count_u32": (c_int, [c_void_p, c_uint64, c_void_p, c_uint64, POINTER(c_uint32), c_void_p]),
     "rs_emit_u32": (c_int, [c_void_p, c_uint64, c_uint64, c_uint64, c_uint32, c_void_p, c_uint64, POINTER(c_uint64), c_void_p]),
+    "rs_emit_part_u32": (c_int, [c_void_p, c_uint64, c_uint32, c_uint32, c_void_p, c_uint64, POINTER(c_uint64),
+                                 POINTER(c_uint64), c_void_p]),
     "rs_bucket_hist_u32": (c_int, [c_void_p, c_uint64, c_uint64, c_void_p, c_uint32, c_void_p]),
     "rs_partition_u32": (c_int, [c_void_p, c_uint64, c_uint64, POINTER(c_uint32), c_uint32, c_void_p, POINTER(c_uint64), c_void_p]),
     "rs_kv_place_u32": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_void_p, c_uint64, POINTER(c_uint64),

@@ -2099,6 +2099,47 @@ rs_status rs_count_u32(const uint32_t* keys, uint64_t n, uint32_t* counts, uint6
   });
 }
 
+rs_status rs_emit_part_u32(const uint32_t* counts, uint64_t cells, uint32_t part, uint32_t parts, uint32_t* out,
+                           uint64_t out_capacity, uint64_t* h_written, uint64_t* h_cells, void* stream) {
+  return guarded([&] {
+    ensure_device();
+    if (parts == 0 || part >= parts || parts > 1024) fail(RS_INVALID_ARGUMENT, "part must be < parts <= 1024");
+    if (cells == 0 || cells > 0xFFFFFFFFull) fail(RS_INVALID_ARGUMENT, "cells out of range");
+    Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
+    // cut r (1 <= r < parts) = 1 + the cell whose inclusive prefix first
+    // reaches ceil(r * total / parts): the global prefix and the cuts on the
+    // device, two cut values back to the host
+    uint64_t lo = 0, hi = cells;
+    if (parts > 1) {
+      auto* excl = ws.get<uint32_t>(kSlotTmpKeys, cells);
+      auto* tot = ws.get<unsigned long long>(kSlotScratch, 4 + 1024);
+      auto* cuts = tot + 4;
+      RS_CUDA(cudaMemsetAsync(cuts, 0xff, (parts - 1) * sizeof(unsigned long long), ws.stream));  // ~0: past the grid
+      exscan_u32(ws, counts, cells, excl, tot);
+      k_grid_cuts<<<stream_grid(cells, kThreads * 4), kThreads, 0, ws.stream>>>(excl, counts, cells, tot, parts, cuts);
+      RS_LAUNCH_CHECK();
+      std::vector<unsigned long long> h(parts - 1);
+      RS_CUDA(cudaMemcpyAsync(h.data(), cuts, (parts - 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                              ws.stream));
+      RS_CUDA(cudaStreamSynchronize(ws.stream));
+      // monotone and inside the grid (dist.cell_ranges' clamping)
+      uint64_t prev = 0;
+      for (uint32_t r = 1; r < parts; ++r) {
+        const uint64_t c = std::max<uint64_t>(prev, std::min<uint64_t>(h[r - 1], cells));
+        if (r == part) lo = c;
+        if (r == part + 1) hi = c;
+        prev = c;
+      }
+    }
+    if (h_cells) {
+      h_cells[0] = lo;
+      h_cells[1] = hi;
+    }
+    const rs_status st = rs_emit_u32(counts, cells, lo, hi, 0, out, out_capacity, h_written, stream);
+    if (st != RS_OK) throw Failure{st, g_last_error};
+  });
+}
+
 rs_status rs_emit_u32(const uint32_t* counts, uint64_t cells, uint64_t cell_lo, uint64_t cell_hi,
                       uint32_t key_base, uint32_t* out, uint64_t out_capacity,
                       uint64_t* h_written, void* stream) {

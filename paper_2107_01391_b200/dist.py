@@ -116,6 +116,16 @@ class GpuOps:
                                             self._stream()))
         return out[: written.value]
 
+    def emit_part(self, counts: torch.Tensor, part: int, parts: int, cap: int) -> torch.Tensor:
+        """Range `part` of `parts` of the global grid (cuts as cell_ranges),
+        emitted in one library call (rs_emit_part_u32)."""
+        out = torch.empty(max(cap, 1), dtype=torch.int32, device=counts.device)
+        written = ctypes.c_uint64()
+        self._check(self._lib().rs_emit_part_u32(ctypes.c_void_p(counts.data_ptr()), counts.numel(), part, parts,
+                                                 ctypes.c_void_p(out.data_ptr()), out.numel(), ctypes.byref(written),
+                                                 None, self._stream()))
+        return out[: written.value]
+
     def bucket_hist(self, keys: torch.Tensor, divisor: int, buckets: int) -> torch.Tensor:
         hist = torch.zeros(buckets, dtype=torch.int64, device=keys.device)
         self._check(self._lib().rs_bucket_hist_u32(ctypes.c_void_p(keys.data_ptr()), keys.numel(), divisor,
@@ -134,7 +144,9 @@ class GpuOps:
     def sort_kv(self, keys: torch.Tensor, vals: torch.Tensor, cells: int) -> tuple[torch.Tensor, torch.Tensor]:
         from . import DEFAULT_CELL_BUDGET, sort_u32_kv
 
-        k, v, _ = sort_u32_kv(keys, vals, max_cells=max(cells, DEFAULT_CELL_BUDGET))
+        # the grid's width bounds every key (keys >= cells were rejected by the count)
+        digits = len(str(max(cells - 1, 0)))
+        k, v, _ = sort_u32_kv(keys, vals, max_cells=max(cells, DEFAULT_CELL_BUDGET), key_digits=digits)
         return k, v
 
     def part_counts(self, keys: torch.Tensor, divisor: int, bounds: list[int]) -> list[int]:
@@ -220,13 +232,10 @@ def sharded_grid_sort(keys: torch.Tensor, cells: int, ops=None, group=None) -> t
         raise ValueError("sharded_grid_sort: fewer than 2^32 keys in total (world x shard) per call")
     counts = ops.count(keys, cells)
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)  # C1: the grid over NVLink
-    prefix = torch.cumsum(counts, 0, dtype=torch.int64)
-    # this rank's cell range and key count, cut on the device: one 24-byte copy back
-    bounds = cell_bounds_device(prefix, world)
-    lo_hi = bounds[rank:rank + 2]
-    ends = torch.where(lo_hi > 0, prefix[(lo_hi - 1).clamp(min=0)], torch.zeros_like(lo_hi))
-    lo, hi, n_out = (int(v) for v in torch.stack([lo_hi[0], lo_hi[1], ends[1] - ends[0]]).cpu())
-    return ops.emit(counts, lo, hi, n_out)
+    # this rank's contiguous cell range (cut_rank .. cut_rank+1, cell_ranges'
+    # rule) emitted in one library call; a slice can exceed the even share
+    # by at most one cell's keys, so the output is sized for the whole input
+    return ops.emit_part(counts, rank, world, keys.numel() * world)
 
 
 def kv_placement(grids: torch.Tensor, rank: int, world: int):

@@ -29,6 +29,14 @@ class NumpyOps:
         assert out.size == n_out
         return torch.from_numpy(out)
 
+    def emit_part(self, counts, part, parts, cap):
+        prefix = torch.cumsum(counts.to(torch.int64), 0)
+        lo, hi = cell_ranges(prefix, parts)[part]
+        c = counts.numpy()[lo:hi].astype(np.int64)
+        out = np.repeat(np.arange(lo, hi, dtype=np.int64), c).astype(np.int32)
+        assert out.size <= cap
+        return torch.from_numpy(out)
+
     def bucket_hist(self, keys, divisor, buckets):
         b = (keys.numpy().view(np.uint32).astype(np.int64) // divisor)
         return torch.from_numpy(np.bincount(b, minlength=buckets).astype(np.int64))

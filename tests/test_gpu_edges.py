@@ -187,3 +187,32 @@ def test_partition_ranges_under_shifting_buckets(rs, oracle, pattern):
     want, wrep = oracle.sort_integers_u32(keys)
     assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
     assert (rep.written, rep.cells_traversed) == wrep[:2]
+
+
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_emit_part_cuts_match_cell_ranges(rs, oracle, parts):
+    """rs_emit_part_u32 (the sharded grid's emit): the device cuts equal
+    dist.cell_ranges' rule on a skewed grid, and the parts concatenate to
+    the whole sorted sequence."""
+    import torch
+
+    from paper_2107_01391_b200.dist import GpuOps, cell_ranges
+
+    lib = rs._lib.load()
+    keys = oracle.gen_u32(82, 0, 3_000_017, 10**6)
+    keys[::5] = 123_456  # a hot cell
+    k = torch.from_numpy(keys.view(np.int32)).cuda()
+    ops = GpuOps()
+    counts = ops.count(k, 10**6)
+    prefix = torch.cumsum(counts.to(torch.int64), 0).cpu()
+    want_ranges = cell_ranges(prefix, parts)
+    outs = []
+    for p in range(parts):
+        out = torch.empty(keys.size, dtype=torch.int32, device="cuda")
+        written = ctypes.c_uint64()
+        cells = (ctypes.c_uint64 * 2)()
+        rs._check(lib.rs_emit_part_u32(rs._ptr(counts), 10**6, p, parts, rs._ptr(out), out.numel(),
+                                       ctypes.byref(written), cells, rs._stream()))
+        assert (cells[0], cells[1]) == want_ranges[p]
+        outs.append(out[: written.value].cpu().numpy().view(np.uint32))
+    assert np.array_equal(np.concatenate(outs), np.sort(keys))
