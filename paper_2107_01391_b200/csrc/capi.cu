@@ -1094,7 +1094,8 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
         const uint32_t lcap = static_cast<uint32_t>(std::min<size_t>((smem - grid_b) / 2, 65535));
         RS_CUDA(cudaFuncSetAttribute(k_leaf_grid<K, Emit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-        k_leaf_grid<K, Emit><<<h[1], kLeafGridThreads, smem, ws.stream>>>(dst, leaf_grid, shift, lcap, emit);
+        k_leaf_grid<K, Emit><<<h[1], kLeafGridThreads, smem, ws.stream>>>(dst, leaf_grid, shift, lcap, emit, h[1],
+                                                                           static_cast<uint32_t>(sm_count()));
       }
       if (h[2]) k_leaf_bitonic<K, Emit><<<h[2], kMsdThreads, 0, ws.stream>>>(dst, leaf_small, emit);
       RS_LAUNCH_CHECK();

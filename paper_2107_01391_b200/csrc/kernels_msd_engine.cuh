@@ -456,10 +456,21 @@ __device__ __forceinline__ uint32_t leaf_gw(uint32_t w) { return w ^ ((w >> 5) &
 template <class K, class Emit>
 __global__ void __launch_bounds__(kLeafGridThreads) k_leaf_grid(const K* __restrict__ src,
                                                                 const MsdSeg* __restrict__ segs, uint32_t rem_bits,
-                                                                uint32_t cap, Emit emit) {
+                                                                uint32_t cap, Emit emit, uint32_t nsegs,
+                                                                uint32_t ahead) {
   extern __shared__ uint32_t s_w[];
   __shared__ uint32_t s_scan[kLeafGridThreads / 32];
   const MsdSeg g = segs[blockIdx.x];
+  // One CTA per SM: the leaf `ahead` launches later (about the next wave on
+  // this SM) is pulled into L2 now, one 128-byte line per thread, so its
+  // first key loads hit L2 instead of waiting out DRAM latency.
+  if (blockIdx.x + ahead < nsegs) {
+    const MsdSeg h = segs[blockIdx.x + ahead];
+    const char* base = reinterpret_cast<const char*>(src + h.start);
+    const uint64_t bytes = (uint64_t)h.size * sizeof(K);
+    for (uint64_t off = (uint64_t)threadIdx.x * 128; off < bytes; off += (uint64_t)kLeafGridThreads * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+  }
   const uint32_t cells = 1u << rem_bits;
   const uint32_t words = (cells + 1) / 2;
   uint16_t* s_out = reinterpret_cast<uint16_t*>(s_w + words);
