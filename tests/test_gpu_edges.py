@@ -216,3 +216,22 @@ def test_emit_part_cuts_match_cell_ranges(rs, oracle, parts):
         assert (cells[0], cells[1]) == want_ranges[p]
         outs.append(out[: written.value].cpu().numpy().view(np.uint32))
     assert np.array_equal(np.concatenate(outs), np.sort(keys))
+
+
+@pytest.mark.parametrize("cells", [2_000_000, 2_560_000, 1_280_001])
+def test_count_grids_with_two_buckets_per_store_thread(rs, oracle, cells):
+    """Grids of 129-256 outer buckets: the warp-specialised partition's store
+    threads keep two buckets each (rs_count_u32, the multi-GPU count phase,
+    takes any grid size).  Counts against a bincount."""
+    import torch
+
+    lib = rs._lib.load()
+    n = 5_000_011
+    keys = oracle.gen_u32(83, 0, n, cells)
+    keys[::11] = cells - 1
+    k = torch.from_numpy(keys.view(np.int32)).cuda()
+    counts = torch.empty(cells, dtype=torch.int32, device="cuda")
+    mx = ctypes.c_uint32()
+    rs._check(lib.rs_count_u32(rs._ptr(k), n, rs._ptr(counts), cells, ctypes.byref(mx), rs._stream()))
+    assert mx.value == cells - 1
+    assert np.array_equal(counts.cpu().numpy().astype(np.int64), np.bincount(keys.astype(np.int64), minlength=cells))
