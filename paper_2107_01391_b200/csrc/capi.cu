@@ -1536,7 +1536,8 @@ rs_status rs_sort_u32_kv(const uint32_t* keys, const uint32_t* vals, uint64_t n,
       return;
     }
     if (!keys || !vals || !keys_out || !vals_out) fail(RS_INVALID_ARGUMENT, "null device pointer");
-    if (n >= (1ull << 30)) fail(RS_INVALID_ARGUMENT, "rs_sort_u32_kv takes fewer than 2^30 records per call");
+    // positions and per-chunk offsets are uint32: fewer than 2^32 records per call
+    if (n > 0xFFFFFFFFull) fail(RS_INVALID_ARGUMENT, "rs_sort_u32_kv takes fewer than 2^32 records per call");
     Workspace& ws = workspace_for(static_cast<cudaStream_t>(stream));
     const uint32_t hint = opt ? opt->key_digits : 0;
     const bool hinted = hint >= 1 && hint <= 10 && pow10u(hint) <= budget;

@@ -235,3 +235,27 @@ def test_count_grids_with_two_buckets_per_store_thread(rs, oracle, cells):
     rs._check(lib.rs_count_u32(rs._ptr(k), n, rs._ptr(counts), cells, ctypes.byref(mx), rs._stream()))
     assert mx.value == cells - 1
     assert np.array_equal(counts.cpu().numpy().astype(np.int64), np.bincount(keys.astype(np.int64), minlength=cells))
+
+
+def test_kv_above_2_pow_31_records(rs, oracle):
+    """Stable key/value over 2^31 + 3 records (uint32 positions and
+    offsets throughout): sorted, stable (payload = index), every payload
+    pointing at its key."""
+    import torch
+
+    lib = rs._lib.load()
+    n = (1 << 31) + 3
+    k = torch.empty(n, dtype=torch.int32, device="cuda")
+    rs._check(lib.rs_gen_u32(oracle.config_seed(2), 0, n, 10**6, rs._ptr(k), rs._stream()))
+    v = torch.empty_like(k)
+    rs._check(lib.rs_gen_iota_u32(0, n, rs._ptr(v), rs._stream()))
+    ko, vo, rep = rs.sort_u32_kv(k, v, key_digits=6)
+    assert rep.written == n and rep.cells_traversed == 10**6
+    assert bool((ko[1:] >= ko[:-1]).all())
+    same = ko[1:] == ko[:-1]
+    idx = vo.to(torch.int64) & 0xFFFFFFFF  # payloads past 2^31 are negative as int32
+    assert bool((idx[1:][same] > idx[:-1][same]).all())
+    del same
+    assert torch.equal(k[idx], ko)
+    del k, v, ko, vo
+    torch.cuda.empty_cache()
