@@ -118,7 +118,7 @@ class ClockSampler:
                 "samples": len(sms), "reasons": sorted(reasons)}
 
 
-class stdout_to_stderr:
+class StdoutToStderr:
     """File descriptor 1 points at stderr inside the block (C libraries'
     prints included)."""
 
@@ -610,7 +610,7 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29517")
         # NCCL's init lines (the rank count among them) go to the log on
         # stderr, so stdout carries only the JSON line
-        with stdout_to_stderr():
+        with StdoutToStderr():
             dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
             dist.barrier()
     b = Bench(args, rank, world, use_dist)

@@ -4,7 +4,8 @@ GPU over torch.distributed (NCCL on the GPU box).
 Small grids (cfg1-3): every rank counts its contiguous key shard into the full
 grid (rs_count_u32), the grids are summed with one all-reduce over NVLink,
 and each rank then emits a contiguous range of cells holding about total/G
-keys (rs_emit_u32).  No key moves between GPUs: rank r's output is slice r
+keys (rs_emit_part_u32: global prefix, cuts and the range emit in one call).  No
+key moves between GPUs: rank r's output is slice r
 of the globally sorted sequence.
 
 Stable key/value (cfg2 KV): the per-rank grids are all-gathered (a G x cells
@@ -107,14 +108,6 @@ class GpuOps:
         self._check(self._lib().rs_count_u32(ctypes.c_void_p(keys.data_ptr()), keys.numel(),
                                              ctypes.c_void_p(counts.data_ptr()), cells, None, self._stream()))
         return counts
-
-    def emit(self, counts: torch.Tensor, lo: int, hi: int, n_out: int) -> torch.Tensor:
-        out = torch.empty(max(n_out, 1), dtype=torch.int32, device=counts.device)
-        written = ctypes.c_uint64()
-        self._check(self._lib().rs_emit_u32(ctypes.c_void_p(counts.data_ptr()), counts.numel(), lo, hi, 0,
-                                            ctypes.c_void_p(out.data_ptr()), out.numel(), ctypes.byref(written),
-                                            self._stream()))
-        return out[: written.value]
 
     def emit_part(self, counts: torch.Tensor, part: int, parts: int, cap: int) -> torch.Tensor:
         """Range `part` of `parts` of the global grid (cuts as cell_ranges),

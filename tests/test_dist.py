@@ -23,12 +23,6 @@ class NumpyOps:
     def count(self, keys, cells):
         return torch.from_numpy(np.bincount(keys.numpy().astype(np.int64), minlength=cells).astype(np.int32))
 
-    def emit(self, counts, lo, hi, n_out):
-        c = counts.numpy()[lo:hi].astype(np.int64)
-        out = np.repeat(np.arange(lo, hi, dtype=np.int64), c).astype(np.int32)
-        assert out.size == n_out
-        return torch.from_numpy(out)
-
     def emit_part(self, counts, part, parts, cap):
         prefix = torch.cumsum(counts.to(torch.int64), 0)
         lo, hi = cell_ranges(prefix, parts)[part]

@@ -1,8 +1,9 @@
-"""A/B of the cfg2 / cfg3 partition variants (RSB_PARTITION env, read once
-per process): per-pass device times of the cfg2 key-only step and the cfg3
-float64 step.
+"""Per-pass device times of the cfg2 key-only step (and, with --cfg3, the
+cfg3 float64 step), with an exactness check of cfg2.  Used for A/B runs of
+partition variants (a build with a temporary switch, read once per process
+from RSB_* environment variables; the committed library has none).
 
-    RSB_PARTITION=tma python tools/ab_partition.py
+    python tools/ab_partition.py [--cfg3]
 """
 import ctypes
 import json
@@ -49,7 +50,7 @@ def main():
     k = torch.empty(n, dtype=torch.int32, device="cuda")
     rs._check(lib.rs_gen_u32(o.config_seed(2), 0, n, 10**6, rs._ptr(k), rs._stream()))
     out = torch.empty_like(k)
-    res = {"variant": os.environ.get("RSB_PARTITION", "default")}
+    res = {"env": {x: os.environ[x] for x in os.environ if x.startswith("RSB_")}}
     res["cfg2"] = profile(lambda: rs.sort_u32(k, out=out, key_digits=6))
     want = torch.bincount(k.long(), minlength=10**6)
     got = torch.bincount(out.long(), minlength=10**6)
