@@ -200,8 +200,22 @@ MapF64T<G> make_map_f64(uint32_t scale) {
   // every element leaves the fast domain (limit -1)
   const bool fast = scale <= 15;
   const double P = fast ? static_cast<double>(checked_pow(10, scale)) : 1.0;
-  return MapF64T<G>{P, 2.0 * P, fast ? 9007199254740992.0 / 100.0 : -1.0,
-                    fast ? 1.0000001 * std::pow(10.0, -static_cast<double>(scale + 3)) : 0.0, scale};
+  const double limit = fast ? 9007199254740992.0 / 100.0 : -1.0;
+  const double tiny = fast ? 1.0000001 * std::pow(10.0, -static_cast<double>(scale + 3)) : 0.0;
+  MapF64T<G> m{P, limit, tiny, scale, 0, 0, 0, ~0ull};
+  if (fast) {
+    // the integer fast path tests bit patterns: positive doubles order as
+    // their bits, so x * P < limit <=> bits(x) < bits(xlim) for the least
+    // such xlim (found from limit / P by stepping, exact IEEE products)
+    double xl = limit / P;
+    while (xl * P >= limit) xl = std::nextafter(xl, 0.0);
+    while (xl * P < limit) xl = std::nextafter(xl, INFINITY);
+    std::memcpy(&m.xlim_bits, &xl, 8);
+    std::memcpy(&m.tiny_bits, &tiny, 8);
+    m.Pi = checked_pow(10, scale);
+    m.zero_bits = 0;
+  }
+  return m;
 }
 constexpr unsigned kF64Errors = kFlagNegative | kFlagNonFinite | kFlagBudget;
 
@@ -273,10 +287,7 @@ __global__ void __launch_bounds__(kThreads) k_f64_map_u64(const double* __restri
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const double v = __ldcs(x + i);
-    bool und;
-    unsigned long long k = map.fast(v, und);
-    if (und) k = map(v, flags);
-    out[i] = k;
+    out[i] = map(v, flags);
   }
   flags = warp_or(flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(&st->flags, flags);

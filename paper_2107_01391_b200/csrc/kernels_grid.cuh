@@ -122,24 +122,16 @@ struct MapU64 {
 //    half-up result is decided by x*P versus m+1/2, exactly.
 // IEEE division of two exact doubles (m < 2^53, P <= 10^15) is correctly
 // rounded, so every "rounds to x" test is exact.
-// Is x == RN(c / d) (d > 0)?  Without dividing: with h = d * ulp(x) / 2
-// (exact) the exact residual c - x*d is below h iff c/d lies inside x's
-// rounding interval, and r = fma(-x, d, c) rounds it once, so r < h proves
-// it and r > h refutes it (rounding is monotone and h is representable).
-// r == h (a tie or a rounding onto h) and powers of two (narrower spacing
-// below x) stay undecided.  1 yes, 0 no, -1 undecided.
-__device__ __forceinline__ int quotient_is(double x, double c, double d) {
-  const unsigned long long xb = static_cast<unsigned long long>(__double_as_longlong(x));
-  const double ulp = __longlong_as_double(static_cast<long long>((xb & 0x7ff0000000000000ull) - (52ull << 52)));
-  const double h = d * ulp * 0.5;
-  const double r = fabs(fma(-x, d, c));
-  const bool pow2 = (xb & 0x000fffffffffffffull) == 0;
-  return (pow2 || r == h) ? -1 : (r < h ? 1 : 0);
+// The exact float64 mapping out of line: the hot loops keep their registers
+// for the fast tests and pay a call only for the keys those leave undecided.
+template <class Map>
+__device__ __noinline__ unsigned long long map_exact(const Map& map, double x, unsigned& flags) {
+  return map.exact(x, flags);
 }
 
 // kGeneral = false: the lean mapper of the hot kernels — a value outside
 // the fast domain raises kFlagDomain and the host redoes the sort with
-// kGeneral = true, whose operator() takes the exact general search for
+// kGeneral = true, whose exact() takes the exact general search for
 // those values (a call the hot kernels' register budget never pays for).
 template <bool kGeneral>
 struct MapF64T {
@@ -147,11 +139,22 @@ struct MapF64T {
   using Key = unsigned long long;
   static constexpr bool kMapFirst = true;  // a separate streaming map pass, then the uint32 partition
   double P;      // 10^scale
-  double P2;     // 2 * 10^scale
   double limit;  // 2^53 / 100
   double tiny;   // just above 10^-(scale+3)
   uint32_t scale;
+  unsigned long long Pi;         // 10^scale; 0 outside the fast domain (scale > 15)
+  unsigned long long xlim_bits;  // bits of the least x with RN(x * P) >= limit
+  unsigned long long tiny_bits;  // bits of tiny
+  unsigned long long zero_bits;  // 0: +0 is decided by fast(); ~0 (scale > 15): it is not
+  // The mapping every kernel calls: the fast tests below, the exact path
+  // (out of line) for the keys they leave undecided.
   __device__ __forceinline__ unsigned long long operator()(double x, unsigned& flags) const {
+    bool und;
+    const double kd = fast(x, und);
+    return und ? map_exact(*this, x, flags) : static_cast<unsigned long long>(kd);
+  }
+  // The exact mapping (also classifies bad inputs).
+  __device__ __forceinline__ unsigned long long exact(double x, unsigned& flags) const {
     if (!isfinite(x)) {
       flags |= kFlagNonFinite;
       return 0;
@@ -187,33 +190,44 @@ struct MapF64T {
       const unsigned long long c = fr < 0.5 ? m : m + 1;
       if (static_cast<double>(c) / P == x) return c;
     } else if (fr > 0.48 && fr < 0.52) {
-      if (static_cast<double>(2 * m + 1) / P2 == x) return m + 1;
+      if (static_cast<double>(2 * m + 1) / (2.0 * P) == x) return m + 1;
     }
     const bool up = fr > 0.5 || (fr == 0.5 && err > 0.0);
     return up ? m + 1 : m;
   }
-  // The same mapping without branches or division (the map pass has the ILP
-  // to interleave many keys): the candidate test is quotient_is; keys it
-  // cannot decide and keys outside the domain set `undecided` and go through
-  // operator() (mirrored by tests/test_f64_mapping.py::kernel_f64_fast).
-  __device__ __forceinline__ unsigned long long fast(double x, bool& undecided) const {
+  // The same mapping for the hot kernels.  Away from the half-way point the
+  // candidate tests of exact() cannot change the result: with fr < 0.02
+  // the integer candidate is m and the half-up rule also gives m, with
+  // fr > 0.98 both give m + 1, and in between (|fr - 1/2| > 0.02) the
+  // shortest numeral lies within 0.01 of x * P and rounds like it.  So the
+  // mantissa is rint(x * P) unless |fr - 1/2| <= 0.02, where the half-integer
+  // candidate (2m+1) / 2P is tested without a division: x == RN(c / d) iff
+  // the exact residual c - x*d lies inside x's rounding interval, of
+  // half-width h = d * ulp(x) / 2 (exact: an exponent shift of d's bits);
+  // r = |fma(-x, d, c)| rounds it once, so r < h proves it and r > h refutes
+  // it.  r == h and powers of two (narrower spacing below x) stay
+  // undecided, as do keys outside the fast domain (one unsigned range check
+  // on the bits of x: non-negative doubles order as their bit patterns):
+  // those go through exact() (mirrored by
+  // tests/test_f64_mapping.py::kernel_f64_fast).  +0 is decided (rint gives
+  // 0) unless scale > 15 (zero_bits).  Returns the mantissa as a double
+  // (exact: < 2^53 / 100); meaningless when undecided.
+  __device__ __forceinline__ double fast(double x, bool& undecided) const {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+    undecided = u - tiny_bits >= xlim_bits - tiny_bits && u != zero_bits;
     const double p = x * P;
-    const bool bad = !(x >= 0.0) || !(p < limit) || (x > 0.0 && x < tiny);
-    const double err = fma(x, P, -p);
-    double f = floor(p);
-    f = (p == f && err < 0.0) ? f - 1.0 : f;
-    const double fr = p - f;
-    const bool near_int = fr < 0.02 || fr > 0.98;
-    const bool near_half = fr > 0.48 && fr < 0.52;
-    // candidates in double (exact: f < 2^53 / 100): nearest integer, or the half-integer 2f+1 over 2P
-    const double ci = fr < 0.5 ? f : f + 1.0;
-    const double cv = near_int ? ci : 2.0 * f + 1.0;
-    const double dv = near_int ? P : P2;
-    const int q = x == 0.0 ? 1 : ((near_int || near_half) ? quotient_is(x, cv, dv) : 0);  // 0 maps to 0
-    undecided = bad || q < 0;
-    const bool up = fr > 0.5 || (fr == 0.5 && err > 0.0);
-    const double r = q > 0 ? (near_int ? ci : f + 1.0) : (up ? f + 1.0 : f);
-    return static_cast<unsigned long long>(bad ? 0.0 : r);  // one conversion
+    const double c = rint(p);
+    const double d = p - c;  // exact, in [-1/2, 1/2]
+    if ((__double2hiint(d) & 0x7FFFFFFF) < 0x3FDEB851) return c;  // |d| < 0.48 (widened by < 2^-20)
+    const double m = d >= 0.0 ? c : c - 1.0;  // floor(p): p is no integer here
+    const double dv = 2.0 * P;
+    const long long hb = __double_as_longlong(dv) + (static_cast<long long>(static_cast<int>(u >> 52) - 1076) << 52);
+    const long long rb = __double_as_longlong(fma(-x, dv, fma(m, 2.0, 1.0))) & 0x7FFFFFFFFFFFFFFFll;
+    undecided = undecided || (u & ((1ull << 52) - 1)) == 0 || rb == hb;
+    if (rb < hb) return m + 1.0;  // the shortest numeral is m + 1/2: half-up
+    const double fr = p - m;      // exact
+    const bool up = fr > 0.5 || (fr == 0.5 && fma(x, P, -p) > 0.0);
+    return up ? m + 1.0 : m;
   }
 };
 using MapF64 = MapF64T<false>;
@@ -233,49 +247,62 @@ struct map_first<M, std::void_t<decltype(M::kMapFirst)>> : std::true_type {};
 // still lies outside any grid the two-level split serves), so the tuned
 // uint32 partition runs on the cells; max key and flags as in the fused path.
 template <class Map>
-__global__ void __launch_bounds__(kThreads) k_map_cells(const typename Map::In* __restrict__ in, uint64_t n, Map map,
+__global__ void __launch_bounds__(kThreads, 4) k_map_cells(const typename Map::In* __restrict__ in, uint64_t n, Map map,
                                                         bool aligned, uint32_t* __restrict__ out, DevStats* st) {
   using In = typename Map::In;
   unsigned long long mx = 0;
   unsigned flags = 0;
-  auto cell = [&](In x) -> uint32_t {
-    unsigned long long k;
-    if constexpr (is_f64_map<Map>::value) {
-      bool und;
-      k = map.fast(x, und);
-      if (und) k = map(x, flags);  // rare: exact path (also classifies bad inputs)
-    } else {
-      k = map(x, flags);
-    }
-    mx = k > mx ? k : mx;
-    return k < 0xFFFFFFFFull ? static_cast<uint32_t>(k) : 0xFFFFFFFFu;
-  };
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if constexpr (sizeof(In) == 8) {
+  if constexpr (is_f64_map<Map>::value) {
+    // float64: the fast tests, the exact path for the keys they leave
+    // undecided; the converted cell saturates at 0xFFFFFFFF, the max runs
+    // over the cells (the exact key only past the saturation, rarely)
+    uint32_t mx32 = 0;
+    auto cell = [&](double x) -> uint32_t {
+      bool und;
+      const double kd = map.fast(x, und);
+      uint32_t c = __double2uint_rz(kd);
+      if (und) {
+        const unsigned long long k = map_exact(map, x, flags);
+        mx = k > mx ? k : mx;
+        c = k < 0xFFFFFFFFull ? static_cast<uint32_t>(k) : 0xFFFFFFFFu;
+      } else if (c == 0xFFFFFFFFu) {
+        const unsigned long long k = static_cast<unsigned long long>(kd);
+        mx = k > mx ? k : mx;
+      }
+      mx32 = max(mx32, c);
+      return c;
+    };
     if (aligned) {  // two inputs per 16-byte load, four loads in flight, two cells per 8-byte store
       const uint64_t pairs = n / 2;
-      const auto* src = reinterpret_cast<const ulonglong2*>(in);
+      const auto* src = reinterpret_cast<const double2*>(in);
       auto* dst = reinterpret_cast<uint2*>(out);
       uint64_t p = i;
       for (; p + 3 * stride < pairs; p += 4 * stride) {
-        ulonglong2 w[4];
+        double2 w[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) w[u] = __ldcs(src + p + u * stride);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          dst[p + u * stride] = make_uint2(cell(*reinterpret_cast<const In*>(&w[u].x)),
-                                           cell(*reinterpret_cast<const In*>(&w[u].y)));
+        for (int u = 0; u < 4; ++u) dst[p + u * stride] = make_uint2(cell(w[u].x), cell(w[u].y));
       }
       for (; p < pairs; p += stride) {
-        const ulonglong2 w = __ldcs(src + p);
-        dst[p] = make_uint2(cell(*reinterpret_cast<const In*>(&w.x)), cell(*reinterpret_cast<const In*>(&w.y)));
+        const double2 w = __ldcs(src + p);
+        dst[p] = make_uint2(cell(w.x), cell(w.y));
       }
       if ((n & 1) && i == 0) out[n - 1] = cell(in[n - 1]);
       i = n;  // done
     }
+    for (; i < n; i += stride) out[i] = cell(in[i]);
+    mx = mx32 > mx ? mx32 : mx;
+  } else {
+    auto cell = [&](In x) -> uint32_t {
+      const unsigned long long k = map(x, flags);
+      mx = k > mx ? k : mx;
+      return k < 0xFFFFFFFFull ? static_cast<uint32_t>(k) : 0xFFFFFFFFu;
+    };
+    for (; i < n; i += stride) out[i] = cell(in[i]);
   }
-  for (; i < n; i += stride) out[i] = cell(in[i]);
   warp_max_to(mx, &st->max_key);
   flags = warp_or(flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(&st->flags, flags);

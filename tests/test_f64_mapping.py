@@ -14,7 +14,7 @@ LIMIT = 9007199254740992.0 / 100.0
 
 
 def kernel_f64(x: float, scale: int):
-    """Line-by-line mirror of MapF64::operator()."""
+    """Line-by-line mirror of MapF64::exact (what operator() falls back to)."""
     P = float(10 ** scale)
     P2 = 2.0 * P
     if math.isnan(x) or math.isinf(x):
@@ -41,84 +41,103 @@ def kernel_f64(x: float, scale: int):
     return m + 1 if up else m
 
 
+def _bits(x: float) -> int:
+    return np.float64(x).view(np.uint64).item()
+
+
+def _xlim_bits(scale: int) -> int:
+    """make_map_f64 (capi.cu): bits of the least x with x * 10^scale >= LIMIT."""
+    P = float(10 ** scale)
+    xl = LIMIT / P
+    while xl * P >= LIMIT:
+        xl = float(np.nextafter(xl, 0.0))
+    while xl * P < LIMIT:
+        xl = float(np.nextafter(xl, np.inf))
+    return _bits(xl)
+
+
 def _fma(a: float, b: float, c: float) -> float:
     """Exactly rounded a*b + c (IEEE fma)."""
     return float(Fraction(a) * Fraction(b) + Fraction(c))
 
 
-def quotient_is(x: float, c: float, d: float):
-    """Mirror of quotient_is (kernels_grid.cuh): is x == RN(c / d)?  1 yes,
-    0 no, -1 undecided (the kernel then takes the exact path)."""
-    xb = np.float64(x).view(np.uint64).item()
-    ulp = np.uint64((xb & 0x7FF0000000000000) - (52 << 52)).view(np.float64).item()
-    h = d * ulp * 0.5
-    r = abs(_fma(-x, d, c))
-    if (xb & ((1 << 52) - 1)) == 0 or r == h:
-        return -1
-    return 1 if r < h else 0
+def _sbits(x: float) -> int:
+    return np.float64(x).view(np.int64).item()
 
 
 def kernel_f64_fast(x: float, scale: int):
-    """Mirror of MapF64::fast; None = undecided (the kernel falls back to
-    MapF64::operator(), mirrored by kernel_f64)."""
-    P = float(10 ** scale)
+    """Line-by-line mirror of MapF64::fast; None = undecided (the kernel
+    falls back to MapF64::exact, mirrored by kernel_f64)."""
+    fast = scale <= 15
+    P = float(10 ** scale) if fast else 1.0
+    u = _bits(x)
+    zero_bits = 0 if fast else 2 ** 64 - 1
+    tiny_bits = _bits(1.0000001 * 10.0 ** -(scale + 3)) if fast else 0
+    xlim_bits = _xlim_bits(scale) if fast else 0
+    undecided = ((u - tiny_bits) & (2 ** 64 - 1)) >= ((xlim_bits - tiny_bits) & (2 ** 64 - 1)) and u != zero_bits
+    if undecided:
+        return None  # (the kernel computes on; its value is not used)
     p = x * P
-    if not (x >= 0.0) or not (p < LIMIT) or (x > 0.0 and x < 1.0000001 * 10.0 ** -(scale + 3)):
+    c = float(round(p))  # rint: ties to even
+    d = p - c
+    if (_sbits(d) >> 32) & 0x7FFFFFFF < 0x3FDEB851:
+        return int(c)
+    m = c if d >= 0.0 else c - 1.0
+    dv = 2.0 * P
+    hb = _sbits(dv) + (((u >> 52) - 1076) << 52)
+    rb = _sbits(_fma(-x, dv, _fma(m, 2.0, 1.0))) & 0x7FFFFFFFFFFFFFFF
+    if (u & ((1 << 52) - 1)) == 0 or rb == hb:
         return None
-    err = _fma(x, P, -p)
-    f = float(math.floor(p))
-    if p == f and err < 0.0:
-        f -= 1.0
-    m = int(f)
-    fr = p - f
-    near_int = fr < 0.02 or fr > 0.98
-    near_half = 0.48 < fr < 0.52
-    c = m if fr < 0.5 else m + 1
-    cv, dv = (float(c), P) if near_int else (float(2 * m + 1), 2.0 * P)
-    q = 1 if x == 0.0 else (quotient_is(x, cv, dv) if (near_int or near_half) else 0)
-    if q == -1:
-        return None
-    if q == 1:
-        return c if near_int else m + 1
-    return m + 1 if (fr > 0.5 or (fr == 0.5 and err > 0.0)) else m
+    if rb < hb:
+        return int(m) + 1
+    fr = p - m
+    up = fr > 0.5 or (fr == 0.5 and _fma(x, P, -p) > 0.0)
+    return int(m) + 1 if up else int(m)
 
 
 def test_fast_path_matches_exact_path(oracle):
     rng = np.random.default_rng(5)
-    undecided = decided = 0
+    decided = undecided = 0
     for scale in (0, 1, 2, 3, 6, 9, 12, 15):
         xs = [float(v) / 10.0 ** scale for v in rng.integers(0, 10 ** 7, 2000)]
         xs += [(2 * float(v) + 1) / (2 * 10.0 ** scale) for v in rng.integers(0, 10 ** 7, 1000)]
         xs += [float(np.nextafter((2 * float(v) + 1) / (2 * 10.0 ** scale), np.inf if v % 2 else 0.0))
                for v in rng.integers(0, 10 ** 7, 500)]
         xs += list(rng.random(1000) * 1e3) + [2.0 ** e for e in range(-40, 30)] + [0.0]
+        # powers of two and their neighbours, and values at the fast domain's edges
+        xs += [float(np.nextafter(2.0 ** e, t)) for e in range(-50, 40) for t in (0.0, np.inf)]
+        top = LIMIT / 10.0 ** scale
+        xs += [float(np.nextafter(top, 0.0)), top, 1.0000001 * 10.0 ** -(scale + 3)]
         for x in xs:
-            if not in_domain(x, scale):
-                continue
             got = kernel_f64_fast(x, scale)
+            if not in_domain(x, scale):
+                assert got is None or x == 0.0, (x, scale)
+                continue
             if got is None:
                 undecided += 1
-            else:
-                decided += 1
-                assert got == kernel_f64(x, scale) == oracle.float_to_decimal(x, scale), (x, scale)
-    assert undecided < decided / 20
+                continue
+            decided += 1
+            assert got == kernel_f64(x, scale) == oracle.float_to_decimal(x, scale), (x, scale)
+    assert decided > 30000 and undecided < decided / 20
 
 
-def test_quotient_test_agrees_with_division():
-    """Whenever the division-free test decides, it agrees with IEEE division."""
-    rng = np.random.default_rng(7)
-    decided = 0
-    for _ in range(20000):
-        scale = int(rng.integers(0, 16))
-        d = float(10 ** scale) * (2.0 if rng.random() < 0.3 else 1.0)
-        c = float(int(rng.integers(0, 2 ** 40)))
-        q = c / d
-        for x in (q, float(np.nextafter(q, np.inf)), float(np.nextafter(q, 0.0))):
-            t = quotient_is(x, c, d)
-            if t != -1:
-                decided += 1
-                assert (t == 1) == (c / d == x), (x, c, d)
-    assert decided > 50000
+def test_fast_path_neighbours():
+    """Decimals scaled by 1, 1/2 and 1/4 and the doubles either side of them,
+    against the division of exact()."""
+    rng = np.random.default_rng(11)
+    checked = 0
+    for _ in range(4000):
+        scale = int(rng.integers(1, 16))
+        P = 10 ** scale
+        x = float(rng.integers(1, 2 ** 40)) / float(P) * float(rng.choice([1.0, 0.5, 0.25]))
+        if not in_domain(x, scale) or x == 0.0:
+            continue
+        for y in (x, float(np.nextafter(x, np.inf)), float(np.nextafter(x, 0.0))):
+            got = kernel_f64_fast(y, scale)
+            if in_domain(y, scale) and y > 0.0 and got is not None:
+                assert got == kernel_f64(y, scale), (y, scale)
+                checked += 1
+    assert checked > 5000
 
 
 def in_domain(x: float, scale: int) -> bool:
@@ -170,3 +189,20 @@ def test_cfg3_values(oracle):
     for k in range(0, 10 ** 6, 97):
         x = k / 1000.0
         assert kernel_f64(x, 3) == oracle.float_to_decimal(x, 3) == k
+
+
+def test_fast_path_product_rounded_onto_integer():
+    """x = v / 10^scale whose product x * 10^scale rounds up onto the integer
+    v (fr == 0, err < 0): the fast path takes no fix-up there (both
+    candidates and the half-up rule give floor(p) = v)."""
+    rng = np.random.default_rng(3)
+    seen = 0
+    for scale in (1, 2, 3, 6, 9):
+        P = 10.0 ** scale
+        for v in rng.integers(0, 10 ** 7, 3000).tolist():
+            x = float(v) / P
+            p = x * P
+            if p == math.floor(p) and _fma(x, P, -p) < 0.0:
+                seen += 1
+                assert kernel_f64_fast(x, scale) == kernel_f64(x, scale) == v, (x, scale)
+    assert seen > 1000

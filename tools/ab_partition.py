@@ -3,7 +3,7 @@ cfg3 float64 step), with an exactness check of cfg2.  Used for A/B runs of
 partition variants (a build with a temporary switch, read once per process
 from RSB_* environment variables; the committed library has none).
 
-    python tools/ab_partition.py [--cfg3]
+    python tools/ab_partition.py [--cfg3 | --only-cfg3]
 """
 import ctypes
 import json
@@ -51,12 +51,13 @@ def main():
     rs._check(lib.rs_gen_u32(o.config_seed(2), 0, n, 10**6, rs._ptr(k), rs._stream()))
     out = torch.empty_like(k)
     res = {"env": {x: os.environ[x] for x in os.environ if x.startswith("RSB_")}}
-    res["cfg2"] = profile(lambda: rs.sort_u32(k, out=out, key_digits=6))
-    want = torch.bincount(k.long(), minlength=10**6)
-    got = torch.bincount(out.long(), minlength=10**6)
-    res["cfg2_ok"] = bool(torch.equal(want, got)) and bool((out[1:] >= out[:-1]).all())
+    if "--only-cfg3" not in sys.argv:
+        res["cfg2"] = profile(lambda: rs.sort_u32(k, out=out, key_digits=6))
+        want = torch.bincount(k.long(), minlength=10**6)
+        got = torch.bincount(out.long(), minlength=10**6)
+        res["cfg2_ok"] = bool(torch.equal(want, got)) and bool((out[1:] >= out[:-1]).all())
     del k, out
-    if "--cfg3" in sys.argv:
+    if "--cfg3" in sys.argv or "--only-cfg3" in sys.argv:
         cdf = torch.from_numpy(o.zipf_cdf()).cuda()
         x = torch.empty(n, dtype=torch.float64, device="cuda")
         rs._check(lib.rs_gen_f64_cfg3(o.config_seed(3), 0, n, rs._ptr(cdf), cdf.numel(), rs._ptr(x), rs._stream()))
