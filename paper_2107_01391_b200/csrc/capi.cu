@@ -332,14 +332,13 @@ bool div_magic32(uint64_t d, unsigned long long& magic, uint32_t& shift) {
 }
 
 // Which partition kernel a two-level count uses.  The warp-specialised kernel
-// (kernels_partition_ws.cuh) is the faster one on 4-byte keys as the caller
-// gives them (cfg2: 0.52 vs 0.575 ms at 2^28); the TMA-fed kernel, whose lane
-// replicas absorb a hot bucket, on cfg3's Zipf-skewed mapped cells (0.64 vs
-// ~0.97 ms) and on 8-byte inputs, where the warp-specialised ranker's
-// registers spill (profiles/r02_summary.md).
+// (kernels_partition_ws.cuh) is the faster one on keys as the caller gives
+// them (cfg2: 0.53 vs 0.575 ms at 2^28; the same keys as int64: 0.73 vs
+// 0.93 ms); the TMA-fed kernel, whose lane replicas absorb a hot bucket, on
+// cfg3's Zipf-skewed mapped cells (0.64 vs ~0.97 ms; profiles/r02_summary.md).
 template <class Map>
 bool use_ws_partition(bool mapped) {
-  return sizeof(typename Map::In) == 4 && !mapped;
+  return !mapped;
 }
 
 // Geometry of the two-level split: ~10^4 inner cells per outer bucket
@@ -368,11 +367,10 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t, bool ws) {
   }();
   static const int per_sm_ws = [] {
     int b = 0;
-    if constexpr (sizeof(typename Map::In) == 4) {
-      cudaFuncSetAttribute(k_page_partition_ws<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(page_ws_smem(256)));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_page_partition_ws<Map>, kWsThreads, page_ws_smem(100));
-    }
+    constexpr uint32_t kIn = sizeof(typename Map::In);
+    cudaFuncSetAttribute(k_page_partition_ws<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(page_ws_smem(256, kIn)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_page_partition_ws<Map>, kWsThreads, page_ws_smem(100, kIn));
     return b < 1 ? 1 : b;
   }();
   uint64_t G = (uint64_t)sm_count() * (ws ? per_sm_ws : per_sm_tma);  // one persistent wave
@@ -409,15 +407,9 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
   RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
   {
     PassTimer pt_(RS_PASS_PARTITION, ws.stream);
-    bool launched = false;
-    if constexpr (sizeof(typename Map::In) == 4) {
-      if (al && t.B <= 256 && use_ws) {  // warp-specialised: rankers + page-store warps
-        k_page_partition_ws<Map><<<t.G, kWsThreads, page_ws_smem(t.B), ws.stream>>>(
-            in, n, map, t, pages, page_bucket, page_fill, pc_bm, counts, ws.stats);
-        launched = true;
-      }
-    }
-    if (launched) {
+    if (al && t.B <= 256 && use_ws) {  // warp-specialised: rankers + page-store warps
+      k_page_partition_ws<Map><<<t.G, kWsThreads, page_ws_smem(t.B, sizeof(typename Map::In)), ws.stream>>>(
+          in, n, map, t, pages, page_bucket, page_fill, pc_bm, counts, ws.stats);
     } else if (al && t.B <= 256) {  // TMA-fed tiles, bulk-stored pages
       k_page_partition_tma<Map><<<t.G, kTlThreads, page_tma_smem<Map>(), ws.stream>>>(
           in, n, map, t, pages, page_bucket, page_fill, pc_bm, ws.stats);

@@ -1,8 +1,10 @@
 // kernels_partition_ws.cuh — the counting pass's partition (K1 of
 // kernels_two_level.cuh) with warp-specialised roles.
 //
-// Ranking warps (kWsRankThreads) stream tiles of 4096 keys (16-byte loads,
-// prefetched one tile ahead into registers) and rank + stage every key with
+// Ranking warps (kWsRankThreads) stream tiles of 4096 keys (4-byte keys:
+// 16-byte loads prefetched one tile ahead into registers; 8-byte keys: TMA
+// bulk copies two tiles ahead into shared memory, mapped to saturated 32-bit
+// cells as they are read out) and rank + stage every key with
 // one shared atomic and one uint16 store: each bucket owns a slot range of the
 // tile's staging buffer, sized from the bucket's count two tiles earlier
 // (c + c/2 + 32 slots, a multiple of 8), and one shared word (range end << 16 |
@@ -46,9 +48,13 @@ __device__ __forceinline__ void nbar_arrive(int buf) {
 __host__ __device__ constexpr uint32_t ws_stage_slots(uint32_t B) {
   return (uint32_t)kTlTile + (uint32_t)kTlTile / 2 + B * 40u;
 }
-// staging[2], s_w[2][260] (+ the dummy bucket), s_off[2][256], skew[2]
-__host__ __device__ constexpr size_t page_ws_smem(uint32_t B) {
+// staging[2], s_w[2][260] (+ the dummy bucket), s_off[2][256], skew[2];
+// 8-byte inputs add two 32 KB key tiles (filled by TMA bulk copies)
+__host__ __device__ constexpr size_t page_ws_meta_end(uint32_t B) {
   return 2 * (size_t)ws_stage_slots(B) * 2 + 2 * 260 * 4 + 2 * 256 * 4 + 16;
+}
+__host__ __device__ constexpr size_t page_ws_smem(uint32_t B, uint32_t in_bytes = 4) {
+  return in_bytes == 8 ? ((page_ws_meta_end(B) + 127) & ~(size_t)127) + 2 * (size_t)kTlTile * 8 : page_ws_meta_end(B);
 }
 
 template <class Map>
@@ -66,8 +72,11 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   uint32_t* s_w = reinterpret_cast<uint32_t*>(sm + 2 * (size_t)SLOTS * 2);  // [2][260]: end << 16 | next slot
   uint32_t* s_off = s_w + 2 * 260;                                          // [2][256]: range start
   uint32_t* s_skew = s_off + 2 * 256;                                       // [2]
+  // 8-byte keys: [2][kTlTile] tiles landing by TMA (4-byte keys are prefetched into registers)
+  unsigned long long* s_in = reinterpret_cast<unsigned long long*>(sm + ((page_ws_meta_end(t.B) + 127) & ~(size_t)127));
   __shared__ uint32_t s_scan[kWsStoreThreads / 32];
   __shared__ uint32_t s_next;
+  __shared__ __align__(8) unsigned long long s_inbar[2];
   const int lane = threadIdx.x & 31;
   const uint32_t B = t.B;
   const uint32_t ntiles = blockIdx.x < t.T ? (t.T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -88,6 +97,11 @@ __global__ void __launch_bounds__(kWsThreads, 2)
   if (threadIdx.x == 0) {
     s_next = 0;
     s_skew[0] = s_skew[1] = 0xffffffffu;
+    if constexpr (!k32) {
+      mbar_init(&s_inbar[0], 1);
+      mbar_init(&s_inbar[1], 1);
+      fence_mbar_init();
+    }
   }
   __syncthreads();
 
@@ -100,6 +114,10 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     unsigned long long mx64 = 0;
     unsigned flags = 0;
     In cur[4][4], nxt[4][4];
+    // 8-byte keys: the tile's cells, mapped as the tile is read out of shared
+    // memory (saturated at 0xFFFFFFFF, which no grid reaches: kc < cells is
+    // the in-grid test, as for 4-byte keys)
+    uint32_t kc[16];
     const uint64_t full_tiles = n / kTlTile;
     // the 16 keys of (tile, this thread): four 16-byte vectors (bounds-checked
     // only in the last, partial tile)
@@ -146,10 +164,8 @@ __global__ void __launch_bounds__(kWsThreads, 2)
               ing = ok && kk < cells32;
             }
           } else {
-            const unsigned long long k64 = ok ? map(cur[q][e], flags) : 0ull;
-            mx64 = k64 > mx64 ? k64 : mx64;
-            ing = ok && k64 < t.cells;
-            kk = static_cast<uint32_t>(k64);
+            kk = kc[q * 4 + e];
+            ing = kk < cells32;
           }
           uint32_t bk = __umulhi(kk, magic32) >> shift32;
           bk = ing ? bk : B;  // the dummy bucket: an empty range, never staged
@@ -182,28 +198,83 @@ __global__ void __launch_bounds__(kWsThreads, 2)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const uint32_t rr = r[q * 4 + e], pos = rr & 0xffffu;
-          unsigned f = 0;
           uint32_t kk;
-          if constexpr (k32) kk = map.key32(cur[q][e], f);
-          else kk = static_cast<uint32_t>(map(cur[q][e], f));
+          if constexpr (k32) {
+            unsigned f = 0;
+            kk = map.key32(cur[q][e], f);
+          } else {
+            kk = kc[q * 4 + e];
+          }
           if (pos < (rr >> 16)) {
             stage[pos] = static_cast<uint16_t>(kk - (__umulhi(kk, magic32) >> shift32) * S);
           } else {
             // the bucket's range is full: count the key directly (a key
             // outside the grid or past the input ranked into the dummy bucket)
             bool ing = kk < cells32;
-            if constexpr (!k32) ing = map(cur[q][e], f) < t.cells;
-            if constexpr (!kFull) ing = ing && tile * kTlTile + q * 1024 + threadIdx.x * 4 + e < n;
+            if constexpr (k32 && !kFull) ing = ing && tile * kTlTile + q * 1024 + threadIdx.x * 4 + e < n;
             if (ing && (rr >> 16) != 0) atomicAdd(&grid[kk], 1u);
           }
         }
       }
     };
+    // 8-byte keys: a full tile lands in s_in[buf] by one TMA bulk copy, two
+    // tiles ahead; each ranker maps its 16 keys out of it (conflict-free
+    // 16-byte reads), then the rankers sync and the buffer is refilled
+    auto issue = [&](uint64_t tl, int b) {  // one thread
+      fence_proxy_async_smem();
+      mbar_expect_tx(&s_inbar[b], kTlTile * 8);
+      bulk_g2s(s_in + (size_t)b * kTlTile, in + tl * kTlTile, kTlTile * 8, &s_inbar[b]);
+    };
+    auto map_tile = [&](uint64_t tl, int b, unsigned& phase) {
+      if constexpr (!k32) {
+      if (tl < full_tiles) {
+        mbar_wait(&s_inbar[b], (phase >> b) & 1u);
+        phase ^= 1u << b;
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(s_in + (size_t)b * kTlTile);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const ulonglong2 x = src[h * kWsRankThreads + threadIdx.x];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const unsigned long long k64 = map(from_bits64(e ? x.y : x.x, (In*)nullptr), flags);
+            mx64 = k64 > mx64 ? k64 : mx64;
+            kc[h * 2 + e] = k64 < 0xFFFFFFFFull ? static_cast<uint32_t>(k64) : 0xFFFFFFFFu;
+          }
+        }
+        asm volatile("bar.sync 6, %0;" ::"n"(kWsRankThreads) : "memory");  // every ranker has read s_in[b]
+        const uint64_t ahead = tl + 2ull * gridDim.x;
+        if (threadIdx.x == 0 && ahead < full_tiles) issue(ahead, b);
+      } else {  // the partial last tile, from global memory with bounds
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          In v[4];
+          Load4<In>::run(in, tl * kTlTile + q * 1024 + threadIdx.x * 4, n, false, v);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const bool ok = tl * kTlTile + q * 1024 + threadIdx.x * 4 + e < n;
+            const unsigned long long k64 = ok ? map(v[e], flags) : 0ull;
+            mx64 = k64 > mx64 ? k64 : mx64;
+            kc[q * 4 + e] = ok && k64 < 0xFFFFFFFFull ? static_cast<uint32_t>(k64) : 0xFFFFFFFFu;
+          }
+        }
+      }
+      }
+    };
+    unsigned in_phase = 0;
     uint64_t tile = blockIdx.x;
-    if (ntiles) load(tile, cur);
+    if constexpr (k32) {
+      if (ntiles) load(tile, cur);
+    } else if (threadIdx.x == 0) {
+      for (uint32_t k = 0; k < 2 && k < ntiles; ++k)
+        if (tile + (uint64_t)k * gridDim.x < full_tiles) issue(tile + (uint64_t)k * gridDim.x, k);
+    }
     for (uint32_t i = 0; i < ntiles; ++i, tile += gridDim.x) {
       const int buf = i & 1;
-      if (i + 1 < ntiles) load(tile + gridDim.x, nxt);
+      if constexpr (k32) {
+        if (i + 1 < ntiles) load(tile + gridDim.x, nxt);
+      } else {
+        map_tile(tile, buf, in_phase);
+      }
       if (i >= 2) nbar_sync<kFree, kWsThreads>(buf);  // the store warps set this buffer's ranges
       uint32_t* w = s_w + buf * 260;
       uint16_t* stage = s_stage + buf * SLOTS;
@@ -215,10 +286,12 @@ __global__ void __launch_bounds__(kWsThreads, 2)
         rank_tile(std::false_type{}, std::false_type{}, tile, w, stage, hot);
       }
       nbar_arrive<kRanked, kWsThreads>(buf);
+      if constexpr (k32) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) cur[q][e] = nxt[q][e];
+          for (int e = 0; e < 4; ++e) cur[q][e] = nxt[q][e];
+      }
     }
     const unsigned long long mx = k32 ? (unsigned long long)mx32 : mx64;
     warp_max_to(mx, &st->max_key);

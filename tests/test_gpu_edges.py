@@ -259,3 +259,48 @@ def test_kv_above_2_pow_31_records(rs, oracle):
     assert torch.equal(k[idx], ko)
     del k, v, ko, vo
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n", [(1 << 22) + 77, 4096 * 700 + 1])
+def test_int64_partition_matches_reference(rs, oracle, n):
+    """int64 input (sort_integers' span<const int64_t>) through the two-level
+    count: the warp-specialised partition maps 8-byte keys out of TMA-filled
+    shared-memory tiles into saturated 32-bit cells (the bounds-checked
+    global path for the partial last tile)."""
+    import torch
+
+    keys = oracle.gen_u32(82, 0, n, 10**6).astype(np.int64)
+    keys[-3:] = [999_999, 0, 500_000]  # the partial tile's keys
+    out, rep = rs.sort_i64(torch.from_numpy(keys).cuda())
+    want, wrep = oracle.sort_integers_i64(keys)
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert (rep.written, rep.cells_traversed) == wrep[:2] and rep.spec.total_digits == 6
+
+
+def test_int64_partition_key_beyond_32_bits(rs, oracle):
+    """With a declared 6-digit width, a key of 11 digits (> 2^33) saturates
+    to an out-of-grid cell in the partition; the sort is redone at the true
+    width from the exact 64-bit max, whose 10^11 cells exceed the budget —
+    the reference's error for the same keys."""
+    import torch
+
+    keys = oracle.gen_u32(83, 0, (1 << 21) + 9, 10**6).astype(np.int64)
+    keys[12345] = 10**10 + 3
+    with pytest.raises(oracle_error_type()):
+        oracle.sort_integers_i64(keys)
+    with pytest.raises(rs.Error) as e:
+        rs.sort_i64(torch.from_numpy(keys).cuda(), key_digits=6)
+    assert e.value.code == "cell_budget_exceeded"
+    assert "needs 100000000000 cells" in str(e.value)
+    # in budget: the same keys below 10^7 after the redo (7 digits), as the reference
+    keys[12345] = 9_999_999
+    out, rep = rs.sort_i64(torch.from_numpy(keys).cuda(), key_digits=6)
+    want, wrep = oracle.sort_integers_i64(keys)
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert (rep.written, rep.cells_traversed) == wrep[:2] and rep.spec.total_digits == 7
+
+
+def oracle_error_type():
+    from oracle import OracleError
+
+    return OracleError

@@ -3,7 +3,7 @@ cfg3 float64 step), with an exactness check of cfg2.  Used for A/B runs of
 partition variants (a build with a temporary switch, read once per process
 from RSB_* environment variables; the committed library has none).
 
-    python tools/ab_partition.py [--cfg3 | --only-cfg3]
+    python tools/ab_partition.py [--cfg3 | --only-cfg3] [--i64]
 """
 import ctypes
 import json
@@ -57,6 +57,15 @@ def main():
         got = torch.bincount(out.long(), minlength=10**6)
         res["cfg2_ok"] = bool(torch.equal(want, got)) and bool((out[1:] >= out[:-1]).all())
     del k, out
+    if "--i64" in sys.argv:  # cfg2 keys as int64 through rs_sort_i64 without key_digits (facade_i64)
+        k2 = torch.empty(n, dtype=torch.int32, device="cuda")
+        rs._check(lib.rs_gen_u32(o.config_seed(2), 0, n, 10**6, rs._ptr(k2), rs._stream()))
+        k64 = k2.long()
+        del k2
+        res["i64"] = profile(lambda: rs.sort_i64(k64))
+        o64, _ = rs.sort_i64(k64)
+        res["i64_ok"] = bool(torch.equal(o64, torch.sort(k64).values))
+        del k64, o64
     if "--cfg3" in sys.argv or "--only-cfg3" in sys.argv:
         cdf = torch.from_numpy(o.zipf_cdf()).cuda()
         x = torch.empty(n, dtype=torch.float64, device="cuda")
