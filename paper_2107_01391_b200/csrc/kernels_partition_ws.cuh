@@ -227,37 +227,37 @@ __global__ void __launch_bounds__(kWsThreads, 2)
     };
     auto map_tile = [&](uint64_t tl, int b, unsigned& phase) {
       if constexpr (!k32) {
-      if (tl < full_tiles) {
-        mbar_wait(&s_inbar[b], (phase >> b) & 1u);
-        phase ^= 1u << b;
-        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(s_in + (size_t)b * kTlTile);
+        if (tl < full_tiles) {
+          mbar_wait(&s_inbar[b], (phase >> b) & 1u);
+          phase ^= 1u << b;
+          const ulonglong2* src = reinterpret_cast<const ulonglong2*>(s_in + (size_t)b * kTlTile);
 #pragma unroll
-        for (int h = 0; h < 8; ++h) {
-          const ulonglong2 x = src[h * kWsRankThreads + threadIdx.x];
+          for (int h = 0; h < 8; ++h) {
+            const ulonglong2 x = src[h * kWsRankThreads + threadIdx.x];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const unsigned long long k64 = map(from_bits64(e ? x.y : x.x, (In*)nullptr), flags);
-            mx64 = k64 > mx64 ? k64 : mx64;
-            kc[h * 2 + e] = k64 < 0xFFFFFFFFull ? static_cast<uint32_t>(k64) : 0xFFFFFFFFu;
+            for (int e = 0; e < 2; ++e) {
+              const unsigned long long k64 = map(from_bits64(e ? x.y : x.x, (In*)nullptr), flags);
+              mx64 = k64 > mx64 ? k64 : mx64;
+              kc[h * 2 + e] = k64 < 0xFFFFFFFFull ? static_cast<uint32_t>(k64) : 0xFFFFFFFFu;
+            }
+          }
+          asm volatile("bar.sync 6, %0;" ::"n"(kWsRankThreads) : "memory");  // every ranker has read s_in[b]
+          const uint64_t ahead = tl + 2ull * gridDim.x;
+          if (threadIdx.x == 0 && ahead < full_tiles) issue(ahead, b);
+        } else {  // the partial last tile, from global memory with bounds
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            In v[4];
+            Load4<In>::run(in, tl * kTlTile + q * 1024 + threadIdx.x * 4, n, false, v);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const bool ok = tl * kTlTile + q * 1024 + threadIdx.x * 4 + e < n;
+              const unsigned long long k64 = ok ? map(v[e], flags) : 0ull;
+              mx64 = k64 > mx64 ? k64 : mx64;
+              kc[q * 4 + e] = ok && k64 < 0xFFFFFFFFull ? static_cast<uint32_t>(k64) : 0xFFFFFFFFu;
+            }
           }
         }
-        asm volatile("bar.sync 6, %0;" ::"n"(kWsRankThreads) : "memory");  // every ranker has read s_in[b]
-        const uint64_t ahead = tl + 2ull * gridDim.x;
-        if (threadIdx.x == 0 && ahead < full_tiles) issue(ahead, b);
-      } else {  // the partial last tile, from global memory with bounds
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          In v[4];
-          Load4<In>::run(in, tl * kTlTile + q * 1024 + threadIdx.x * 4, n, false, v);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const bool ok = tl * kTlTile + q * 1024 + threadIdx.x * 4 + e < n;
-            const unsigned long long k64 = ok ? map(v[e], flags) : 0ull;
-            mx64 = k64 > mx64 ? k64 : mx64;
-            kc[q * 4 + e] = ok && k64 < 0xFFFFFFFFull ? static_cast<uint32_t>(k64) : 0xFFFFFFFFu;
-          }
-        }
-      }
       }
     };
     unsigned in_phase = 0;
