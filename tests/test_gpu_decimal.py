@@ -106,3 +106,43 @@ def test_large_column_on_device(rs):
     for i in (0, 1, n // 2, n - 1):
         k = int(np.sort(scaled)[i])
         assert text[off[i]:off[i + 1]].decode() == f"{k // 1000}.{str(k % 1000).rjust(3, '0')}"
+
+
+@pytest.mark.parametrize("misalign", [0, 1, 3, 7])
+def test_parse_every_shape_and_alignment(rs, misalign):
+    """rs_parse_decimals over numerals of every length 1-19 with the point at
+    every position (the SWAR fast path takes <= 16 bytes with at most one
+    point that is not the last byte; longer numerals take the byte loop), each
+    starting at every byte alignment, in a column whose first byte sits at
+    `misalign` bytes past an 8-byte boundary, the last numerals ending at the
+    column's last byte (where the fast path's third word would run past it)."""
+    import ctypes
+
+    import torch
+
+    rng = np.random.default_rng(100 + misalign)
+    vals = []
+    for length in range(1, 20):
+        for dot in [None] + list(range(0, length - 1)):
+            for _ in range(3):
+                nd = length - (dot is not None)
+                digits = "".join(str(d) for d in rng.integers(0, 10, nd))
+                vals.append(digits if dot is None else digits[:dot] + "." + digits[dot:])
+    rng.shuffle(vals)
+    vals += ["0", "7.5", "12.34"]  # short numerals at the very end
+    data = "".join(vals).encode()
+    offsets = np.zeros(len(vals) + 1, dtype=np.uint64)
+    offsets[1:] = np.cumsum([len(v) for v in vals])
+    buf = torch.zeros(len(data) + misalign, dtype=torch.uint8, device="cuda")
+    buf[misalign:] = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+    chars = buf[misalign:]
+    off = torch.from_numpy(offsets.view(np.int64)).cuda()
+    mant = torch.empty(len(vals), dtype=torch.int64, device="cuda")
+    scales = torch.empty(len(vals), dtype=torch.int32, device="cuda")
+    lib = rs._lib.load()
+    rs._check(lib.rs_parse_decimals(ctypes.c_void_p(chars.data_ptr()), rs._ptr(off), len(vals), rs._ptr(mant),
+                                    rs._ptr(scales), rs._stream()))
+    want_m = [int(v.replace(".", "")) for v in vals]
+    want_s = [len(v) - v.index(".") - 1 if "." in v else 0 for v in vals]
+    assert [int(x) for x in mant.cpu().numpy().view(np.uint64)] == want_m
+    assert scales.cpu().tolist() == want_s
