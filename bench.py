@@ -487,24 +487,28 @@ def e2e_single(b: Bench, keys, out, opts) -> dict:
         e2e_step()
     dt_sync = (time.perf_counter() - t0) / reps
     ok = bool(torch.equal(h_out, want))
-    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
-    d_in = [torch.empty_like(keys) for _ in range(2)]
-    d_out = [torch.empty_like(keys) for _ in range(2)]
-    h_outs = [torch.empty(n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
-    reps2 = [rs.RsReport(), rs.RsReport()]
+    # three streams and buffer sets: step k+3's H2D queues behind step k's D2H
+    # on its stream, so with three in rotation the H2D engine never waits on a
+    # D2H (with two it idled for one sort per step)
+    NS = 3
+    streams = [torch.cuda.Stream() for _ in range(NS)]
+    d_in = [torch.empty_like(keys) for _ in range(NS)]
+    d_out = [torch.empty_like(keys) for _ in range(NS)]
+    h_outs = [torch.empty(n, dtype=torch.int32, pin_memory=True) for _ in range(NS)]
+    reps2 = [rs.RsReport() for _ in range(NS)]
 
     def pipe_step(k):
-        s, i = streams[k & 1], k & 1
+        s, i = streams[k % NS], k % NS
         with torch.cuda.stream(s):
             d_in[i].copy_(h_in, non_blocking=True)
             rs._check(lib.rs_sort_u32(rs._ptr(d_in[i]), n, rs._ptr(d_out[i]), n, ctypes.byref(opts),
                                       ctypes.byref(reps2[i]), ctypes.c_void_p(s.cuda_stream)))
             h_outs[i].copy_(d_out[i], non_blocking=True)
 
-    for k in range(2):
+    for k in range(NS):
         pipe_step(k)
     torch.cuda.synchronize()
-    steps2 = max(4, b.args.steps)
+    steps2 = max(6, b.args.steps)
     t0 = time.perf_counter()
     for k in range(steps2):
         pipe_step(k)
@@ -513,7 +517,7 @@ def e2e_single(b: Bench, keys, out, opts) -> dict:
     ok = ok and all(bool(torch.equal(h, want)) for h in h_outs)
     return {"value": n / dt / 1e9, "unit": "Gkeys/s", "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
             "ms_per_step": dt * 1e3,
-            "api": "rs_sort_u32 on two CUDA streams (pinned host buffers; H2D of step k+1 overlaps D2H of step k)",
+            "api": "rs_sort_u32 on three CUDA streams (pinned host buffers; H2D of step k+1 overlaps D2H of step k)",
             "sync_api": {"value": n / dt_sync / 1e9, "ms_per_step": dt_sync * 1e3,
                          "api": "rs_sort_u32_host (one call per step: H2D, sort, D2H)"},
             "checked": ok, "checked_how": "every output element of every e2e step against the device sort"}

@@ -20,6 +20,7 @@
 #include "kernels_kv.cuh"
 #include "kernels_two_level.cuh"
 #include "kernels_partition_ws.cuh"
+#include "kernels_partition_direct.cuh"
 #include "kernels_msd.cuh"
 #include "kernels_msd_engine.cuh"
 #include "kernels_decimal.cuh"
@@ -389,6 +390,11 @@ template <class Map>
 void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, const TwoLevel& t,
                      uint32_t* counts, bool use_ws) {
   const bool al = aligned16(in);
+  bool direct = false;
+  if constexpr (sizeof(typename Map::In) == 4) {
+    static const bool kNoDirect = getenv("RSB_NODIRECT") != nullptr;  // A/B only
+    direct = al && use_ws && t.B <= kDirMaxBuckets && !kNoDirect;
+  }
   const uint64_t P = (uint64_t)t.G * t.pages_per_cta;
   const uint64_t bg = (uint64_t)t.B * t.G;
   auto* pages = ws.get<uint16_t>(kSlotLows, P * kPage);
@@ -407,7 +413,20 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
   RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
   {
     PassTimer pt_(RS_PASS_PARTITION, ws.stream);
-    if (al && t.B <= 256 && use_ws) {  // warp-specialised: rankers + page-store warps
+    if constexpr (sizeof(typename Map::In) == 4) {
+      if (direct) {  // 4-byte keys straight into shared page chunks, TMA bulk-stored
+        static const bool attr = [] {
+          cudaFuncSetAttribute(k_page_partition_direct<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(page_dir_smem(kDirMaxBuckets)));
+          return true;
+        }();
+        (void)attr;
+        k_page_partition_direct<Map><<<t.G, kDirThreads, page_dir_smem(t.B), ws.stream>>>(
+            in, n, map, t, pages, page_bucket, page_fill, pc_bm, counts, ws.stats);
+      }
+    }
+    if (direct) {
+    } else if (al && t.B <= 256 && use_ws) {  // warp-specialised: rankers + page-store warps
       k_page_partition_ws<Map><<<t.G, kWsThreads, page_ws_smem(t.B, sizeof(typename Map::In)), ws.stream>>>(
           in, n, map, t, pages, page_bucket, page_fill, pc_bm, counts, ws.stats);
     } else if (al && t.B <= 256) {  // TMA-fed tiles, bulk-stored pages

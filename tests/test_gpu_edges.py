@@ -189,6 +189,34 @@ def test_partition_ranges_under_shifting_buckets(rs, oracle, pattern):
     assert (rep.written, rep.cells_traversed) == wrep[:2]
 
 
+@pytest.mark.parametrize("pattern", ["hot-bucket", "one-value", "two-values"])
+def test_direct_partition_overflowing_rings(rs, oracle, pattern):
+    """The direct partition (4-byte keys) gives each bucket a 512-slot shared
+    ring per tile window; a bucket taking more keys than its writable chunks
+    hold counts the rest straight into the grid (warp-aggregated global
+    atomics).  Inputs that overflow the rings on every tile: 60% of the keys
+    spread over bucket 0's 10^4 cells, every key one value, half the keys on
+    each of two cells of one bucket."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    n = (1 << 22) + 1234
+    keys = oracle.gen_u32(82, 0, n, 10**6)
+    if pattern == "hot-bucket":
+        hot = rng.random(n) < 0.6
+        keys[hot] = rng.integers(0, 10**4, int(hot.sum()))
+    elif pattern == "one-value":
+        keys[:] = 777_777
+    else:
+        keys[:] = np.where(rng.random(n) < 0.5, 500_001, 509_999)
+    keys[-1] = 999_999  # the grid stays 10^6 cells (two-level split)
+    keys = keys.astype(np.uint32)
+    out, rep = rs.sort_u32(torch.from_numpy(keys.view(np.int32)).cuda(), key_digits=6)
+    want, wrep = oracle.sort_integers_u32(keys)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
+    assert (rep.written, rep.cells_traversed) == wrep[:2]
+
+
 @pytest.mark.parametrize("parts", [2, 3, 8])
 def test_emit_part_cuts_match_cell_ranges(rs, oracle, parts):
     """rs_emit_part_u32 (the sharded grid's emit): the device cuts equal
