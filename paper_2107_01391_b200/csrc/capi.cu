@@ -392,8 +392,7 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
   const bool al = aligned16(in);
   bool direct = false;
   if constexpr (sizeof(typename Map::In) == 4) {
-    static const bool kNoDirect = getenv("RSB_NODIRECT") != nullptr;  // A/B only
-    direct = al && use_ws && t.B <= kDirMaxBuckets && !kNoDirect;
+    direct = al && use_ws && t.B <= kDirMaxBuckets;
   }
   const uint64_t P = (uint64_t)t.G * t.pages_per_cta;
   const uint64_t bg = (uint64_t)t.B * t.G;
