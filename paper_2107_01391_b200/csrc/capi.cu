@@ -390,10 +390,7 @@ template <class Map>
 void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, const TwoLevel& t,
                      uint32_t* counts, bool use_ws) {
   const bool al = aligned16(in);
-  bool direct = false;
-  if constexpr (sizeof(typename Map::In) == 4) {
-    direct = al && use_ws && t.B <= kDirMaxBuckets;
-  }
+  const bool direct = al && use_ws && t.B <= kDirMaxBuckets;
   const uint64_t P = (uint64_t)t.G * t.pages_per_cta;
   const uint64_t bg = (uint64_t)t.B * t.G;
   auto* pages = ws.get<uint16_t>(kSlotLows, P * kPage);
@@ -412,8 +409,8 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
   RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
   {
     PassTimer pt_(RS_PASS_PARTITION, ws.stream);
-    if constexpr (sizeof(typename Map::In) == 4) {
-      if (direct) {  // 4-byte keys straight into shared page chunks, TMA bulk-stored
+    if constexpr (!map_first<Map>::value) {  // (mapped float64 cells arrive as MapU32)
+      if (direct) {  // keys straight into shared page chunks, TMA bulk-stored
         static const bool attr = [] {
           cudaFuncSetAttribute(k_page_partition_direct<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(page_dir_smem(kDirMaxBuckets)));
@@ -709,7 +706,10 @@ void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, cons
   grid_sort(ws, in, n, map, pow10u(digits), out, sorted, 10, 0, 0);
   check_flags(ws.h_stats->flags);
   if (ws.h_stats->overflow) {  // declared (or sampled) width too small: redo with the derived one
-    const unsigned long long mx = ws.h_stats->max_key;
+    unsigned long long mx = ws.h_stats->max_key;
+    // the direct partition reports 8-byte keys' max as a saturated 32-bit
+    // cell; a key at or past 2^32 - 1 needs the exact max
+    if (sizeof(typename Map::In) == 8 && mx >= 0xFFFFFFFFull) mx = device_max(ws, in, n, map);
     digits = digit_count(mx);
     if (msd_u32 && opt && opt->msd && pow10u(digits) > budget) {
       key_bits = 1;

@@ -37,13 +37,13 @@
 
 namespace rsb {
 
-constexpr int kDirPer = 8;                // keys per ranker thread per tile
 constexpr uint32_t kDirMaxBuckets = 104;  // owner threads 0..B-1 of 128; B + 1 words per set
 constexpr int kDirRankers = 384;
 constexpr int kDirOwners = 128;
 constexpr int kDirThreads = kDirRankers + kDirOwners;
-constexpr uint32_t kDirTile = kDirRankers * kDirPer;  // 3072 keys
 constexpr uint32_t kDirChunk = 128;
+template <class In>
+constexpr int kDirPerT = 32 / sizeof(In);  // 32 bytes of keys per ranker thread per tile
 constexpr uint32_t kDirRing = 2 * kDirChunk;
 
 __host__ __device__ constexpr size_t page_dir_smem(uint32_t B) {
@@ -57,7 +57,10 @@ __global__ void __launch_bounds__(kDirThreads, 2)
                              uint16_t* __restrict__ page_fill, uint32_t* __restrict__ pc_bm,
                              uint32_t* __restrict__ grid, DevStats* st) {
   using In = typename Map::In;
-  static_assert(sizeof(In) == 4, "4-byte keys");
+  constexpr bool k32 = sizeof(In) == 4;
+  constexpr uint32_t kDirTile = kDirRankers * kDirPerT<In>;    // 3072 4-byte or 1536 8-byte keys
+  constexpr bool kInt64 = std::is_same_v<Map, MapI64> || std::is_same_v<Map, MapU64>;
+  using Mx = std::conditional_t<k32 || kInt64, uint32_t, unsigned long long>;
   constexpr uint32_t kCPP = kPage / kDirChunk;
   constexpr int kRanked = 1, kFlushed = 3;  // named barrier ids (+ set)
   extern __shared__ __align__(128) unsigned char sm[];
@@ -82,12 +85,13 @@ __global__ void __launch_bounds__(kDirThreads, 2)
 
   if (tid < kDirRankers) {
     // ------------------------------------------------------------ rankers
-    uint32_t mx = 0;
+    Mx mx = 0;
     unsigned flags = 0;
-    In cur[kDirPer], nxt[kDirPer];
-    auto load = [&](uint32_t tile, In (&v)[kDirPer]) {
+    uint32_t neg = 0;  // int64 keys: OR of the high halves (sign bit: a negative value)
+    In cur[kDirPerT<In>], nxt[kDirPerT<In>];
+    auto load = [&](uint32_t tile, In (&v)[kDirPerT<In>]) {
 #pragma unroll
-      for (int h = 0; h < kDirPer / 4; ++h) {
+      for (int h = 0; h < kDirPerT<In> / 4; ++h) {
         In x[4];
         Load4<In>::run(in, (uint64_t)tile * kDirTile + h * (kDirTile / 2) + tid * 4, n, tile < full_tiles, x);
 #pragma unroll
@@ -97,31 +101,49 @@ __global__ void __launch_bounds__(kDirThreads, 2)
     auto index_of = [&](uint32_t tile, int j) {
       return (uint64_t)tile * kDirTile + (j / 4) * (kDirTile / 2) + tid * 4 + (j & 3);
     };
-    auto rank_tile = [&](auto full_c, uint32_t tile, int s, In (&cur)[kDirPer]) {
+    auto rank_tile = [&](auto full_c, uint32_t tile, int s, In (&cur)[kDirPerT<In>]) {
       constexpr bool kFull = decltype(full_c)::value;
       uint32_t* ws = w + s * 128;
       uint16_t* rs = ring + (size_t)s * B * kDirRing;
-      uint32_t r[kDirPer];
+      // each key's 32-bit cell (8-byte keys saturate at 0xFFFFFFFF, which no
+      // grid reaches, so kc < cells is the in-grid test for both widths)
+      uint32_t kc[kDirPerT<In>], r[kDirPerT<In>];
 #pragma unroll
-      for (int j = 0; j < kDirPer; ++j) {
-        const uint32_t kk = map.key32(cur[j], flags);
+      for (int j = 0; j < kDirPerT<In>; ++j) {
+        Mx k;
+        if constexpr (k32) {
+          k = map.key32(cur[j], flags);
+          kc[j] = k;
+        } else if constexpr (kInt64) {
+          // from the two 32-bit halves: a nonzero high half saturates the
+          // cell (and, signed, flags a negative value); the max is taken
+          // over the saturated cells (the host asks for the exact max if
+          // a redo needs it)
+          const unsigned long long u = static_cast<unsigned long long>(cur[j]);
+          const uint32_t hi = static_cast<uint32_t>(u >> 32), lo = static_cast<uint32_t>(u);
+          if constexpr (std::is_same_v<Map, MapI64>) neg |= hi;
+          kc[j] = hi ? 0xFFFFFFFFu : lo;
+          k = kc[j];
+        } else {
+          k = map(cur[j], flags);
+          kc[j] = k < 0xFFFFFFFFull ? static_cast<uint32_t>(k) : 0xFFFFFFFFu;
+        }
         bool ing;
         if constexpr (kFull) {
-          mx = kk > mx ? kk : mx;
-          ing = kk < cells32;
+          mx = k > mx ? k : mx;
+          ing = kc[j] < cells32;
         } else {
           const bool ok = index_of(tile, j) < n;
-          mx = (ok && kk > mx) ? kk : mx;
-          ing = ok && kk < cells32;
+          mx = (ok && k > mx) ? k : mx;
+          ing = ok && kc[j] < cells32;
         }
-        const uint32_t bk = ing ? __umulhi(kk, magic32) >> shift32 : B;
+        const uint32_t bk = ing ? __umulhi(kc[j], magic32) >> shift32 : B;
         r[j] = atomicAdd(&ws[bk], 1u);
       }
       unsigned fb = 0;
 #pragma unroll
-      for (int j = 0; j < kDirPer; ++j) {
-        unsigned f = 0;
-        const uint32_t kk = map.key32(cur[j], f);
+      for (int j = 0; j < kDirPerT<In>; ++j) {
+        const uint32_t kk = kc[j];
         const uint32_t pos = r[j] & 0xffffu, lim = r[j] >> 16;
         const uint32_t bk = __umulhi(kk, magic32) >> shift32;
         if (pos < lim) rs[bk * kDirRing + (pos & (kDirRing - 1))] = static_cast<uint16_t>(kk - bk * S);
@@ -129,10 +151,9 @@ __global__ void __launch_bounds__(kDirThreads, 2)
       }
       if (__any_sync(0xffffffffu, fb)) {
 #pragma unroll
-        for (int j = 0; j < kDirPer; ++j) {
+        for (int j = 0; j < kDirPerT<In>; ++j) {
           const bool mine = (fb >> j) & 1u;
-          unsigned f = 0;
-          const uint32_t kk = map.key32(cur[j], f);
+          const uint32_t kk = kc[j];
           const unsigned peers = __match_any_sync(0xffffffffu, mine ? kk : 0xffffffffu);
           if (mine && lane == static_cast<uint32_t>(__ffs(peers) - 1))
             atomicAdd(&grid[kk], static_cast<uint32_t>(__popc(peers)));
@@ -144,19 +165,20 @@ __global__ void __launch_bounds__(kDirThreads, 2)
     if (ntiles > 1) load(tile + gridDim.x, nxt);
     for (uint32_t i = 0; i < ntiles; ++i, tile += gridDim.x) {
       const int s = i & 1;
-      In nx2[kDirPer];
+      In nx2[kDirPerT<In>];
       if (i + 2 < ntiles) load(tile + 2 * gridDim.x, nx2);
       if (i >= 2) nbar_sync<kFlushed, kDirThreads>(s);  // set s flushed after tile i-2
       if (tile < full_tiles) rank_tile(std::true_type{}, tile, s, cur);
       else rank_tile(std::false_type{}, tile, s, cur);
       nbar_arrive<kRanked, kDirThreads>(s);
 #pragma unroll
-      for (int j = 0; j < kDirPer; ++j) {
+      for (int j = 0; j < kDirPerT<In>; ++j) {
         cur[j] = nxt[j];
         nxt[j] = nx2[j];
       }
     }
-    warp_max_to(mx, &st->max_key);
+    if (static_cast<int32_t>(neg) < 0) flags |= kFlagNegative;
+    warp_max_to(static_cast<unsigned long long>(mx), &st->max_key);
     flags = warp_or(flags | (mx >= t.cells ? 0x80000000u : 0u));
     if (lane == 0 && flags) {
       if (flags & 0x7fffffffu) atomicOr(&st->flags, flags & 0x7fffffffu);
