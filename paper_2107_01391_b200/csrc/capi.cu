@@ -105,6 +105,20 @@ void Workspace::release() {
   if (h_stats) cudaFreeHost(h_stats);
   stats = nullptr;
   h_stats = nullptr;
+  if (side) cudaStreamDestroy(side);
+  if (fork) cudaEventDestroy(fork);
+  if (join) cudaEventDestroy(join);
+  side = nullptr;
+  fork = join = nullptr;
+}
+
+void Workspace::ensure_side() {
+  if (side) return;
+  int lo = 0, hi = 0;  // the highest priority: its small CTAs start ahead of the main stream's waiting ones
+  RS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  RS_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
+  RS_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
 }
 
 namespace {
@@ -607,14 +621,22 @@ void grid_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, u
     }
     scan_pass(ws, static_cast<const unsigned long long*>(wide), cells, n);
   }
-  emit_pass(ws, n, out);
-  (void)sorted;
+  // the report (one small latency-bound CTA over the occupied-cell list)
+  // runs on the side stream beside the emit, which reads the same list and
+  // writes only the output
+  ws.ensure_side();
+  RS_CUDA(cudaEventRecord(ws.fork, ws.stream));
+  RS_CUDA(cudaStreamWaitEvent(ws.side, ws.fork, 0));
   {
-    PassTimer pt_(RS_PASS_REPORT, ws.stream);
-    k_report<uint32_t><<<1, report_threads(radix), 0, ws.stream>>>(static_cast<const uint32_t*>(ws.buf[kSlotOccCell]), 0,
+    PassTimer pt_(RS_PASS_REPORT, ws.side);
+    k_report<uint32_t><<<1, report_threads(radix), 0, ws.side>>>(static_cast<const uint32_t*>(ws.buf[kSlotOccCell]), 0,
                                                 radix, total_digits, frac_digits, 0, ws.stats, true);
     RS_LAUNCH_CHECK();
   }
+  RS_CUDA(cudaEventRecord(ws.join, ws.side));
+  emit_pass(ws, n, out);
+  (void)sorted;
+  RS_CUDA(cudaStreamWaitEvent(ws.stream, ws.join, 0));
   pull_stats(ws);
 }
 

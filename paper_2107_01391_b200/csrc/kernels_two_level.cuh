@@ -646,19 +646,20 @@ __global__ void k_page_work(const uint32_t* __restrict__ po_bm, const unsigned l
     const uint32_t hi = (b + 1 < t.B) ? po_bm[(uint64_t)(b + 1) * t.G] : static_cast<uint32_t>(*total);
     g = (hi - lo + t.group_pages - 1) / t.group_pages;
   }
-  s_w[threadIdx.x] = g;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t r = 0;
-    for (uint32_t i = 0; i < blockDim.x; ++i) {
-      const uint32_t c = s_w[i];
-      s_w[i] = r;
-      r += c;
-    }
-    work_start[t.B] = r;
+  // exclusive scan of the group counts: warp scans, then the warp totals
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t inc = g;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
   }
+  if (lane == 31) s_w[wid] = inc;
   __syncthreads();
-  if (b < t.B) work_start[b] = s_w[b];
+  uint32_t before = 0;
+  for (uint32_t q = 0; q < wid; ++q) before += s_w[q];
+  if (b < t.B) work_start[b] = before + inc - g;
+  if (threadIdx.x == blockDim.x - 1) work_start[t.B] = before + inc;
 }
 
 // --------------------------------------------------------------- K2

@@ -116,6 +116,11 @@ struct Workspace {
   size_t cap[kSlots] = {};
   DevStats* stats = nullptr;   // device
   DevStats* h_stats = nullptr; // pinned host mirror
+  // a second stream for work that overlaps the main one inside a call (the
+  // report beside the emit), forked and joined with the two events
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  void ensure_side();
 
   void* raw(int slot, size_t bytes);
   template <class T>
