@@ -217,6 +217,32 @@ def test_direct_partition_overflowing_rings(rs, oracle, pattern):
     assert (rep.written, rep.cells_traversed) == wrep[:2]
 
 
+@pytest.mark.parametrize("n", [(1 << 22) + 1, 3072 * 1000 + 7, 1536 * 999 + 5, 5_000_003])
+@pytest.mark.parametrize("bound", [10**5, 10**6])
+@pytest.mark.parametrize("width", [4, 8])
+def test_direct_partition_tiles_and_tails(rs, oracle, n, bound, width):
+    """The direct partition's tile geometry (3072 4-byte or 1536 8-byte keys
+    per tile, two ring sets, partial last tile) and its tails (each bucket's
+    last ring chunks padded into the page) on 10- and 100-bucket grids,
+    through the reference semantics (no declared width) for uint32 and int64
+    input."""
+    import torch
+
+    keys = oracle.gen_u32(83 + n % 7, 0, n, bound)
+    keys[n // 3] = bound - 1  # the grid is 10^digits(bound - 1)
+    if width == 4:
+        want, wrep = oracle.sort_integers_u32(keys)
+        out, rep = rs.sort_u32(torch.from_numpy(keys.view(np.int32)).cuda())
+        got = out.cpu().numpy().view(np.uint32)
+    else:
+        vals = keys.astype(np.int64)
+        want, wrep = oracle.sort_integers_i64(vals)
+        out, rep = rs.sort_i64(torch.from_numpy(vals).cuda())
+        got = out.cpu().numpy()
+    assert np.array_equal(got, want)
+    assert (rep.written, rep.cells_traversed) == wrep[:2]
+
+
 @pytest.mark.parametrize("parts", [2, 3, 8])
 def test_emit_part_cuts_match_cell_ranges(rs, oracle, parts):
     """rs_emit_part_u32 (the sharded grid's emit): the device cuts equal
