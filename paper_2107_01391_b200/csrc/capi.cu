@@ -448,8 +448,14 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
     }
     RS_LAUNCH_CHECK();
   }
-  exscan_u32(ws, pc_bm, bg, po_bm, total);
-  {
+  if (bg <= kPageScanMax && t.B <= (uint32_t)kPageScanThreads) {  // one CTA: scan + work list
+    PassTimer pt_(RS_PASS_SCAN, ws.stream, 2);
+    k_page_scan<<<1, kPageScanThreads, 0, ws.stream>>>(pc_bm, static_cast<uint32_t>(bg), po_bm, total, t, work);
+    RS_LAUNCH_CHECK();
+    k_page_list<<<t.G, 256, t.B * sizeof(uint32_t), ws.stream>>>(page_bucket, po_bm, pc_bm, t, list);
+    RS_LAUNCH_CHECK();
+  } else {
+    exscan_u32(ws, pc_bm, bg, po_bm, total);
     PassTimer pt_(RS_PASS_SCAN, ws.stream, 2);
     k_page_list<<<t.G, 256, t.B * sizeof(uint32_t), ws.stream>>>(page_bucket, po_bm, pc_bm, t, list);
     RS_LAUNCH_CHECK();

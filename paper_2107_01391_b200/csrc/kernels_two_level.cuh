@@ -634,6 +634,98 @@ __global__ void k_page_list(const uint16_t* __restrict__ page_bucket, const uint
   }
 }
 
+// The page table's scan and the page-count work list in one CTA, for page
+// tables of at most kPageScanMax (bucket, CTA) entries (cfg2: 100 x 296):
+// po_bm = exclusive scan of pc_bm, *total = the page count, and
+// work_start = exclusive scan over buckets of ceil(pages_b / group_pages)
+// (k_page_work's list) — in place of the look-back scan, its descriptor
+// reset and k_page_work (three launches).
+constexpr int kPageScanThreads = 1024;
+constexpr uint32_t kPageScanPer = 32;
+constexpr uint64_t kPageScanMax = (uint64_t)kPageScanThreads * kPageScanPer;
+__global__ void __launch_bounds__(kPageScanThreads) k_page_scan(const uint32_t* __restrict__ pc_bm, uint32_t count,
+                                                                 uint32_t* __restrict__ po_bm,
+                                                                 unsigned long long* total, TwoLevel t,
+                                                                 uint32_t* __restrict__ work_start) {
+  __shared__ uint32_t s_w[kPageScanThreads / 32];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto block_scan = [&](uint32_t v, uint32_t& excl, uint32_t& all) {
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[wid] = inc;
+    __syncthreads();
+    const uint32_t tw = s_w[lane];
+    uint32_t ti = tw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    excl = __shfl_sync(0xffffffffu, ti - tw, wid) + inc - v;
+    all = __shfl_sync(0xffffffffu, ti, 31);
+    __syncthreads();
+  };
+  // warp w scans entries [w*1024, (w+1)*1024) as 32 coalesced rows of 32
+  const uint32_t base_e = wid * (32 * kPageScanPer);
+  uint32_t ex[kPageScanPer];
+  uint32_t carry = 0;
+#pragma unroll
+  for (uint32_t i = 0; i < kPageScanPer; ++i) {
+    const uint32_t e = base_e + i * 32 + lane;
+    ex[i] = e < count ? __ldcg(pc_bm + e) : 0u;
+  }
+#pragma unroll
+  for (uint32_t i = 0; i < kPageScanPer; ++i) {
+    const uint32_t x = ex[i];
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    ex[i] = carry + inc - x;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  uint32_t wbase, all;
+  if (lane == 0) s_w[wid] = carry;
+  __syncthreads();
+  {
+    const uint32_t tw = s_w[lane];
+    uint32_t ti = tw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    wbase = __shfl_sync(0xffffffffu, ti - tw, wid);
+    all = __shfl_sync(0xffffffffu, ti, 31);
+  }
+  __syncthreads();
+#pragma unroll
+  for (uint32_t i = 0; i < kPageScanPer; ++i) {
+    const uint32_t e = base_e + i * 32 + lane;
+    if (e < count) po_bm[e] = wbase + ex[i];
+  }
+  if (threadIdx.x == 0) *total = all;
+  __syncthreads();  // po_bm visible to the CTA (global writes, same CTA)
+  // bucket b's pages: [po_bm[b*G], po_bm[(b+1)*G]) -> groups of group_pages
+  const uint32_t b = threadIdx.x;
+  uint32_t g = 0;
+  if (b < t.B) {
+    const uint32_t lo = __ldcg(po_bm + (uint64_t)b * t.G);
+    const uint32_t hi = (b + 1 < t.B) ? __ldcg(po_bm + (uint64_t)(b + 1) * t.G) : all;
+    g = (hi - lo + t.group_pages - 1) / t.group_pages;
+  }
+  uint32_t ws, wall;
+  block_scan(g, ws, wall);
+  if (b < t.B) work_start[b] = ws;
+  if (threadIdx.x == 0) work_start[t.B] = wall;
+}
+
 // Work list: bucket b owns list entries [po_bm[b*G], po_bm[(b+1)*G]), cut
 // into groups of group_pages; work_start = exclusive scan of group counts.
 __global__ void k_page_work(const uint32_t* __restrict__ po_bm, const unsigned long long* total, TwoLevel t,
