@@ -81,7 +81,11 @@ def _torch():
 
 
 def _stream():
-    return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+    torch = _torch()
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # skips building a Stream object per call
+    if raw is not None:
+        return ctypes.c_void_p(raw(torch.cuda.current_device()))
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def _ptr(t) -> ctypes.c_void_p:
@@ -94,7 +98,7 @@ def _cuda_tensor(t, dtypes, what):
         raise TypeError(f"{what} must be a CUDA tensor")
     if t.dtype not in dtypes:
         raise TypeError(f"{what} must have dtype in {dtypes}, got {t.dtype}")
-    return t.contiguous()
+    return t if t.is_contiguous() else t.contiguous()
 
 
 # ----------------------------------------------------------- device API

@@ -702,7 +702,9 @@ void integer_sort(const typename Map::In* in, uint64_t n, Map map, Out out, cons
       // the grid fits shared memory and the budget
       small_sort(ws, in, n, map, 0u, out, 10u, 0u, 0u, true, budget);
       check_flags(ws.h_stats->flags);
-      if (ws.h_stats->overflow != 2) {
+      // 1: a key past the sampled grid, 2: the grid does not qualify; either
+      // way the exact max is known and the general path below takes over
+      if (ws.h_stats->overflow == 0) {
         const uint32_t d = static_cast<uint32_t>(ws.h_stats->report_digits);
         if (report) *report = rs_report{n, ws.h_stats->cells_traversed, rs_key_spec{10, d, d}};
         return;

@@ -924,6 +924,7 @@ __global__ void k_report(const K* __restrict__ sorted, uint64_t n, uint32_t radi
 // or a flagged input skips the emit (the host redoes or raises).
 constexpr uint64_t kSmallMax = 1ull << 22;
 constexpr int kSmallThreads = 1024;
+constexpr uint64_t kSmallSample = 4096;  // keys of the strided sample that sizes an undeclared grid
 
 // With auto_cells (decimal integers without a declared width) the grid is
 // derived in the same launch: a max phase, a first barrier, cells =
@@ -953,22 +954,44 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_sort(const typename Map
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* bar = gcount + kSmemCellsMax;  // two barrier counters
   if (auto_cells) {
+    // the grid from the max of a strided sample that every CTA reads alike
+    // (no grid-wide max pass and barrier); the count below folds in the
+    // true max, and a key past the sampled grid makes the host redo the
+    // sort with it (st->overflow = 1, no emit)
     unsigned long long m = 0;
     unsigned fl = 0;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-      const unsigned long long k = map(__ldcs(in + i), fl);
+    const uint64_t ns = n < kSmallSample ? n : kSmallSample, step = n / ns;
+    for (uint64_t j = threadIdx.x; j < ns; j += blockDim.x) {
+      const unsigned long long k = map(__ldcg(in + j * step), fl);
       m = k > m ? k : m;
     }
-    warp_max_to(m, &st->max_key);
-    fl = warp_or(fl);
-    if (lane == 0 && fl) atomicOr(&st->flags, fl);
-    grid_barrier(bar + 1);
-    if (*reinterpret_cast<volatile unsigned*>(&st->flags)) return;  // the host raises
-    const unsigned long long mxk = *reinterpret_cast<volatile unsigned long long*>(&st->max_key);
-    const uint32_t d = d_digit_count(mxk);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // the last key too (sorted or nearly sorted inputs)
+      const unsigned long long k = map(__ldcg(in + n - 1), fl);
+      m = k > m ? k : m;
+    }
+    m = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(m >> 32)) == 0
+            ? __reduce_max_sync(0xffffffffu, static_cast<unsigned>(m))
+            : (static_cast<unsigned long long>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(m >> 32))) << 32) |
+                  0xffffffffu;
+    if (lane == 0) s_span[warp] = m;
+    __syncthreads();
+    unsigned long long smax = 0;
+    for (int w = 0; w < kSmallThreads / 32; ++w) smax = s_span[w] > smax ? s_span[w] : smax;
+    __syncthreads();
+    const uint32_t d = d_digit_count(smax);
     const unsigned long long need = d_pow(10, d);
     if (need > kSmemCellsMax || need > budget) {
+      // the grid does not qualify: the exact max (and flags) for the host's multi-pass path
+      unsigned long long mm = 0;
+      unsigned ff = fl;
+      const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+      for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const unsigned long long k = map(__ldcs(in + i), ff);
+        mm = k > mm ? k : mm;
+      }
+      warp_max_to(mm, &st->max_key);
+      ff = warp_or(ff);
+      if (lane == 0 && ff) atomicOr(&st->flags, ff);
       if (blockIdx.x == 0 && threadIdx.x == 0) st->overflow = 2;  // multi-pass path (or the budget error)
       return;
     }

@@ -243,6 +243,24 @@ def test_direct_partition_tiles_and_tails(rs, oracle, n, bound, width):
     assert (rep.written, rep.cells_traversed) == wrep[:2]
 
 
+@pytest.mark.parametrize("n,outlier", [(100, None), (4097, None), (1 << 20, None), (1 << 20, 999_999),
+                                       (1 << 20, 1_234_567), ((1 << 22) - 3, 54_321), (1 << 20, 1000)])
+def test_small_sort_sampled_grid(rs, oracle, n, outlier):
+    """The one-launch small sort sizes an undeclared grid from a strided
+    sample's max; a key past the sampled grid (an outlier off the sample's
+    stride) makes the host redo the sort with the exact max, on the small
+    path or the multi-pass one."""
+    import torch
+
+    keys = oracle.gen_u32(84, 0, n, 1000)
+    if outlier is not None:
+        keys[n // 2 + 1] = outlier  # off the sample's stride
+    want, wrep = oracle.sort_integers_u32(keys)
+    out, rep = rs.sort_u32(torch.from_numpy(keys.view(np.int32)).cuda())
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
+    assert (rep.written, rep.cells_traversed, (rep.spec.radix, rep.spec.total_digits, rep.spec.integer_digits)) == wrep
+
+
 @pytest.mark.parametrize("parts", [2, 3, 8])
 def test_emit_part_cuts_match_cell_ranges(rs, oracle, parts):
     """rs_emit_part_u32 (the sharded grid's emit): the device cuts equal
