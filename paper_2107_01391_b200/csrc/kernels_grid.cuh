@@ -924,7 +924,7 @@ __global__ void k_report(const K* __restrict__ sorted, uint64_t n, uint32_t radi
 // or a flagged input skips the emit (the host redoes or raises).
 constexpr uint64_t kSmallMax = 1ull << 22;
 constexpr int kSmallThreads = 1024;
-constexpr uint64_t kSmallSample = 4096;  // keys of the strided sample that sizes an undeclared grid
+constexpr uint64_t kSmallSample = 1024;  // keys of the strided sample that sizes an undeclared grid (one per thread)
 
 // With auto_cells (decimal integers without a declared width) the grid is
 // derived in the same launch: a max phase, a first barrier, cells =
