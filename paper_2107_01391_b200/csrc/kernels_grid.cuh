@@ -369,8 +369,9 @@ __global__ void __launch_bounds__(kThreads) k_max_sample(const typename Map::In*
                                                          uint32_t samples, Map map, DevStats* st) {
   unsigned long long mx = 0;
   unsigned flags = 0;
+  const uint64_t step = n / samples > 0 ? n / samples : 1;  // one 64-bit division, not one per sample
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < samples; s += gridDim.x * blockDim.x) {
-    const uint64_t i = static_cast<uint64_t>((static_cast<unsigned __int128>(s) * n) / samples);
+    const uint64_t i = (uint64_t)s * step < n ? (uint64_t)s * step : n - 1;
     const unsigned long long k = map(__ldg(in + i), flags);
     mx = k > mx ? k : mx;
   }
