@@ -404,7 +404,7 @@ template <class Map>
 void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, const TwoLevel& t,
                      uint32_t* counts, bool use_ws) {
   const bool al = aligned16(in);
-  const bool direct = al && use_ws && t.B <= kDirMaxBuckets;
+  const bool direct = al && t.B <= kDirMaxBuckets;
   const uint64_t P = (uint64_t)t.G * t.pages_per_cta;
   const uint64_t bg = (uint64_t)t.B * t.G;
   auto* pages = ws.get<uint16_t>(kSlotLows, P * kPage);
@@ -431,8 +431,20 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
           return true;
         }();
         (void)attr;
-        k_page_partition_direct<Map><<<t.G, kDirThreads, page_dir_smem(t.B), ws.stream>>>(
-            in, n, map, t, pages, page_bucket, page_fill, pc_bm, counts, ws.stats);
+        if (use_ws) {
+          k_page_partition_direct<Map><<<t.G, kDirThreads, page_dir_smem(t.B), ws.stream>>>(
+              in, n, map, t, pages, page_bucket, page_fill, pc_bm, counts, ws.stats);
+        } else {  // mapped float64 cells (cfg3: a Zipf-hot bucket): the variant that counts a hot bucket in place
+          static const bool attr_h = [] {
+            cudaFuncSetAttribute(k_page_partition_direct<Map, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(page_dir_hot_smem(kDirMaxBuckets, kTlMaxInner)));
+            return true;
+          }();
+          (void)attr_h;
+          k_page_partition_direct<Map, true><<<t.G, kDirThreads, page_dir_hot_smem(t.B, t.S),
+                                               ws.stream>>>(in, n, map, t, pages, page_bucket, page_fill, pc_bm,
+                                                            counts, ws.stats);
+        }
       }
     }
     if (direct) {

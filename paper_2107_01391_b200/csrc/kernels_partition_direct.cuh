@@ -50,7 +50,22 @@ __host__ __device__ constexpr size_t page_dir_smem(uint32_t B) {
   return 2 * (size_t)B * kDirRing * sizeof(uint16_t) + 2 * 128 * sizeof(uint32_t);
 }
 
-template <class Map>
+// kHot (skewed inputs, e.g. cfg3's Zipf-hot mapped cells): a shared uint32
+// histogram of one bucket's S inner cells: the first bucket whose ring
+// overflows becomes the CTA's hot bucket and its keys are counted there
+// directly (one shared atomic each, no ring, no page), the histogram flushed
+// into the grid at the end.
+// The hot variant's ring chunks are 64 entries, which leaves room for the
+// histogram while two CTAs still share an SM.
+template <bool kHot>
+__host__ __device__ constexpr uint32_t dir_chunk() { return kHot ? 64u : kDirChunk; }
+__host__ __device__ constexpr size_t page_dir_hot_smem(uint32_t B, uint32_t S) {
+  return 2 * (size_t)B * 2 * dir_chunk<true>() * sizeof(uint16_t) + 2 * 128 * sizeof(uint32_t) +
+         (size_t)S * sizeof(uint32_t);
+}
+constexpr uint32_t kDirNoHot = 0xffffffffu;
+
+template <class Map, bool kHot = false>
 __global__ void __launch_bounds__(kDirThreads, 2)
     k_page_partition_direct(const typename Map::In* __restrict__ in, uint64_t n, Map map, TwoLevel t,
                              uint16_t* __restrict__ pages, uint16_t* __restrict__ page_bucket,
@@ -58,7 +73,10 @@ __global__ void __launch_bounds__(kDirThreads, 2)
                              uint32_t* __restrict__ grid, DevStats* st) {
   using In = typename Map::In;
   constexpr bool k32 = sizeof(In) == 4;
-  constexpr uint32_t kDirTile = kDirRankers * kDirPerT<In>;    // 3072 4-byte or 1536 8-byte keys
+  constexpr int kRk = kDirRankers, kThr = kDirThreads;
+  constexpr uint32_t kDirTile = kRk * kDirPerT<In>;    // 3072 4-byte or 1536 8-byte keys
+  constexpr uint32_t kDirChunk = dir_chunk<kHot>();
+  constexpr uint32_t kDirRing = 2 * kDirChunk;
   constexpr bool kInt64 = std::is_same_v<Map, MapI64> || std::is_same_v<Map, MapU64>;
   using Mx = std::conditional_t<k32 || kInt64, uint32_t, unsigned long long>;
   constexpr uint32_t kCPP = kPage / kDirChunk;
@@ -67,7 +85,8 @@ __global__ void __launch_bounds__(kDirThreads, 2)
   const uint32_t B = t.B;
   uint16_t* ring = reinterpret_cast<uint16_t*>(sm);                                            // [2][B][kDirRing]
   uint32_t* w = reinterpret_cast<uint32_t*>(sm + 2 * (size_t)B * kDirRing * sizeof(uint16_t));  // [2][128]
-  __shared__ uint32_t s_next;
+  uint32_t* s_hh = w + 2 * 128;  // kHot: [S] counts of the hot bucket's inner cells
+  __shared__ uint32_t s_next, s_hot;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   const uint32_t T = static_cast<uint32_t>((n + kDirTile - 1) / kDirTile);
   const uint32_t ntiles = blockIdx.x < T ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -80,10 +99,15 @@ __global__ void __launch_bounds__(kDirThreads, 2)
     const uint32_t b = tid & 127;
     w[tid] = b < B ? kDirRing << 16 : 0u;  // both chunks writable; the dummy word B: limit 0
   }
-  if (tid == 0) s_next = 0;
+  if (tid == 0) {
+    s_next = 0;
+    s_hot = kDirNoHot;
+  }
+  if constexpr (kHot)
+    for (uint32_t c = tid; c < t.S; c += kThr) s_hh[c] = 0;
   __syncthreads();
 
-  if (tid < kDirRankers) {
+  if (tid < kRk) {
     // ------------------------------------------------------------ rankers
     Mx mx = 0;
     unsigned flags = 0;
@@ -108,6 +132,7 @@ __global__ void __launch_bounds__(kDirThreads, 2)
       // each key's 32-bit cell (8-byte keys saturate at 0xFFFFFFFF, which no
       // grid reaches, so kc < cells is the in-grid test for both widths)
       uint32_t kc[kDirPerT<In>], r[kDirPerT<In>];
+      const uint32_t hot = kHot ? *reinterpret_cast<volatile uint32_t*>(&s_hot) : kDirNoHot;
 #pragma unroll
       for (int j = 0; j < kDirPerT<In>; ++j) {
         Mx k;
@@ -138,7 +163,12 @@ __global__ void __launch_bounds__(kDirThreads, 2)
           ing = ok && kc[j] < cells32;
         }
         const uint32_t bk = ing ? __umulhi(kc[j], magic32) >> shift32 : B;
-        r[j] = atomicAdd(&ws[bk], 1u);
+        if (kHot && bk == hot) {  // counted in place; r = 0 (limit 0): no ring store, no fallback
+          atomicAdd(&s_hh[kc[j] - bk * S], 1u);
+          r[j] = 0;
+        } else {
+          r[j] = atomicAdd(&ws[bk], 1u);
+        }
       }
       unsigned fb = 0;
 #pragma unroll
@@ -167,10 +197,10 @@ __global__ void __launch_bounds__(kDirThreads, 2)
       const int s = i & 1;
       In nx2[kDirPerT<In>];
       if (i + 2 < ntiles) load(tile + 2 * gridDim.x, nx2);
-      if (i >= 2) nbar_sync<kFlushed, kDirThreads>(s);  // set s flushed after tile i-2
+      if (i >= 2) nbar_sync<kFlushed, kThr>(s);  // set s flushed after tile i-2
       if (tile < full_tiles) rank_tile(std::true_type{}, tile, s, cur);
       else rank_tile(std::false_type{}, tile, s, cur);
-      nbar_arrive<kRanked, kDirThreads>(s);
+      nbar_arrive<kRanked, kThr>(s);
 #pragma unroll
       for (int j = 0; j < kDirPerT<In>; ++j) {
         cur[j] = nxt[j];
@@ -184,10 +214,10 @@ __global__ void __launch_bounds__(kDirThreads, 2)
       if (flags & 0x7fffffffu) atomicOr(&st->flags, flags & 0x7fffffffu);
       if (flags & 0x80000000u) atomicOr(&st->overflow, 1u);
     }
-    return;
-  }
+    if constexpr (!kHot) return;
+  } else {
   // -------------------------------------------------------------- owners
-  const uint32_t b = tid - kDirRankers;
+  const uint32_t b = tid - kRk;
   uint32_t issued0 = 0, issued1 = 0, pg = 0, q = kCPP, np = 0;
   auto open_page = [&]() {
     if (q == kCPP) {
@@ -206,7 +236,10 @@ __global__ void __launch_bounds__(kDirThreads, 2)
     const uint32_t v = ws[b];
     uint32_t next = v & 0xffffu;
     const uint32_t lim = v >> 16;
-    if (next > lim) next = lim;
+    if (next > lim) {  // the keys past the limit were counted in the grid
+      next = lim;
+      if (kHot && s_hot == kDirNoHot) atomicCAS(&s_hot, kDirNoHot, b);  // skew: b's keys count in place from now on
+    }
     bulk_wait_read1();  // set s's bulk stores of two tiles ago have read their chunks
     const uint32_t free_upto = issued;
     const uint32_t full = next / kDirChunk;
@@ -232,10 +265,10 @@ __global__ void __launch_bounds__(kDirThreads, 2)
   };
   auto step = [&](auto s_c, uint32_t i) {
     constexpr int s = decltype(s_c)::value;
-    nbar_sync<kRanked, kDirThreads>(s);  // tile i ranked into set s
+    nbar_sync<kRanked, kThr>(s);  // tile i ranked into set s
     if (b < B) flush(s_c);
     if (b == B) w[s * 128 + B] = 0;
-    if (i + 2 < ntiles) nbar_arrive<kFlushed, kDirThreads>(s);
+    if (i + 2 < ntiles) nbar_arrive<kFlushed, kThr>(s);
   };
   for (uint32_t i = 0; i < ntiles; i += 2) {
     step(std::integral_constant<int, 0>{}, i);
@@ -262,6 +295,16 @@ __global__ void __launch_bounds__(kDirThreads, 2)
     if (q < kCPP) page_fill[page0 + pg] = static_cast<uint16_t>(q * kDirChunk);
     pc_bm[(uint64_t)b * t.G + blockIdx.x] = np;
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  }  // owners
+  if constexpr (kHot) {  // the hot bucket's counts into the grid
+    __syncthreads();
+    const uint32_t hot = s_hot;
+    if (hot != kDirNoHot)
+      for (uint32_t c = tid; c < S; c += kThr) {
+        const uint32_t v = s_hh[c];
+        if (v && (uint64_t)hot * S + c < t.cells) atomicAdd(&grid[hot * S + c], v);
+      }
   }
 }
 
