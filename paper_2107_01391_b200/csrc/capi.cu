@@ -401,10 +401,16 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t, bool ws) {
 }
 
 template <class Map>
-void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, const TwoLevel& t,
+void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, const TwoLevel& t0,
                      uint32_t* counts, bool use_ws) {
   const bool al = aligned16(in);
-  const bool direct = al && t.B <= kDirMaxBuckets;
+  const bool direct = al && t0.B <= kDirMaxBuckets;
+  TwoLevel t = t0;
+  if (direct && t.G != 2u * sm_count()) {  // the direct partition: two CTAs per SM, one persistent wave
+    t.G = static_cast<uint32_t>(std::min<uint64_t>(2ull * sm_count(), t.T));
+    const uint64_t tiles_per = (t.T + t.G - 1) / t.G;
+    t.pages_per_cta = static_cast<uint32_t>((tiles_per * (kTlTile + 7ull * t.B) + kPage - 1) / kPage + t.B);
+  }
   const uint64_t P = (uint64_t)t.G * t.pages_per_cta;
   const uint64_t bg = (uint64_t)t.B * t.G;
   auto* pages = ws.get<uint16_t>(kSlotLows, P * kPage);
