@@ -183,6 +183,7 @@ __global__ void __launch_bounds__(kDirThreads, 2)
 #pragma unroll
         for (int j = 0; j < kDirPerT<In>; ++j) {
           const bool mine = (fb >> j) & 1u;
+          if (!__any_sync(0xffffffffu, mine)) continue;  // a match only for the key slots that need one
           const uint32_t kk = kc[j];
           const unsigned peers = __match_any_sync(0xffffffffu, mine ? kk : 0xffffffffu);
           if (mine && lane == static_cast<uint32_t>(__ffs(peers) - 1))
