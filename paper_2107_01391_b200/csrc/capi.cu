@@ -429,8 +429,10 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
   RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
   {
     PassTimer pt_(RS_PASS_PARTITION, ws.stream);
+    bool launched = false;
     if constexpr (!map_first<Map>::value) {  // (mapped float64 cells arrive as MapU32)
       if (direct) {  // keys straight into shared page chunks, TMA bulk-stored
+        launched = true;
         static const bool attr = [] {
           cudaFuncSetAttribute(k_page_partition_direct<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(page_dir_smem(kDirMaxBuckets)));
@@ -453,7 +455,7 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
         }
       }
     }
-    if (direct) {
+    if (launched) {
     } else if (al && t.B <= 256 && use_ws) {  // warp-specialised: rankers + page-store warps
       k_page_partition_ws<Map><<<t.G, kWsThreads, page_ws_smem(t.B, sizeof(typename Map::In)), ws.stream>>>(
           in, n, map, t, pages, page_bucket, page_fill, pc_bm, counts, ws.stats);
