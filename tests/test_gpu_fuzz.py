@@ -80,3 +80,56 @@ def test_small_path_switch(rs, oracle, n, bound):
         out, rep = rs.sort_u32(_t(keys), key_digits=hint, max_cells=10**9)
         assert np.array_equal(out.cpu().numpy().view(np.uint32), want), hint
         assert (rep.written, rep.cells_traversed) == wrep[:2], hint
+
+
+def _skewed(rng, n, bound):
+    """Keys in [0, bound): uniform, a few hot values, one hot outer bucket
+    (a tenth of the range), or sorted runs."""
+    keys = rng.integers(0, bound, n, dtype=np.uint64)
+    mode = rng.integers(0, 4)
+    if mode == 1 and n > 10:
+        hot = rng.integers(0, bound, 3, dtype=np.uint64)
+        pick = rng.random(n) < 0.6
+        keys[pick] = hot[rng.integers(0, 3, int(pick.sum()))]
+    elif mode == 2 and n > 10:
+        pick = rng.random(n) < 0.5
+        keys[pick] = rng.integers(0, max(bound // 10, 1), int(pick.sum()), dtype=np.uint64)
+    elif mode == 3:
+        keys = np.sort(keys)
+    return keys
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_sort_i64_direct_partition_fuzz(rs, oracle, seed):
+    """int64 keys through the direct partition (grids of <= 104 outer
+    buckets) and the warp-specialised one (more), across tile tails and
+    skew, against the reference semantics (sort_integers)."""
+    import torch
+
+    rng = np.random.default_rng(300 + seed)
+    n = int(rng.choice([4_194_305, 1536 * 997 + 3, 3_000_001, 5_500_007]))
+    bound = int(rng.choice([10**5, 10**6, 2 * 10**6]))
+    vals = _skewed(rng, n, bound).astype(np.int64)
+    want, wrep = oracle.sort_integers_i64(vals, max_cells=10**9)
+    out, rep = rs.sort_i64(torch.from_numpy(vals).cuda(), max_cells=10**9)
+    assert np.array_equal(out.cpu().numpy(), want), seed
+    assert (rep.written, rep.cells_traversed) == wrep[:2], seed
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_sort_f64_hot_bucket_fuzz(rs, oracle, seed):
+    """float64 values k/1000 whose mapped cells skew one outer bucket (the
+    direct partition's hot variant counts it in place), against the oracle."""
+    import torch
+
+    rng = np.random.default_rng(400 + seed)
+    n = int(rng.choice([4_194_305, 3_000_001, 2_500_003]))
+    k = _skewed(rng, n, 10**6)
+    if seed % 2:  # a geometric head on top: the shape of cfg3's Zipf half
+        head = rng.random(n) < 0.45
+        k[head] = np.minimum(rng.geometric(0.002, int(head.sum())), 10**6 - 1).astype(np.uint64)
+    x = k.astype(np.float64) / 1000.0
+    want, wrep = oracle.sort_f64(x, 3)
+    out, rep = rs.sort_f64(torch.from_numpy(x).cuda(), 3)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), want), seed
+    assert (rep.written, rep.cells_traversed, (rep.spec.radix, rep.spec.total_digits, rep.spec.integer_digits)) == wrep, seed
