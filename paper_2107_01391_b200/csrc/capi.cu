@@ -148,6 +148,25 @@ Workspace& workspace_for(cudaStream_t stream) {
   return *w;
 }
 
+// The dynamic shared memory limit of a kernel, raised once per (kernel,
+// device): function attributes belong to a device's context, so a process
+// driving several GPUs (rs_sort_u32_multi) sets them on each.
+void set_smem(const void* fn, size_t bytes) {
+  int dev = 0;
+  RS_CUDA(cudaGetDevice(&dev));
+  static std::mutex m;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  std::lock_guard<std::mutex> lock(m);
+  size_t& cur = done[{fn, dev}];
+  if (cur >= bytes) return;
+  RS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  cur = bytes;
+}
+template <class F>
+void set_smem(F* fn, size_t bytes) {
+  set_smem(reinterpret_cast<const void*>(fn), bytes);
+}
+
 int sm_count() {
   static int sms = [] {
     int dev = 0, v = 0;
@@ -375,16 +394,14 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t, bool ws) {
   // CTAs per SM of each partition kernel, once per mapper (one device type per process)
   static const int per_sm_tma = [] {
     int b = 0;
-    cudaFuncSetAttribute(k_page_partition_tma<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(page_tma_smem<Map>()));
+    set_smem(k_page_partition_tma<Map>, page_tma_smem<Map>());
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_page_partition_tma<Map>, kTlThreads, page_tma_smem<Map>());
     return b < 1 ? 1 : b;
   }();
   static const int per_sm_ws = [] {
     int b = 0;
     constexpr uint32_t kIn = sizeof(typename Map::In);
-    cudaFuncSetAttribute(k_page_partition_ws<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(page_ws_smem(256, kIn)));
+    set_smem(k_page_partition_ws<Map>, page_ws_smem(256, kIn));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_page_partition_ws<Map>, kWsThreads, page_ws_smem(100, kIn));
     return b < 1 ? 1 : b;
   }();
@@ -422,9 +439,7 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
   auto* total = ws.get<unsigned long long>(kSlotScratch, 4);
   auto* work = ws.get<uint32_t>(kSlotMisc, t.B + 1ull);
   const size_t smem = kPagePartitionSmem(t.B);
-  if (smem > 48 * 1024)
-    RS_CUDA(cudaFuncSetAttribute(k_page_partition<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
+  if (smem > 48 * 1024) set_smem(k_page_partition<Map>, smem);
   // zeroed before the partition: keys whose staging range is full are counted straight into it
   RS_CUDA(cudaMemsetAsync(counts, 0, t.cells * sizeof(uint32_t), ws.stream));
   {
@@ -433,22 +448,12 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
     if constexpr (!map_first<Map>::value) {  // (mapped float64 cells arrive as MapU32)
       if (direct) {  // keys straight into shared page chunks, TMA bulk-stored
         launched = true;
-        static const bool attr = [] {
-          cudaFuncSetAttribute(k_page_partition_direct<Map>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(page_dir_smem(kDirMaxBuckets)));
-          return true;
-        }();
-        (void)attr;
         if (use_ws) {
+          set_smem(k_page_partition_direct<Map>, page_dir_smem(t.B));
           k_page_partition_direct<Map><<<t.G, kDirThreads, page_dir_smem(t.B), ws.stream>>>(
               in, n, map, t, pages, page_bucket, page_fill, pc_bm, counts, ws.stats);
         } else {  // mapped float64 cells (cfg3: a Zipf-hot bucket): the variant that counts a hot bucket in place
-          static const bool attr_h = [] {
-            cudaFuncSetAttribute(k_page_partition_direct<Map, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(page_dir_hot_smem(kDirMaxBuckets, kTlMaxInner)));
-            return true;
-          }();
-          (void)attr_h;
+          set_smem(k_page_partition_direct<Map, true>, page_dir_hot_smem(t.B, t.S));
           k_page_partition_direct<Map, true><<<t.G, kDirThreads, page_dir_hot_smem(t.B, t.S),
                                                ws.stream>>>(in, n, map, t, pages, page_bucket, page_fill, pc_bm,
                                                             counts, ws.stats);
@@ -457,9 +462,11 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
     }
     if (launched) {
     } else if (al && t.B <= 256 && use_ws) {  // warp-specialised: rankers + page-store warps
+      set_smem(k_page_partition_ws<Map>, page_ws_smem(t.B, sizeof(typename Map::In)));
       k_page_partition_ws<Map><<<t.G, kWsThreads, page_ws_smem(t.B, sizeof(typename Map::In)), ws.stream>>>(
           in, n, map, t, pages, page_bucket, page_fill, pc_bm, counts, ws.stats);
     } else if (al && t.B <= 256) {  // TMA-fed tiles, bulk-stored pages
+      set_smem(k_page_partition_tma<Map>, page_tma_smem<Map>());
       k_page_partition_tma<Map><<<t.G, kTlThreads, page_tma_smem<Map>(), ws.stream>>>(
           in, n, map, t, pages, page_bucket, page_fill, pc_bm, ws.stats);
     } else {
@@ -484,9 +491,7 @@ void two_level_count(Workspace& ws, const typename Map::In* in, uint64_t n, Map 
   }
   const uint64_t max_groups = P / t.group_pages + t.B + 1;
   const size_t cnt_smem = (t.S + 1) * sizeof(uint32_t);  // + the dump bin of pad entries
-  if (cnt_smem > 48 * 1024)
-    RS_CUDA(cudaFuncSetAttribute(k_page_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(cnt_smem)));
+  if (cnt_smem > 48 * 1024) set_smem(k_page_count, cnt_smem);
   {
     PassTimer pt_(RS_PASS_COUNT, ws.stream);
     k_page_count<<<static_cast<unsigned>(max_groups), kGatherThreads, cnt_smem, ws.stream>>>(
@@ -586,9 +591,7 @@ void small_sort(Workspace& ws, const typename Map::In* in, uint64_t n, Map map, 
   RS_CUDA(cudaMemsetAsync(g, 0, (kSmemCellsMax + 2) * sizeof(uint32_t), ws.stream));
   auto* kern = k_small_sort<Map, Out>;
   const size_t smem = (kSmemCellsMax + 1) * sizeof(uint32_t);
-  static const bool attr = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(smem)), true);
-  (void)attr;
+  set_smem(kern, smem);
   // at most one CTA per SM: the flush into the global grid is cells x CTAs atomics
   const uint64_t want = (n + 4 * kSmallThreads - 1) / (4 * kSmallThreads);
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(want, (uint64_t)sm_count()));
@@ -793,8 +796,7 @@ KvPass kv_pass(uint32_t g, uint32_t digits, uint64_t n) {
   const uint64_t tiles = (n + kKvTile - 1) / kKvTile;
   static int per_sm = 0;
   if (!per_sm) {
-    cudaFuncSetAttribute(k_kv_chunk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kKvSmemBytes));
+    set_smem(k_kv_chunk_scatter, kKvSmemBytes);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kv_chunk_scatter, kKvThreads, kKvSmemBytes);
     if (per_sm < 1) per_sm = 1;
   }
@@ -811,12 +813,7 @@ void kv_sort(Workspace& ws, const uint32_t* keys, const uint32_t* vals, uint64_t
   reset_stats(ws);
   uint32_t* tk = ws.get<uint32_t>(kSlotTmpKeys, n);
   uint32_t* tv = ws.get<uint32_t>(kSlotTmpVals, n);
-  static bool attr_set = false;
-  if (!attr_set) {
-    RS_CUDA(cudaFuncSetAttribute(k_kv_chunk_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kKvSmemBytes)));
-    attr_set = true;
-  }
+  set_smem(k_kv_chunk_scatter, kKvSmemBytes);
   auto* total = ws.get<unsigned long long>(kSlotScratch, 4);
   const uint32_t* sk = keys;
   const uint32_t* sv = vals;
@@ -1118,12 +1115,8 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
     exscan_u32(ws, table, nchunks * kMsdBins, off, total);
     {
       PassTimer pt_(RS_PASS_MSD_SCATTER, ws.stream);
-      static const bool attr = (cudaFuncSetAttribute(k_msd_scatter<Load>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     static_cast<int>(msd_scatter_smem<Load>())),
-                                cudaFuncSetAttribute(k_msd_scatter<LoadKeys<K>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     static_cast<int>(msd_scatter_smem<LoadKeys<K>>())),
-                                true);
-      (void)attr;
+      set_smem(k_msd_scatter<Load>, msd_scatter_smem<Load>());
+      set_smem(k_msd_scatter<LoadKeys<K>>, msd_scatter_smem<LoadKeys<K>>());
       if (level == 0)
         k_msd_scatter<<<nchunks, kMsdThreads, msd_scatter_smem<Load>(), ws.stream>>>(load0, segs_in, chunk_seg, shift,
                                                                                       off, dst);
@@ -1146,9 +1139,7 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
       PassTimer pt_(RS_PASS_BUCKET, ws.stream,
                     (h[1] ? 1 : 0) + (h[2] ? 1 : 0) + (h[3] ? 1 : 0) + (h[4] ? 1 : 0) + (h[5] ? 1 : 0));
       if (h[5]) {  // buffers sized to the largest leaf of the list
-        static const bool attr = (cudaFuncSetAttribute(k_leaf_radix<K, Emit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       static_cast<int>(leaf_radix_smem<K>(kLeafRadixMax))), true);
-        (void)attr;
+        set_smem(k_leaf_radix<K, Emit>, leaf_radix_smem<K>(kLeafRadixMax));
         const uint32_t lcap = (h[8] + 15) & ~15u;
         k_leaf_radix<K, Emit><<<h[5], kLeafRadixThreads, leaf_radix_smem<K>(lcap), ws.stream>>>(dst, leaf_radix, shift,
                                                                                                  lcap, emit);
@@ -1163,8 +1154,7 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
         const size_t grid_b = leaf_grid_words(shift) * sizeof(uint32_t);
         const size_t smem = std::min<size_t>(grid_b + 2 * 65536, smem_optin() - 1024);
         const uint32_t lcap = static_cast<uint32_t>(std::min<size_t>((smem - grid_b) / 2, 65535));
-        RS_CUDA(cudaFuncSetAttribute(k_leaf_grid<K, Emit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
+        set_smem(k_leaf_grid<K, Emit>, smem);
         k_leaf_grid<K, Emit><<<h[1], kLeafGridThreads, smem, ws.stream>>>(dst, leaf_grid, shift, lcap, emit, h[1],
                                                                            static_cast<uint32_t>(sm_count()));
       }
