@@ -1081,7 +1081,10 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
   auto* leaf_radix = ws.get<MsdSeg>(kSlotExtra1, cap);
   auto* cnt = ws.get<unsigned>(kSlotScratch, 10);  // [0..5] list counts, [6..7] u64 total, [8] largest radix leaf
   auto* total = reinterpret_cast<unsigned long long*>(cnt + 6);
-  MsdSeg first{0, static_cast<uint32_t>(n), 0, 0};
+  // the first level's one segment, its chunks already assigned (no count,
+  // scan and read-back for it)
+  const uint32_t first_chunks = static_cast<uint32_t>((n + kMsdChunk - 1) / kMsdChunk);
+  MsdSeg first{0, static_cast<uint32_t>(n), 0, first_chunks};
   RS_CUDA(cudaMemcpyAsync(segs_a, &first, sizeof(MsdSeg), cudaMemcpyHostToDevice, ws.stream));
   uint32_t nseg = 1;
   uint32_t shift = key_bits > kMsdDigitBits ? key_bits - kMsdDigitBits : 0;
@@ -1089,16 +1092,18 @@ void msd_sort(Workspace& ws, Load load0, uint64_t n, uint32_t key_bits, Emit emi
   MsdSeg* segs_out = segs_b;
   for (int level = 0; nseg > 0; ++level) {
     // chunks of every open segment
-    auto* ccount = ws.get<uint32_t>(kSlotMisc, 2ull * nseg + 2);
-    uint32_t* cstart = ccount + nseg + 1;
-    k_msd_chunk_counts<<<(nseg + 255) / 256, 256, 0, ws.stream>>>(segs_in, nseg, ccount);
-    RS_LAUNCH_CHECK();
-    exscan_u32(ws, ccount, nseg, cstart, total);
-    k_msd_chunk_assign<<<(nseg + 255) / 256, 256, 0, ws.stream>>>(segs_in, nseg, ccount, cstart);
-    RS_LAUNCH_CHECK();
-    unsigned long long nchunks = 0;
-    RS_CUDA(cudaMemcpyAsync(&nchunks, total, sizeof(nchunks), cudaMemcpyDeviceToHost, ws.stream));
-    RS_CUDA(cudaStreamSynchronize(ws.stream));
+    unsigned long long nchunks = first_chunks;
+    if (level > 0) {
+      auto* ccount = ws.get<uint32_t>(kSlotMisc, 2ull * nseg + 2);
+      uint32_t* cstart = ccount + nseg + 1;
+      k_msd_chunk_counts<<<(nseg + 255) / 256, 256, 0, ws.stream>>>(segs_in, nseg, ccount);
+      RS_LAUNCH_CHECK();
+      exscan_u32(ws, ccount, nseg, cstart, total);
+      k_msd_chunk_assign<<<(nseg + 255) / 256, 256, 0, ws.stream>>>(segs_in, nseg, ccount, cstart);
+      RS_LAUNCH_CHECK();
+      RS_CUDA(cudaMemcpyAsync(&nchunks, total, sizeof(nchunks), cudaMemcpyDeviceToHost, ws.stream));
+      RS_CUDA(cudaStreamSynchronize(ws.stream));
+    }
     auto* chunk_seg = ws.get<uint32_t>(kSlotTileFirst, nchunks);
     auto* table = ws.get<uint32_t>(kSlotCounts, nchunks * kMsdBins);
     auto* off = ws.get<uint32_t>(kSlotOccEnd, nchunks * kMsdBins);
