@@ -19,3 +19,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 300 python tools/profile_one.py > $O/plain_full.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_page_partition|k_page_count|k_emit" -s 3 -c 3 \
   -o $O/full python tools/profile_one.py > $O/ncu_full.log 2>&1; echo "ncu full rc=$?"
+# key/value: launch list and one full capture of the scatter
+timeout 600 python tools/profile_one.py --no-cfg2 --kv > $O/plain_kv.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  --log-file $O/launches_kv.csv python tools/profile_one.py --no-cfg2 --kv > $O/ncu_kv_launch.log 2>&1; echo "kv launch list rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_kv_chunk_scatter" -s 3 -c 1 \
+  -o $O/full_kv python tools/profile_one.py --no-cfg2 --kv > $O/ncu_full_kv.log 2>&1; echo "ncu full kv rc=$?"
