@@ -388,6 +388,7 @@ bool plan_two_level(uint64_t cells, uint64_t n, TwoLevel& t, bool ws) {
   if (S > kTlMaxInner) return false;
   t.cells = cells;
   t.S = static_cast<uint32_t>(S);
+  t.negS = 0u - t.S;
   t.B = static_cast<uint32_t>((cells + S - 1) / S);
   if (!div_magic32(S, t.magic, t.shift) || t.shift < 32) return false;  // S == 1: never (cells > smem grid)
   t.T = static_cast<uint32_t>((n + kTlTile - 1) / kTlTile);

@@ -5,9 +5,12 @@
 // The page-count kernel only needs, per outer bucket, every inner digit of the
 // bucket's keys in some 2 KB page; order is free.  So each bucket owns a ring
 // of two 128-entry chunks (256 B each) in shared memory and one shared word
-// (limit << 16 | next slot); a key's atomicAdd on that word returns its ring
-// slot: one shared atomic and one uint16 store per key, no staging buffer and
-// no run copies through registers.
+// (limit and next slot, in ring bytes: dir_word below); a key's atomicAdd on
+// that word returns its ring slot: one shared atomic and one uint16 store per
+// key, no staging buffer and no run copies through registers.  The word's
+// encoding keeps the ranker at ~18 instructions per key (was 23): the
+// writable test is a shift and a compare, the slot address one LOP3 over a
+// ring-size-aligned base, the inner digit one multiply-add by -S.
 //
 // Two warp roles.  Twelve ranking warps stream 3072-key tiles (8 keys per
 // thread, 16-byte loads two tiles ahead in registers) and rank them into two
@@ -46,8 +49,10 @@ template <class In>
 constexpr int kDirPerT = 32 / sizeof(In);  // 32 bytes of keys per ranker thread per tile
 constexpr uint32_t kDirRing = 2 * kDirChunk;
 
+// + one ring of slack: the kernel starts its rings on a ring-size boundary of
+// the shared window, so a ring slot's address is (word & mask) | ring base
 __host__ __device__ constexpr size_t page_dir_smem(uint32_t B) {
-  return 2 * (size_t)B * kDirRing * sizeof(uint16_t) + 2 * 128 * sizeof(uint32_t);
+  return 2 * (size_t)B * kDirRing * sizeof(uint16_t) + 2 * 128 * sizeof(uint32_t) + kDirRing * sizeof(uint16_t);
 }
 
 // kHot (skewed inputs, e.g. cfg3's Zipf-hot mapped cells): a shared uint32
@@ -61,9 +66,27 @@ template <bool kHot>
 __host__ __device__ constexpr uint32_t dir_chunk() { return kHot ? 64u : kDirChunk; }
 __host__ __device__ constexpr size_t page_dir_hot_smem(uint32_t B, uint32_t S) {
   return 2 * (size_t)B * 2 * dir_chunk<true>() * sizeof(uint16_t) + 2 * 128 * sizeof(uint32_t) +
-         (size_t)S * sizeof(uint32_t);
+         (size_t)S * sizeof(uint32_t) + 2 * dir_chunk<true>() * sizeof(uint16_t);
 }
 constexpr uint32_t kDirNoHot = 0xffffffffu;
+
+// A bucket's shared word counts ring BYTES: (2 * limit - 1) << 16 | 2 * next
+// (0 for limit 0).  With r the value an atomicAdd of 2 returns, the slot is
+// writable iff (r << 16) < r (next < limit, two instructions), its byte offset
+// in the ring is r & (ring bytes - 1), and "limit != 0" is r > 0xffff.
+__host__ __device__ constexpr uint32_t dir_word(uint32_t limit, uint32_t next) {
+  return limit ? ((2u * limit - 1u) << 16) | (2u * next) : 0u;
+}
+__device__ __forceinline__ uint32_t dir_word_next(uint32_t v) { return (v & 0xffffu) >> 1; }
+__device__ __forceinline__ uint32_t dir_word_limit(uint32_t v) { return ((v >> 16) + 1u) >> 1; }
+__device__ __forceinline__ uint32_t atoms_add(uint32_t saddr, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(saddr), "r"(v));
+  return r;
+}
+__device__ __forceinline__ void sts_u16(uint32_t saddr, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(saddr), "h"(static_cast<uint16_t>(v)));
+}
 
 template <class Map, bool kHot = false>
 __global__ void __launch_bounds__(kDirThreads, 2)
@@ -83,8 +106,12 @@ __global__ void __launch_bounds__(kDirThreads, 2)
   constexpr int kRanked = 1, kFlushed = 3;  // named barrier ids (+ set)
   extern __shared__ __align__(128) unsigned char sm[];
   const uint32_t B = t.B;
-  uint16_t* ring = reinterpret_cast<uint16_t*>(sm);                                            // [2][B][kDirRing]
-  uint32_t* w = reinterpret_cast<uint32_t*>(sm + 2 * (size_t)B * kDirRing * sizeof(uint16_t));  // [2][128]
+  constexpr uint32_t kRingBytes = kDirRing * sizeof(uint16_t);
+  const uint32_t sm_sa = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+  const uint32_t pad = (0u - sm_sa) & (kRingBytes - 1);  // rings start on a ring-size boundary
+  uint16_t* ring = reinterpret_cast<uint16_t*>(sm + pad);                                            // [2][B][kDirRing]
+  uint32_t* w = reinterpret_cast<uint32_t*>(sm + pad + 2 * (size_t)B * kRingBytes);  // [2][128]
+  const uint32_t ring_sa = sm_sa + pad, w_sa = ring_sa + 2 * B * kRingBytes;
   uint32_t* s_hh = w + 2 * 128;  // kHot: [S] counts of the hot bucket's inner cells
   __shared__ uint32_t s_next, s_hot;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
@@ -97,7 +124,7 @@ __global__ void __launch_bounds__(kDirThreads, 2)
   const uint32_t full_tiles = static_cast<uint32_t>(n / kDirTile);
   if (tid < 2 * 128) {
     const uint32_t b = tid & 127;
-    w[tid] = b < B ? kDirRing << 16 : 0u;  // both chunks writable; the dummy word B: limit 0
+    w[tid] = b < B ? dir_word(kDirRing, 0) : 0u;  // both chunks writable; the dummy word B: limit 0
   }
   if (tid == 0) {
     s_next = 0;
@@ -127,8 +154,8 @@ __global__ void __launch_bounds__(kDirThreads, 2)
     };
     auto rank_tile = [&](auto full_c, uint32_t tile, int s, In (&cur)[kDirPerT<In>]) {
       constexpr bool kFull = decltype(full_c)::value;
-      uint32_t* ws = w + s * 128;
-      uint16_t* rs = ring + (size_t)s * B * kDirRing;
+      const uint32_t ws_sa = w_sa + s * 512, rs_sa = ring_sa + s * B * kRingBytes;
+      const uint32_t negS = t.negS;  // inner digit = cell + bucket * (-S): one multiply-add
       // each key's 32-bit cell (8-byte keys saturate at 0xFFFFFFFF, which no
       // grid reaches, so kc < cells is the in-grid test for both widths)
       uint32_t kc[kDirPerT<In>], r[kDirPerT<In>];
@@ -167,22 +194,22 @@ __global__ void __launch_bounds__(kDirThreads, 2)
           atomicAdd(&s_hh[kc[j] - bk * S], 1u);
           r[j] = 0;
         } else {
-          r[j] = atomicAdd(&ws[bk], 1u);
+          r[j] = atoms_add(ws_sa + bk * 4, 2u);
         }
       }
-      unsigned fb = 0;
+      bool fb = false;
 #pragma unroll
       for (int j = 0; j < kDirPerT<In>; ++j) {
-        const uint32_t kk = kc[j];
-        const uint32_t pos = r[j] & 0xffffu, lim = r[j] >> 16;
+        const uint32_t kk = kc[j], rr = r[j];
         const uint32_t bk = __umulhi(kk, magic32) >> shift32;
-        if (pos < lim) rs[bk * kDirRing + (pos & (kDirRing - 1))] = static_cast<uint16_t>(kk - bk * S);
-        fb |= (pos >= lim && lim != 0) ? 1u << j : 0u;
+        const bool writable = (rr << 16) < rr;
+        if (writable) sts_u16((rr & (kRingBytes - 1)) | (rs_sa + bk * kRingBytes), kk + bk * negS);
+        fb |= !writable && rr > 0xffffu;
       }
       if (__any_sync(0xffffffffu, fb)) {
 #pragma unroll
         for (int j = 0; j < kDirPerT<In>; ++j) {
-          const bool mine = (fb >> j) & 1u;
+          const bool mine = !((r[j] << 16) < r[j]) && r[j] > 0xffffu;  // past a nonzero limit
           if (!__any_sync(0xffffffffu, mine)) continue;  // a match only for the key slots that need one
           const uint32_t kk = kc[j];
           const unsigned peers = __match_any_sync(0xffffffffu, mine ? kk : 0xffffffffu);
@@ -235,8 +262,8 @@ __global__ void __launch_bounds__(kDirThreads, 2)
     uint32_t* ws = w + s * 128;
     const uint16_t* rs = ring + ((size_t)s * B + b) * kDirRing;
     const uint32_t v = ws[b];
-    uint32_t next = v & 0xffffu;
-    const uint32_t lim = v >> 16;
+    uint32_t next = dir_word_next(v);
+    const uint32_t lim = dir_word_limit(v);
     if (next > lim) {  // the keys past the limit were counted in the grid
       next = lim;
       if (kHot && s_hot == kDirNoHot) atomicCAS(&s_hot, kDirNoHot, b);  // skew: b's keys count in place from now on
@@ -262,7 +289,7 @@ __global__ void __launch_bounds__(kDirThreads, 2)
       nlim -= m * kDirRing;
       issued -= m * 2;
     }
-    ws[b] = (nlim << 16) | next;
+    ws[b] = dir_word(nlim, next);
   };
   auto step = [&](auto s_c, uint32_t i) {
     constexpr int s = decltype(s_c)::value;
@@ -279,7 +306,7 @@ __global__ void __launch_bounds__(kDirThreads, 2)
     auto tail = [&](auto s_c) {
       constexpr int s = decltype(s_c)::value;
       const uint32_t is = s ? issued1 : issued0;
-      const uint32_t next = w[s * 128 + b] & 0xffffu;
+      const uint32_t next = dir_word_next(w[s * 128 + b]);
       const uint32_t rem = next - is * kDirChunk;
       if (rem) {
         uint16_t* rc = ring + ((size_t)s * B + b) * kDirRing + (is & 1) * kDirChunk;

@@ -55,6 +55,7 @@ struct TwoLevel {
   uint32_t G;                // persistent partition CTAs
   uint32_t pages_per_cta;    // page region of one CTA
   uint32_t group_pages;      // pages per K2 work item
+  uint32_t negS;             // 0 - S: inner digit = cell + bucket * negS, one multiply-add from the constant bank
 };
 
 __device__ __forceinline__ uint32_t tl_bucket(uint32_t cell, const TwoLevel& t) {
