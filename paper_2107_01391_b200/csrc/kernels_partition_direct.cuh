@@ -51,8 +51,9 @@ constexpr uint32_t kDirRing = 2 * kDirChunk;
 
 // + one ring of slack: the kernel starts its rings on a ring-size boundary of
 // the shared window, so a ring slot's address is (word & mask) | ring base
+// B + 1 rings per set: ring B takes the keys outside the grid (never flushed)
 __host__ __device__ constexpr size_t page_dir_smem(uint32_t B) {
-  return 2 * (size_t)B * kDirRing * sizeof(uint16_t) + 2 * 128 * sizeof(uint32_t) + kDirRing * sizeof(uint16_t);
+  return 2 * (size_t)(B + 1) * kDirRing * sizeof(uint16_t) + 2 * 128 * sizeof(uint32_t) + kDirRing * sizeof(uint16_t);
 }
 
 // kHot (skewed inputs, e.g. cfg3's Zipf-hot mapped cells): a shared uint32
@@ -65,7 +66,7 @@ __host__ __device__ constexpr size_t page_dir_smem(uint32_t B) {
 template <bool kHot>
 __host__ __device__ constexpr uint32_t dir_chunk() { return kHot ? 64u : kDirChunk; }
 __host__ __device__ constexpr size_t page_dir_hot_smem(uint32_t B, uint32_t S) {
-  return 2 * (size_t)B * 2 * dir_chunk<true>() * sizeof(uint16_t) + 2 * 128 * sizeof(uint32_t) +
+  return 2 * (size_t)(B + 1) * 2 * dir_chunk<true>() * sizeof(uint16_t) + 2 * 128 * sizeof(uint32_t) +
          (size_t)S * sizeof(uint32_t) + 2 * dir_chunk<true>() * sizeof(uint16_t);
 }
 constexpr uint32_t kDirNoHot = 0xffffffffu;
@@ -109,9 +110,14 @@ __global__ void __launch_bounds__(kDirThreads, 2)
   constexpr uint32_t kRingBytes = kDirRing * sizeof(uint16_t);
   const uint32_t sm_sa = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
   const uint32_t pad = (0u - sm_sa) & (kRingBytes - 1);  // rings start on a ring-size boundary
-  uint16_t* ring = reinterpret_cast<uint16_t*>(sm + pad);                                            // [2][B][kDirRing]
-  uint32_t* w = reinterpret_cast<uint32_t*>(sm + pad + 2 * (size_t)B * kRingBytes);  // [2][128]
-  const uint32_t ring_sa = sm_sa + pad, w_sa = ring_sa + 2 * B * kRingBytes;
+  uint16_t* ring = reinterpret_cast<uint16_t*>(sm + pad);                                  // [2][B + 1][kDirRing]
+  uint32_t* w = reinterpret_cast<uint32_t*>(sm + pad + 2 * (size_t)(B + 1) * kRingBytes);  // [2][128]
+  const uint32_t ring_sa = sm_sa + pad, w_sa = ring_sa + 2 * (B + 1) * kRingBytes;
+  // The word of "bucket" B takes the keys outside the grid.  Its limit never
+  // binds (their digits go to ring B, which nobody reads), so "not writable"
+  // alone means a full ring; the hot variant keeps limit 0 there instead (its
+  // hot keys carry word 0: no store, no fallback).
+  constexpr uint32_t kDummyWord = kHot ? 0u : dir_word(0x8000u, 0);
   uint32_t* s_hh = w + 2 * 128;  // kHot: [S] counts of the hot bucket's inner cells
   __shared__ uint32_t s_next, s_hot;
   const uint32_t tid = threadIdx.x, lane = tid & 31;
@@ -124,7 +130,7 @@ __global__ void __launch_bounds__(kDirThreads, 2)
   const uint32_t full_tiles = static_cast<uint32_t>(n / kDirTile);
   if (tid < 2 * 128) {
     const uint32_t b = tid & 127;
-    w[tid] = b < B ? dir_word(kDirRing, 0) : 0u;  // both chunks writable; the dummy word B: limit 0
+    w[tid] = b < B ? dir_word(kDirRing, 0) : kDummyWord;  // both chunks writable
   }
   if (tid == 0) {
     s_next = 0;
@@ -154,11 +160,14 @@ __global__ void __launch_bounds__(kDirThreads, 2)
     };
     auto rank_tile = [&](auto full_c, uint32_t tile, int s, In (&cur)[kDirPerT<In>]) {
       constexpr bool kFull = decltype(full_c)::value;
-      const uint32_t ws_sa = w_sa + s * 512, rs_sa = ring_sa + s * B * kRingBytes;
-      const uint32_t negS = t.negS;  // inner digit = cell + bucket * (-S): one multiply-add
+      uint32_t ws_sa = w_sa + s * 512, rs_sa = ring_sa + s * (B + 1) * kRingBytes;
+      asm volatile("" : "+r"(ws_sa), "+r"(rs_sa));  // once per tile, not per key
+      // inner digit = cell + bucket * (-S): one multiply-add; the shuffle keeps
+      // -S in a register (ptxas reloads a plain parameter for every key)
+      const uint32_t negS = __shfl_sync(0xffffffffu, t.negS, 0);
       // each key's 32-bit cell (8-byte keys saturate at 0xFFFFFFFF, which no
       // grid reaches, so kc < cells is the in-grid test for both widths)
-      uint32_t kc[kDirPerT<In>], r[kDirPerT<In>];
+      uint32_t kc[kDirPerT<In>], r[kDirPerT<In>], bkv[kDirPerT<In>];
       const uint32_t hot = kHot ? *reinterpret_cast<volatile uint32_t*>(&s_hot) : kDirNoHot;
 #pragma unroll
       for (int j = 0; j < kDirPerT<In>; ++j) {
@@ -180,16 +189,18 @@ __global__ void __launch_bounds__(kDirThreads, 2)
           k = map(cur[j], flags);
           kc[j] = k < 0xFFFFFFFFull ? static_cast<uint32_t>(k) : 0xFFFFFFFFu;
         }
-        bool ing;
+        // a cell past the last bucket clamps to B; the few cells between the
+        // grid's end and the last bucket's end stay in that bucket (the page
+        // count drops them; the max flags the pass anyway)
+        uint32_t bk = min(__umulhi(kc[j], magic32) >> shift32, B);
         if constexpr (kFull) {
           mx = k > mx ? k : mx;
-          ing = kc[j] < cells32;
         } else {
           const bool ok = index_of(tile, j) < n;
           mx = (ok && k > mx) ? k : mx;
-          ing = ok && kc[j] < cells32;
+          bk = ok ? bk : B;
         }
-        const uint32_t bk = ing ? __umulhi(kc[j], magic32) >> shift32 : B;
+        bkv[j] = bk;
         if (kHot && bk == hot) {  // counted in place; r = 0 (limit 0): no ring store, no fallback
           atomicAdd(&s_hh[kc[j] - bk * S], 1u);
           r[j] = 0;
@@ -197,19 +208,23 @@ __global__ void __launch_bounds__(kDirThreads, 2)
           r[j] = atoms_add(ws_sa + bk * 4, 2u);
         }
       }
-      bool fb = false;
+      bool nw[kDirPerT<In>];  // key j found its ring full
 #pragma unroll
       for (int j = 0; j < kDirPerT<In>; ++j) {
         const uint32_t kk = kc[j], rr = r[j];
-        const uint32_t bk = __umulhi(kk, magic32) >> shift32;
+        const uint32_t bk = bkv[j];
         const bool writable = (rr << 16) < rr;
         if (writable) sts_u16((rr & (kRingBytes - 1)) | (rs_sa + bk * kRingBytes), kk + bk * negS);
-        fb |= !writable && rr > 0xffffu;
+        nw[j] = kHot ? !writable && rr > 0xffffu : !writable;
       }
+      bool fb = false;
+#pragma unroll
+      for (int j = 0; j < kDirPerT<In>; ++j) fb = fb || nw[j];
       if (__any_sync(0xffffffffu, fb)) {
 #pragma unroll
         for (int j = 0; j < kDirPerT<In>; ++j) {
-          const bool mine = !((r[j] << 16) < r[j]) && r[j] > 0xffffu;  // past a nonzero limit
+          // past a (nonzero) limit; a cell beyond the grid in the last bucket is dropped
+          const bool mine = !((r[j] << 16) < r[j]) && (!kHot || r[j] > 0xffffu) && kc[j] < cells32;
           if (!__any_sync(0xffffffffu, mine)) continue;  // a match only for the key slots that need one
           const uint32_t kk = kc[j];
           const unsigned peers = __match_any_sync(0xffffffffu, mine ? kk : 0xffffffffu);
@@ -260,7 +275,7 @@ __global__ void __launch_bounds__(kDirThreads, 2)
     constexpr int s = decltype(s_c)::value;
     uint32_t& issued = s ? issued1 : issued0;
     uint32_t* ws = w + s * 128;
-    const uint16_t* rs = ring + ((size_t)s * B + b) * kDirRing;
+    const uint16_t* rs = ring + ((size_t)s * (B + 1) + b) * kDirRing;
     const uint32_t v = ws[b];
     uint32_t next = dir_word_next(v);
     const uint32_t lim = dir_word_limit(v);
@@ -295,7 +310,7 @@ __global__ void __launch_bounds__(kDirThreads, 2)
     constexpr int s = decltype(s_c)::value;
     nbar_sync<kRanked, kThr>(s);  // tile i ranked into set s
     if (b < B) flush(s_c);
-    if (b == B) w[s * 128 + B] = 0;
+    if (b == B) w[s * 128 + B] = kDummyWord;
     if (i + 2 < ntiles) nbar_arrive<kFlushed, kThr>(s);
   };
   for (uint32_t i = 0; i < ntiles; i += 2) {
@@ -309,7 +324,7 @@ __global__ void __launch_bounds__(kDirThreads, 2)
       const uint32_t next = dir_word_next(w[s * 128 + b]);
       const uint32_t rem = next - is * kDirChunk;
       if (rem) {
-        uint16_t* rc = ring + ((size_t)s * B + b) * kDirRing + (is & 1) * kDirChunk;
+        uint16_t* rc = ring + ((size_t)s * (B + 1) + b) * kDirRing + (is & 1) * kDirChunk;
         for (uint32_t e = rem; e < kDirChunk; ++e) rc[e] = kPagePad;
         open_page();
         fence_proxy_async_smem();
