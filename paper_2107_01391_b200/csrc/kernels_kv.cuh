@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
     uint32_t* in_v = in_k + kKvTile;
     // striped order: record t0 + warp*512 + j*32 + lane (input order =
     // warp-major, then j, then lane)
-    uint32_t k[kKvItems], v[kKvItems], rank[kKvItems];
-    uint32_t d[kKvItems];
+    uint32_t k[kKvItems], v[kKvItems];
+    uint32_t d[kKvItems];  // digit (0xffff: no record) | the record's rank << 16 once ranked
     if (full) {
       mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
       phase ^= 1u << buf;
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
         bm[d[j]] = 0u;
       }
       __syncwarp();
-      rank[j] = base + __popc(peers & lt);
+      d[j] |= (base + __popc(peers & lt)) << 16;
     }
     __syncthreads();
     // per digit: exclusive prefix across warps (in s_wh) and tile count
@@ -240,9 +240,12 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
       for (int w = 0; w < warp; ++w) before += s_scan[w];
       if (b < p.bins) {
         const uint32_t start = before + inc - c;
-        s_start[b] = start;
         s_cnt[b] = s_cur[b] - start;  // this tile's destination base: dest(i) = s_cnt[b] + i
         s_cur[b] += c;
+        // the digit's start in the tile folded into its warp prefixes: one
+        // lookup per staged record
+#pragma unroll 1
+        for (int w = 0; w < kKvWarps; ++w) s_wh[w * kKvBins + b] += static_cast<uint16_t>(start);
       }
       if (b == 127) s_total = before + inc;
     }
@@ -252,10 +255,11 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
     unsigned long long* stage = reinterpret_cast<unsigned long long*>(in_k);
 #pragma unroll
     for (int j = 0; j < kKvItems; ++j) {
-      if (d[j] != 0xffffu) {
-        const uint32_t pos = s_start[d[j]] + wh[d[j]] + rank[j];
+      const uint32_t dj = d[j] & 0xffffu;
+      if (dj != 0xffffu) {
+        const uint32_t pos = wh[dj] + (d[j] >> 16);
         stage[pos] = (static_cast<unsigned long long>(v[j]) << 32) | k[j];
-        s_dig[pos] = static_cast<uint8_t>(d[j]);
+        s_dig[pos] = static_cast<uint8_t>(dj);
       }
     }
     __syncthreads();
