@@ -8,7 +8,7 @@
 // (limit and next slot, in ring bytes: dir_word below); a key's atomicAdd on
 // that word returns its ring slot: one shared atomic and one uint16 store per
 // key, no staging buffer and no run copies through registers.  The word's
-// encoding keeps the ranker at ~18 instructions per key (was 23): the
+// encoding keeps the ranker at ~15 instructions per key (was 23): the
 // writable test is a shift and a compare, the slot address one LOP3 over a
 // ring-size-aligned base, the inner digit one multiply-add by -S.
 //
@@ -26,8 +26,11 @@
 // A bucket that takes more keys in one tile than its writable chunks hold
 // (more than 128-255 keys of a 3072-key tile: skewed input) counts the rest
 // straight into the grid with warp-aggregated global atomics — correct,
-// slower; cfg3's Zipf-skewed mapped cells keep the TMA-fed partition.  Keys
-// outside the grid rank into a dummy word whose limit is 0.
+// slower; cfg3's Zipf-skewed mapped cells run the hot variant below.  Keys
+// outside the grid rank into the word of a spare ring (index B) whose limit
+// never binds and whose contents nobody reads, so a ranker's only unwritable
+// case is a full ring (the hot variant keeps limit 0 there: its in-place
+// counted keys carry word 0).
 //
 // Replaces the loop of hashing.cpp:40-52 (hash_insert of every key) with the
 // two-level grid of kernels_two_level.cuh; the pages are the same as

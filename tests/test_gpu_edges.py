@@ -112,6 +112,35 @@ def test_count_phase_rejects_keys_outside_the_grid(rs):
     assert lib.rs_status_name(st).decode() == "out_of_range"
 
 
+@pytest.mark.parametrize("cells", [823543, 123457, 1000000])
+def test_direct_partition_cells_past_a_partial_last_bucket(rs, cells):
+    """A grid whose last outer bucket is partial (cells not a multiple of the
+    inner size): cells between the grid's end and that bucket's end share its
+    bucket index in the direct partition.  In-grid keys count exactly; a key
+    in that gap, or far outside, fails with out_of_range and nothing is
+    written past the grid."""
+    import torch
+
+    lib = rs._lib.load()
+    n = 1 << 22
+    g = torch.Generator(device="cuda").manual_seed(cells)
+    k = torch.randint(0, cells, (n,), dtype=torch.int32, device="cuda", generator=g)
+    k[:64] = cells - 1  # the last cell is occupied
+    guard = 4096
+    buf = torch.full((cells + guard,), -7, dtype=torch.int32, device="cuda")
+    rs._check(lib.rs_count_u32(rs._ptr(k), n, rs._ptr(buf), cells, None, rs._stream()))
+    assert torch.equal(buf[:cells].long(), torch.bincount(k.long(), minlength=cells))
+    assert bool((buf[cells:] == -7).all())
+    for bad in (cells, cells + 3, cells + 60000, 0x7fffffff):
+        kb = k.clone()
+        kb[12345] = bad
+        kb[n - 1] = bad
+        buf.fill_(-7)
+        st = lib.rs_count_u32(rs._ptr(kb), n, rs._ptr(buf), cells, None, rs._stream())
+        assert lib.rs_status_name(st).decode() == "out_of_range"
+        assert bool((buf[cells:] == -7).all())
+
+
 def test_kv_place_rejects_keys_outside_the_grid(rs):
     """rs_kv_place_u32 never stores a record whose key lies outside the
     placement tables (it would index past them and write into a peer's
