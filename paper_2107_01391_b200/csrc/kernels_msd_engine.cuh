@@ -871,21 +871,21 @@ __device__ __forceinline__ uint32_t rec_ord(const uint8_t* r, uint32_t j, uint32
 
 __global__ void k_report_recs(const uint8_t* __restrict__ recs, uint64_t n, uint32_t width, uint32_t w,
                               uint32_t radix, const uint16_t* __restrict__ ord, DevStats* st) {
+  // one warp: lane l finds the first record whose first ordinal is >= r
+  // (r = base + l); the end of r's run is lane l + 1's answer, so each lane
+  // makes one binary search (lane 31 only supplies lane 30's end)
   unsigned long long span = 0;
-  for (uint32_t r = threadIdx.x; r < radix; r += blockDim.x) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t base = 0; base < radix; base += 31) {
+    const uint32_t r = base + lane;
     uint64_t a = 0, b = n;  // first record with first ordinal >= r
     while (a < b) {
       const uint64_t mid = (a + b) >> 1;
       if (rec_ord(recs + mid * width, 0, width, ord) >= r) b = mid;
       else a = mid + 1;
     }
-    uint64_t c = a, e = n;  // first record with first ordinal >= r+1
-    while (c < e) {
-      const uint64_t mid = (c + e) >> 1;
-      if (rec_ord(recs + mid * width, 0, width, ord) >= r + 1) e = mid;
-      else c = mid + 1;
-    }
-    if (a < c) {
+    const uint64_t c = __shfl_down_sync(0xffffffffu, a, 1);  // first record with first ordinal >= r + 1
+    if (lane < 31 && r < radix && a < c) {
       unsigned long long lo = 0, hi = 0;
       for (uint32_t j = 1; j < w; ++j) {
         lo = lo * radix + rec_ord(recs + a * width, j, width, ord);
