@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kKvThreads) k_kv_chunk_hist(const uint32_t* __
 // are in registers its buffer becomes that tile's output staging.
 constexpr size_t kKvSmemBytes = 2 * (size_t)kKvTile * 8  // s_in[2] (keys | vals)
                                 + kKvWarps * kKvBins * 2  // s_wh
-                                + kKvBins * 4 * 3         // s_cnt, s_start, s_cur
+                                + kKvBins * 4 * 2         // s_cnt, s_cur
                                 + kKvTile                 // s_dig
                                 + kKvWarps * kKvBins * 4;  // s_bm
 
@@ -126,8 +126,7 @@ __global__ void __launch_bounds__(kKvThreads, 3) k_kv_chunk_scatter(const uint32
   uint32_t* s_in = reinterpret_cast<uint32_t*>(kv_smem);              // [2][2][kKvTile]
   uint16_t* s_wh = reinterpret_cast<uint16_t*>(s_in + 4 * kKvTile);   // [kKvWarps][kKvBins]
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_wh + kKvWarps * kKvBins);
-  uint32_t* s_start = s_cnt + kKvBins;
-  uint32_t* s_cur = s_start + kKvBins;
+  uint32_t* s_cur = s_cnt + kKvBins;
   uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_cur + kKvBins);  // [kKvTile]
   uint32_t* s_bm = reinterpret_cast<uint32_t*>(s_dig + kKvTile);  // [kKvWarps][kKvBins] lane bitmaps
   __shared__ uint32_t s_scan[kKvWarps];
